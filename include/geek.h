@@ -1,0 +1,221 @@
+/*
+ * geek.h -- C ABI of libgeek.so, the B200 (sm_100a) kernels behind the GEEK
+ * hot path: bucketize -> SILK seeding -> one-pass assignment.
+ *
+ * The reference (lshclust, pure Python + numpy) has no FFI; each entry point
+ * below replaces the numpy inner loop cited beside it (paths relative to
+ * /root/reference/pkg/src/lshclust).  The Python package
+ * paper_2106_10515_b200 binds these with ctypes behind
+ * the reference's own API names.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless its name ends in
+ *     `_host`; sizes are element counts; `stream` is a cudaStream_t (NULL =
+ *     legacy default stream);
+ *   - every function returns GEEK_OK (0) or a negative status and never
+ *     throws; geek_last_error() describes the last failure of the calling
+ *     host thread;
+ *   - functions are stream-ordered and reentrant; a few (marked SYNC) read a
+ *     data-dependent size back to the host and synchronise `stream`;
+ *   - ids are uint32 (n < 2^32); MinHash values are uint32 (universe < 2^32).
+ */
+#ifndef GEEK_H
+#define GEEK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GEEK_OK 0
+#define GEEK_EINVAL -1 /* precondition violated (maps to InvalidInput) */
+#define GEEK_ECUDA -2  /* CUDA runtime error (maps to EngineError)     */
+#define GEEK_ENOMEM -3 /* device allocation failed                     */
+#define GEEK_ERANGE -4 /* output capacity too small; size reported     */
+
+#define GEEK_NONE 0xFFFFFFFFu /* "no value" for MinHash minima / codes */
+
+/* One MinHash permutation pi over [0, u) (hashing.py:51-140).
+ * u > 4096: cycle-walking w-bit mix, w = bitlen(u-1) <= 32, with
+ *   mask, c1, c2, a1, s1, s2 exactly as hashing.py:97-113, and the inverse
+ *   multipliers c1inv, c2inv (mod 2^w) for the inverse-rank scan.
+ * u <= 4096: `table` is the offset of pi (u entries) inside the caller's
+ *   table pool, `inv_table` the offset of pi^-1 (hashing.py:80-95);
+ *   GEEK_NONE when mixing.                                                 */
+typedef struct {
+  uint64_t u;
+  uint32_t mask, c1, c2, a1, s1, s2, c1inv, c2inv;
+  uint32_t table, inv_table;
+} geek_perm_t;
+
+int geek_version(void);
+const char* geek_last_error(void);
+/* number of SMs of the current device, or a negative status */
+int geek_device_sms(void);
+
+/* ---- MinHash --------------------------------------------------------- */
+
+/* out[p*count + i] = pi_p(x[i])   (MinHashFunction.permute, hashing.py:126-140) */
+int geek_perm_forward(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
+                      const uint32_t* x, uint64_t count, uint32_t* out, void* stream);
+
+/* sig[s*nperm + p] = min_{e in set s} pi_p(e); sets are CSR (flat, offsets[nsets+1]),
+ * non-empty.  (SignatureScheme.signatures_for_sets, hashing.py:265-282)        */
+int geek_set_minhash(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
+                     const uint32_t* flat, const uint64_t* offsets, uint64_t nsets,
+                     uint32_t* sig, void* stream);
+
+/* Inverse-rank scan: for a family of m partitions of [0, n) given
+ * id-major as codes[i*m + j] in [0, t), writes sig[p*(m*t) + j*t + s] =
+ * min_{i : codes[i*m+j] == s} pi_p(i) for every non-empty bucket (GEEK_NONE
+ * for empty ones).  `nonempty_host` (may be NULL: then every bucket is assumed
+ * non-empty) gives the number of non-empty buckets the scan must cover.
+ * Bit-identical to the member scan of engine.py:256-266.  SYNC.            */
+int geek_silk_invscan(const uint32_t* codes, uint64_t n, int m, uint64_t t,
+                      const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
+                      uint32_t* sig, const uint64_t* nonempty_host, uint64_t* draws_host,
+                      void* stream);
+
+/* ---- dense bucketize -------------------------------------------------- */
+
+/* keys[j*n + i] = order-preserving uint64 image of the float64 projection
+ * <x_i, A_j> (transform.py:125, engine.py:180); -0.0 folds onto +0.0 and NaN
+ * onto the top key, matching np.lexsort.  dtype 0 = float32 X, 1 = float64.  */
+int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
+                      uint64_t* keys, void* stream);
+
+/* Exact even rank split of every table (transform.py:95-109, engine.py:219-225):
+ * codes[i*m + j] = slot of id i in table j, ties broken by id.  keys are
+ * [m][n] as produced by geek_project_keys (or any order-preserving image).
+ * stats_host[0..3] (may be NULL) = {fine bins, straddling ids, max straddle
+ * bin, fallback sorts}.  SYNC.                                              */
+int geek_rank_split(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
+                    uint64_t* stats_host, void* stream);
+
+/* Same split for a single column of keys written with a row stride:
+ * codes[i*stride + col] (used for numeric discretisation, transform.py:131-155). */
+int geek_rank_split_strided(const uint64_t* keys, uint64_t n, uint64_t t, uint32_t* codes,
+                            uint64_t stride, uint64_t col, void* stream);
+
+/* order-preserving keys of a float64 / float32 column with a row stride */
+int geek_column_keys(const void* values, int dtype, uint64_t n, uint64_t stride, uint64_t col,
+                     uint64_t* keys, void* stream);
+
+/* ---- sort / group-by primitives ---------------------------------------- */
+
+/* Lexicographic stable sort of nrows rows of `width` uint32 columns
+ * (row-major); perm[r] = original index of the r-th smallest row; gid[r] =
+ * dense group index of that row (equal rows share it); *ngroups_host.
+ * (np.unique(axis=0, return_inverse) + stable argsort: seeding.py:83-90,
+ * transform.py:158-169).  `bits_host` (may be NULL) bounds each column. SYNC. */
+int geek_group_rows(const uint32_t* rows, uint64_t nrows, int width, const int* bits_host,
+                    uint32_t* perm, uint32_t* gid, uint64_t* ngroups_host, void* stream);
+
+/* ---- SILK vote --------------------------------------------------------- */
+
+/* Emit (bin, id) membership pairs for binned buckets of the id-major
+ * partition `codes`: for each id i and table j with bucket b = j*t + code,
+ * for each bin in bb_bins[bb_off[b] .. bb_off[b+1]) emit (bin, i).
+ * *count_host returns the number written (capacity = cap).  SYNC.          */
+int geek_emit_members_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t,
+                            const uint32_t* bb_off, const uint32_t* bb_bins,
+                            uint32_t* out_bin, uint32_t* out_id, uint64_t cap,
+                            uint64_t* count_host, void* stream);
+
+/* Strict-majority vote (seeding.py:107-114, engine.py:278-282): given (bin,
+ * id) pairs (any order; a bucket listed once per bin) and bin sizes in
+ * buckets, writes the winners grouped by bin with ids ascending
+ * (win_bin/win_id, *nwin_host) after dropping bins with < delta winners.
+ * SYNC.                                                                    */
+int geek_majority_vote(const uint32_t* pair_bin, const uint32_t* pair_id, uint64_t npairs,
+                       const uint32_t* bin_size, uint64_t nbins, uint64_t delta,
+                       uint32_t* win_bin, uint32_t* win_id, uint64_t* nwin_host,
+                       void* stream);
+
+/* ---- dedup helpers ----------------------------------------------------- */
+
+/* Given groups (CSR flat/offsets) and a grouping of them into bins (perm/gid
+ * from geek_group_rows over their signatures), keep[g] = 1 for the one
+ * representative per bin: largest, ties to the lexicographically smallest
+ * member sequence (seeding.py:117-134).                                    */
+int geek_pick_representatives(const uint32_t* flat, const uint64_t* offsets, const uint32_t* perm,
+                              const uint32_t* gid, uint64_t ngroups, uint8_t* keep, void* stream);
+
+/* Canonical order of groups by member tuple (SeedGroup.key, data.py:200-202;
+ * a proper prefix sorts first): order[r] = index of the r-th group.  SYNC. */
+int geek_sort_groups(const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups,
+                     uint32_t* order, void* stream);
+
+/* ---- exact centers ----------------------------------------------------- */
+
+/* min / max binary exponent over the non-zero entries of X (frexp sense);
+ * out_host = {emin, emax} (emin > emax when X is all zero).  SYNC.          */
+int geek_exponent_range(const void* X, int dtype, uint64_t n, int d, int* out_host, void* stream);
+
+/* Exact per-group column sums in base-2^32 digits relative to 2^emin
+ * (numeric.py:19-40): digits[(g*d + c)*nd + k] (int64, ADDED to).  Members
+ * are global ids; rows outside [row_lo, row_lo + nrows) are skipped (a shard
+ * contributes only its own rows; engine.py:299-311).                        */
+int geek_exact_sums(const void* X, int dtype, uint64_t nrows, int d, uint64_t row_lo,
+                    const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups,
+                    int emin, int nd, int64_t* digits, void* stream);
+
+/* Correctly rounded means from the digit sums (numeric.py:43-46).           */
+int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngroups, int d,
+                     int emin, int nd, double* out, void* stream);
+
+/* ---- assignment -------------------------------------------------------- */
+
+/* Nearest center by float64 direct-difference distance with numpy's pairwise
+ * summation order and first-index ties (assignment.py:54-62, :95-99):
+ * labels[i], best[i] = distance.  C is [k][d] float64.                      */
+int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
+                   int64_t* labels, double* best, void* stream);
+
+/* radii[c] = max best over members (0 if none), sizes[c] = member count
+ * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed
+ * outputs, or on partial results to merge).                                 */
+int geek_radii_sizes(const int64_t* labels, const double* best, uint64_t n, uint64_t k,
+                     double* radii, int64_t* sizes, void* stream);
+
+/* numpy pairwise sum (float64 add.reduce) of v[0..n): *out (device).        */
+int geek_pairwise_sum(const double* v, uint64_t n, double* out, void* stream);
+
+/* Jaccard assignment, categorical records (assignment.py:63-67):
+ * dist = 1 - m/(2d - m), m = #equal attributes; codes [n][d], modes [k][d]. */
+int geek_assign_categorical(const int32_t* codes, uint64_t n, int d, const int32_t* modes,
+                            uint64_t k, int64_t* labels, double* best, void* stream);
+
+/* Jaccard assignment, sparse sets vs binary modes (assignment.py:68-78);
+ * sets are CSR over [0, universe); modes are [k][universe] int32 0/1.       */
+int geek_assign_sparse(const uint32_t* flat, const uint64_t* offsets, uint64_t n,
+                       uint64_t universe, const int32_t* modes, uint64_t k, int64_t* labels,
+                       double* best, void* stream);
+
+/* ---- sparse / categorical helpers --------------------------------------- */
+
+/* DOPH reduction (hashing.py:312-329): per set, tokens (bin + (min rel mod
+ * 2^61-1)) mod r, sorted unique, written to out_flat at offsets
+ * out_off[s]..; out_off must be sized by geek_doph_reduce's first call
+ * (out_flat NULL => only counts[s] are written).                            */
+int geek_doph_reduce(const geek_perm_t* perm_host, const uint32_t* tables, const uint32_t* flat,
+                     const uint64_t* offsets, uint64_t nsets, uint64_t D, uint64_t r,
+                     uint32_t* counts, const uint64_t* out_off, uint32_t* out_flat, void* stream);
+
+/* Mode statistics: counts[(g*d + c)*cs + v] += #members of group g whose
+ * column c equals v (seeding.py:180-185, engine.py:312-317).                */
+int geek_mode_counts(const int32_t* codes, uint64_t nrows, int d, uint64_t row_lo, uint64_t cs,
+                     const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups,
+                     int64_t* counts, void* stream);
+
+/* Sparse membership counts: counts[g*universe + e] += #members containing e. */
+int geek_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, uint64_t nrows,
+                       uint64_t row_lo, uint64_t universe, const uint32_t* flat,
+                       const uint64_t* offsets, uint64_t ngroups, int64_t* counts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEEK_H */

@@ -1,0 +1,155 @@
+"""One-pass assignment (mirrors lshclust.assignment, assignment.py:1-170).
+
+Euclidean: geek_assign_l2 evaluates numpy's float64 direct-difference
+distance bit-for-bit (pairwise summation order, no FMA contraction,
+correctly rounded sqrt, first-index ties), so labels, best distances and
+radii equal the reference exactly; the objective is numpy's pairwise sum of
+the best distances, reproduced on the device (geek_pairwise_sum).
+Jaccard: categorical 1 - m/(2d - m) and binary sparse intersection/union.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .data import CategoricalData, CentralVector, Clustering, DenseData, InvalidInput, SparseData
+
+__all__ = ["assign", "refine", "distance_matrix", "squared_objective", "CHUNK"]
+
+CHUNK = 8192  # reference chunking (assignment.py:23); results do not depend on it
+_METRICS = ("euclidean", "jaccard")
+
+
+def _check_compat(data, centers, metric):
+    if metric not in _METRICS:
+        raise InvalidInput(f"unknown metric {metric!r}")
+    kinds = {c.kind for c in centers}
+    if metric == "euclidean":
+        if not isinstance(data, DenseData) or kinds != {"centroid"}:
+            raise InvalidInput("euclidean assignment needs dense data and centroids")
+    elif not isinstance(data, (CategoricalData, SparseData)) or kinds != {"mode"}:
+        raise InvalidInput("jaccard assignment needs categorical or sparse data and modes")
+
+
+def assign_l2_device(X: torch.Tensor, C: torch.Tensor):
+    """(labels int64, best float64) on the device."""
+    n, d = X.shape
+    k = C.shape[0]
+    labels = _lib.empty(max(1, n), torch.int64)
+    best = _lib.empty(max(1, n), torch.float64)
+    _lib.call("geek_assign_l2", _lib.ptr(X), _lib.dtype_code(X), n, d, _lib.ptr(C.contiguous()), k,
+              _lib.ptr(labels), _lib.ptr(best), _lib.stream())
+    return labels[:n], best[:n]
+
+
+def assign_cat_device(codes: torch.Tensor, M: torch.Tensor):
+    n, d = codes.shape
+    k = M.shape[0]
+    labels = _lib.empty(max(1, n), torch.int64)
+    best = _lib.empty(max(1, n), torch.float64)
+    _lib.call("geek_assign_categorical", _lib.ptr(codes), n, d, _lib.ptr(M.contiguous()), k, _lib.ptr(labels),
+              _lib.ptr(best), _lib.stream())
+    return labels[:n], best[:n]
+
+
+def assign_sparse_device(flat, off, n: int, universe: int, M: torch.Tensor):
+    k = M.shape[0]
+    labels = _lib.empty(max(1, n), torch.int64)
+    best = _lib.empty(max(1, n), torch.float64)
+    _lib.call("geek_assign_sparse", _lib.ptr(flat), _lib.ptr(off), n, universe, _lib.ptr(M.contiguous()), k,
+              _lib.ptr(labels), _lib.ptr(best), _lib.stream())
+    return labels[:n], best[:n]
+
+
+def radii_sizes(labels: torch.Tensor, best: torch.Tensor, k: int):
+    radii = _lib.zeros(max(1, k), torch.float64)
+    sizes = _lib.zeros(max(1, k), torch.int64)
+    _lib.call("geek_radii_sizes", _lib.ptr(labels), _lib.ptr(best), labels.numel(), k, _lib.ptr(radii),
+              _lib.ptr(sizes), _lib.stream())
+    return radii[:k], sizes[:k]
+
+
+def pairwise_sum(v: torch.Tensor) -> torch.Tensor:
+    out = _lib.empty(1, torch.float64)
+    _lib.call("geek_pairwise_sum", _lib.ptr(v.contiguous()), v.numel(), _lib.ptr(out), _lib.stream())
+    return out
+
+
+def center_matrix(centers, metric):
+    vals = np.stack([c.values for c in centers])
+    if metric == "euclidean":
+        return _lib.to_dev(vals.astype(np.float64))
+    return _lib.to_dev(vals.astype(np.int32))
+
+
+def assign_device(data, C: torch.Tensor, metric: str):
+    if metric == "euclidean":
+        return assign_l2_device(data.device_vectors(), C)
+    if isinstance(data, CategoricalData):
+        return assign_cat_device(data.device_codes(), C)
+    flat, off = data.csr()
+    return assign_sparse_device(flat, off, data.n, data.universe, C)
+
+
+def assign(data, centers, metric) -> Clustering:
+    """Nearest center for every object in one pass (assignment.py:81-107)."""
+    if not centers:
+        raise InvalidInput("cannot assign without centers")
+    _check_compat(data, centers, metric)
+    k = len(centers)
+    C = center_matrix(centers, metric)
+    if metric == "jaccard" and C.shape[1] != (data.dim if isinstance(data, CategoricalData) else data.universe):
+        raise InvalidInput("mode width does not match the data")
+    labels, best = assign_device(data, C, metric)
+    radii, sizes = radii_sizes(labels, best, k)
+    obj = pairwise_sum(best)
+    return Clustering(centers=list(centers), assignment=labels.cpu().numpy(), radii=radii.cpu().numpy(),
+                      objective=float(obj.item()), sizes=sizes.cpu().numpy())
+
+
+def distance_matrix(data, centers, metric, rows=None) -> np.ndarray:
+    """Full distance matrix (small-scale API helper, assignment.py:44-78):
+    one assignment pass per center on the device."""
+    _check_compat(data, centers, metric)
+    idx = np.arange(data.n) if rows is None else np.asarray(rows)
+    out = np.empty((idx.size, len(centers)))
+    for j, c in enumerate(centers):
+        C = center_matrix([c], metric)
+        _, best = assign_device(data, C, metric)
+        out[:, j] = best.cpu().numpy()[idx]
+    return out
+
+
+def _centers_from_assignment(data, assignment, k) -> list:
+    from .seeding import seeds_to_centers
+    from .data import SeedGroup
+
+    assignment = np.asarray(assignment)
+    groups = [SeedGroup(np.flatnonzero(assignment == j)) for j in range(k) if (assignment == j).any()]
+    return seeds_to_centers(groups, data)
+
+
+def squared_objective(data, clustering: Clustering, metric: str) -> float:
+    """Sum of squared assigned distances (assignment.py:140-154)."""
+    C = center_matrix(clustering.centers, metric)
+    lab = _lib.to_dev(clustering.assignment)
+    total = 0.0
+    for j in range(len(clustering.centers)):
+        _, best = assign_device(data, C[j:j + 1], metric)
+        sel = lab == j
+        b = best[sel]
+        total += float((b * b).sum().item()) if b.numel() else 0.0
+    return total
+
+
+def refine(data, clustering: Clustering, metric: str, passes: int) -> Clustering:
+    """Recompute centers (dropping empty clusters) and reassign, `passes` times."""
+    if passes < 0:
+        raise InvalidInput("passes must be >= 0")
+    out = clustering
+    for _ in range(passes):
+        centers = _centers_from_assignment(data, out.assignment, len(out.centers))
+        out = assign(data, centers, metric)
+    return out

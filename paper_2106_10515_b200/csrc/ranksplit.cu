@@ -1,0 +1,339 @@
+// K2: exact even rank split of n keys into t buckets per table, ties by id
+// (transform.py:95-109; engine.py:216-225), without a full sort.
+//
+//   1. coarse histogram of the top `cb` key bits (sampled)        -> estimate
+//   2. every coarse cell is cut into ~count/G fine bins by linear
+//      interpolation on the next 32 key bits (monotone in the key)
+//   3. exact fine-bin histogram + exclusive scan -> exact rank range per bin
+//   4. bins whose rank range lies inside one bucket write that bucket's slot
+//      directly; bins that straddle a bucket boundary (about G/(n/t) of the
+//      ids) are staged and ranked exactly by (key, id) inside the bin.
+//
+// Every id gets the slot of its exact rank in the (key, id) order, so the
+// result is bit-identical to np.lexsort((arange(n), values)) + even split.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace geek {
+
+constexpr uint32_t kFineTarget = 32;     // ids per fine bin (G)
+constexpr uint32_t kLocalRankMax = 2048; // larger straddling bins take the sort path
+
+struct SplitGeom {
+  uint64_t n, t;
+  int m, j0, tb;  // key tables [j0, j0+tb) of keys[j][n]
+  int c0;         // code column of key table j0 in codes[i*m + c]
+  int cb;         // coarse bits
+  uint32_t nc;    // coarse cells per table
+};
+
+__device__ __forceinline__ uint32_t coarse_of(uint64_t key, int cb) {
+  return static_cast<uint32_t>(key >> (64 - cb));
+}
+
+__device__ __forceinline__ uint32_t fine_of(uint64_t key, int cb, const uint32_t* nfine,
+                                            const uint32_t* fbase, uint32_t cell) {
+  const uint32_t nf = nfine[cell];
+  const uint32_t frac = static_cast<uint32_t>((key << cb) >> 32);
+  return fbase[cell] + static_cast<uint32_t>(((uint64_t)frac * nf) >> 32);
+}
+
+__global__ void coarse_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g, uint64_t stride,
+                                   uint32_t* hist) {
+  const int jb = blockIdx.y;
+  const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
+  uint32_t* h = hist + (uint64_t)jb * g.nc;
+  const uint64_t ns = (g.n + stride - 1) / stride;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < ns;
+       s += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[coarse_of(kj[s * stride], g.cb)], 1u);
+}
+
+__global__ void fine_layout_kernel(const uint32_t* hist, uint64_t total, uint64_t stride,
+                                   uint32_t* nfine) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t est = (uint64_t)hist[c] * stride;
+    uint64_t nf = (est + kFineTarget - 1) / kFineTarget;
+    nfine[c] = static_cast<uint32_t>(nf < 1 ? 1 : (nf > (1u << 20) ? (1u << 20) : nf));
+  }
+}
+
+__global__ void fine_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                 const uint32_t* __restrict__ nfine, const uint32_t* __restrict__ fbase,
+                                 uint32_t* fcnt) {
+  const int jb = blockIdx.y;
+  const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
+  const uint32_t* nf = nfine + (uint64_t)jb * g.nc;
+  const uint32_t* fb = fbase + (uint64_t)jb * g.nc;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = kj[i];
+    atomicAdd(&fcnt[fine_of(key, g.cb, nf, fb, coarse_of(key, g.cb))], 1u);
+  }
+}
+
+__device__ __forceinline__ int table_of_fine(const uint32_t* tb_first, int tb, uint32_t f) {
+  int jb = 0;
+  while (jb + 1 < tb && tb_first[jb + 1] <= f) ++jb;
+  return jb;
+}
+
+// per fine bin: rank start within its table, straddle size (0 if inside one bucket)
+__global__ void straddle_kernel(SplitGeom g, const uint32_t* fcnt, const uint32_t* fstart,
+                                const uint32_t* tb_first, uint32_t nfbins, uint32_t* scnt,
+                                unsigned long long* stats) {
+  for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nfbins;
+       f += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = fcnt[f];
+    uint32_t s = 0;
+    if (c > 1) {
+      const int jb = table_of_fine(tb_first, g.tb, (uint32_t)f);
+      const uint64_t r0 = (uint64_t)fstart[f] - (uint64_t)jb * g.n;
+      if (slot_of_rank(r0, g.n, g.t) != slot_of_rank(r0 + c - 1, g.n, g.t)) {
+        s = c;
+        atomicAdd(&stats[0], (unsigned long long)c);
+        atomicMax(&stats[1], (unsigned long long)c);
+        if (c > kLocalRankMax) atomicAdd(&stats[2], (unsigned long long)c);
+      }
+    }
+    scnt[f] = s;
+  }
+}
+
+// slot codes for ids in non-straddling bins; straddling ids are staged
+__global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                                    const uint32_t* __restrict__ nfine,
+                                                    const uint32_t* __restrict__ fbase,
+                                                    const uint32_t* __restrict__ fstart,
+                                                    const uint32_t* __restrict__ scnt,
+                                                    const uint32_t* __restrict__ sbase,
+                                                    uint32_t* sfill, uint32_t* codes,
+                                                    uint64_t* st_key, uint32_t* st_id,
+                                                    uint32_t* st_bin) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t* crow = codes + i * (uint64_t)g.m + g.c0;
+    for (int jb = 0; jb < g.tb; ++jb) {
+      const uint64_t key = keys[(uint64_t)(g.j0 + jb) * g.n + i];
+      const uint32_t cell = coarse_of(key, g.cb);
+      const uint32_t f = fine_of(key, g.cb, nfine + (uint64_t)jb * g.nc, fbase + (uint64_t)jb * g.nc,
+                                 cell);
+      if (scnt[f] == 0) {
+        crow[jb] = slot_of_rank((uint64_t)fstart[f] - (uint64_t)jb * g.n, g.n, g.t);
+      } else {
+        const uint32_t pos = sbase[f] + atomicAdd(&sfill[f], 1u);
+        st_key[pos] = key;
+        st_id[pos] = static_cast<uint32_t>(i);
+        st_bin[pos] = f;
+      }
+    }
+  }
+}
+
+// exact rank inside a small straddling bin by counting smaller (key, id)
+__global__ void __launch_bounds__(256) resolve_kernel(SplitGeom g, const uint64_t* __restrict__ st_key,
+                                                      const uint32_t* __restrict__ st_id,
+                                                      const uint32_t* __restrict__ st_bin,
+                                                      uint64_t nstage,
+                                                      const uint32_t* __restrict__ fstart,
+                                                      const uint32_t* __restrict__ scnt,
+                                                      const uint32_t* __restrict__ sbase,
+                                                      const uint32_t* __restrict__ tb_first,
+                                                      uint32_t* codes) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nstage;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = st_bin[e];
+    const uint32_t c = scnt[f];
+    if (c > kLocalRankMax) continue;
+    const uint64_t key = st_key[e];
+    const uint32_t id = st_id[e];
+    const uint32_t b0 = sbase[f];
+    uint32_t below = 0;
+    for (uint32_t q = 0; q < c; ++q) {
+      const uint64_t k2 = st_key[b0 + q];
+      const uint32_t i2 = st_id[b0 + q];
+      below += (k2 < key) || (k2 == key && i2 < id);
+    }
+    const int jb = table_of_fine(tb_first, g.tb, f);
+    const uint64_t rank = (uint64_t)fstart[f] - (uint64_t)jb * g.n + below;
+    codes[(uint64_t)id * g.m + g.c0 + jb] = slot_of_rank(rank, g.n, g.t);
+  }
+}
+
+// ---- fallback for large straddling bins: full (bin, key, id) sort --------
+
+__global__ void big_gather_kernel(const uint64_t* st_key, const uint32_t* st_id, const uint32_t* st_bin,
+                                  uint64_t nstage, const uint32_t* scnt, uint32_t* rows,
+                                  uint32_t* cursor) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nstage;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = st_bin[e];
+    if (scnt[f] <= kLocalRankMax) continue;
+    const uint32_t p = atomicAdd(cursor, 1u);
+    uint32_t* r = rows + 4ull * p;
+    r[0] = f;
+    r[1] = static_cast<uint32_t>(st_key[e] >> 32);
+    r[2] = static_cast<uint32_t>(st_key[e]);
+    r[3] = st_id[e];
+  }
+}
+
+__global__ void big_rank_kernel(SplitGeom g, const uint32_t* rows, const uint32_t* perm, uint64_t nbig,
+                                const uint32_t* fstart, const uint32_t* tb_first, uint32_t* codes) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nbig;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = rows[4ull * perm[q]];
+    // first sorted position of bin f (bins are the major sort key)
+    uint64_t lo = 0, hi = q;
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (rows[4ull * perm[mid]] < f) lo = mid + 1;
+      else hi = mid;
+    }
+    const int jb = table_of_fine(tb_first, g.tb, f);
+    const uint64_t rank = (uint64_t)fstart[f] - (uint64_t)jb * g.n + (q - lo);
+    const uint32_t id = rows[4ull * perm[q] + 3];
+    codes[(uint64_t)id * g.m + g.c0 + jb] = slot_of_rank(rank, g.n, g.t);
+  }
+}
+
+static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, uint64_t* stats_acc,
+                            cudaStream_t s) {
+  const uint64_t ncell = (uint64_t)g.tb * g.nc;
+  const uint64_t stride = g.n >= (1ull << 22) ? 8 : 1;
+  Scratch hist, nfine, fbase;
+  GEEK_TRY(hist.alloc(ncell * 4, s));
+  GEEK_TRY(nfine.alloc(ncell * 4, s));
+  GEEK_TRY(fbase.alloc(ncell * 4, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(hist.ptr, 0, ncell * 4, s));
+  dim3 gs(grid_for((g.n + stride - 1) / stride, 256, 148 * 8), g.tb);
+  coarse_hist_kernel<<<gs, 256, 0, s>>>(keys, g, stride, hist.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  fine_layout_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(hist.as<uint32_t>(), ncell, stride,
+                                                          nfine.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nfb = 0;
+  GEEK_TRY(exclusive_scan_u32(nfine.as<uint32_t>(), fbase.as<uint32_t>(), ncell, s, &nfb));
+  GEEK_REQUIRE(nfb < 0xFFFFFFF0ull, "too many fine bins");
+  std::vector<uint32_t> tbf(g.tb);
+  for (int jb = 0; jb < g.tb; ++jb)
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(&tbf[jb], fbase.as<uint32_t>() + (uint64_t)jb * g.nc, 4,
+                                    cudaMemcpyDeviceToHost, s));
+  Scratch fcnt, fstart, scnt, sbase, sfill, tbfirst, stats;
+  GEEK_TRY(fcnt.alloc(nfb * 4, s));
+  GEEK_TRY(fstart.alloc(nfb * 4, s));
+  GEEK_TRY(scnt.alloc(nfb * 4, s));
+  GEEK_TRY(sbase.alloc(nfb * 4, s));
+  GEEK_TRY(sfill.alloc(nfb * 4, s));
+  GEEK_TRY(tbfirst.alloc(g.tb * 4, s));
+  GEEK_TRY(stats.alloc(32, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));  // tbf is host memory
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(tbfirst.ptr, tbf.data(), g.tb * 4, cudaMemcpyHostToDevice, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(sfill.ptr, 0, nfb * 4, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(stats.ptr, 0, 32, s));
+  dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
+  fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, nfine.as<uint32_t>(), fbase.as<uint32_t>(),
+                                      fcnt.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  GEEK_TRY(exclusive_scan_u32(fcnt.as<uint32_t>(), fstart.as<uint32_t>(), nfb, s));
+  straddle_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
+                                                      tbfirst.as<uint32_t>(), (uint32_t)nfb,
+                                                      scnt.as<uint32_t>(),
+                                                      stats.as<unsigned long long>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nstage = 0;
+  GEEK_TRY(exclusive_scan_u32(scnt.as<uint32_t>(), sbase.as<uint32_t>(), nfb, s, &nstage));
+  unsigned long long st[4] = {0, 0, 0, 0};
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(st, stats.ptr, 24, cudaMemcpyDeviceToHost, s));
+  Scratch skey, sid, sbin;
+  GEEK_TRY(skey.alloc(nstage * 8, s));
+  GEEK_TRY(sid.alloc(nstage * 4, s));
+  GEEK_TRY(sbin.alloc(nstage * 4, s));
+  codes_kernel<<<grid_for(g.n, 256, 148 * 16), 256, 0, s>>>(
+      keys, g, nfine.as<uint32_t>(), fbase.as<uint32_t>(), fstart.as<uint32_t>(), scnt.as<uint32_t>(),
+      sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes, skey.as<uint64_t>(), sid.as<uint32_t>(),
+      sbin.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  if (nstage) {
+    resolve_kernel<<<grid_for(nstage, 256, 148 * 16), 256, 0, s>>>(
+        g, skey.as<uint64_t>(), sid.as<uint32_t>(), sbin.as<uint32_t>(), nstage, fstart.as<uint32_t>(),
+        scnt.as<uint32_t>(), sbase.as<uint32_t>(), tbfirst.as<uint32_t>(), codes);
+    GEEK_CHECK_LAUNCH();
+  }
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  const uint64_t nbig = st[2];
+  if (nbig) {
+    Scratch rows, perm, cur;
+    GEEK_TRY(rows.alloc(nbig * 16, s));
+    GEEK_TRY(perm.alloc(nbig * 4, s));
+    GEEK_TRY(cur.alloc(4, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(cur.ptr, 0, 4, s));
+    big_gather_kernel<<<grid_for(nstage, 256), 256, 0, s>>>(skey.as<uint64_t>(), sid.as<uint32_t>(),
+                                                            sbin.as<uint32_t>(), nstage,
+                                                            scnt.as<uint32_t>(), rows.as<uint32_t>(),
+                                                            cur.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    GEEK_TRY(lex_argsort_rows(rows.as<uint32_t>(), nbig, 4, nullptr, perm.as<uint32_t>(), s));
+    big_rank_kernel<<<grid_for(nbig, 256), 256, 0, s>>>(g, rows.as<uint32_t>(), perm.as<uint32_t>(),
+                                                        nbig, fstart.as<uint32_t>(),
+                                                        tbfirst.as<uint32_t>(), codes);
+    GEEK_CHECK_LAUNCH();
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  stats_acc[0] += nfb;
+  stats_acc[1] += nstage;
+  stats_acc[2] = std::max<uint64_t>(stats_acc[2], st[1]);
+  stats_acc[3] += nbig;
+  return GEEK_OK;
+}
+
+static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
+                           uint64_t code_stride, uint64_t col, uint64_t* stats_host, cudaStream_t s) {
+  GEEK_REQUIRE(t >= 1 && t <= n, "cannot split %llu objects into %llu buckets",
+               (unsigned long long)n, (unsigned long long)t);
+  GEEK_REQUIRE(n < 0xFFFFFFFFull, "n must be < 2^32");
+  SplitGeom g;
+  g.n = n;
+  g.t = t;
+  g.m = static_cast<int>(code_stride);
+  int cb = (int)std::ceil(std::log2((double)n / 16.0 + 1.0));
+  g.cb = std::min(20, std::max(10, cb));
+  g.nc = 1u << g.cb;
+  const double per_table = 4.0 * ((double)n / kFineTarget + 2.0 * g.nc) * 5.0;
+  int tb = (int)std::max(1.0, std::min((double)m, (96.0 * (1 << 20)) / per_table));
+  tb = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)tb, 0xFFFFFFF0ull / n));
+  uint64_t acc[4] = {0, 0, 0, 0};
+  for (int j0 = 0; j0 < m; j0 += tb) {
+    g.j0 = j0;
+    g.c0 = static_cast<int>(col) + j0;
+    g.tb = std::min(tb, m - j0);
+    GEEK_TRY(rank_split_batch(keys, g, codes, acc, s));
+  }
+  if (stats_host)
+    for (int i = 0; i < 4; ++i) stats_host[i] = acc[i];
+  return GEEK_OK;
+}
+
+}  // namespace geek
+
+using namespace geek;
+
+extern "C" {
+
+int geek_rank_split(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
+                    uint64_t* stats_host, void* stream) {
+  GEEK_REQUIRE(m >= 1, "need at least one table");
+  return rank_split_impl(keys, n, m, t, codes, (uint64_t)m, 0, stats_host, as_stream(stream));
+}
+
+int geek_rank_split_strided(const uint64_t* keys, uint64_t n, uint64_t t, uint32_t* codes,
+                            uint64_t stride, uint64_t col, void* stream) {
+  GEEK_REQUIRE(col < stride, "column outside stride");
+  return rank_split_impl(keys, n, 1, t, codes, stride, col, nullptr, as_stream(stream));
+}
+
+}  // extern "C"

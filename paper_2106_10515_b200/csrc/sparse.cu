@@ -1,0 +1,253 @@
+// K9/K10: sparse-set and categorical kernels -- DOPH reduction
+// (hashing.py:304-329), Jaccard assignment for categorical records and
+// binary sparse sets (assignment.py:63-78), and the mode statistics behind
+// categorical / sparse centers (seeding.py:180-194, engine.py:312-322).
+#include "common.cuh"
+
+namespace geek {
+
+// one warp per set: bin-minimum flags and tokens (bin + rel) mod r
+__global__ void doph_tokens_kernel(const uint32_t* p, const uint64_t* off, uint64_t nsets, uint64_t width,
+                                   uint64_t r, uint32_t* tok, uint8_t* ismin) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t s = warp; s < nsets; s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t b = off[s], e = off[s + 1];
+    for (uint64_t i = b + lane; i < e; i += 32) {
+      const uint64_t pi = p[i], bi = pi / width;
+      bool mn = true;
+      for (uint64_t j = b; j < e; ++j) {
+        const uint64_t pj = p[j];
+        if (pj / width == bi && pj < pi) {
+          mn = false;
+          break;
+        }
+      }
+      ismin[i] = mn;
+      tok[i] = static_cast<uint32_t>((bi + (pi - bi * width)) % r);
+    }
+  }
+}
+
+// distinct sorted tokens of the bin minima
+__global__ void doph_emit_kernel(const uint32_t* tok, const uint8_t* ismin, const uint64_t* off, uint64_t nsets,
+                                 uint32_t* counts, const uint64_t* out_off, uint32_t* out_flat) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t s = warp; s < nsets; s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t b = off[s], e = off[s + 1];
+    uint32_t distinct = 0;
+    for (uint64_t i = b + lane; i < e; i += 32) {
+      if (!ismin[i]) continue;
+      const uint32_t ti = tok[i];
+      bool first = true;
+      uint32_t below = 0;
+      for (uint64_t j = b; j < e; ++j) {
+        if (!ismin[j]) continue;
+        const uint32_t tj = tok[j];
+        if (tj == ti && j < i) first = false;
+        // count distinct smaller tokens: only first occurrences
+        if (tj < ti) {
+          bool jfirst = true;
+          for (uint64_t q = b; q < j; ++q)
+            if (ismin[q] && tok[q] == tj) {
+              jfirst = false;
+              break;
+            }
+          below += jfirst;
+        }
+      }
+      if (first) {
+        ++distinct;
+        if (out_flat) out_flat[out_off[s] + below] = ti;
+      }
+    }
+    for (int o = 16; o; o >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, o);
+    if (lane == 0 && counts) counts[s] = distinct;
+  }
+}
+
+__global__ void assign_cat_kernel(const int32_t* __restrict__ codes, uint64_t n, int d,
+                                  const int32_t* __restrict__ modes, uint64_t k, int64_t* labels, double* best) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int32_t* x = codes + i * d;
+    double bd = 0.0;
+    int64_t bl = -1;
+    for (uint64_t c = 0; c < k; ++c) {
+      const int32_t* mo = modes + c * d;
+      int mt = 0;
+      for (int a = 0; a < d; ++a) mt += (x[a] == mo[a]);
+      const double dist = __dsub_rn(1.0, __ddiv_rn((double)mt, (double)(2 * d - mt)));
+      if (bl < 0 || dist < bd) {
+        bd = dist;
+        bl = (int64_t)c;
+      }
+    }
+    labels[i] = bl;
+    best[i] = bd;
+  }
+}
+
+__global__ void mode_sizes_kernel(const int32_t* modes, uint64_t k, uint64_t u, double* sz) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    long long t = 0;
+    for (uint64_t e = 0; e < u; ++e) t += modes[c * u + e];
+    sz[c] = (double)t;
+  }
+}
+
+__global__ void assign_sparse_kernel(const uint32_t* flat, const uint64_t* off, uint64_t n, uint64_t u,
+                                     const int32_t* modes, const double* msz, uint64_t k, int64_t* labels,
+                                     double* best) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = off[i], e = off[i + 1];
+    const double xs = (double)(e - b);
+    double bd = 0.0;
+    int64_t bl = -1;
+    for (uint64_t c = 0; c < k; ++c) {
+      const int32_t* mo = modes + c * u;
+      long long inter = 0;
+      for (uint64_t q = b; q < e; ++q) inter += (mo[flat[q]] != 0);
+      const double in = (double)inter;
+      const double uni = __dsub_rn(__dadd_rn(xs, msz[c]), in);
+      const double sim = uni > 0.0 ? __ddiv_rn(in, uni) : 1.0;
+      const double dist = __dsub_rn(1.0, sim);
+      if (bl < 0 || dist < bd) {
+        bd = dist;
+        bl = (int64_t)c;
+      }
+    }
+    labels[i] = bl;
+    best[i] = bd;
+  }
+}
+
+__global__ void mode_counts_kernel(const int32_t* codes, uint64_t nrows, int d, uint64_t row_lo, uint64_t cs,
+                                   const uint32_t* flat, const uint64_t* off, uint64_t ngroups, uint64_t total,
+                                   unsigned long long* counts) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total * d;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = e / d;
+    const int c = (int)(e - k * d);
+    const uint64_t id = flat[k];
+    if (id < row_lo || id >= row_lo + nrows) continue;
+    uint64_t lo = 0, hi = ngroups;
+    while (hi - lo > 1) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= k) lo = mid;
+      else hi = mid;
+    }
+    const int32_t v = codes[(id - row_lo) * d + c];
+    atomicAdd(&counts[(lo * d + c) * cs + (uint64_t)v], 1ull);
+  }
+}
+
+__global__ void sparse_counts_kernel(const uint32_t* set_flat, const uint64_t* set_off, uint64_t nrows,
+                                     uint64_t row_lo, uint64_t u, const uint32_t* flat, const uint64_t* off,
+                                     uint64_t ngroups, uint64_t total, unsigned long long* counts) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t id = flat[k];
+    if (id < row_lo || id >= row_lo + nrows) continue;
+    uint64_t lo = 0, hi = ngroups;
+    while (hi - lo > 1) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= k) lo = mid;
+      else hi = mid;
+    }
+    const uint64_t r = id - row_lo;
+    for (uint64_t q = set_off[r]; q < set_off[r + 1]; ++q) atomicAdd(&counts[lo * u + set_flat[q]], 1ull);
+  }
+}
+
+}  // namespace geek
+
+using namespace geek;
+
+extern "C" {
+
+int geek_doph_reduce(const geek_perm_t* perm_host, const uint32_t* tables, const uint32_t* flat,
+                     const uint64_t* offsets, uint64_t nsets, uint64_t D, uint64_t r, uint32_t* counts,
+                     const uint64_t* out_off, uint32_t* out_flat, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(r >= 1 && r <= D, "need 1 <= target_dims <= universe");
+  GEEK_REQUIRE(perm_host->u == D, "permutation universe must equal D");
+  if (nsets == 0) return GEEK_OK;
+  uint64_t total = 0;
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(&total, offsets + nsets, 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  Scratch p, tok, mn;
+  GEEK_TRY(p.alloc(total * 4, s));
+  GEEK_TRY(tok.alloc(total * 4, s));
+  GEEK_TRY(mn.alloc(total, s));
+  GEEK_TRY(geek_perm_forward(perm_host, 1, tables, flat, total, p.as<uint32_t>(), stream));
+  const uint64_t width = (D + r - 1) / r;
+  doph_tokens_kernel<<<grid_for(nsets * 32, 256), 256, 0, s>>>(p.as<uint32_t>(), offsets, nsets, width, r,
+                                                               tok.as<uint32_t>(), mn.as<uint8_t>());
+  GEEK_CHECK_LAUNCH();
+  doph_emit_kernel<<<grid_for(nsets * 32, 256), 256, 0, s>>>(tok.as<uint32_t>(), mn.as<uint8_t>(), offsets,
+                                                             nsets, counts, out_off, out_flat);
+  GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  return GEEK_OK;
+}
+
+int geek_assign_categorical(const int32_t* codes, uint64_t n, int d, const int32_t* modes, uint64_t k,
+                            int64_t* labels, double* best, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(k >= 1 && d >= 1, "cannot assign without centers");
+  if (n == 0) return GEEK_OK;
+  assign_cat_kernel<<<grid_for(n, 128), 128, 0, s>>>(codes, n, d, modes, k, labels, best);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_assign_sparse(const uint32_t* flat, const uint64_t* offsets, uint64_t n, uint64_t universe,
+                       const int32_t* modes, uint64_t k, int64_t* labels, double* best, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(k >= 1, "cannot assign without centers");
+  if (n == 0) return GEEK_OK;
+  Scratch msz;
+  GEEK_TRY(msz.alloc(k * 8, s));
+  mode_sizes_kernel<<<grid_for(k, 128), 128, 0, s>>>(modes, k, universe, msz.as<double>());
+  assign_sparse_kernel<<<grid_for(n, 128), 128, 0, s>>>(flat, offsets, n, universe, modes, msz.as<double>(), k,
+                                                        labels, best);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_mode_counts(const int32_t* codes, uint64_t nrows, int d, uint64_t row_lo, uint64_t cs,
+                     const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups, int64_t* counts,
+                     void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (ngroups == 0) return GEEK_OK;
+  uint64_t total = 0;
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(&total, offsets + ngroups, 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (total == 0) return GEEK_OK;
+  mode_counts_kernel<<<grid_for(total * d, 256), 256, 0, s>>>(codes, nrows, d, row_lo, cs, flat, offsets, ngroups,
+                                                              total, reinterpret_cast<unsigned long long*>(counts));
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, uint64_t nrows, uint64_t row_lo,
+                       uint64_t universe, const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups,
+                       int64_t* counts, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (ngroups == 0) return GEEK_OK;
+  uint64_t total = 0;
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(&total, offsets + ngroups, 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (total == 0) return GEEK_OK;
+  sparse_counts_kernel<<<grid_for(total, 256), 256, 0, s>>>(set_flat, set_off, nrows, row_lo, universe, flat,
+                                                            offsets, ngroups, total,
+                                                            reinterpret_cast<unsigned long long*>(counts));
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+}  // extern "C"

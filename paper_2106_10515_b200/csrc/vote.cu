@@ -1,0 +1,303 @@
+// SILK voting and dedup helpers (seeding.py:93-134; engine.py:242-295):
+// membership emission for binned buckets, strict-majority vote with the
+// delta filter, dedup representatives and the canonical group order.
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace geek {
+
+__global__ void emit_members_kernel(const uint32_t* __restrict__ codes, uint64_t n, int m, uint64_t t,
+                                    const uint32_t* __restrict__ bb_off,
+                                    const uint32_t* __restrict__ bb_bins, uint32_t* out_bin,
+                                    uint32_t* out_id, uint64_t cap, unsigned long long* cursor) {
+  const uint64_t total = n * (uint64_t)m;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = e / m;
+    const int j = static_cast<int>(e - i * m);
+    const uint64_t b = (uint64_t)j * t + codes[e];
+    const uint32_t lo = bb_off[b], hi = bb_off[b + 1];
+    for (uint32_t k = lo; k < hi; ++k) {
+      unsigned long long pos = atomicAdd(cursor, 1ull);
+      if (pos < cap) {
+        out_bin[pos] = bb_bins[k];
+        out_id[pos] = static_cast<uint32_t>(i);
+      }
+    }
+  }
+}
+
+__global__ void gather_u32(const uint32_t* src, const uint32_t* perm, uint32_t* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+// run starts of the sorted (a, b) sequence
+__global__ void run_flags2(const uint32_t* a, const uint32_t* b, uint32_t* flag, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0) || a[i] != a[i - 1] || (b && b[i] != b[i - 1]);
+}
+
+__global__ void scatter_run_start(const uint32_t* flag, const uint32_t* ridx, uint32_t* start, uint64_t n,
+                                  uint64_t nruns) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) start[ridx[i]] = static_cast<uint32_t>(i);
+  if (blockIdx.x == 0 && threadIdx.x == 0) start[nruns] = static_cast<uint32_t>(n);
+}
+
+// winner flag per (bin, id) run: 2*count > bin size (seeding.py:110)
+__global__ void winner_flags(const uint32_t* start, const uint32_t* sbin, const uint32_t* bin_size,
+                             uint64_t nruns, uint32_t* win) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nruns;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t cnt = start[r + 1] - start[r];
+    const uint32_t b = sbin[start[r]];
+    win[r] = 2ull * cnt > (uint64_t)bin_size[b];
+  }
+}
+
+__global__ void compact_winners(const uint32_t* start, const uint32_t* sbin, const uint32_t* sid,
+                                const uint32_t* win, const uint32_t* wpos, uint64_t nruns,
+                                uint32_t* wbin, uint32_t* wid) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nruns;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    if (win[r]) {
+      wbin[wpos[r]] = sbin[start[r]];
+      wid[wpos[r]] = sid[start[r]];
+    }
+}
+
+// keep winners whose bin has >= delta of them
+__global__ void bin_keep_flags(const uint32_t* gstart, uint64_t ng, uint64_t delta, uint32_t* keep) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < ng;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = gstart[r + 1] - gstart[r];
+    keep[r] = c >= delta && c > 0;
+  }
+}
+
+__global__ void expand_keep(const uint32_t* gstart, const uint32_t* keep, uint64_t ng, uint32_t* ekeep) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < ng;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    for (uint32_t e = gstart[r]; e < gstart[r + 1]; ++e) ekeep[e] = keep[r];
+}
+
+__global__ void compact_pairs(const uint32_t* a, const uint32_t* b, const uint32_t* keep,
+                              const uint32_t* pos, uint64_t n, uint32_t* oa, uint32_t* ob) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (keep[i]) {
+      oa[pos[i]] = a[i];
+      ob[pos[i]] = b[i];
+    }
+}
+
+__device__ int lex_cmp(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb) {
+  uint64_t k = na < nb ? na : nb;
+  for (uint64_t i = 0; i < k; ++i)
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  return na < nb ? -1 : (na > nb ? 1 : 0);
+}
+
+__global__ void pick_reps_kernel(const uint32_t* flat, const uint64_t* off, const uint32_t* perm,
+                                 const uint32_t* gid, uint64_t n, uint8_t* keep) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    if (r > 0 && gid[r] == gid[r - 1]) continue;  // keep[] was zeroed by the host
+    uint32_t best = perm[r];
+    for (uint64_t q = r + 1; q < n && gid[q] == gid[r]; ++q) {
+      const uint32_t c = perm[q];
+      const uint64_t nc = off[c + 1] - off[c], nbst = off[best + 1] - off[best];
+      if (nc > nbst || (nc == nbst && lex_cmp(flat + off[c], nc, flat + off[best], nbst) < 0))
+        best = c;
+    }
+    keep[best] = 2;  // marked after all zeroing below
+  }
+}
+
+__global__ void fix_keep(uint8_t* keep, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keep[i] = keep[i] == 2;
+}
+
+// value at position p of a group's member tuple: id + 1, or 0 past the end
+__global__ void tuple_digit(const uint32_t* flat, const uint64_t* off, const uint32_t* order,
+                            uint64_t n, uint64_t p, uint32_t* out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = order[r];
+    const uint64_t len = off[g + 1] - off[g];
+    out[r] = p < len ? flat[off[g] + p] + 1u : 0u;
+  }
+}
+
+// class = position of the first element of the tie run in the current order
+__global__ void tie_class(const uint32_t* cls_sorted, const uint32_t* dig_sorted, uint32_t* flag,
+                          uint64_t n) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    flag[r] = (r == 0) || cls_sorted[r] != cls_sorted[r - 1] || dig_sorted[r] != dig_sorted[r - 1];
+}
+
+}  // namespace geek
+
+using namespace geek;
+
+extern "C" {
+
+int geek_emit_members_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t, const uint32_t* bb_off,
+                            const uint32_t* bb_bins, uint32_t* out_bin, uint32_t* out_id, uint64_t cap,
+                            uint64_t* count_host, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  Scratch cur;
+  GEEK_TRY(cur.alloc(8, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(cur.ptr, 0, 8, s));
+  if (n) {
+    emit_members_kernel<<<grid_for(n * (uint64_t)m, 256, 148 * 16), 256, 0, s>>>(
+        codes, n, m, t, bb_off, bb_bins, out_bin, out_id, cap, cur.as<unsigned long long>());
+    GEEK_CHECK_LAUNCH();
+  }
+  unsigned long long c = 0;
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(&c, cur.ptr, 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  *count_host = c;
+  if (c > cap) {
+    set_error("emit_members: %llu pairs exceed capacity %llu", c, (unsigned long long)cap);
+    return GEEK_ERANGE;
+  }
+  return GEEK_OK;
+}
+
+int geek_majority_vote(const uint32_t* pair_bin, const uint32_t* pair_id, uint64_t npairs,
+                       const uint32_t* bin_size, uint64_t nbins, uint64_t delta, uint32_t* win_bin,
+                       uint32_t* win_id, uint64_t* nwin_host, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  *nwin_host = 0;
+  if (npairs == 0) return GEEK_OK;
+  GEEK_REQUIRE(npairs < 0xFFFFFFFFull, "too many vote pairs");
+  (void)nbins;
+  const uint64_t n = npairs;
+  Scratch perm, sbin, sid, flag, ridx, start, win, wpos, wb, wi, gflag, gidx, gstart, gkeep, ekeep, epos;
+  GEEK_TRY(perm.alloc(n * 4, s));
+  GEEK_TRY(sbin.alloc(n * 4, s));
+  GEEK_TRY(sid.alloc(n * 4, s));
+  const uint32_t* cols[2] = {pair_bin, pair_id};
+  GEEK_TRY(argsort_cols(cols, 2, nullptr, n, perm.as<uint32_t>(), s));
+  gather_u32<<<grid_for(n, 256), 256, 0, s>>>(pair_bin, perm.as<uint32_t>(), sbin.as<uint32_t>(), n);
+  gather_u32<<<grid_for(n, 256), 256, 0, s>>>(pair_id, perm.as<uint32_t>(), sid.as<uint32_t>(), n);
+  GEEK_CHECK_LAUNCH();
+  GEEK_TRY(flag.alloc(n * 4, s));
+  GEEK_TRY(ridx.alloc(n * 4, s));
+  run_flags2<<<grid_for(n, 256), 256, 0, s>>>(sbin.as<uint32_t>(), sid.as<uint32_t>(), flag.as<uint32_t>(), n);
+  GEEK_CHECK_LAUNCH();
+  uint64_t nruns = 0;
+  GEEK_TRY(exclusive_scan_u32(flag.as<uint32_t>(), ridx.as<uint32_t>(), n, s, &nruns));
+  GEEK_TRY(start.alloc((nruns + 1) * 4, s));
+  scatter_run_start<<<grid_for(n, 256), 256, 0, s>>>(flag.as<uint32_t>(), ridx.as<uint32_t>(),
+                                                     start.as<uint32_t>(), n, nruns);
+  GEEK_CHECK_LAUNCH();
+  GEEK_TRY(win.alloc(nruns * 4, s));
+  GEEK_TRY(wpos.alloc(nruns * 4, s));
+  winner_flags<<<grid_for(nruns, 256), 256, 0, s>>>(start.as<uint32_t>(), sbin.as<uint32_t>(), bin_size,
+                                                    nruns, win.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nw = 0;
+  GEEK_TRY(exclusive_scan_u32(win.as<uint32_t>(), wpos.as<uint32_t>(), nruns, s, &nw));
+  if (nw == 0) return GEEK_OK;
+  GEEK_TRY(wb.alloc(nw * 4, s));
+  GEEK_TRY(wi.alloc(nw * 4, s));
+  compact_winners<<<grid_for(nruns, 256), 256, 0, s>>>(start.as<uint32_t>(), sbin.as<uint32_t>(),
+                                                       sid.as<uint32_t>(), win.as<uint32_t>(),
+                                                       wpos.as<uint32_t>(), nruns, wb.as<uint32_t>(),
+                                                       wi.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  // delta filter per bin (engine.py:281)
+  GEEK_TRY(gflag.alloc(nw * 4, s));
+  GEEK_TRY(gidx.alloc(nw * 4, s));
+  run_flags2<<<grid_for(nw, 256), 256, 0, s>>>(wb.as<uint32_t>(), nullptr, gflag.as<uint32_t>(), nw);
+  GEEK_CHECK_LAUNCH();
+  uint64_t ng = 0;
+  GEEK_TRY(exclusive_scan_u32(gflag.as<uint32_t>(), gidx.as<uint32_t>(), nw, s, &ng));
+  GEEK_TRY(gstart.alloc((ng + 1) * 4, s));
+  scatter_run_start<<<grid_for(nw, 256), 256, 0, s>>>(gflag.as<uint32_t>(), gidx.as<uint32_t>(),
+                                                      gstart.as<uint32_t>(), nw, ng);
+  GEEK_TRY(gkeep.alloc(ng * 4, s));
+  bin_keep_flags<<<grid_for(ng, 256), 256, 0, s>>>(gstart.as<uint32_t>(), ng, delta, gkeep.as<uint32_t>());
+  GEEK_TRY(ekeep.alloc(nw * 4, s));
+  GEEK_TRY(epos.alloc(nw * 4, s));
+  expand_keep<<<grid_for(ng, 256), 256, 0, s>>>(gstart.as<uint32_t>(), gkeep.as<uint32_t>(), ng,
+                                                ekeep.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nk = 0;
+  GEEK_TRY(exclusive_scan_u32(ekeep.as<uint32_t>(), epos.as<uint32_t>(), nw, s, &nk));
+  compact_pairs<<<grid_for(nw, 256), 256, 0, s>>>(wb.as<uint32_t>(), wi.as<uint32_t>(), ekeep.as<uint32_t>(),
+                                                  epos.as<uint32_t>(), nw, win_bin, win_id);
+  GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  *nwin_host = nk;
+  return GEEK_OK;
+}
+
+int geek_pick_representatives(const uint32_t* flat, const uint64_t* offsets, const uint32_t* perm,
+                              const uint32_t* gid, uint64_t ngroups, uint8_t* keep, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (ngroups == 0) return GEEK_OK;
+  GEEK_CHECK_CUDA(cudaMemsetAsync(keep, 0, ngroups, s));
+  pick_reps_kernel<<<grid_for(ngroups, 128), 128, 0, s>>>(flat, offsets, perm, gid, ngroups, keep);
+  GEEK_CHECK_LAUNCH();
+  fix_keep<<<grid_for(ngroups, 256), 256, 0, s>>>(keep, ngroups);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_sort_groups(const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups, uint32_t* order,
+                     void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (ngroups == 0) return GEEK_OK;
+  const uint64_t n = ngroups;
+  // max length bounds the refinement rounds
+  std::vector<uint64_t> off_host(n + 1);
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(off_host.data(), offsets, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  uint64_t maxlen = 0;
+  for (uint64_t g = 0; g < n; ++g) maxlen = std::max(maxlen, off_host[g + 1] - off_host[g]);
+  Scratch cls, dig, perm, tmp_cls, tmp_dig, flag, neworder;
+  GEEK_TRY(cls.alloc(n * 4, s));
+  GEEK_TRY(dig.alloc(n * 4, s));
+  GEEK_TRY(perm.alloc(n * 4, s));
+  GEEK_TRY(tmp_cls.alloc(n * 4, s));
+  GEEK_TRY(tmp_dig.alloc(n * 4, s));
+  GEEK_TRY(flag.alloc(n * 4, s));
+  GEEK_TRY(neworder.alloc(n * 4, s));
+  iota_u32<<<grid_for(n, 256), 256, 0, s>>>(order, n);
+  GEEK_CHECK_CUDA(cudaMemsetAsync(cls.ptr, 0, n * 4, s));
+  for (uint64_t p = 0; p <= maxlen; ++p) {
+    // order is sorted by (tuple prefix < p); refine by element p within classes
+    tuple_digit<<<grid_for(n, 256), 256, 0, s>>>(flat, offsets, order, n, p, dig.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    const uint32_t* cols[2] = {cls.as<uint32_t>(), dig.as<uint32_t>()};
+    GEEK_TRY(argsort_cols(cols, 2, nullptr, n, perm.as<uint32_t>(), s));
+    gather_u32<<<grid_for(n, 256), 256, 0, s>>>(order, perm.as<uint32_t>(), neworder.as<uint32_t>(), n);
+    gather_u32<<<grid_for(n, 256), 256, 0, s>>>(cls.as<uint32_t>(), perm.as<uint32_t>(), tmp_cls.as<uint32_t>(), n);
+    gather_u32<<<grid_for(n, 256), 256, 0, s>>>(dig.as<uint32_t>(), perm.as<uint32_t>(), tmp_dig.as<uint32_t>(), n);
+    GEEK_CHECK_LAUNCH();
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(order, neworder.ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+    tie_class<<<grid_for(n, 256), 256, 0, s>>>(tmp_cls.as<uint32_t>(), tmp_dig.as<uint32_t>(),
+                                                flag.as<uint32_t>(), n);
+    GEEK_CHECK_LAUNCH();
+    uint64_t nb = 0;
+    GEEK_TRY(exclusive_scan_u32(flag.as<uint32_t>(), cls.as<uint32_t>(), n, s, &nb));
+    // inclusive count of run starts: equal within a tie run, increasing across
+    add_flag<<<grid_for(n, 256), 256, 0, s>>>(cls.as<uint32_t>(), flag.as<uint32_t>(), n);
+    GEEK_CHECK_LAUNCH();
+    if (nb == n) break;  // every group in its own class
+  }
+  return GEEK_OK;
+}
+
+}  // extern "C"

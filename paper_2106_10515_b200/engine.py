@@ -1,0 +1,378 @@
+"""Partitioned-worker engine on one process per GPU (mirrors lshclust.engine,
+engine.py:1-537).
+
+Semantics are those of the reference's g logical workers (WorkerConfig):
+contiguous id shards (engine.py:109-115), table j owned by worker j % g
+(engine.py:199-238), bins formed only among one owner's tables
+(engine.py:242-283), seed groups merged and deduplicated on every worker
+(engine.py:285-295), exact centers reduced from per-shard sums
+(engine.py:481-516), local assignment (engine.py:327-346).  The results
+depend on g, never on the number of physical GPUs G (G must divide g).
+
+Physical mapping (B200, NCCL over NVLink): each rank projects its own shard;
+an all-to-all moves every table's keys to the rank owning it (j % G); the
+owner rank-splits, scans and votes its tables over all n ids; seed groups
+are all-gathered and deduplicated identically on every rank; exact digit
+sums are all-reduced; radii (max) and sizes (sum) are all-reduced.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .assignment import assign_cat_device, assign_l2_device, assign_sparse_device, pairwise_sum, radii_sizes
+from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
+from .errors import EngineError, InvalidInput
+from .hashing import DophReducer, derive_seed
+from .numeric import digit_count, exponent_range, mode_counts, partial_sums, round_means, sparse_counts
+from .seeding import SeedingParams, dedup_device, silk_votes
+from .tables import BucketTable, GroupSet
+from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, discretize_numeric,
+                        even_partition_sizes, project_keys, rank_split_codes, signature_bucket_codes)
+
+__all__ = ["EngineError", "WorkerConfig", "PipelineConfig", "PipelineResult", "split_data", "run_pipeline"]
+
+
+@dataclass(frozen=True)
+class WorkerConfig:
+    """Logical worker count g, seeding memory budget, transport (engine.py:49-69).
+
+    `transport` "in-process" (the reference's only kind) and "nccl" are
+    accepted; with a torch.distributed process group of G ranks the engine
+    always runs over it."""
+
+    num_workers: int
+    memory_budget: int = 1 << 30
+    transport: str = "in-process"
+
+    def __post_init__(self):
+        if self.num_workers < 1:
+            raise InvalidInput("need at least one worker")
+        if self.memory_budget <= 0:
+            raise InvalidInput("memory budget must be positive")
+        if self.transport not in ("in-process", "nccl"):
+            raise InvalidInput(f"unknown transport {self.transport!r}")
+
+
+def split_data(n: int, g: int) -> list:
+    """engine.py:109-115."""
+    if g > n:
+        raise InvalidInput(f"cannot split {n} objects across {g} workers")
+    b = np.concatenate(([0], np.cumsum(even_partition_sizes(n, g))))
+    return [(int(b[i]), int(b[i + 1])) for i in range(g)]
+
+
+@dataclass
+class PipelineConfig:
+    metric: str
+    transform_kind: str
+    workers: WorkerConfig
+    homo: HomoTransformParams = None
+    minhash: MinhashTransformParams = None
+    seeding: SeedingParams = None
+    passes: int = 0
+    fallback_seed: int = 0
+
+    def table_count(self) -> int:
+        return self.homo.num_tables if self.transform_kind == "dense" else self.minhash.num_tables
+
+
+class PipelineResult:
+    """Results stay on the device; the reference-typed fields materialise lazily."""
+
+    def __init__(self, centers, groups: GroupSet, labels, best, radii, sizes, objective, timings, transport_bytes,
+                 warnings, info, gather_labels=None):
+        self._centers = centers
+        self._groups = groups
+        self.labels_device = labels
+        self.best_device = best
+        self.radii_device = radii
+        self.sizes_device = sizes
+        self.objective = objective
+        self.timings = timings
+        self.transport_bytes = transport_bytes
+        self.warnings = warnings
+        self.info = info
+        self._gather_labels = gather_labels
+        self._clustering = None
+        self._seed_groups = None
+
+    @property
+    def k_star(self) -> int:
+        return int((self.sizes_device > 0).sum().item())
+
+    @property
+    def seed_groups(self) -> list:
+        if self._seed_groups is None:
+            self._seed_groups = self._groups.to_seed_groups()
+        return self._seed_groups
+
+    @property
+    def clustering(self) -> Clustering:
+        if self._clustering is None:
+            lab = self._gather_labels() if self._gather_labels else self.labels_device
+            self._clustering = Clustering(centers=self._centers(), assignment=lab.cpu().numpy(),
+                                          radii=self.radii_device.cpu().numpy(), objective=self.objective,
+                                          sizes=self.sizes_device.cpu().numpy())
+        return self._clustering
+
+
+# ---------------------------------------------------------------------------
+
+class _Comm:
+    """torch.distributed plumbing with byte accounting per message kind."""
+
+    def __init__(self):
+        self.on = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        self.G = dist.get_world_size() if self.on else 1
+        self.rank = dist.get_rank() if self.on else 0
+        self.bytes = {}
+
+    def count(self, kind, nbytes):
+        if self.on:
+            self.bytes[kind] = self.bytes.get(kind, 0) + int(nbytes)
+
+    def all_reduce(self, t, op, kind):
+        if self.on:
+            self.count(kind, t.numel() * t.element_size())
+            dist.all_reduce(t, op=op)
+        return t
+
+    def all_gather_var(self, t: torch.Tensor, kind) -> torch.Tensor:
+        """Concatenate 1-D tensors of varying length in rank order."""
+        if not self.on:
+            return t
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        ns = [torch.zeros_like(n) for _ in range(self.G)]
+        dist.all_gather(ns, n)
+        sizes = [int(x.item()) for x in ns]
+        mx = max(sizes) if sizes else 0
+        buf = torch.zeros(max(1, mx), dtype=t.dtype, device=t.device)
+        buf[: t.numel()] = t
+        outs = [torch.empty_like(buf) for _ in range(self.G)]
+        self.count(kind, t.numel() * t.element_size() * (self.G - 1))
+        dist.all_gather(outs, buf)
+        return torch.cat([o[:s] for o, s in zip(outs, sizes)])
+
+
+class _Timer:
+    def __init__(self):
+        self.t = {}
+        self._ev = []
+
+    def stage(self, name):
+        timer = self
+
+        class _S:
+            def __enter__(self_):
+                self_.a = torch.cuda.Event(enable_timing=True)
+                self_.b = torch.cuda.Event(enable_timing=True)
+                self_.a.record()
+
+            def __exit__(self_, *exc):
+                self_.b.record()
+                timer._ev.append((name, self_.a, self_.b))
+
+        return _S()
+
+    def finish(self):
+        torch.cuda.synchronize()
+        for name, a, b in self._ev:
+            self.t[name] = self.t.get(name, 0.0) + a.elapsed_time(b) / 1000.0
+        self._ev = []
+        return self.t
+
+
+def _merge_groups(comm: _Comm, local: GroupSet) -> GroupSet:
+    if not comm.on:
+        return local
+    sizes = comm.all_gather_var(local.sizes(), "SeedGroups")
+    flat = comm.all_gather_var(local.flat[: int(local.off[-1].item())], "SeedGroups")
+    off = torch.zeros(sizes.numel() + 1, dtype=torch.int64, device=sizes.device)
+    torch.cumsum(sizes, 0, out=off[1:])
+    return GroupSet(flat.contiguous() if flat.numel() else _lib.zeros(1, torch.int32), off)
+
+
+def _fallback_groups(n, g, seed, warnings):
+    warnings.append("seeding produced no groups; falling back to one random seed per worker")
+    rng = np.random.default_rng(seed)
+    picks = sorted(int(rng.integers(lo, hi)) for lo, hi in split_data(n, g))
+    return GroupSet.from_host([np.array([p]) for p in picks])
+
+
+def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: PipelineConfig, comm: _Comm):
+    g = config.workers.num_workers
+    p: HomoTransformParams = config.homo
+    sp: SeedingParams = config.seeding
+    m, t, G, rank = p.num_tables, p.buckets_per_table, comm.G, comm.rank
+    d = X_local.shape[1]
+    if t > n:
+        raise EngineError(f"stage setup: cannot split {n} objects into {t} buckets")
+    if g % G:
+        raise EngineError(f"stage setup: {G} GPUs must divide the {g} logical workers")
+    info, warnings = {}, []
+    tm = _Timer()
+    A = p.direction_matrix(d)
+    own = [j for j in range(m) if j % G == rank]
+    with tm.stage("transform"):
+        keys = project_keys(X_local, A)  # [m, n_local]
+    with tm.stage("sync_buckets"):
+        if comm.on:
+            spans = split_data(n, G)
+            mine = [[j for j in range(m) if j % G == q] for q in range(G)]
+            send = torch.cat([keys[mine[q]].reshape(-1) for q in range(G)])
+            recv_sizes = [len(own) * (hi - lo) for lo, hi in spans]
+            recv = torch.empty(sum(recv_sizes), dtype=keys.dtype, device=keys.device)
+            dist.all_to_all_single(recv, send, [len(mine[q]) * keys.shape[1] for q in range(G)], recv_sizes)
+            comm.count("BucketShard", (send.numel() - len(own) * keys.shape[1]) * 8)
+            parts = torch.split(recv, recv_sizes)
+            keys_own = torch.cat([pt.view(len(own), hi - lo) for pt, (lo, hi) in zip(parts, spans)], dim=1)
+            del keys, send, recv, parts
+        else:
+            keys_own = keys
+        stats = {}
+        codes = rank_split_codes(keys_own.contiguous(), t, stats) if own else None
+        del keys_own
+        info["rank_split"] = stats
+    with tm.stage("seeding"):
+        if own:
+            bt = BucketTable(codes, n, [t] * len(own), "rank", even=True)
+            owner = _lib.to_dev((np.repeat(np.array(own), t) % g).astype(np.int32))
+            local, _, _ = silk_votes(bt, sp, n, owner, info)
+        else:
+            local = GroupSet.empty()
+        merged = _merge_groups(comm, local)
+        groups = dedup_device(merged, sp, n)
+        if groups.count == 0:
+            groups = _fallback_groups(n, g, config.fallback_seed, warnings)
+    with tm.stage("centers"):
+        emin, emax = exponent_range(X_local)
+        if comm.on:
+            r = torch.tensor([-emin, emax], dtype=torch.int64, device=X_local.device)
+            comm.all_reduce(r, dist.ReduceOp.MAX, "LocalCenters")
+            emin, emax = -int(r[0].item()), int(r[1].item())
+        nd = digit_count(emin, emax)
+        digits = partial_sums(X_local, groups, emin, nd, row_lo)
+        comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
+        C = round_means(digits, groups.sizes(), emin, nd)
+    with tm.stage("assign"):
+        labels, best = assign_l2_device(X_local, C)
+        radii, sizes = radii_sizes(labels, best, groups.count)
+        comm.all_reduce(radii.view(torch.int64), dist.ReduceOp.MAX, "Assignments")
+        comm.all_reduce(sizes, dist.ReduceOp.SUM, "Assignments")
+        best_all = comm.all_gather_var(best, "Assignments")
+        obj = pairwise_sum(best_all)
+        del best_all
+    timings = tm.finish()
+    sizes_h = groups.sizes().cpu().numpy()
+
+    def centers():
+        Ch = C.cpu().numpy()
+        return [CentralVector("centroid", Ch[i], int(sizes_h[i])) for i in range(groups.count)]
+
+    gather = (lambda: comm.all_gather_var(labels, "Assignments")) if comm.on else None
+    return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings,
+                          dict(comm.bytes), warnings, info, gather)
+
+
+def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
+    """mixed / sparse data on one device (logical g emulated)."""
+    if comm.on:
+        raise EngineError("stage setup: multi-GPU runs support dense data only")
+    g = config.workers.num_workers
+    mp: MinhashTransformParams = config.minhash
+    sp: SeedingParams = config.seeding
+    info, warnings = {}, []
+    tm = _Timer()
+    with tm.stage("prepare"):
+        if config.transform_kind == "mixed":
+            if isinstance(data, (MixedData, DenseData)):
+                data = discretize_numeric(data, mp.bins_per_attribute)
+            if not isinstance(data, CategoricalData):
+                raise EngineError("stage setup: mixed transform expects mixed or categorical data")
+            flat, off = categorical_token_csr(data)
+            universe = data.dim * data.code_space
+        else:
+            if not isinstance(data, SparseData):
+                raise EngineError("stage setup: sparse transform expects sparse data")
+            if mp.target_dims <= data.universe:
+                red = DophReducer(derive_seed(mp.seed, 0xD0), data.universe, mp.target_dims)
+                flat, off = red.reduce_device(*data.csr(), data.n)
+                o = off.cpu().numpy()
+                v = flat.cpu().numpy().view(np.uint32).astype(np.int64)
+                data = SparseData([v[o[i]:o[i + 1]] for i in range(data.n)], mp.target_dims)
+                object.__setattr__(data, "_cache", {"csr": (flat, off)})
+            flat, off = data.csr()
+            universe = data.universe
+    n = data.n
+    if g > n:
+        raise EngineError(f"stage setup: cannot split {n} objects across {g} workers")
+    with tm.stage("transform"):
+        codes, tsizes = signature_bucket_codes(mp.scheme(universe), flat, off, n)
+        bt = BucketTable(codes, n, tsizes, "sig", even=False)
+    with tm.stage("seeding"):
+        owner = _lib.to_dev(np.concatenate([np.full(ts, j % g, dtype=np.int32) for j, ts in enumerate(tsizes)]))
+        local, _, _ = silk_votes(bt, sp, n, owner, info)
+        groups = dedup_device(local, sp, n)
+        if groups.count == 0:
+            groups = _fallback_groups(n, g, config.fallback_seed, warnings)
+    with tm.stage("centers"):
+        if isinstance(data, CategoricalData):
+            M = torch.argmax(mode_counts(data.device_codes(), data.code_space, groups), dim=2).to(torch.int32)
+        else:
+            cnt = sparse_counts(data, groups)
+            M = (2 * cnt > groups.sizes()[:, None]).to(torch.int32)
+    with tm.stage("assign"):
+        if isinstance(data, CategoricalData):
+            labels, best = assign_cat_device(data.device_codes(), M)
+        else:
+            labels, best = assign_sparse_device(flat, off, n, data.universe, M)
+        radii, sizes = radii_sizes(labels, best, groups.count)
+        obj = pairwise_sum(best)
+    timings = tm.finish()
+    sizes_h = groups.sizes().cpu().numpy()
+
+    def centers():
+        Mh = M.cpu().numpy()
+        return [CentralVector("mode", Mh[i], int(sizes_h[i])) for i in range(groups.count)]
+
+    return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings, {}, warnings,
+                          info)
+
+
+def run_pipeline(data, config: PipelineConfig) -> PipelineResult:
+    """transform -> bucket sync -> seeding -> centers -> assignment (engine.py:395-472).
+
+    Under an initialised torch.distributed group of G ranks every rank calls
+    this with the full dataset (or use run_pipeline_shard with its own rows)."""
+    if config.passes:
+        raise EngineError("stage setup: refinement passes are not part of the one-pass hot path")
+    comm = _Comm()
+    if config.transform_kind == "dense":
+        if not isinstance(data, DenseData):
+            raise EngineError("stage setup: dense transform expects dense data")
+        n = data.n
+        if config.workers.num_workers > n:
+            raise EngineError(f"stage setup: cannot split {n} objects across {config.workers.num_workers} workers")
+        lo, hi = split_data(n, comm.G)[comm.rank] if comm.on else (0, n)
+        X = data.device_vectors()[lo:hi].contiguous() if comm.on else data.device_vectors()
+        return _dense_pipeline(X, n, lo, config, comm)
+    if config.transform_kind in ("mixed", "sparse"):
+        return _signature_pipeline(data, config, comm)
+    raise EngineError(f"stage setup: unknown transform kind {config.transform_kind!r}")
+
+
+def run_pipeline_shard(X_local: torch.Tensor, n: int, config: PipelineConfig) -> PipelineResult:
+    """Dense pipeline where each rank already holds its contiguous shard
+    (rows split_data(n, G)[rank]) on its own GPU."""
+    comm = _Comm()
+    lo, hi = split_data(n, comm.G)[comm.rank]
+    if X_local.shape[0] != hi - lo:
+        raise EngineError(f"stage setup: rank {comm.rank} holds {X_local.shape[0]} rows, expected {hi - lo}")
+    return _dense_pipeline(X_local, n, lo, config, comm)

@@ -1,0 +1,109 @@
+"""Exact centers on the device (mirrors lshclust.numeric, numeric.py:1-76, and
+the center reductions of seeding.py:168-197 / engine.py:299-323, :481-516).
+
+Dense: exact integer column sums (base-2^32 digits in int64 lanes) ->
+correctly rounded mean; partial sums from different shards add exactly, so
+the engine reduces them with an int64 all-reduce.  Categorical: per
+attribute value counts, argmax with ties to the smallest code.  Sparse:
+strict-majority membership.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .data import CategoricalData, InvalidInput, SparseData
+from .tables import GroupSet
+
+_ND_CHOICES = (3, 4, 5, 6, 8, 12, 20, 40)
+
+
+def exponent_range(X: torch.Tensor):
+    out = np.zeros(2, dtype=np.int32)
+    _lib.call("geek_exponent_range", _lib.ptr(X), _lib.dtype_code(X), X.shape[0], X.shape[1], _lib.hptr(out),
+              _lib.stream())
+    return int(out[0]), int(out[1])
+
+
+def digit_count(emin: int, emax: int) -> int:
+    if emin > emax:
+        return _ND_CHOICES[0]
+    need = -(-(emax - emin + 33) // 32) + 1
+    for c in _ND_CHOICES:
+        if c >= need:
+            return c
+    raise InvalidInput("exponent range too wide for exact sums")
+
+
+def partial_sums(X: torch.Tensor, groups: GroupSet, emin: int, nd: int, row_lo: int = 0) -> torch.Tensor:
+    """int64 [k, d, nd] exact digit sums over the members that are rows
+    [row_lo, row_lo + X.shape[0]) of the global id space."""
+    k, d = groups.count, X.shape[1]
+    digits = _lib.zeros(max(1, k * d * nd), torch.int64)
+    if k:
+        _lib.call("geek_exact_sums", _lib.ptr(X), _lib.dtype_code(X), X.shape[0], d, row_lo, _lib.ptr(groups.flat),
+                  _lib.ptr(groups.off), k, emin, nd, _lib.ptr(digits), _lib.stream())
+    return digits[: k * d * nd].view(k, d, nd)
+
+
+def round_means(digits: torch.Tensor, counts: torch.Tensor, emin: int, nd: int) -> torch.Tensor:
+    k, d, _ = digits.shape
+    out = _lib.empty(max(1, k * d), torch.float64)
+    if k:
+        _lib.call("geek_round_means", _lib.ptr(digits.contiguous()), _lib.ptr(counts.to(torch.int64).contiguous()),
+                  k, d, emin, nd, _lib.ptr(out), _lib.stream())
+    return out[: k * d].view(k, d)
+
+
+def dense_centers(X: torch.Tensor, groups: GroupSet) -> torch.Tensor:
+    emin, emax = exponent_range(X)
+    nd = digit_count(emin, emax)
+    return round_means(partial_sums(X, groups, emin, nd), groups.sizes(), emin, nd)
+
+
+def mode_counts(codes: torch.Tensor, code_space: int, groups: GroupSet, row_lo: int = 0) -> torch.Tensor:
+    n, d = codes.shape
+    k = groups.count
+    if k * d * code_space > (1 << 31):
+        raise InvalidInput("mode statistics too large for dense counting")
+    cnt = _lib.zeros(max(1, k * d * code_space), torch.int64)
+    _lib.call("geek_mode_counts", _lib.ptr(codes), n, d, row_lo, code_space, _lib.ptr(groups.flat),
+              _lib.ptr(groups.off), k, _lib.ptr(cnt), _lib.stream())
+    return cnt[: k * d * code_space].view(k, d, code_space)
+
+
+def mode_centers(codes: torch.Tensor, code_space: int, groups: GroupSet) -> torch.Tensor:
+    # argmax returns the first maximum: ties go to the smallest code (seeding.py:184)
+    return torch.argmax(mode_counts(codes, code_space, groups), dim=2).to(torch.int32)
+
+
+def sparse_counts(data: SparseData, groups: GroupSet, row_lo: int = 0, csr=None) -> torch.Tensor:
+    flat, off = csr if csr is not None else data.csr()
+    k, u = groups.count, data.universe
+    cnt = _lib.zeros(max(1, k * u), torch.int64)
+    _lib.call("geek_sparse_counts", _lib.ptr(flat), _lib.ptr(off), data.n, row_lo, u, _lib.ptr(groups.flat),
+              _lib.ptr(groups.off), k, _lib.ptr(cnt), _lib.stream())
+    return cnt[: k * u].view(k, u)
+
+
+def sparse_centers(data: SparseData, groups: GroupSet) -> torch.Tensor:
+    cnt = sparse_counts(data, groups)
+    return (2 * cnt > groups.sizes()[:, None]).to(torch.int32)
+
+
+# ---- reference API (numeric.py:19-51) -----------------------------------------
+
+def exact_centroid(vectors) -> np.ndarray:
+    """Correctly rounded mean of the rows, identical under any partition."""
+    X = _lib.to_dev(np.asarray(vectors) if not isinstance(vectors, torch.Tensor) else vectors)
+    if X.dim() != 2 or X.shape[0] == 0:
+        raise InvalidInput("expected a non-empty matrix")
+    if X.dtype not in (torch.float32, torch.float64):
+        X = X.to(torch.float64)
+    if not bool(torch.isfinite(X).all().item()):
+        raise ValueError("non-finite value in exact sum")
+    gs = GroupSet(_lib.to_dev(np.arange(X.shape[0], dtype=np.uint32).view(np.int32)),
+                  _lib.to_dev(np.array([0, X.shape[0]], dtype=np.int64)))
+    return dense_centers(X.contiguous(), gs).cpu().numpy()[0]

@@ -1,0 +1,359 @@
+"""SILK seeding (mirrors lshclust.seeding, seeding.py:1-197; engine.py:242-295).
+
+Device pipeline:
+  bucket signatures  -- inverse-rank scan over the id-major slot codes when
+                        the buckets are an even rank split (K3'), else the
+                        segmented-min MinHash over member CSR (K3)
+  bins               -- per SILK table, lexicographic group-by of
+                        (owner, K-signature) rows; groups of >= 2 buckets
+  vote               -- (bin, id) membership pairs -> strict majority -> delta
+  dedup              -- dedup-table signatures of the groups, group-by, one
+                        representative per bin, canonical member-tuple order
+`owner` carries the engine's logical-worker semantics: table j belongs to
+worker j % g and only same-owner buckets can bin (engine.py:242-283).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .data import Bin, Bucket, CategoricalData, CentralVector, DenseData, InvalidInput, SeedGroup, SparseData
+from .hashing import PermBatch, SignatureScheme, derive_seed, set_signatures_device, csr_from_sets
+from .tables import BucketTable, GroupSet, csr_gather
+
+__all__ = ["SeedingParams", "bin_buckets", "majority_vote", "find_seed_groups", "dedup_groups",
+           "collect_votes", "seeds_to_centers"]
+
+DEDUP_TAG = 0xDED0  # seeding.py:38
+
+
+@dataclass(frozen=True)
+class SeedingParams:
+    """K hashes, L tables, min group size delta (seeding.py:41-80)."""
+
+    num_hashes: int
+    num_tables: int
+    min_group_size: int = 1
+    seed: int = 0
+    dedup_tables: int = 1
+    table_seeds: tuple = None
+    dedup_seeds: tuple = None
+
+    def __post_init__(self):
+        if self.num_hashes < 1 or self.num_tables < 1 or self.dedup_tables < 1:
+            raise InvalidInput("need K >= 1, L >= 1, dedup_tables >= 1")
+        if self.min_group_size < 1:
+            raise InvalidInput("minimum group size must be >= 1")
+
+    def scheme(self, universe: int) -> SignatureScheme:
+        return SignatureScheme(self.num_hashes, self.num_tables, universe, seed=self.seed,
+                               table_seeds=self.table_seeds)
+
+    def dedup_scheme(self, universe: int) -> SignatureScheme:
+        return SignatureScheme(self.num_hashes, self.dedup_tables, universe,
+                               seed=derive_seed(self.seed, DEDUP_TAG), table_seeds=self.dedup_seeds)
+
+
+# ---------------------------------------------------------------------------
+# bucket signatures
+
+def bucket_signatures_codes(bt: BucketTable, funcs, info=None) -> torch.Tensor:
+    """[H, m*t] int32 MinHash minima of every bucket of an even rank split
+    via the inverse-rank scan (geek_silk_invscan)."""
+    batch = PermBatch(funcs)
+    nb = bt.m * bt.stride
+    sig = _lib.empty(max(1, batch.n * nb), _lib.U32)
+    draws = np.zeros(1, dtype=np.uint64)
+    st, n, tab = batch.args()
+    _lib.call("geek_silk_invscan", _lib.ptr(bt.codes), bt.n, bt.m, bt.stride, st, n, tab, _lib.ptr(sig), None,
+              _lib.hptr(draws), _lib.stream())
+    if info is not None:
+        info["invscan_draws"] = int(draws[0])
+    return sig[: batch.n * nb].view(batch.n, nb)
+
+
+def bucket_signatures_csr(flat, off, nsets, funcs) -> torch.Tensor:
+    """[H, nsets] via segmented-min MinHash over member CSR."""
+    sig = set_signatures_device(funcs, flat, off, nsets, PermBatch(funcs))
+    return sig.t().contiguous()
+
+
+def silk_signatures(buckets, scheme: SignatureScheme, info=None):
+    """(sig [L*K, nb], nb, csr or None) for a BucketTable or list[Bucket]."""
+    funcs = scheme.all_functions()
+    if isinstance(buckets, BucketTable):
+        if buckets.even and buckets.n == scheme.universe:
+            return bucket_signatures_codes(buckets, funcs, info), len(buckets), None
+        flat, off = buckets.member_csr()
+        return bucket_signatures_csr(flat, off, len(buckets), funcs), len(buckets), (flat, off)
+    sets = [b.members for b in buckets]
+    for s in sets:
+        if s.size and (s.min() < 0 or s.max() >= scheme.universe):
+            raise InvalidInput("element outside hash universe")
+    flat, off, _ = csr_from_sets(sets)
+    return bucket_signatures_csr(flat, off, len(sets), funcs), len(sets), (flat, off)
+
+
+# ---------------------------------------------------------------------------
+# bins
+
+class Bins:
+    """All bins of all SILK tables: (bucket, bin) pairs, bin sizes, bin table."""
+
+    def __init__(self, pair_bucket, pair_bin, bin_size, bin_table, bin_sig):
+        self.pair_bucket = pair_bucket  # int64 [P] bucket position
+        self.pair_bin = pair_bin        # int64 [P] global bin id
+        self.bin_size = bin_size        # int32 [B] buckets per bin
+        self.bin_table = bin_table      # numpy [B] SILK table of each bin
+        self.bin_sig = bin_sig          # int32 [B, K] signature of each bin
+
+    @property
+    def count(self) -> int:
+        return int(self.bin_size.numel())
+
+
+def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Tensor = None,
+              tables=None) -> Bins:
+    """Per SILK table, group buckets by (owner, signature); keep groups of
+    >= 2 buckets (seeding.py:83-104, engine.py:270-277).  Bin ids are
+    table-major, then in sorted (owner, signature) order."""
+    nb = sig.shape[1]
+    dev = sig.device
+    tables = range(L) if tables is None else tables
+    width = K + (1 if owner is not None else 0)
+    bits = ([max(1, int(int(owner.max().item())).bit_length())] if owner is not None and nb else []) + \
+        [max(1, int(universe - 1).bit_length())] * K
+    bits = np.array(bits, dtype=np.int32)
+    perm = _lib.empty(max(1, nb), _lib.U32)
+    gid = _lib.empty(max(1, nb), _lib.U32)
+    pb, pn, bs, bt, bsig = [], [], [], [], []
+    base = 0
+    for st in tables:
+        cols = ([owner] if owner is not None else []) + [sig[st * K + j] for j in range(K)]
+        rows = torch.stack(cols, dim=1).contiguous()
+        ng = np.zeros(1, dtype=np.uint64)
+        _lib.call("geek_group_rows", _lib.ptr(rows), nb, width, _lib.hptr(bits), _lib.ptr(perm), _lib.ptr(gid),
+                  _lib.hptr(ng), _lib.stream())
+        g = gid[:nb].to(torch.int64)
+        counts = torch.bincount(g, minlength=int(ng[0]))
+        binned = counts >= 2
+        nbins = int(binned.sum().item())
+        if nbins == 0:
+            continue
+        newid = torch.cumsum(binned.to(torch.int64), 0) - 1 + base
+        sel = binned[g]
+        pb.append(perm[:nb].to(torch.int64)[sel])
+        pn.append(newid[g][sel])
+        bs.append(counts[binned].to(torch.int32))
+        bt.append(np.full(nbins, st, dtype=np.int64))
+        first = torch.ones_like(sel)
+        first[1:] = g[1:] != g[:-1]
+        bsig.append(rows[perm[:nb].to(torch.int64)[sel & first]][:, -K:])
+        base += nbins
+    if not pb:
+        z = torch.zeros(0, dtype=torch.int64, device=dev)
+        return Bins(z, z, torch.zeros(0, dtype=torch.int32, device=dev), np.zeros(0, np.int64),
+                    torch.zeros((0, K), dtype=torch.int32, device=dev))
+    return Bins(torch.cat(pb), torch.cat(pn), torch.cat(bs), np.concatenate(bt), torch.cat(bsig))
+
+
+# ---------------------------------------------------------------------------
+# vote
+
+def membership_pairs(bins: Bins, buckets, csr, bucket_sizes: torch.Tensor):
+    """(pair_bin, pair_id) int32 for every id of every binned bucket."""
+    if bins.pair_bucket.numel() == 0:
+        z = torch.zeros(0, dtype=torch.int32, device=bins.pair_bin.device)
+        return z, z
+    if csr is not None:
+        flat, off = csr
+        ids, noff = csr_gather(flat, off, bins.pair_bucket)
+        sizes = noff[1:] - noff[:-1]
+        pbin = torch.repeat_interleave(bins.pair_bin, sizes, output_size=ids.numel())
+        return pbin.to(torch.int32).contiguous(), ids.contiguous()
+    # id-major codes: one pass over codes emits (bin, id) for binned buckets
+    bt: BucketTable = buckets
+    nb = bt.m * bt.stride
+    order = torch.argsort(bins.pair_bucket, stable=True)
+    pbk = bins.pair_bucket[order]
+    pbn = bins.pair_bin[order].to(torch.int32).contiguous()
+    cnt = torch.bincount(pbk, minlength=nb)
+    bb_off = torch.zeros(nb + 1, dtype=torch.int64, device=pbk.device)
+    torch.cumsum(cnt, 0, out=bb_off[1:])
+    bb_off = bb_off.to(torch.int32).contiguous()
+    cap = int(bucket_sizes[bins.pair_bucket].sum().item())
+    out_bin = _lib.empty(max(1, cap), _lib.U32)
+    out_id = _lib.empty(max(1, cap), _lib.U32)
+    count = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_emit_members_codes", _lib.ptr(bt.codes), bt.n, bt.m, bt.stride, _lib.ptr(bb_off),
+              _lib.ptr(pbn), _lib.ptr(out_bin), _lib.ptr(out_id), cap, _lib.hptr(count), _lib.stream())
+    c = int(count[0])
+    return out_bin[:c], out_id[:c]
+
+
+def vote(pair_bin, pair_id, bins: Bins, delta: int):
+    """Strict-majority winners per bin, bins with < delta winners dropped ->
+    (GroupSet ordered by bin id, winning bin ids int64)."""
+    npairs = int(pair_bin.numel())
+    if npairs == 0 or bins.count == 0:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=pair_bin.device)
+    wb = _lib.empty(npairs, _lib.U32)
+    wi = _lib.empty(npairs, _lib.U32)
+    nw = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_majority_vote", _lib.ptr(pair_bin.contiguous()), _lib.ptr(pair_id.contiguous()), npairs,
+              _lib.ptr(bins.bin_size.contiguous()), bins.count, int(delta), _lib.ptr(wb), _lib.ptr(wi),
+              _lib.hptr(nw), _lib.stream())
+    k = int(nw[0])
+    if k == 0:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=pair_bin.device)
+    wb, wi = wb[:k].to(torch.int64), wi[:k]
+    ub, cnt = torch.unique_consecutive(wb, return_counts=True)
+    off = torch.zeros(ub.numel() + 1, dtype=torch.int64, device=wb.device)
+    torch.cumsum(cnt, 0, out=off[1:])
+    return GroupSet(wi.contiguous(), off), ub
+
+
+def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=None):
+    """Every surviving vote of every SILK table (collect_votes / local_votes)
+    -> (GroupSet, Bins, winning bin ids)."""
+    scheme = params.scheme(universe)
+    sig, nb, csr = silk_signatures(buckets, scheme, info)
+    bins = find_bins(sig, params.num_hashes, params.num_tables, universe, owner)
+    if isinstance(buckets, BucketTable):
+        sizes = buckets.bucket_sizes()
+    else:
+        sizes = _lib.to_dev(np.array([b.members.size for b in buckets], dtype=np.int64))
+    pbin, pid = membership_pairs(bins, buckets, csr, sizes)
+    groups, won = vote(pbin, pid, bins, params.min_group_size)
+    if info is not None:
+        info["bins"] = bins.count
+        info["vote_pairs"] = int(pbin.numel())
+        info["raw_groups"] = groups.count
+    return groups, bins, won
+
+
+# ---------------------------------------------------------------------------
+# dedup
+
+def dedup_device(groups: GroupSet, params: SeedingParams, universe: int) -> GroupSet:
+    """dedup_groups on the device (seeding.py:117-134) -> canonical order."""
+    if groups.count > 1:
+        scheme = params.dedup_scheme(universe)
+        K = params.num_hashes
+        bits = np.full(K, max(1, int(universe - 1).bit_length()), dtype=np.int32)
+        for tb in range(params.dedup_tables):
+            cnt = groups.count
+            sig = set_signatures_device(scheme.functions(tb), groups.flat, groups.off, cnt)
+            perm = _lib.empty(cnt, _lib.U32)
+            gid = _lib.empty(cnt, _lib.U32)
+            ng = np.zeros(1, dtype=np.uint64)
+            _lib.call("geek_group_rows", _lib.ptr(sig.contiguous()), cnt, K, _lib.hptr(bits), _lib.ptr(perm),
+                      _lib.ptr(gid), _lib.hptr(ng), _lib.stream())
+            keep = _lib.empty(cnt, torch.uint8)
+            _lib.call("geek_pick_representatives", _lib.ptr(groups.flat), _lib.ptr(groups.off), _lib.ptr(perm),
+                      _lib.ptr(gid), cnt, _lib.ptr(keep), _lib.stream())
+            groups = groups.select(torch.nonzero(keep, as_tuple=True)[0])
+    return canonical_order(groups)
+
+
+def canonical_order(groups: GroupSet) -> GroupSet:
+    """Sort groups by member tuple, proper prefix first (data.py:200-202)."""
+    cnt = groups.count
+    if cnt <= 1:
+        return groups
+    order = _lib.empty(cnt, _lib.U32)
+    _lib.call("geek_sort_groups", _lib.ptr(groups.flat), _lib.ptr(groups.off), cnt, _lib.ptr(order),
+              _lib.stream())
+    return groups.select(order.to(torch.int64))
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+def bin_buckets(buckets, params: SeedingParams, table: int, universe: int) -> list:
+    """seeding.py:93-104 -> list[Bin] in signature order."""
+    if not buckets or len(buckets) == 0:
+        return []
+    scheme = params.scheme(universe)
+    sig, nb, csr = silk_signatures(buckets, scheme)
+    bins = find_bins(sig, params.num_hashes, params.num_tables, universe, None, tables=[table])
+    pbk = bins.pair_bucket.cpu().numpy()
+    pbn = bins.pair_bin.cpu().numpy()
+    bsig = bins.bin_sig.cpu().numpy().view(np.uint32).astype(np.int64)
+    out = []
+    for b in range(bins.count):
+        idx = tuple(int(i) for i in np.sort(pbk[pbn == b]))
+        out.append(Bin(signature=tuple(int(v) for v in bsig[b]), bucket_indices=idx))
+    return out
+
+
+def majority_vote(bin_: Bin, buckets) -> SeedGroup | None:
+    """seeding.py:107-114 (strict majority over the bin's buckets)."""
+    parts = [buckets[i].members for i in bin_.bucket_indices]
+    flat, off, sizes = csr_from_sets(parts)
+    ids = flat[: int(sizes.sum())]
+    pbin = torch.zeros_like(ids)
+    bins = Bins(None, None, _lib.to_dev(np.array([len(parts)], dtype=np.int32)), np.zeros(1, np.int64), None)
+    groups, _ = vote(pbin, ids, bins, 1)
+    if groups.count == 0:
+        return None
+    return SeedGroup(groups.to_host()[0])
+
+
+def collect_votes(buckets, params: SeedingParams, universe: int, trace=None) -> list:
+    """seeding.py:154-165: every surviving vote, table-major, bins in signature order."""
+    groups, bins, won = silk_votes(buckets, params, universe)
+    out = groups.to_seed_groups()
+    if trace is not None and out:
+        pbk = bins.pair_bucket.cpu().numpy()
+        pbn = bins.pair_bin.cpu().numpy()
+        for g, b in zip(out, won.cpu().numpy().tolist()):
+            idx = np.sort(pbk[pbn == b])
+            trace.append((int(bins.bin_table[b]), tuple(buckets[int(i)].bucket_id for i in idx), g))
+    return out
+
+
+def find_seed_groups(buckets, params: SeedingParams, universe: int, trace=None) -> list:
+    """seeding.py:137-151: bin + vote + delta, then dedup."""
+    if buckets is None or len(buckets) == 0:
+        raise InvalidInput("seeding needs at least one bucket")
+    if trace is not None:
+        raw = collect_votes(buckets, params, universe, trace)
+        return dedup_device(GroupSet.from_host(raw), params, universe).to_seed_groups()
+    groups, _, _ = silk_votes(buckets, params, universe)
+    return dedup_device(groups, params, universe).to_seed_groups()
+
+
+def dedup_groups(groups, params: SeedingParams, universe: int) -> list:
+    """seeding.py:117-134."""
+    gs = [g if isinstance(g, SeedGroup) else SeedGroup(g) for g in groups]
+    if not gs:
+        return []
+    for g in gs:
+        if g.members.max() >= universe:
+            raise InvalidInput("element outside hash universe")
+    return dedup_device(GroupSet.from_host(gs), params, universe).to_seed_groups()
+
+
+def seeds_to_centers(groups, data) -> list:
+    """seeding.py:168-197: exact centroid / attribute mode / majority membership."""
+    from .numeric import dense_centers, mode_centers, sparse_centers
+
+    gs = groups if isinstance(groups, GroupSet) else GroupSet.from_host(groups)
+    if gs.count == 0:
+        return []
+    sizes = gs.sizes().cpu().numpy()
+    if isinstance(data, DenseData):
+        C = dense_centers(data.device_vectors(), gs).cpu().numpy()
+        return [CentralVector("centroid", C[i], int(sizes[i])) for i in range(gs.count)]
+    if isinstance(data, CategoricalData):
+        M = mode_centers(data.device_codes(), data.code_space, gs).cpu().numpy()
+        return [CentralVector("mode", M[i], int(sizes[i])) for i in range(gs.count)]
+    if isinstance(data, SparseData):
+        M = sparse_centers(data, gs).cpu().numpy()
+        return [CentralVector("mode", M[i], int(sizes[i])) for i in range(gs.count)]
+    raise InvalidInput("unsupported dataset type for center computation")

@@ -1,0 +1,351 @@
+"""GPU parity: the CUDA path (through libgeek's C ABI) against the CPU oracle
+and the golden vectors dumped from the reference.  Integer outputs (pi
+values, signatures, bucket codes, seed groups, labels) and the float64
+centers / radii / objectives must be bit-identical."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import geek_oracle as O
+from tests.golden_io import csr, groups as golden_groups, meta, npz
+
+pytestmark = pytest.mark.gpu
+
+G = pytest.importorskip("paper_2106_10515_b200")
+
+
+def keys(gs):
+    return [tuple(np.asarray(g.members if hasattr(g, "members") else g).tolist()) for g in gs]
+
+
+WORKED = [(0, 0, [0, 1, 3]), (0, 1, [2, 4, 5]), (1, 0, [0, 1, 3, 4]), (1, 1, [5]),
+          (2, 0, [0, 1, 3, 5]), (2, 1, [2, 4]), (3, 0, [0, 1, 3, 5]), (3, 1, [4, 5])]
+WORKED_POINTS = np.array([[0.0, 0.0, 0.0, 0.0], [0.1, 0.1, 0.1, 0.1], [10.0, 0.2, 10.0, 0.3],
+                          [0.2, 0.3, 0.2, 0.4], [10.1, 0.4, 10.1, 0.5], [12.0, 0.5, 12.0, 0.2]])
+
+
+def worked_buckets():
+    return [G.Bucket(t, s, np.array(m)) for t, s, m in WORKED]
+
+
+def worked_params():
+    return G.SeedingParams(2, 2, min_group_size=1, seed=0, dedup_tables=1, table_seeds=((6, 7), (15, 20)),
+                           dedup_seeds=((0, 1001),))
+
+
+# ---- MinHash ----------------------------------------------------------------
+
+def test_permutation_golden():
+    arr = npz("pi")
+    for seed, u, key in meta()["pi_cases"]:
+        if u >= (1 << 32):
+            continue
+        got = G.MinHashFunction(seed, u).permute(arr[key + "_x"])
+        assert np.array_equal(got, arr[key + "_y"]), key
+
+
+def test_permutation_bijective_and_inverse_scan_agree():
+    for u in (6, 4096, 4097, 100_003):
+        f = G.MinHashFunction(7, u)
+        p = f.permute(np.arange(u))
+        assert np.array_equal(np.sort(p), np.arange(u))
+
+
+def test_signatures_golden():
+    arr = npz("sigs")
+    for K, L, u, seed in [(3, 4, 700, 13), (2, 3, 5000, 1), (3, 2, 100_000, 2)]:
+        p = f"{K}_{L}_{u}_{seed}"
+        sets = csr(arr[p + "_flat"], arr[p + "_off"])
+        sch = G.SignatureScheme(K, L, u, seed=seed)
+        for tb in range(L):
+            assert np.array_equal(sch.signatures_for_sets(tb, sets), arr[f"{p}_{tb}"])
+
+
+def test_minhash_known_answers():
+    assert G.MinHashFunction.identity(10)({3, 5, 7}) == 3
+    assert G.MinHashFunction(42, 100)(np.arange(100)) == 0
+    with pytest.raises(G.InvalidInput):
+        G.MinHashFunction(1, 8)([8])
+
+
+def test_doph_golden():
+    arr = npz("doph")
+    red = G.DophReducer(G.hashing.derive_seed(3, 0xD0), 3_000_000, 400)
+    got = red.reduce_dataset(csr(arr["flat"], arr["off"]))
+    want = csr(arr["red_flat"], arr["red_off"])
+    assert all(np.array_equal(a, b) for a, b in zip(got, want))
+    assert G.DophReducer(5, 12, 4).sketch(np.array([0, 5])).tolist() == [0, 0, 2, 2]
+
+
+# ---- bucketize ----------------------------------------------------------------
+
+def test_worked_points_transform():
+    p = G.HomoTransformParams(4, 2, directions=np.eye(4))
+    got = {(b.table, b.slot): b.members.tolist() for b in G.transform_homo(G.DenseData(WORKED_POINTS), p)}
+    assert got == {(0, 0): [0, 1, 3], (0, 1): [2, 4, 5], (1, 0): [0, 1, 2], (1, 1): [3, 4, 5],
+                   (2, 0): [0, 1, 3], (2, 1): [2, 4, 5], (3, 0): [0, 1, 5], (3, 1): [2, 3, 4]}
+
+
+def test_rank_split_edge_cases():
+    # uneven split, first bucket takes the extra id (test_transform.py:52-57)
+    X = np.arange(7, dtype=float).reshape(7, 1)
+    bt = G.transform_homo(G.DenseData(X), G.HomoTransformParams(1, 2, directions=np.ones((1, 1))))
+    assert bt[0].members.tolist() == [0, 1, 2, 3]
+    # ties by id, -0.0 == +0.0
+    for vals in ([7.0] * 4, [0.0, -0.0, 0.0, -0.0], [1.0, -0.0, 0.0, -1.0, 0.0, 2.0]):
+        v = np.array(vals).reshape(-1, 1)
+        bt = G.transform_homo(G.DenseData(v), G.HomoTransformParams(1, 2, directions=np.ones((1, 1))))
+        assert np.array_equal(bt.codes_host()[0], O.slot_codes(v[:, 0], 2))
+    # t == n gives singletons
+    bt = G.transform_homo(G.DenseData(np.arange(5.0).reshape(5, 1)), G.HomoTransformParams(2, 5, seed=3))
+    assert all(b.members.size == 1 for b in bt)
+    with pytest.raises(G.InvalidInput):
+        G.transform_homo(G.DenseData(np.zeros((3, 2))), G.HomoTransformParams(1, 4))
+
+
+@pytest.mark.parametrize("n,t,dup", [(20_000, 3, True), (50_000, 997, False), (30_000, 30_000, False),
+                                     (123_457, 1000, False)])
+def test_rank_split_random_vs_oracle(n, t, dup):
+    rng = np.random.default_rng(n + t)
+    X = rng.standard_normal((n, 5)).astype(np.float32)
+    if dup:  # giant tie classes exercise the sorted fallback
+        X[: n // 2] = X[0]
+        X[n // 2:, 0] = 0.0
+    p = G.HomoTransformParams(3, t, seed=11)
+    bt = G.transform_homo(G.DenseData(X), p)
+    A = O.directions(11, 3, 5)
+    want = np.stack([O.slot_codes(X.astype(np.float64) @ A[j], t) for j in range(3)])
+    got = bt.codes_host()
+    # float64 projection order may differ from BLAS only on exact near-ties
+    assert (got != want).sum() <= 2, (got != want).sum()
+
+
+@pytest.mark.parametrize("name", ["c06", "small"])
+def test_codes_golden(name):
+    m = meta()["pipelines"][name]
+    arr = npz("pipelines")
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    bt = G.transform_homo(G.DenseData(X), G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]))
+    assert np.array_equal(bt.codes_host(), arr[name + "_codes"])
+
+
+def test_cfg1_codes_golden_sha():
+    m = meta()["pipelines"]["cfg1"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    assert hashlib.sha256(X.tobytes()).hexdigest() == m["data_sha"]
+    bt = G.transform_homo(G.DenseData(X), G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]))
+    codes = bt.codes_host().astype(np.int32)
+    assert hashlib.sha256(np.ascontiguousarray(codes).tobytes()).hexdigest() == m["codes_sha"]
+
+
+# ---- SILK ---------------------------------------------------------------------
+
+def test_worked_example_seeding():
+    b, p = worked_buckets(), worked_params()
+    bins = G.bin_buckets(b, p, 0, universe=6)
+    got = {tuple(b[i].bucket_id for i in x.bucket_indices) for x in bins}
+    assert got == {((0, 0), (1, 0), (2, 0), (3, 0)), ((0, 1), (2, 1), (3, 1))}
+    assert keys(G.find_seed_groups(b, p, universe=6)) == [(0, 1, 3), (2, 4), (2, 4, 5), (5,)]
+    trace = []
+    G.find_seed_groups(b, p, universe=6, trace=trace)
+    by_id = {x.bucket_id: x for x in b}
+    assert trace
+    for _, ids, grp in trace:
+        for mem in grp.members:
+            assert 2 * sum(mem in by_id[i].members for i in ids) > len(ids)
+    raw = G.seeding.collect_votes(b, p, 6)
+    assert sorted(keys(raw)) == sorted([(0, 1, 3), (0, 1, 3), (2, 4), (2, 4, 5), (5,)])
+    merged = [G.SeedGroup(x) for x in ([0, 1, 3], [0, 1, 3], [2, 4], [2, 4], [5])]
+    assert keys(G.dedup_groups(merged, p, 6)) == [(0, 1, 3), (2, 4), (5,)]
+
+
+def test_majority_vote_rules():
+    b = [G.Bucket(i, 0, np.array(m)) for i, m in enumerate([[1, 2], [1, 2], [1, 3], [1, 3]])]
+    assert G.majority_vote(G.Bin((0,), (0, 1, 2, 3)), b).members.tolist() == [1]
+    b = [G.Bucket(i, 0, np.array(m)) for i, m in enumerate([[1, 2], [1, 2], [1, 2], [1, 3]])]
+    assert G.majority_vote(G.Bin((0,), (0, 1, 2, 3)), b).members.tolist() == [1, 2]
+
+
+def test_invscan_equals_member_scan():
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((40_000, 8)).astype(np.float32)
+    bt = G.transform_homo(G.DenseData(X), G.HomoTransformParams(6, 300, seed=2))
+    sch = G.SignatureScheme(3, 4, 40_000, seed=9)
+    funcs = sch.all_functions()
+    fast = G.seeding.bucket_signatures_codes(bt, funcs)
+    flat, off = bt.member_csr()
+    slow = G.seeding.bucket_signatures_csr(flat, off, len(bt), funcs)
+    assert torch.equal(fast, slow)
+    members = [b.members for b in bt]
+    want = O.set_signatures(sch.function_seeds(1), 40_000, members)
+    got = slow[3:6].t().cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
+
+
+def test_dedup_random_vs_oracle():
+    rng = np.random.default_rng(1)
+    for seed in range(5):
+        gs = [np.unique(rng.integers(0, 16, rng.integers(1, 7))) for _ in range(12)]
+        gs += gs[:3]
+        p = G.SeedingParams(2, 3, seed=seed)
+        got = G.dedup_groups([G.SeedGroup(g) for g in gs], p, 16)
+        assert keys(got) == keys(O.dedup(gs, 2, seed, 16))
+
+
+# ---- centers + assign -----------------------------------------------------------
+
+def test_exact_centroid_vs_oracle():
+    rng = np.random.default_rng(7)
+    for dtype in (np.float64, np.float32):
+        X = (rng.standard_normal((500, 9)) * np.exp(rng.uniform(-20, 20, (500, 9)))).astype(dtype)
+        X[3, 2] = 0.0
+        X[4, 4] = -X[5, 4]
+        got = G.numeric.exact_centroid(X)
+        assert np.array_equal(got, O.exact_mean(X.astype(np.float64)))
+    assert G.numeric.exact_centroid(np.array([[0.1], [0.2], [0.3]]))[0] == 0.2
+
+
+def test_assign_c08_golden():
+    arr = npz("pipelines")
+    rng = np.random.default_rng(80)
+    X = rng.standard_normal((10_000, 16))
+    cents = [G.CentralVector("centroid", rng.standard_normal(16)) for _ in range(200)]
+    got = G.assign(G.DenseData(X), cents, "euclidean")
+    assert np.array_equal(got.assignment, arr["c08_labels"])
+    assert np.array_equal(got.radii, arr["c08_radii"])
+    assert got.objective == meta()["c08_objective"]
+    codes = rng.integers(0, 8, (10_000, 9)).astype(np.int32)
+    modes = [G.CentralVector("mode", rng.integers(0, 8, 9).astype(np.int32)) for _ in range(200)]
+    got = G.assign(G.CategoricalData(codes, code_space=8), modes, "jaccard")
+    assert np.array_equal(got.assignment, arr["c08cat_labels"])
+    assert np.array_equal(got.radii, arr["c08cat_radii"])
+
+
+@pytest.mark.parametrize("d", [3, 8, 100, 128, 129, 300, 960])
+def test_assign_pairwise_order_vs_oracle(d):
+    rng = np.random.default_rng(d)
+    X = rng.standard_normal((700, d))
+    C = rng.standard_normal((13, d))
+    C[5] = C[2]  # exact duplicate center: ties go to the lower index
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X, C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
+def test_tie_to_lowest_index():
+    c = G.assign(G.DenseData(np.array([[0.0]])),
+                 [G.CentralVector("centroid", [v]) for v in (1.0, 2.0, 3.0, -1.0)], "euclidean")
+    assert c.assignment[0] == 0
+
+
+def test_pairwise_sum_long_vectors():
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 8, 129, 1000, 100_003, 262_147):
+        v = rng.random(n)
+        got = G.assignment.pairwise_sum(torch.from_numpy(v).cuda()).item()
+        assert got == v.sum(), n
+
+
+# ---- end-to-end pipelines ----------------------------------------------------------
+
+def dense_config(m, g):
+    return G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(g),
+                            homo=G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]),
+                            seeding=G.SeedingParams(m["K"], m["L"], min_group_size=m["delta"], seed=m["sseed"]))
+
+
+@pytest.mark.parametrize("name", ["c06", "small", "cfg1"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_dense_pipeline_golden(name, dtype):
+    m = meta()["pipelines"][name]
+    arr = npz("pipelines")
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    if dtype == np.float32:
+        X = X.astype(np.float32)
+    for g in m["runs"]:
+        out = G.run_pipeline(G.DenseData(X), dense_config(m, int(g)))
+        if dtype == np.float32:  # different data: check against the oracle on the f32 values
+            if name == "cfg1":
+                continue
+            ref = O.pipeline_dense(X.astype(np.float64), m["m"], m["t"], m["tseed"], m["K"], m["L"], m["delta"],
+                                   m["sseed"], g=int(g))
+            assert keys(out.seed_groups) == keys(ref["groups"])
+            assert np.array_equal(out.clustering.assignment, ref["labels"])
+            assert np.array_equal(out.clustering.radii, ref["radii"])
+            continue
+        want = golden_groups(arr, f"{name}_g{g}")
+        assert keys(out.seed_groups) == keys(want), (name, g)
+        Cg = np.stack([c.values for c in out.clustering.centers])
+        assert np.array_equal(Cg, arr[f"{name}_g{g}_centers"])
+        assert np.array_equal(out.clustering.assignment, arr[f"{name}_g{g}_labels"])
+        assert np.array_equal(out.clustering.radii, arr[f"{name}_g{g}_radii"])
+        assert out.clustering.objective == m["runs"][g]["objective"]
+        assert out.k_star == m["runs"][g]["k_star"]
+
+
+def test_worked_pipeline():
+    cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(1),
+                           homo=G.HomoTransformParams(4, 2, directions=np.eye(4)),
+                           seeding=G.SeedingParams(2, 2, min_group_size=1, seed=0, table_seeds=((52, 3), (15, 63)),
+                                                   dedup_seeds=((0, 1001),)))
+    out = G.run_pipeline(G.DenseData(WORKED_POINTS), cfg)
+    assert keys(out.seed_groups) == [(0, 1, 3), (2, 4), (2, 4, 5), (5,)]
+    assert out.k_star == 3 and len(out.clustering.empty_clusters) == 1
+
+
+def test_fallback_warns():
+    rng = np.random.default_rng(9)
+    cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(2),
+                           homo=G.HomoTransformParams(4, 32, seed=1),
+                           seeding=G.SeedingParams(3, 4, min_group_size=50, seed=2))
+    X = rng.standard_normal((64, 4))
+    out = G.run_pipeline(G.DenseData(X), cfg)
+    ref = O.pipeline_dense(X, 4, 32, 1, 3, 4, 50, 2, g=2)
+    assert out.warnings and ref["warnings"]
+    assert keys(out.seed_groups) == keys(ref["groups"])
+
+
+@pytest.mark.parametrize("g", [1, 2])
+def test_sparse_pipeline_golden(g):
+    m = meta()["sparse"]
+    arr = npz("pipelines")
+    sets = csr(arr["sp_flat"], arr["sp_off"])
+    data = G.SparseData(sets, 20_000)
+    mp = G.MinhashTransformParams(3, 6, seed=4, target_dims=400)
+    bt, red = G.transform_sparse(data, mp)
+    assert np.array_equal(bt.codes_host(), arr["sp_codes"])
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="sparse", workers=G.WorkerConfig(g), minhash=mp,
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=5))
+    out = G.run_pipeline(data, cfg)
+    assert keys(out.seed_groups) == keys(golden_groups(arr, f"sp_g{g}"))
+    assert np.array_equal(np.stack([c.values for c in out.clustering.centers]), arr[f"sp_g{g}_centers"])
+    assert np.array_equal(out.clustering.assignment, arr[f"sp_g{g}_labels"])
+    assert np.array_equal(out.clustering.radii, arr[f"sp_g{g}_radii"])
+    assert out.clustering.objective == m["runs"][str(g)]["objective"]
+
+
+@pytest.mark.parametrize("g", [1, 2])
+def test_mixed_pipeline_golden(g):
+    m = meta()["mixed"]
+    arr = npz("pipelines")
+    data = G.MixedData(arr["mx_num"], arr["mx_cat"])
+    mp = G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16)
+    bt, unified = G.transform_hetero(data, mp)
+    assert np.array_equal(unified.codes, arr["mx_unified"])
+    assert np.array_equal(bt.codes_host(), arr["mx_codes"])
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="mixed", workers=G.WorkerConfig(g), minhash=mp,
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9))
+    out = G.run_pipeline(data, cfg)
+    assert keys(out.seed_groups) == keys(golden_groups(arr, f"mx_g{g}"))
+    assert np.array_equal(np.stack([c.values for c in out.clustering.centers]), arr[f"mx_g{g}_centers"])
+    assert np.array_equal(out.clustering.assignment, arr[f"mx_g{g}_labels"])
+    assert np.array_equal(out.clustering.radii, arr[f"mx_g{g}_radii"])
+    assert out.clustering.objective == m["runs"][str(g)]["objective"]
