@@ -174,6 +174,10 @@ int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngr
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
                    int64_t* labels, double* best, void* stream);
 
+/* number of points the last geek_assign_l2 call re-checked exactly because
+ * the float32 screen could not separate their two nearest centers        */
+uint64_t geek_assign_last_rechecked(void);
+
 /* radii[c] = max best over members (0 if none), sizes[c] = member count
  * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed
  * outputs, or on partial results to merge).                                 */

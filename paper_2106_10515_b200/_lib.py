@@ -62,6 +62,7 @@ _SIGS = {
     "geek_exact_sums": (i32, [vp, i32, u64, i32, u64, vp, vp, u64, i32, i32, vp, vp]),
     "geek_round_means": (i32, [vp, vp, u64, i32, i32, i32, vp, vp]),
     "geek_assign_l2": (i32, [vp, i32, u64, i32, vp, u64, vp, vp, vp]),
+    "geek_assign_last_rechecked": (u64, []),
     "geek_radii_sizes": (i32, [vp, vp, u64, u64, vp, vp, vp]),
     "geek_pairwise_sum": (i32, [vp, u64, vp, vp]),
     "geek_assign_categorical": (i32, [vp, u64, i32, vp, u64, vp, vp, vp]),
@@ -119,8 +120,42 @@ def check(status: int, what: str = ""):
     raise EngineError(f"{what} failed ({status}): {msg}")
 
 
+class CallTimer:
+    """Brackets every libgeek entry point with CUDA events on the current
+    stream (bench.py uses it to time the dominant kernel live)."""
+
+    def __init__(self):
+        self.events = []
+
+    def ms_by_name(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b in self.events:
+            s = out.setdefault(name, [0.0, 0])
+            s[0] += a.elapsed_time(b)
+            s[1] += 1
+        return out
+
+
+_timer = None
+
+
+def set_call_timer(t):
+    global _timer
+    _timer = t
+
+
 def call(name: str, *args):
     L = lib()
+    if _timer is not None:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        st = getattr(L, name)(*args)
+        b.record()
+        _timer.events.append((name, a, b))
+        check(st, name)
+        return
     check(getattr(L, name)(*args), name)
 
 

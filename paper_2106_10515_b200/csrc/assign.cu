@@ -95,10 +95,11 @@ template <class T>
 __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restrict__ X, uint64_t n, int d,
                                                                 const double* __restrict__ C, uint64_t k,
                                                                 const PwPlan plan, int64_t* labels,
-                                                                double* best) {
+                                                                double* best, const uint32_t* idx) {
   extern __shared__ double sC[];  // [kAsgCenters][d]
-  const uint64_t i = blockIdx.x * (uint64_t)kAsgThreads + threadIdx.x;
-  const bool valid = i < n;
+  const uint64_t q = blockIdx.x * (uint64_t)kAsgThreads + threadIdx.x;
+  const bool valid = q < n;
+  const uint64_t i = (idx && valid) ? idx[q] : q;
   const T* xr = X + (valid ? i : 0) * d;
   double bd = 0.0;
   int64_t bl = -1;
@@ -129,12 +130,26 @@ __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restr
 
 __global__ void radii_sizes_kernel(const int64_t* labels, const double* best, uint64_t n, double* radii,
                                    int64_t* sizes) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const int64_t l = labels[i];
-    atomicMax(reinterpret_cast<unsigned long long*>(radii) + l,
-              (unsigned long long)__double_as_longlong(best[i]));  // best >= 0
-    atomicAdd(reinterpret_cast<unsigned long long*>(sizes) + l, 1ull);
+  // warp-aggregated: ids are cluster-contiguous, so a warp mostly shares a label
+  const unsigned lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    const long long l = valid ? labels[i] : -1ll - lane;
+    // best >= 0, so its bit pattern orders like the value
+    unsigned long long bits = valid ? (unsigned long long)__double_as_longlong(best[i]) : 0ull;
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    // 64-bit max over the peer group as (hi, lo) lexicographic 32-bit maxima
+    const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+    const unsigned mhi = __reduce_max_sync(peers, hi);
+    const unsigned mlo = __reduce_max_sync(peers, hi == mhi ? lo : 0u);
+    const unsigned long long mx = ((unsigned long long)mhi << 32) | mlo;
+    const int leader = __ffs(peers) - 1;
+    if (valid && (int)lane == leader) {
+      atomicMax(reinterpret_cast<unsigned long long*>(radii) + l, mx);
+      atomicAdd(reinterpret_cast<unsigned long long*>(sizes) + l, (unsigned long long)__popc(peers));
+    }
   }
 }
 
@@ -214,6 +229,165 @@ __global__ void combine_kernel(const uint32_t* node, const uint32_t* left, const
     val[node[q]] = __dadd_rn(val[left[q]], val[right[q]]);
 }
 
+// ---- screened assignment (float32 data) -----------------------------------
+//
+// screen: s(x, c) = |c|^2 - 2 x.c in float32 (SIMT register-blocked GEMM,
+// 128 points x 128 centers per tile, 8x8 per thread) with a running top-2
+// per point.  |s - S| <= E(x) for the exact S = |c|^2 - 2 x.c (rounding of
+// c to float32, the dot product, |c|^2 and the subtraction, bounded with
+// |x| |c| by Cauchy-Schwarz).  When s2 - s1 > T(x) = 2E + 2E64 + margin the
+// exact float64 (numpy-order) distances have the same strict argmin, so the
+// label is final and only best = dist(x, c_label) is evaluated exactly;
+// otherwise the point is re-scanned exactly over all centers.
+
+static uint64_t& last_ambiguous() {
+  static uint64_t v = 0;
+  return v;
+}
+
+constexpr int kScrP = 128, kScrC = 128, kScrK = 16, kScrThreads = 256;
+
+__global__ void center_prep_kernel(const double* C, uint64_t k, int d, float* Cf, float* c2f,
+                                   unsigned long long* cmax_bits) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k; c += (uint64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double v = C[c * d + j];
+      Cf[c * d + j] = (float)v;
+      s = fma(v, v, s);
+    }
+    c2f[c] = (float)s;
+    atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(s) * (1.0 + 1e-12)));
+  }
+}
+
+__global__ void __launch_bounds__(kScrThreads, 2) screen_kernel(const float* __restrict__ X, uint64_t n, int d,
+                                                                 const float* __restrict__ Cf,
+                                                                 const float* __restrict__ c2f,
+                                                                 const double* __restrict__ C, uint64_t k,
+                                                                 const unsigned long long* cmax_bits,
+                                                                 const PwPlan plan, int64_t* labels, double* best,
+                                                                 uint32_t* amb, unsigned long long* namb) {
+  extern __shared__ float smem[];
+  const int xs_ld = kScrP + 4;
+  float* Xs = smem;                                 // [d][xs_ld]
+  float* Cs = Xs + (size_t)d * xs_ld;               // [kScrK][kScrC + 4]
+  float* rs1 = Cs + kScrK * (kScrC + 4);            // [kScrP] merged top-2
+  float* rs2 = rs1 + kScrP;
+  int* ri1 = reinterpret_cast<int*>(rs2 + kScrP);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const uint64_t p0 = blockIdx.x * (uint64_t)kScrP;
+  for (int e = threadIdx.x; e < kScrP * d; e += kScrThreads) {
+    const int p = e / d, j = e - p * d;
+    Xs[j * xs_ld + p] = (p0 + p < n) ? X[(p0 + p) * d + j] : 0.f;
+  }
+  float s1[8], s2[8];
+  int i1[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    s1[a] = INFINITY;
+    s2[a] = INFINITY;
+    i1[a] = -1;
+  }
+  for (uint64_t c0 = 0; c0 < k; c0 += kScrC) {
+    float acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+    for (int k0 = 0; k0 < d; k0 += kScrK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kScrC * kScrK; e += kScrThreads) {
+        const int c = e / kScrK, kk = e - c * kScrK;
+        Cs[kk * (kScrC + 4) + c] = (c0 + c < k && k0 + kk < d) ? Cf[(c0 + c) * d + k0 + kk] : 0.f;
+      }
+      __syncthreads();
+      const int kn = min(kScrK, d - k0);
+      for (int kk = 0; kk < kn; ++kk) {
+        const float4 xa = *reinterpret_cast<const float4*>(Xs + (k0 + kk) * xs_ld + ty * 8);
+        const float4 xb = *reinterpret_cast<const float4*>(Xs + (k0 + kk) * xs_ld + ty * 8 + 4);
+        const float4 ca = *reinterpret_cast<const float4*>(Cs + kk * (kScrC + 4) + tx * 8);
+        const float4 cb = *reinterpret_cast<const float4*>(Cs + kk * (kScrC + 4) + tx * 8 + 4);
+        const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+        const float cv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(xv[a], cv[b], acc[a][b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint64_t c = c0 + tx * 8 + b;
+      if (c >= k) break;
+      const float cc = c2f[c];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const float sv = cc - 2.f * acc[a][b];
+        if (sv < s1[a]) {
+          s2[a] = s1[a];
+          s1[a] = sv;
+          i1[a] = (int)c;
+        } else if (sv < s2[a]) {
+          s2[a] = sv;
+        }
+      }
+    }
+  }
+  // merge the 16 column groups (lanes tx within a half warp)
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const float os1 = __shfl_xor_sync(0xffffffffu, s1[a], o);
+      const float os2 = __shfl_xor_sync(0xffffffffu, s2[a], o);
+      const int oi1 = __shfl_xor_sync(0xffffffffu, i1[a], o);
+      const float lo = fminf(s1[a], os1), hi = fmaxf(s1[a], os1);
+      const bool take = os1 < s1[a] || (os1 == s1[a] && oi1 < i1[a] && oi1 >= 0);
+      s2[a] = fminf(hi, fminf(s2[a], os2));
+      if (take) i1[a] = oi1;
+      s1[a] = lo;
+    }
+    if (tx == 0) {
+      rs1[ty * 8 + a] = s1[a];
+      rs2[ty * 8 + a] = s2[a];
+      ri1[ty * 8 + a] = i1[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kScrP) {
+    const int p = threadIdx.x;
+    const uint64_t i = p0 + p;
+    if (i < n) {
+      double xn2 = 0.0;
+      for (int j = 0; j < d; ++j) {
+        const double v = Xs[j * xs_ld + p];
+        xn2 = fma(v, v, xn2);
+      }
+      const double xn = sqrt(xn2) * (1.0 + 1e-12);
+      const double cn = __longlong_as_double((long long)*cmax_bits);
+      const double u = 5.9604644775390625e-08;  // 2^-24
+      const double E = 1.01 * (2.0 * d + 10.0) * u * (xn * cn + cn * cn);
+      const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
+      const double T = 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
+      const int lab = ri1[p];
+      const bool certain = lab >= 0 && (k == 1 || (double)rs2[p] - (double)rs1[p] > T);
+      if (certain) {
+        const double* cr = C + (uint64_t)lab * d;
+        auto get = [&](int j) {
+          const double df = __dsub_rn((double)Xs[j * xs_ld + p], cr[j]);
+          return __dmul_rn(df, df);
+        };
+        labels[i] = lab;
+        best[i] = __dsqrt_rn(pw_sum(plan, get));
+      } else {
+        const unsigned long long q = atomicAdd(namb, 1ull);
+        amb[q] = (uint32_t)i;
+      }
+    }
+  }
+}
+
 }  // namespace geek
 
 using namespace geek;
@@ -230,22 +404,54 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
   PwPlan plan;
   pw_build(plan, 0, d);
   GEEK_REQUIRE(plan.nops <= 64, "pairwise plan too deep");
-  size_t smem = sizeof(double) * kAsgCenters * d;
-  unsigned grid = (unsigned)((n + kAsgThreads - 1) / kAsgThreads);
-  if (dtype == 0) {
-    if (smem > 48 * 1024)
-      GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-    assign_l2_kernel<float><<<grid, kAsgThreads, smem, s>>>((const float*)X, n, d, C, k, plan, labels, best);
-  } else {
-    if (smem > 48 * 1024)
-      GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-    assign_l2_kernel<double><<<grid, kAsgThreads, smem, s>>>((const double*)X, n, d, C, k, plan, labels, best);
+  const size_t smem = sizeof(double) * kAsgCenters * d;
+  if (smem > 48 * 1024) {
+    GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+    GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
   }
+  const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
+  const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;
+  if (!screened) {
+    unsigned grid = (unsigned)((n + kAsgThreads - 1) / kAsgThreads);
+    if (dtype == 0)
+      assign_l2_kernel<float><<<grid, kAsgThreads, smem, s>>>((const float*)X, n, d, C, k, plan, labels, best,
+                                                               nullptr);
+    else
+      assign_l2_kernel<double><<<grid, kAsgThreads, smem, s>>>((const double*)X, n, d, C, k, plan, labels, best,
+                                                                nullptr);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
+  Scratch cf, c2, amb, cnt;
+  GEEK_TRY(cf.alloc(k * d * 4, s));
+  GEEK_TRY(c2.alloc(k * 4, s));
+  GEEK_TRY(amb.alloc(n * 4, s));
+  GEEK_TRY(cnt.alloc(16, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 16, s));
+  unsigned long long* namb = cnt.as<unsigned long long>();
+  unsigned long long* cmax = namb + 1;
+  center_prep_kernel<<<grid_for(k, 128), 128, 0, s>>>(C, k, d, cf.as<float>(), c2.as<float>(), cmax);
   GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scr_smem));
+  const unsigned grid = (unsigned)((n + kScrP - 1) / kScrP);
+  screen_kernel<<<grid, kScrThreads, scr_smem, s>>>((const float*)X, n, d, cf.as<float>(), c2.as<float>(), C, k,
+                                                    cmax, plan, labels, best, amb.as<uint32_t>(), namb);
+  GEEK_CHECK_LAUNCH();
+  unsigned long long na = 0;
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(&na, namb, 8, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  last_ambiguous() = na;
+  if (na) {
+    assign_l2_kernel<float><<<(unsigned)((na + kAsgThreads - 1) / kAsgThreads), kAsgThreads, smem, s>>>(
+        (const float*)X, na, d, C, k, plan, labels, best, amb.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  }
   return GEEK_OK;
 }
+
+uint64_t geek_assign_last_rechecked(void) { return last_ambiguous(); }
 
 int geek_radii_sizes(const int64_t* labels, const double* best, uint64_t n, uint64_t k, double* radii,
                      int64_t* sizes, void* stream) {

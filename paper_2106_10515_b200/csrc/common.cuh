@@ -46,6 +46,10 @@ struct Status {
     if (_s != GEEK_OK) return _s; \
   } while (0)
 
+// keep the stream-ordered pool's memory cached across synchronisations
+// (the default release threshold of 0 unmaps it at every sync)
+void ensure_pool();
+
 // Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
 struct Scratch {
   void* ptr = nullptr;
@@ -61,6 +65,7 @@ struct Scratch {
     ptr = nullptr;
     stream = s;
     if (bytes == 0) bytes = 16;
+    ensure_pool();
     cudaError_t e = cudaMallocAsync(&ptr, bytes, s);
     if (e != cudaSuccess) {
       set_error("cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));

@@ -239,6 +239,23 @@ def test_assign_pairwise_order_vs_oracle(d):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("d,k,offset", [(128, 37, 0.0), (128, 300, 300.0), (16, 5, 0.0), (200, 64, 50.0)])
+def test_assign_screened_f32_vs_oracle(d, k, offset):
+    """float32 data takes the float32 screen + exact recheck path."""
+    rng = np.random.default_rng(d * 1000 + k)
+    C = rng.standard_normal((k, d)) * 3 + offset
+    lab0 = rng.integers(0, k, 20_000)
+    X = (C[lab0] + rng.standard_normal((20_000, d))).astype(np.float32)
+    C[k // 2] = C[1]                     # duplicate centers: exact tie -> lower index
+    X[:50] = ((C[2] + C[3]) / 2).astype(np.float32)  # equidistant points
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+    assert G._lib.load_library().geek_assign_last_rechecked() >= 50
+
+
 def test_tie_to_lowest_index():
     c = G.assign(G.DenseData(np.array([[0.0]])),
                  [G.CentralVector("centroid", [v]) for v in (1.0, 2.0, 3.0, -1.0)], "euclidean")
