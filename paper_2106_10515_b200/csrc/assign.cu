@@ -9,6 +9,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -388,6 +389,92 @@ __global__ void __launch_bounds__(kScrThreads, 2) screen_kernel(const float* __r
   }
 }
 
+// ---- tensor-core screen: classification and candidate recheck ----------------
+
+int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t sbo, Scratch& img, Scratch& c2,
+                      Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s);
+int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
+                     uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i, float* xnorm,
+                     cudaStream_t s);
+// SWIZZLE_NONE K-major canonical layout strides (bytes): K-adjacent / M,N-adjacent core matrices
+constexpr uint32_t kTcLBO = 128, kTcSBO = 256;
+
+template <class G>
+__device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
+  return __dsqrt_rn(pw_sum(plan, get));
+}
+
+// Bound of |s - S| for the TF32x3 screen (see tc_screen.cu): operand
+// rounding to float32, hi/lo split residuals and the dropped lo*lo term,
+// fp32 accumulation of 3d products, |c'|^2 rounding and the final subtraction.
+__device__ __forceinline__ double tc_threshold(double xn, double cn, int d) {
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  const double E = 1.05 * ((1.9073486328125e-06 + 6.0 * d * 1.1920928955078125e-07 + 8.0 * u) * xn * cn +
+                           2.0 * u * cn * cn);
+  const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
+  return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
+}
+
+// certain points: label + exact best; others: queued with their candidates
+__global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
+                                   uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
+                                   const float* xnorm, const unsigned long long* cmax_bits, int64_t* labels,
+                                   double* best, uint32_t* amb, unsigned long long* namb, uint32_t* full,
+                                   unsigned long long* nfull) {
+  const double cn = __longlong_as_double((long long)*cmax_bits);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float* s = top_s + i * 4;
+    const int* ix = top_i + i * 4;
+    const double T = tc_threshold((double)xnorm[i], cn, d);
+    const double s0 = s[0];
+    if (k == 1 || (double)s[1] - s0 > T) {
+      const int lab = ix[0];
+      const float* xr = X + i * d;
+      const double* cr = C + (uint64_t)lab * d;
+      labels[i] = lab;
+      best[i] = exact_dist(plan, [&](int j) {
+        const double df = __dsub_rn((double)xr[j], cr[j]);
+        return __dmul_rn(df, df);
+      });
+    } else if (k > 4 && (double)s[3] - s0 <= T) {
+      full[atomicAdd(nfull, 1ull)] = (uint32_t)i;  // more than four candidates
+    } else {
+      amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
+    }
+  }
+}
+
+// exact numpy distances over the (<= 4) screen candidates; ties -> lower index
+__global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const double* __restrict__ C, uint64_t k,
+                                  const PwPlan plan, const float* top_s, const int* top_i, const float* xnorm,
+                                  const unsigned long long* cmax_bits, const uint32_t* amb, uint64_t na,
+                                  int64_t* labels, double* best) {
+  const double cn = __longlong_as_double((long long)*cmax_bits);
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < na; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = amb[q];
+    const float* s = top_s + i * 4;
+    const int* ix = top_i + i * 4;
+    const double T = tc_threshold((double)xnorm[i], cn, d);
+    const float* xr = X + i * d;
+    double bd = 0.0;
+    int64_t bl = -1;
+    for (int a = 0; a < 4 && (uint64_t)a < k; ++a) {
+      if ((double)s[a] - (double)s[0] > T || ix[a] < 0) break;
+      const double* cr = C + (uint64_t)ix[a] * d;
+      const double dist = exact_dist(plan, [&](int j) {
+        const double df = __dsub_rn((double)xr[j], cr[j]);
+        return __dmul_rn(df, df);
+      });
+      if (bl < 0 || dist < bd || (dist == bd && ix[a] < bl)) {
+        bd = dist;
+        bl = ix[a];
+      }
+    }
+    labels[i] = bl;
+    best[i] = bd;
+  }
+}
+
 }  // namespace geek
 
 using namespace geek;
@@ -410,6 +497,44 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                          (int)smem));
     GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
+  }
+  if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull && !getenv("GEEK_NO_TC")) {
+    // tensor-core TF32x3 screen -> classification -> candidate / full recheck
+    Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt;
+    GEEK_TRY(cnt.alloc(32, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 32, s));
+    unsigned long long* cmax = cnt.as<unsigned long long>();
+    unsigned long long* namb = cmax + 1;
+    unsigned long long* nfull = cmax + 2;
+    int nct = 0;
+    GEEK_TRY(tc_screen_prepare(C, k, d, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, s));
+    GEEK_TRY(ts.alloc(n * 16, s));
+    GEEK_TRY(ti.alloc(n * 16, s));
+    GEEK_TRY(xn.alloc(n * 4, s));
+    GEEK_TRY(amb.alloc(n * 4, s));
+    GEEK_TRY(full.alloc(n * 4, s));
+    GEEK_TRY(tc_screen_launch((const float*)X, n, d, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
+                              ti.as<int>(), xn.as<float>(), s));
+    tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>((const float*)X, n, d, C, k, plan, ts.as<float>(),
+                                                                 ti.as<int>(), xn.as<float>(), cmax, labels, best,
+                                                                 amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+    GEEK_CHECK_LAUNCH();
+    unsigned long long cnts[2];
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(cnts, namb, 16, cudaMemcpyDeviceToHost, s));
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+    last_ambiguous() = cnts[0] + cnts[1];
+    if (cnts[0]) {
+      tc_recheck_kernel<<<grid_for(cnts[0], 128), 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(),
+                                                               ti.as<int>(), xn.as<float>(), cmax, amb.as<uint32_t>(),
+                                                               cnts[0], labels, best);
+      GEEK_CHECK_LAUNCH();
+    }
+    if (cnts[1]) {
+      assign_l2_kernel<float><<<(unsigned)((cnts[1] + kAsgThreads - 1) / kAsgThreads), kAsgThreads, smem, s>>>(
+          (const float*)X, cnts[1], d, C, k, plan, labels, best, full.as<uint32_t>());
+      GEEK_CHECK_LAUNCH();
+    }
+    return GEEK_OK;
   }
   const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
   const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;

@@ -1,0 +1,516 @@
+// K8 on the 5th-gen tensor cores: the assignment screen s(x, c) = |c'|^2 -
+// 2 x'.c' (x' = x - mu, c' = c - mu) as a tcgen05 TF32x3 GEMM
+// (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM) with a fused top-4
+// epilogue, followed by the exact float64 distance to the winner.
+//
+// Per CTA (persistent over 128-point tiles):
+//   A  = the point tile, hi/lo TF32 split, K-major, resident in SMEM (128 KB)
+//   B  = center tiles of 128 centers, streamed in 32-dim chunks by 1-D bulk
+//        TMA (cp.async.bulk) into a 3-stage SMEM ring (32 KB per stage)
+//   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
+//        of center tile j (tcgen05.ld, one TMEM lane = one point per thread)
+//        overlaps the MMAs of tile j+1
+// One elected thread issues the copies and the MMAs; all 4 warps run the
+// epilogue.  Operands use the SWIZZLE_NONE K-major canonical layout: 8-row x
+// 16-byte core matrices, LBO between K-adjacent, SBO between M/N-adjacent
+// core matrices.
+#include "common.cuh"
+
+#include <cstring>
+
+namespace geek {
+
+constexpr int kTcM = 128;           // points per tile (TMEM lanes)
+constexpr int kTcN = 128;            // centers per tile
+constexpr int kTcKmax = 128;         // padded dimension (<= 128)
+constexpr int kTcChunk = 32;         // dims per B stage
+constexpr int kTcStages = 3;
+constexpr int kTcSliceBytes = kTcM * 8 * 4;                  // one K=8 tf32 slice of 128 rows: 4 KB
+constexpr int kTcStageBytes = 2 * (kTcChunk / 8) * kTcSliceBytes;  // hi + lo: 32 KB
+constexpr int kTcABytes = 2 * (kTcKmax / 8) * kTcSliceBytes;       // hi + lo: 128 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of element (row r, k e) inside one K=8 slice of a 128-row operand
+__device__ __forceinline__ uint32_t core_off(int r, int e, uint32_t lbo, uint32_t sbo) {
+  return (r >> 3) * sbo + (e >> 2) * lbo + (r & 7) * 16 + (e & 3) * 4;
+}
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+// kind::tf32, D=f32, A=B=tf32, K-major both, N>>3 at [17,23), M>>4 at [24,29)
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct Top4 {
+  float s[4];
+  int i[4];
+  __device__ void init() {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      s[a] = INFINITY;
+      i[a] = -1;
+    }
+  }
+  __device__ __forceinline__ void push(float v, int c) {
+    if (!(v < s[3])) return;
+    if (v < s[1]) {
+      s[3] = s[2];
+      i[3] = i[2];
+      s[2] = s[1];
+      i[2] = i[1];
+      if (v < s[0]) {
+        s[1] = s[0];
+        i[1] = i[0];
+        s[0] = v;
+        i[0] = c;
+      } else {
+        s[1] = v;
+        i[1] = c;
+      }
+    } else if (v < s[2]) {
+      s[3] = s[2];
+      i[3] = i[2];
+      s[2] = v;
+      i[2] = c;
+    } else {
+      s[3] = v;
+      i[3] = c;
+    }
+  }
+};
+
+struct TcParams {
+  const float* X;       // [n][d] float32
+  uint64_t n;
+  int d;
+  const float* Bimg;    // center operand image: [nct][4 chunks][32 KB]
+  const float* c2;      // [nct*128] |c'|^2 (float, +inf for padding)
+  const float* mu;      // [d]
+  uint64_t k;
+  int nct;
+  uint32_t lbo, sbo;
+  float* top_s;         // [n][4]
+  int* top_i;           // [n][4]
+  float* xnorm;         // [n] |x'| upper bound
+};
+
+__global__ void __launch_bounds__(128, 1) tc_screen_kernel(const TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* A = smem;                                   // hi: 64 KB, lo: 64 KB
+  uint8_t* B = smem + kTcABytes;                       // 3 stages x 32 KB
+  float* c2s = reinterpret_cast<float*>(B + kTcStages * kTcStageBytes);  // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(c2s + kTcN);  // full[3], empty[3], acc[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 3;
+  uint64_t* accb = bars + 6;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < 8; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = make_idesc(kTcM, kTcN);
+  const int nchunks_k = (P.d + kTcChunk - 1) / kTcChunk;  // chunks per center tile
+  const int kslices = nchunks_k * (kTcChunk / 8);
+  const int total_q = P.nct * nchunks_k;
+  const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
+  // pipeline counters persist across point tiles (barrier phases keep advancing)
+  uint32_t q_issue = 0;   // next chunk index (global count) to be loaded
+  uint32_t q_mma = 0;     // next chunk index (global count) to be consumed
+  uint32_t acc_phase[2] = {0, 0};
+
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t p0 = tile * kTcM;
+    // ---- A: x' = x - mu, split into tf32 hi/lo, canonical K-major layout ----
+    {
+      const uint64_t i = p0 + tid;
+      const bool valid = i < P.n;
+      double xn2 = 0.0;
+      for (int e0 = 0; e0 < kslices * 8; e0 += 4) {
+        float v[4];
+        if (valid && e0 + 3 < P.d && (P.d & 3) == 0) {
+          const float4 q = *reinterpret_cast<const float4*>(P.X + i * P.d + e0);
+          v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] : 0.f;
+        }
+        float hi4[4], lo4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float xv = (e0 + u < P.d && valid) ? v[u] - P.mu[e0 + u] : 0.f;
+          xn2 = fma((double)xv, (double)xv, xn2);
+          hi4[u] = tf32_round(xv);
+          lo4[u] = tf32_round(xv - hi4[u]);
+        }
+        const int sl = e0 >> 3, e = e0 & 7;
+        const uint32_t off = sl * kTcSliceBytes + core_off(tid, e, P.lbo, P.sbo);
+        *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
+        *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+      }
+      if (valid) P.xnorm[i] = (float)(sqrt(xn2) * (1.0 + 1e-6));
+    }
+    fence_proxy_async();
+    __syncthreads();
+    Top4 top;
+    top.init();
+    // prologue: two chunks in flight; chunk q+2 is loaded into the stage of
+    // chunk q-1 right after the MMAs of chunk q are queued behind q-1's
+    if (tid == 0) {
+      while (q_issue < q_mma + kTcStages - 1 && q_issue - q_mma < (uint32_t)total_q) {
+        const uint32_t s = q_issue % kTcStages;
+        if (q_issue >= kTcStages) mbar_wait(&empty[s], ((q_issue / kTcStages) - 1) & 1);
+        const uint32_t local = (q_issue - q_mma);  // chunk index within this tile's sequence
+        mbar_expect_tx(&full[s], kTcStageBytes);
+        bulk_g2s(B + s * kTcStageBytes, reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)local * kTcStageBytes,
+                 kTcStageBytes, &full[s]);
+        ++q_issue;
+      }
+    }
+    const uint32_t qbase = q_mma;  // chunk q of this tile = qbase + local index
+    for (int ct = 0; ct <= P.nct; ++ct) {
+      if (ct < P.nct) {
+        if (tid == 0) {
+          const uint32_t dt = tmem + (ct & 1) * kTcN;
+          for (int kc = 0; kc < nchunks_k; ++kc) {
+            const uint32_t q = q_mma;
+            const uint32_t s = q % kTcStages;
+            mbar_wait(&full[s], (q / kTcStages) & 1);
+            fence_after();
+            const uint32_t bb = smem_u32(B + s * kTcStageBytes);
+            const uint32_t ab = smem_u32(A);
+#pragma unroll
+            for (int j = 0; j < kTcChunk / 8; ++j) {
+              const int ks = kc * (kTcChunk / 8) + j;
+              const uint64_t ahi = make_sdesc(ab + ks * kTcSliceBytes, P.lbo, P.sbo);
+              const uint64_t alo = make_sdesc(ab + kTcABytes / 2 + ks * kTcSliceBytes, P.lbo, P.sbo);
+              const uint64_t bhi = make_sdesc(bb + j * kTcSliceBytes, P.lbo, P.sbo);
+              const uint64_t blo = make_sdesc(bb + kTcStageBytes / 2 + j * kTcSliceBytes, P.lbo, P.sbo);
+              tc_mma(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
+              tc_mma(dt, ahi, blo, idesc, 1u);
+              tc_mma(dt, alo, bhi, idesc, 1u);
+            }
+            tc_commit(&empty[s]);
+            if (kc == nchunks_k - 1) tc_commit(&accb[ct & 1]);
+            ++q_mma;
+            // refill the stage consumed one chunk ago (its MMAs are queued ahead)
+            const uint32_t local_next = q_issue - qbase;
+            if (local_next < (uint32_t)total_q) {
+              const uint32_t s2 = q_issue % kTcStages;
+              if (q_issue >= kTcStages) mbar_wait(&empty[s2], ((q_issue / kTcStages) - 1) & 1);
+              mbar_expect_tx(&full[s2], kTcStageBytes);
+              bulk_g2s(B + s2 * kTcStageBytes,
+                       reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)local_next * kTcStageBytes,
+                       kTcStageBytes, &full[s2]);
+              ++q_issue;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (ct >= 1) {  // epilogue of center tile ct-1 (overlaps the MMAs of tile ct)
+        const int pt = ct - 1;
+        const int buf = pt & 1;
+        c2s[tid] = P.c2[(uint64_t)pt * kTcN + tid];
+        mbar_wait(&accb[buf], acc_phase[buf]);
+        acc_phase[buf] ^= 1;
+        fence_after();
+        __syncthreads();  // c2s visible
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kTcN; c0 += 32) {
+          float v[32];
+          tc_ld32(trow + c0, v);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int c = pt * kTcN + c0 + u;
+            top.push(c2s[c0 + u] - 2.f * v[u], c);
+          }
+        }
+        fence_before();
+        __syncthreads();  // accumulator buffer free; c2s reusable
+      }
+    }
+    const uint64_t i = p0 + tid;
+    if (i < P.n) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        P.top_s[i * 4 + a] = top.s[a];
+        P.top_i[i * 4 + a] = top.i[a];
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// ---- center operand image ------------------------------------------------
+
+__global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint64_t c = 0; c < k; ++c) s += C[c * d + j];
+    mu[j] = (float)(s / (double)k);
+  }
+}
+
+// Bimg[ct][kc] = { hi[128 centers][32 dims], lo[...] } in the canonical layout
+__global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, uint32_t lbo,
+                                    uint32_t sbo, float* Bimg, float* c2, unsigned long long* cmax_bits) {
+  const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
+  const uint64_t total = (uint64_t)nct * kTcN;
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const int ct = (int)(c / kTcN), r = (int)(c % kTcN);
+    double n2 = 0.0;
+    for (int kc = 0; kc < nchunks_k; ++kc) {
+      uint8_t* img = reinterpret_cast<uint8_t*>(Bimg) + ((uint64_t)ct * nchunks_k + kc) * kTcStageBytes;
+      for (int e = 0; e < kTcChunk; ++e) {
+        const int j = kc * kTcChunk + e;
+        float cv = 0.f;
+        if (c < k && j < d) {
+          const double dv = C[c * d + j] - (double)mu[j];
+          cv = (float)dv;
+          n2 = fma((double)cv, (double)cv, n2);
+        }
+        const float hi = tf32_round(cv);
+        const float lo = tf32_round(cv - hi);
+        const uint32_t off = (e >> 3) * kTcSliceBytes + core_off(r, e & 7, lbo, sbo);
+        *reinterpret_cast<float*>(img + off) = hi;
+        *reinterpret_cast<float*>(img + kTcStageBytes / 2 + off) = lo;
+      }
+    }
+    c2[c] = c < k ? (float)n2 : INFINITY;
+    if (c < k) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(n2) * (1.0 + 1e-6)));
+  }
+}
+
+}  // namespace geek
+
+// internal entry used by assign.cu
+namespace geek {
+
+__global__ void selftest_fill(float* X, uint64_t n, int d, double* C, uint64_t k, float offset) {
+  const uint64_t tot = n * d + k * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < tot; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t z = e * 0x9E3779B97F4A7C15ull + 12345;
+    z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 29;
+    const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+    if (e < n * d) X[e] = (float)(u * 3.0 + offset);
+    else C[e - n * d] = u * 3.0 + offset;
+  }
+}
+
+// reference: exact f64 S for the screen's chosen index and the true argmin
+__global__ void selftest_check(const float* X, uint64_t n, int d, const double* C, uint64_t k, const float* mu,
+                               const float* top_s, const int* top_i, const float* xnorm,
+                               const unsigned long long* cmax_bits, double* worst, unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    double best = INFINITY;
+    int bi = -1;
+    double at_idx = 0;
+    for (uint64_t c = 0; c < k; ++c) {
+      double cc = 0, xc = 0;
+      for (int j = 0; j < d; ++j) {
+        const double cv = (double)(float)(C[c * d + j] - (double)mu[j]);
+        const double xv = (double)(X[i * d + j] - mu[j]);
+        cc += cv * cv;
+        xc += xv * cv;
+      }
+      const double S = cc - 2.0 * xc;
+      if (S < best) {
+        best = S;
+        bi = (int)c;
+      }
+      if ((int)c == top_i[i * 4]) at_idx = S;
+    }
+    const double scale = (double)xnorm[i] * __longlong_as_double((long long)*cmax_bits) + 1e-30;
+    const double err = fabs((double)top_s[i * 4] - at_idx) / scale;
+    atomicMax(reinterpret_cast<unsigned long long*>(worst), (unsigned long long)__double_as_longlong(err));
+    if (bi != top_i[i * 4] && best < at_idx) atomicAdd(bad, 1ull);
+  }
+}
+
+}  // namespace geek
+
+extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, double* out_host) {
+  using namespace geek;
+  cudaStream_t s = 0;
+  const uint64_t n = 1000, k = 300;
+  const int d = 128;
+  Scratch X, C, ts, ti, xn, img, c2, mu, misc;
+  GEEK_TRY(X.alloc(n * d * 4, s));
+  GEEK_TRY(C.alloc(k * d * 8, s));
+  GEEK_TRY(ts.alloc(n * 16, s));
+  GEEK_TRY(ti.alloc(n * 16, s));
+  GEEK_TRY(xn.alloc(n * 4, s));
+  GEEK_TRY(misc.alloc(32, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
+  selftest_fill<<<64, 256, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, 40.f);
+  unsigned long long* cmax = misc.as<unsigned long long>();
+  int nct = 0;
+  GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, lbo, sbo, img, c2, mu, cmax, nct, s));
+  GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(),
+                            xn.as<float>(), s));
+  double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
+  unsigned long long* bad = misc.as<unsigned long long>() + 2;
+  selftest_check<<<8, 128, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, mu.as<float>(), ts.as<float>(),
+                                   ti.as<int>(), xn.as<float>(), cmax, worst, bad);
+  GEEK_CHECK_LAUNCH();
+  unsigned long long h[3];
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(h, misc.ptr, 24, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  double w;
+  memcpy(&w, &h[1], 8);
+  out_host[0] = w;
+  out_host[1] = (double)h[2];
+  return GEEK_OK;
+}
+
+namespace geek {
+
+int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t sbo, Scratch& img, Scratch& c2,
+                      Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s) {
+  nct = (int)((k + kTcN - 1) / kTcN);
+  const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
+  GEEK_TRY(img.alloc((size_t)nct * nchunks_k * kTcStageBytes, s));
+  GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
+  GEEK_TRY(mu.alloc((size_t)d * 4, s));
+  center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
+  GEEK_CHECK_LAUNCH();
+  center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(C, k, d, mu.as<float>(), nct, lbo, sbo,
+                                                                          img.as<float>(), c2.as<float>(), cmax_dev);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+size_t tc_screen_smem() {
+  return (size_t)kTcABytes + kTcStages * kTcStageBytes + kTcN * 4 + 8 * 8 + 16;
+}
+
+int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
+                     uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i, float* xnorm,
+                     cudaStream_t s) {
+  GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
+  TcParams P;
+  P.X = X;
+  P.n = n;
+  P.d = d;
+  P.Bimg = img.as<float>();
+  P.c2 = c2.as<float>();
+  P.mu = mu.as<float>();
+  P.k = k;
+  P.nct = nct;
+  P.lbo = lbo;
+  P.sbo = sbo;
+  P.top_s = top_s;
+  P.top_i = top_i;
+  P.xnorm = xnorm;
+  const size_t smem = tc_screen_smem();
+  GEEK_CHECK_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ntiles = (n + kTcM - 1) / kTcM;
+  const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
+  tc_screen_kernel<<<grid, 128, smem, s>>>(P);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+}  // namespace geek

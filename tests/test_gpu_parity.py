@@ -256,6 +256,16 @@ def test_assign_screened_f32_vs_oracle(d, k, offset):
     assert G._lib.load_library().geek_assign_last_rechecked() >= 50
 
 
+def test_tcgen05_screen_selftest():
+    """The tcgen05 TF32x3 screen agrees with float64 far inside its error bound."""
+    import ctypes
+
+    out = (ctypes.c_double * 2)()
+    assert G._lib.load_library().geek_tc_selftest(128, 256, out) == 0
+    assert out[0] < 1e-5  # bound used by the classifier: ~9e-5 * |x'||c'| at d = 128
+    assert out[1] == 0
+
+
 def test_tie_to_lowest_index():
     c = G.assign(G.DenseData(np.array([[0.0]])),
                  [G.CentralVector("centroid", [v]) for v in (1.0, 2.0, 3.0, -1.0)], "euclidean")
