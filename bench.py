@@ -233,9 +233,7 @@ def main():
         e2e = dict(value=n / (e2e_ms / 1e3), unit="points/s", h2d_bytes_per_step=int(Xh.numel() * 4) * world,
                    d2h_bytes_per_step=int(lab_h.numel() * 8) * world, ms_per_step=round(e2e_ms, 3))
 
-    # ---- roofline of the dominant single-kernel entry point ------------------
-    single = {"geek_project_keys", "geek_assign_l2"}
-    dom = max((k for k in calls if k in single), key=lambda k: calls[k][0], default=None)
+    # ---- roofline of the dominant kernel -------------------------------------
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -243,6 +241,23 @@ def main():
     except OSError:
         pass
     roof = None
+    dom = None
+    if info.get("screen_ms"):
+        # tcgen05 TF32x3 screen: algorithmic work = the n x k x d distance GEMM
+        sec = info["screen_ms"] / 1e3
+        kk = info.get("centers", ngroups)
+        flops = 2.0 * (hi - lo) * kk * P["d"]
+        kpad = -(-kk // 128) * 128
+        roof = dict(kernel="tc_screen_kernel", bound="tensor", achieved=flops / sec / 1e12, unit="TFLOP/s",
+                    peak=peaks.get("bf16_tflops", 1590.0), traffic=None,
+                    peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS; TF32 dense is half of it)",
+                    executed_tf32_tflops=3 * 2.0 * (hi - lo) * kpad * P["d"] / sec / 1e12,
+                    kernel_ms=info["screen_ms"],
+                    note=f"algorithmic flops 2*n*k*d with k={kk}, d={P['d']} per launch; the kernel executes "
+                         f"3 TF32 products (hi*hi, hi*lo, lo*hi) over k padded to {kpad}")
+        roof["frac"] = roof["achieved"] / roof["peak"]
+    elif "geek_project_keys" in calls:
+        dom = "geek_project_keys"
     if dom == "geek_project_keys":
         per = calls[dom][0] / calls[dom][1] / 1e3
         nl = hi - lo

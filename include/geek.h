@@ -183,6 +183,8 @@ int geek_tc_selftest(uint32_t lbo, uint32_t sbo, double* out_host);
 /* number of points the last geek_assign_l2 call re-checked exactly because
  * the float32 screen could not separate their two nearest centers        */
 uint64_t geek_assign_last_rechecked(void);
+/* CUDA-event duration (ms) of the last tensor-core screen kernel launch     */
+double geek_assign_last_screen_ms(void);
 
 /* radii[c] = max best over members (0 if none), sizes[c] = member count
  * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed

@@ -246,6 +246,11 @@ static uint64_t& last_ambiguous() {
   return v;
 }
 
+static double& last_screen_ms() {
+  static double v = 0.0;
+  return v;
+}
+
 constexpr int kScrP = 128, kScrC = 128, kScrK = 16, kScrThreads = 256;
 
 __global__ void center_prep_kernel(const double* C, uint64_t k, int d, float* Cf, float* c2f,
@@ -444,6 +449,60 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
   }
 }
 
+// Same classification with 8 lanes per point for 8 <= d <= 128: lane a owns
+// numpy's accumulator r[a] (elements a, a+8, ...), so row loads are coalesced
+// and the summation order is exactly pw_leaf's.
+__global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
+                                    uint64_t k, const float* top_s, const int* top_i, const float* xnorm,
+                                    const unsigned long long* cmax_bits, int64_t* labels, double* best,
+                                    uint32_t* amb, unsigned long long* namb, uint32_t* full,
+                                    unsigned long long* nfull) {
+  const double cn = __longlong_as_double((long long)*cmax_bits);
+  const unsigned lane = threadIdx.x & 31, a = lane & 7;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
+  const int lim = d - (d % 8);
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; i < n + 0; i += stride) {
+    const float* s = top_s + i * 4;
+    const int* ix = top_i + i * 4;
+    const double T = tc_threshold((double)xnorm[i], cn, d);
+    const double s0 = s[0];
+    const bool certain = k == 1 || (double)s[1] - s0 > T;
+    if (certain) {
+      const int lab = ix[0];
+      const float* xr = X + i * d;
+      const double* cr = C + (uint64_t)lab * d;
+      double r;
+      {
+        const double df = __dsub_rn((double)xr[a], cr[a]);
+        r = __dmul_rn(df, df);
+      }
+      for (int e = 8 + (int)a; e < lim; e += 8) {
+        const double df = __dsub_rn((double)xr[e], cr[e]);
+        r = __dadd_rn(r, __dmul_rn(df, df));
+      }
+      // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7))
+      const double p1 = __dadd_rn(r, __shfl_xor_sync(gmask, r, 1));
+      const double p2 = __dadd_rn(p1, __shfl_xor_sync(gmask, p1, 2));
+      const double p4 = __dadd_rn(p2, __shfl_xor_sync(gmask, p2, 4));
+      if (a == 0) {
+        // lane 0 holds ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)): xor-butterfly adds
+        // (r0+r1), then with (r2+r3), then with the upper half -- same tree
+        double res = p4;
+        for (int e = lim; e < d; ++e) {
+          const double df = __dsub_rn((double)xr[e], cr[e]);
+          res = __dadd_rn(res, __dmul_rn(df, df));
+        }
+        labels[i] = lab;
+        best[i] = __dsqrt_rn(res);
+      }
+    } else if (a == 0) {
+      if (k > 4 && (double)s[3] - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
+      else amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
+    }
+  }
+}
+
 // exact numpy distances over the (<= 4) screen candidates; ties -> lower index
 __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const double* __restrict__ C, uint64_t k,
                                   const PwPlan plan, const float* top_s, const int* top_i, const float* xnorm,
@@ -513,16 +572,32 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_TRY(xn.alloc(n * 4, s));
     GEEK_TRY(amb.alloc(n * 4, s));
     GEEK_TRY(full.alloc(n * 4, s));
+    cudaEvent_t ev0, ev1;
+    GEEK_CHECK_CUDA(cudaEventCreate(&ev0));
+    GEEK_CHECK_CUDA(cudaEventCreate(&ev1));
+    GEEK_CHECK_CUDA(cudaEventRecord(ev0, s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
                               ti.as<int>(), xn.as<float>(), s));
-    tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>((const float*)X, n, d, C, k, plan, ts.as<float>(),
-                                                                 ti.as<int>(), xn.as<float>(), cmax, labels, best,
-                                                                 amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+    GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
+    if (d >= 8)
+      tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), cmax, labels, best,
+          amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+    else
+      tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>((const float*)X, n, d, C, k, plan,
+                                                                   ts.as<float>(), ti.as<int>(), xn.as<float>(),
+                                                                   cmax, labels, best, amb.as<uint32_t>(), namb,
+                                                                   full.as<uint32_t>(), nfull);
     GEEK_CHECK_LAUNCH();
     unsigned long long cnts[2];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(cnts, namb, 16, cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
     last_ambiguous() = cnts[0] + cnts[1];
+    float ms = 0.f;
+    GEEK_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    last_screen_ms() = ms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (cnts[0]) {
       tc_recheck_kernel<<<grid_for(cnts[0], 128), 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(),
                                                                ti.as<int>(), xn.as<float>(), cmax, amb.as<uint32_t>(),
@@ -577,6 +652,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
 }
 
 uint64_t geek_assign_last_rechecked(void) { return last_ambiguous(); }
+
+double geek_assign_last_screen_ms(void) { return last_screen_ms(); }
 
 int geek_radii_sizes(const int64_t* labels, const double* best, uint64_t n, uint64_t k, double* radii,
                      int64_t* sizes, void* stream) {

@@ -304,8 +304,11 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   g.cb = std::min(20, std::max(10, cb));
   g.nc = 1u << g.cb;
   const double per_table = 4.0 * ((double)n / kFineTarget + 2.0 * g.nc) * 5.0;
-  int tb = (int)std::max(1.0, std::min((double)m, (96.0 * (1 << 20)) / per_table));
+  // batches of whole tables: codes rows are then written in tb-word runs
+  // (8 tables = one 32-byte sector), counters stay u32 (tb * n < 2^32)
+  int tb = (int)std::max(1.0, std::min((double)m, (1024.0 * (1 << 20)) / per_table));
   tb = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)tb, 0xFFFFFFF0ull / n));
+  if (tb >= 8 && tb < m) tb -= tb % 8;
   uint64_t acc[4] = {0, 0, 0, 0};
   for (int j0 = 0; j0 < m; j0 += tb) {
     g.j0 = j0;
