@@ -10,8 +10,11 @@
 //   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
 //        of center tile j (tcgen05.ld, one TMEM lane = one point per thread)
 //        overlaps the MMAs of tile j+1
-// One elected thread issues the copies and the MMAs; all 4 warps run the
-// epilogue.  Operands use the SWIZZLE_NONE K-major canonical layout: 8-row x
+// Warp-specialised: lane 0 of warp 4 issues the bulk copies and the MMAs;
+// warps 0-3 (TMEM lanes 32w..32w+31) convert the next point tile into A and
+// run the epilogues; the roles hand off through mbarriers only (stage
+// full/empty, accumulator full/empty, point tile full/empty).
+// Operands use the SWIZZLE_NONE K-major canonical layout: 8-row x
 // 16-byte core matrices, LBO between K-adjacent, SBO between M/N-adjacent
 // core matrices.
 #include "common.cuh"
@@ -177,20 +180,37 @@ struct TcParams {
   float* xnorm;         // [n] |x'| upper bound
 };
 
-__global__ void __launch_bounds__(128, 1) tc_screen_kernel(const TcParams P) {
+constexpr int kTcThreads = 160;  // warps 0-3: A loader + epilogue (warp w <-> TMEM lanes 32w..), warp 4: TMA + MMA
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                   // hi: 64 KB, lo: 64 KB
   uint8_t* B = smem + kTcABytes;                       // 3 stages x 32 KB
-  float* c2s = reinterpret_cast<float*>(B + kTcStages * kTcStageBytes);  // [128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(c2s + kTcN);  // full[3], empty[3], acc[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 3;
-  uint64_t* accb = bars + 6;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(B + kTcStages * kTcStageBytes);
+  uint64_t* full = bars;        // [3] stage loaded (TMA tx)
+  uint64_t* empty = bars + 3;   // [3] stage consumed (MMA commit)
+  uint64_t* accf = bars + 6;    // [2] accumulator ready (MMA commit)
+  uint64_t* acce = bars + 8;    // [2] accumulator drained (128 epilogue threads)
+  uint64_t* afull = bars + 10;  // point tile written (128 threads)
+  uint64_t* aempty = bars + 11; // point tile no longer read (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < 8; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 128);
+    }
+    mbar_init(afull, 128);
+    mbar_init(aempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -201,76 +221,42 @@ __global__ void __launch_bounds__(128, 1) tc_screen_kernel(const TcParams P) {
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = make_idesc(kTcM, kTcN);
-  const int nchunks_k = (P.d + kTcChunk - 1) / kTcChunk;  // chunks per center tile
-  const int kslices = nchunks_k * (kTcChunk / 8);
-  const int total_q = P.nct * nchunks_k;
+  const int nck = (P.d + kTcChunk - 1) / kTcChunk;  // B chunks per center tile
+  const int kslices = nck * (kTcChunk / 8);
+  const uint32_t total_q = (uint32_t)P.nct * nck;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
-  // pipeline counters persist across point tiles (barrier phases keep advancing)
-  uint32_t q_issue = 0;   // next chunk index (global count) to be loaded
-  uint32_t q_mma = 0;     // next chunk index (global count) to be consumed
-  uint32_t acc_phase[2] = {0, 0};
+  const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t p0 = tile * kTcM;
-    // ---- A: x' = x - mu, split into tf32 hi/lo, canonical K-major layout ----
-    {
-      const uint64_t i = p0 + tid;
-      const bool valid = i < P.n;
-      double xn2 = 0.0;
-      for (int e0 = 0; e0 < kslices * 8; e0 += 4) {
-        float v[4];
-        if (valid && e0 + 3 < P.d && (P.d & 3) == 0) {
-          const float4 q = *reinterpret_cast<const float4*>(P.X + i * P.d + e0);
-          v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-        } else {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] : 0.f;
-        }
-        float hi4[4], lo4[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float xv = (e0 + u < P.d && valid) ? v[u] - P.mu[e0 + u] : 0.f;
-          xn2 = fma((double)xv, (double)xv, xn2);
-          hi4[u] = tf32_round(xv);
-          lo4[u] = tf32_round(xv - hi4[u]);
-        }
-        const int sl = e0 >> 3, e = e0 & 7;
-        const uint32_t off = sl * kTcSliceBytes + core_off(tid, e, P.lbo, P.sbo);
-        *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
-        *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
-      }
-      if (valid) P.xnorm[i] = (float)(sqrt(xn2) * (1.0 + 1e-6));
-    }
-    fence_proxy_async();
-    __syncthreads();
-    Top4 top;
-    top.init();
-    // prologue: two chunks in flight; chunk q+2 is loaded into the stage of
-    // chunk q-1 right after the MMAs of chunk q are queued behind q-1's
-    if (tid == 0) {
-      while (q_issue < q_mma + kTcStages - 1 && q_issue - q_mma < (uint32_t)total_q) {
-        const uint32_t s = q_issue % kTcStages;
-        if (q_issue >= kTcStages) mbar_wait(&empty[s], ((q_issue / kTcStages) - 1) & 1);
-        const uint32_t local = (q_issue - q_mma);  // chunk index within this tile's sequence
+  if (warp == 4) {
+    if (lane == 0) {  // ---------------- producer + MMA issuer ----------------
+      const uint32_t idesc = make_idesc(kTcM, kTcN);
+      const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
+      uint64_t q_issue = 0, q_mma = 0;
+      auto issue = [&]() {
+        const uint32_t s = (uint32_t)(q_issue % kTcStages);
+        if (q_issue >= kTcStages) mbar_wait(&empty[s], (uint32_t)((q_issue / kTcStages) - 1) & 1);
         mbar_expect_tx(&full[s], kTcStageBytes);
-        bulk_g2s(B + s * kTcStageBytes, reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)local * kTcStageBytes,
+        bulk_g2s(B + s * kTcStageBytes,
+                 reinterpret_cast<const uint8_t*>(P.Bimg) + (q_issue % total_q) * (uint64_t)kTcStageBytes,
                  kTcStageBytes, &full[s]);
         ++q_issue;
-      }
-    }
-    const uint32_t qbase = q_mma;  // chunk q of this tile = qbase + local index
-    for (int ct = 0; ct <= P.nct; ++ct) {
-      if (ct < P.nct) {
-        if (tid == 0) {
-          const uint32_t dt = tmem + (ct & 1) * kTcN;
-          for (int kc = 0; kc < nchunks_k; ++kc) {
-            const uint32_t q = q_mma;
-            const uint32_t s = q % kTcStages;
-            mbar_wait(&full[s], (q / kTcStages) & 1);
+      };
+      while (q_issue < kTcStages - 1 && q_issue < total_chunks) issue();
+      const uint32_t ab = smem_u32(A);
+      for (uint32_t t = 0; t < my_tiles; ++t) {
+        mbar_wait(afull, t & 1);
+        fence_after();
+        for (int ct = 0; ct < P.nct; ++ct) {
+          const uint64_t g = (uint64_t)t * P.nct + ct;
+          const int buf = (int)(g & 1);
+          mbar_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u);
+          fence_after();
+          const uint32_t dt = tmem + buf * kTcN;
+          for (int kc = 0; kc < nck; ++kc) {
+            const uint32_t s = (uint32_t)(q_mma % kTcStages);
+            mbar_wait(&full[s], (uint32_t)(q_mma / kTcStages) & 1);
             fence_after();
             const uint32_t bb = smem_u32(B + s * kTcStageBytes);
-            const uint32_t ab = smem_u32(A);
 #pragma unroll
             for (int j = 0; j < kTcChunk / 8; ++j) {
               const int ks = kc * (kTcChunk / 8) + j;
@@ -283,54 +269,84 @@ __global__ void __launch_bounds__(128, 1) tc_screen_kernel(const TcParams P) {
               tc_mma(dt, alo, bhi, idesc, 1u);
             }
             tc_commit(&empty[s]);
-            if (kc == nchunks_k - 1) tc_commit(&accb[ct & 1]);
             ++q_mma;
-            // refill the stage consumed one chunk ago (its MMAs are queued ahead)
-            const uint32_t local_next = q_issue - qbase;
-            if (local_next < (uint32_t)total_q) {
-              const uint32_t s2 = q_issue % kTcStages;
-              if (q_issue >= kTcStages) mbar_wait(&empty[s2], ((q_issue / kTcStages) - 1) & 1);
-              mbar_expect_tx(&full[s2], kTcStageBytes);
-              bulk_g2s(B + s2 * kTcStageBytes,
-                       reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)local_next * kTcStageBytes,
-                       kTcStageBytes, &full[s2]);
-              ++q_issue;
-            }
+            if (q_issue < total_chunks) issue();  // into the stage of chunk q_mma-2, queued ahead
           }
+          tc_commit(&accf[buf]);
         }
-        __syncwarp();
+        tc_commit(aempty);
       }
-      if (ct >= 1) {  // epilogue of center tile ct-1 (overlaps the MMAs of tile ct)
-        const int pt = ct - 1;
-        const int buf = pt & 1;
-        c2s[tid] = P.c2[(uint64_t)pt * kTcN + tid];
-        mbar_wait(&accb[buf], acc_phase[buf]);
-        acc_phase[buf] ^= 1;
-        fence_after();
-        __syncthreads();  // c2s visible
-        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN;
+    }
+  } else {  // ---------------- warps 0-3: point tiles + epilogue ----------------
+    Top4 cur, prev;
+    cur.init();
+    auto epilogue = [&](uint32_t t, int ct, Top4& top) {
+      const uint64_t g = (uint64_t)t * P.nct + ct;
+      const int buf = (int)(g & 1);
+      mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
+      fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN;
+      const float* c2t = P.c2 + (uint64_t)ct * kTcN;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kTcN; c0 += 32) {
-          float v[32];
-          tc_ld32(trow + c0, v);
+      for (int c0 = 0; c0 < kTcN; c0 += 32) {
+        float v[32];
+        tc_ld32(trow + c0, v);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int c = pt * kTcN + c0 + u;
-            top.push(c2s[c0 + u] - 2.f * v[u], c);
+        for (int u = 0; u < 32; ++u) top.push(__ldg(c2t + c0 + u) - 2.f * v[u], ct * kTcN + c0 + u);
+      }
+      fence_before();
+      mbar_arrive(&acce[buf]);
+    };
+    auto finish = [&](uint32_t t, Top4& top) {
+      epilogue(t, P.nct - 1, top);
+      const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + tid;
+      if (i < P.n) {
+        *reinterpret_cast<float4*>(P.top_s + i * 4) = make_float4(top.s[0], top.s[1], top.s[2], top.s[3]);
+        *reinterpret_cast<int4*>(P.top_i + i * 4) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
+      }
+    };
+    for (uint32_t t = 0; t < my_tiles; ++t) {
+      const uint64_t p0 = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM;
+      mbar_wait(aempty, (t & 1) ^ 1u);  // MMAs of the previous tile no longer read A
+      // x' = x - mu, tf32 hi/lo; warp w writes rows 32w..32w+31, one row per pass, coalesced
+      for (int r = 0; r < 32; ++r) {
+        const int row = warp * 32 + r;
+        const uint64_t i = p0 + row;
+        const bool valid = i < P.n;
+        double xn2 = 0.0;
+        for (int e0 = lane * 4; e0 < kslices * 8; e0 += 128) {
+          float v[4];
+          if (valid && (P.d & 3) == 0 && e0 + 3 < P.d) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(P.X + i * P.d + e0));
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] : 0.f;
           }
-        }
-        fence_before();
-        __syncthreads();  // accumulator buffer free; c2s reusable
-      }
-    }
-    const uint64_t i = p0 + tid;
-    if (i < P.n) {
+          float hi4[4], lo4[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        P.top_s[i * 4 + a] = top.s[a];
-        P.top_i[i * 4 + a] = top.i[a];
+          for (int u = 0; u < 4; ++u) {
+            const float xv = (valid && e0 + u < P.d) ? v[u] - __ldg(P.mu + e0 + u) : 0.f;
+            xn2 = fma((double)xv, (double)xv, xn2);
+            hi4[u] = tf32_round(xv);
+            lo4[u] = tf32_round(xv - hi4[u]);
+          }
+          const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
+          *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
+          *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
+        if (lane == 0 && valid) P.xnorm[i] = (float)(sqrt(xn2) * (1.0 + 1e-6));
       }
+      fence_proxy_async();
+      mbar_arrive(afull);
+      prev = cur;
+      cur.init();
+      if (t > 0) finish(t - 1, prev);
+      for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
     }
+    if (my_tiles > 0) finish(my_tiles - 1, cur);
   }
   fence_before();
   __syncthreads();
@@ -479,7 +495,7 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t
 }
 
 size_t tc_screen_smem() {
-  return (size_t)kTcABytes + kTcStages * kTcStageBytes + kTcN * 4 + 8 * 8 + 16;
+  return (size_t)kTcABytes + kTcStages * kTcStageBytes + 12 * 8 + 16;
 }
 
 int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
@@ -508,7 +524,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, cons
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t ntiles = (n + kTcM - 1) / kTcM;
   const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
-  tc_screen_kernel<<<grid, 128, smem, s>>>(P);
+  tc_screen_kernel<<<grid, kTcThreads, smem, s>>>(P);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
