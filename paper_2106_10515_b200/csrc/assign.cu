@@ -423,14 +423,21 @@ __device__ __forceinline__ double tc_threshold(double xn, double cn, int d) {
 // certain points: label + exact best; others: queued with their candidates
 __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                    uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
-                                   const float* xnorm, const unsigned long long* cmax_bits, int64_t* labels,
-                                   double* best, uint32_t* amb, unsigned long long* namb, uint32_t* full,
-                                   unsigned long long* nfull) {
+                                   float* xnorm, const float* mu, const unsigned long long* cmax_bits,
+                                   int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb,
+                                   uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const float* s = top_s + i * 4;
     const int* ix = top_i + i * 4;
-    const double T = tc_threshold((double)xnorm[i], cn, d);
+    double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
+    for (int j = 0; j < d; ++j) {
+      const double xv = (double)(X[i * d + j] - mu[j]);
+      xn2 = fma(xv, xv, xn2);
+    }
+    const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
+    xnorm[i] = xn;
+    const double T = tc_threshold((double)xn, cn, d);
     const double s0 = s[0];
     if (k == 1 || (double)s[1] - s0 > T) {
       const int lab = ix[0];
@@ -453,19 +460,29 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
 // numpy's accumulator r[a] (elements a, a+8, ...), so row loads are coalesced
 // and the summation order is exactly pw_leaf's.
 __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
-                                    uint64_t k, const float* top_s, const int* top_i, const float* xnorm,
-                                    const unsigned long long* cmax_bits, int64_t* labels, double* best,
-                                    uint32_t* amb, unsigned long long* namb, uint32_t* full,
+                                    uint64_t k, const float* top_s, const int* top_i, float* xnorm,
+                                    const float* mu, const unsigned long long* cmax_bits, int64_t* labels,
+                                    double* best, uint32_t* amb, unsigned long long* namb, uint32_t* full,
                                     unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   const unsigned lane = threadIdx.x & 31, a = lane & 7;
   const unsigned gmask = 0xFFu << (lane & 24);
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
   const int lim = d - (d % 8);
-  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; i < n + 0; i += stride) {
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; i < n; i += stride) {
     const float* s = top_s + i * 4;
     const int* ix = top_i + i * 4;
-    const double T = tc_threshold((double)xnorm[i], cn, d);
+    double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
+    for (int e = (int)a; e < d; e += 8) {
+      const double xv = (double)(X[i * d + e] - mu[e]);
+      xn2 = fma(xv, xv, xn2);
+    }
+    xn2 += __shfl_xor_sync(gmask, xn2, 1);
+    xn2 += __shfl_xor_sync(gmask, xn2, 2);
+    xn2 += __shfl_xor_sync(gmask, xn2, 4);
+    const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
+    if (a == 0) xnorm[i] = xn;
+    const double T = tc_threshold((double)xn, cn, d);
     const double s0 = s[0];
     const bool certain = k == 1 || (double)s[1] - s0 > T;
     if (certain) {
@@ -581,13 +598,12 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
     if (d >= 8)
       tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), cmax, labels, best,
-          amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax,
+          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     else
-      tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>((const float*)X, n, d, C, k, plan,
-                                                                   ts.as<float>(), ti.as<int>(), xn.as<float>(),
-                                                                   cmax, labels, best, amb.as<uint32_t>(), namb,
-                                                                   full.as<uint32_t>(), nfull);
+      tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
+          (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax,
+          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     GEEK_CHECK_LAUNCH();
     unsigned long long cnts[2];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(cnts, namb, 16, cudaMemcpyDeviceToHost, s));

@@ -308,39 +308,62 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     for (uint32_t t = 0; t < my_tiles; ++t) {
       const uint64_t p0 = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM;
       mbar_wait(aempty, (t & 1) ^ 1u);  // MMAs of the previous tile no longer read A
-      // x' = x - mu, tf32 hi/lo; warp w writes rows 32w..32w+31, one row per pass, coalesced
-      for (int r = 0; r < 32; ++r) {
-        const int row = warp * 32 + r;
-        const uint64_t i = p0 + row;
-        const bool valid = i < P.n;
-        double xn2 = 0.0;
-        for (int e0 = lane * 4; e0 < kslices * 8; e0 += 128) {
-          float v[4];
-          if (valid && (P.d & 3) == 0 && e0 + 3 < P.d) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(P.X + i * P.d + e0));
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-          } else {
+      // x' = x - mu, tf32 hi/lo into the canonical layout; warp w owns rows
+      // 32w..32w+31, lane = float4 column, 8 rows of loads in flight
+      if (P.d == kTcKmax) {
+        const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.mu) + lane);
+        const uint32_t off0 = ((lane * 4) >> 3) * kTcSliceBytes;
+#pragma unroll 1
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          float4 q[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] : 0.f;
+          for (int u = 0; u < 8; ++u) {
+            const uint64_t i = p0 + warp * 32 + r0 + u;
+            q[u] = i < P.n ? __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax) + lane)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          float hi4[4], lo4[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float xv = (valid && e0 + u < P.d) ? v[u] - __ldg(P.mu + e0 + u) : 0.f;
-            xn2 = fma((double)xv, (double)xv, xn2);
-            hi4[u] = tf32_round(xv);
-            lo4[u] = tf32_round(xv - hi4[u]);
+          for (int u = 0; u < 8; ++u) {
+            const int row = warp * 32 + r0 + u;
+            const bool valid = p0 + row < P.n;
+            const float x0 = valid ? q[u].x - m4.x : 0.f, x1 = valid ? q[u].y - m4.y : 0.f;
+            const float x2 = valid ? q[u].z - m4.z : 0.f, x3 = valid ? q[u].w - m4.w : 0.f;
+            const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
+            const uint32_t off = off0 + core_off(row, (lane * 4) & 7, P.lbo, P.sbo);
+            *reinterpret_cast<float4*>(A + off) = make_float4(h0, h1, h2, h3);
+            *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) =
+                make_float4(tf32_round(x0 - h0), tf32_round(x1 - h1), tf32_round(x2 - h2), tf32_round(x3 - h3));
           }
-          const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
-          *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
-          *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
         }
+      } else {
+        for (int r = 0; r < 32; ++r) {
+          const int row = warp * 32 + r;
+          const uint64_t i = p0 + row;
+          const bool valid = i < P.n;
+          for (int e0 = lane * 4; e0 < kslices * 8; e0 += 128) {
+            float hi4[4], lo4[4];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);
-        if (lane == 0 && valid) P.xnorm[i] = (float)(sqrt(xn2) * (1.0 + 1e-6));
+            for (int u = 0; u < 4; ++u) {
+              const float xv = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] - __ldg(P.mu + e0 + u) : 0.f;
+              hi4[u] = tf32_round(xv);
+              lo4[u] = tf32_round(xv - hi4[u]);
+            }
+            const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
+            *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
+            *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+          }
+        }
       }
       fence_proxy_async();
       mbar_arrive(afull);
+      {  // pull the next tile of this CTA towards L2 while the MMAs run
+        const uint64_t pn = p0 + (uint64_t)gridDim.x * kTcM;
+        const uint64_t row = pn + tid;
+        if (row < P.n) {
+          const char* base = reinterpret_cast<const char*>(P.X + row * P.d);
+          for (int b = 0; b < P.d * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
+        }
+      }
       prev = cur;
       cur.init();
       if (t > 0) finish(t - 1, prev);
@@ -434,7 +457,12 @@ __global__ void selftest_check(const float* X, uint64_t n, int d, const double* 
       }
       if ((int)c == top_i[i * 4]) at_idx = S;
     }
-    const double scale = (double)xnorm[i] * __longlong_as_double((long long)*cmax_bits) + 1e-30;
+    double xn2 = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double xv = (double)(X[i * d + j] - mu[j]);
+      xn2 += xv * xv;
+    }
+    const double scale = sqrt(xn2) * __longlong_as_double((long long)*cmax_bits) + 1e-30;
     const double err = fabs((double)top_s[i * 4] - at_idx) / scale;
     atomicMax(reinterpret_cast<unsigned long long*>(worst), (unsigned long long)__double_as_longlong(err));
     if (bi != top_i[i * 4] && best < at_idx) atomicAdd(bad, 1ull);
