@@ -420,6 +420,19 @@ __device__ __forceinline__ double tc_threshold(double xn, double cn, int d) {
   return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
 }
 
+// merged top-4 (ascending) of the screen's two column-half lists
+__device__ __forceinline__ void merge_top8(const float* s8, const int* i8, float* s, int* ix) {
+  int a = 0, b = 4;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const bool ta = b >= 8 || (a < 4 && s8[a] <= s8[b]);
+    s[o] = ta ? s8[a] : s8[b];
+    ix[o] = ta ? i8[a] : i8[b];
+    a += ta;
+    b += !ta;
+  }
+}
+
 // certain points: label + exact best; others: queued with their candidates
 __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                    uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
@@ -428,8 +441,9 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
                                    uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const float* s = top_s + i * 4;
-    const int* ix = top_i + i * 4;
+    float s[4];
+    int ix[4];
+    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
     for (int j = 0; j < d; ++j) {
       const double xv = (double)(X[i * d + j] - mu[j]);
@@ -470,8 +484,9 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
   const int lim = d - (d % 8);
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; i < n; i += stride) {
-    const float* s = top_s + i * 4;
-    const int* ix = top_i + i * 4;
+    float s[4];
+    int ix[4];
+    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
     for (int e = (int)a; e < d; e += 8) {
       const double xv = (double)(X[i * d + e] - mu[e]);
@@ -528,8 +543,9 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const doub
   const double cn = __longlong_as_double((long long)*cmax_bits);
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < na; q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = amb[q];
-    const float* s = top_s + i * 4;
-    const int* ix = top_i + i * 4;
+    float s[4];
+    int ix[4];
+    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
     const double T = tc_threshold((double)xnorm[i], cn, d);
     const float* xr = X + i * d;
     double bd = 0.0;
@@ -584,8 +600,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     unsigned long long* nfull = cmax + 2;
     int nct = 0;
     GEEK_TRY(tc_screen_prepare(C, k, d, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, s));
-    GEEK_TRY(ts.alloc(n * 16, s));
-    GEEK_TRY(ti.alloc(n * 16, s));
+    GEEK_TRY(ts.alloc(n * 32, s));
+    GEEK_TRY(ti.alloc(n * 32, s));
     GEEK_TRY(xn.alloc(n * 4, s));
     GEEK_TRY(amb.alloc(n * 4, s));
     GEEK_TRY(full.alloc(n * 4, s));

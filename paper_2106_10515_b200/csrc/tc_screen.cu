@@ -10,9 +10,10 @@
 //   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
 //        of center tile j (tcgen05.ld, one TMEM lane = one point per thread)
 //        overlaps the MMAs of tile j+1
-// Warp-specialised: lane 0 of warp 4 issues the bulk copies and the MMAs;
-// warps 0-3 (TMEM lanes 32w..32w+31) convert the next point tile into A and
-// run the epilogues; the roles hand off through mbarriers only (stage
+// Warp-specialised: lane 0 of warp 8 issues the bulk copies and the MMAs;
+// warps 0-7 convert the next point tile into A and run the epilogues (warp w
+// reads TMEM lanes 32(w%4).. over column half w/4, keeping its own top-4);
+// the roles hand off through mbarriers only (stage
 // full/empty, accumulator full/empty, point tile full/empty).
 // Operands use the SWIZZLE_NONE K-major canonical layout: 8-row x
 // 16-byte core matrices, LBO between K-adjacent, SBO between M/N-adjacent
@@ -175,12 +176,16 @@ struct TcParams {
   uint64_t k;
   int nct;
   uint32_t lbo, sbo;
-  float* top_s;         // [n][4]
-  int* top_i;           // [n][4]
+  float* top_s;         // [n][8]: top-4 of each accumulator column half
+  int* top_i;           // [n][8]
   float* xnorm;         // [n] |x'| upper bound
 };
 
-constexpr int kTcThreads = 160;  // warps 0-3: A loader + epilogue (warp w <-> TMEM lanes 32w..), warp 4: TMA + MMA
+// warps 0-7: A loader + epilogue (warp w reads TMEM lanes 32(w%4).. and
+// accumulator columns 64(w/4)..+64), warp 8: TMA + MMA issuer
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcEpiThreads = kTcEpiWarps * 32;
+constexpr int kTcThreads = kTcEpiThreads + 32;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -207,9 +212,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 128);
+      mbar_init(&acce[b], kTcEpiThreads);
     }
-    mbar_init(afull, 128);
+    mbar_init(afull, kTcEpiThreads);
     mbar_init(aempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
-  if (warp == 4) {
+  if (warp == kTcEpiWarps) {
     if (lane == 0) {  // ---------------- producer + MMA issuer ----------------
       const uint32_t idesc = make_idesc(kTcM, kTcN);
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
@@ -285,46 +290,61 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const int buf = (int)(g & 1);
       mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
-      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + buf * kTcN;
-      const float* c2t = P.c2 + (uint64_t)ct * kTcN;
+      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
+      const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
+      const float4* c2t = reinterpret_cast<const float4*>(P.c2 + (uint64_t)ct * kTcN + ch * (kTcN / 2));
 #pragma unroll 1
-      for (int c0 = 0; c0 < kTcN; c0 += 32) {
+      for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
         float v[32];
         tc_ld32(trow + c0, v);
+        float mn = INFINITY;
 #pragma unroll
-        for (int u = 0; u < 32; ++u) top.push(__ldg(c2t + c0 + u) - 2.f * v[u], ct * kTcN + c0 + u);
+        for (int u = 0; u < 32; u += 4) {
+          const float4 cc = __ldg(c2t + (c0 + u) / 4);
+          v[u] = cc.x - 2.f * v[u];
+          v[u + 1] = cc.y - 2.f * v[u + 1];
+          v[u + 2] = cc.z - 2.f * v[u + 2];
+          v[u + 3] = cc.w - 2.f * v[u + 3];
+          mn = fminf(mn, fminf(fminf(v[u], v[u + 1]), fminf(v[u + 2], v[u + 3])));
+        }
+        if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
+          const int cbase = ct * kTcN + ch * (kTcN / 2) + c0;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) top.push(v[u], cbase + u);
+        }
       }
       fence_before();
       mbar_arrive(&acce[buf]);
     };
     auto finish = [&](uint32_t t, Top4& top) {
       epilogue(t, P.nct - 1, top);
-      const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + tid;
-      if (i < P.n) {
-        *reinterpret_cast<float4*>(P.top_s + i * 4) = make_float4(top.s[0], top.s[1], top.s[2], top.s[3]);
-        *reinterpret_cast<int4*>(P.top_i + i * 4) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
+      const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + (warp & 3) * 32 + lane;
+      if (i < P.n) {  // two column halves -> [n][8]; the classifier merges them
+        const int h = (warp >> 2) * 4;
+        *reinterpret_cast<float4*>(P.top_s + i * 8 + h) = make_float4(top.s[0], top.s[1], top.s[2], top.s[3]);
+        *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
     for (uint32_t t = 0; t < my_tiles; ++t) {
       const uint64_t p0 = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM;
       mbar_wait(aempty, (t & 1) ^ 1u);  // MMAs of the previous tile no longer read A
       // x' = x - mu, tf32 hi/lo into the canonical layout; warp w owns rows
-      // 32w..32w+31, lane = float4 column, 8 rows of loads in flight
+      // 16w..16w+15, lane = float4 column, 8 rows of loads in flight
       if (P.d == kTcKmax) {
         const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.mu) + lane);
         const uint32_t off0 = ((lane * 4) >> 3) * kTcSliceBytes;
 #pragma unroll 1
-        for (int r0 = 0; r0 < 32; r0 += 8) {
+        for (int r0 = 0; r0 < 16; r0 += 8) {
           float4 q[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const uint64_t i = p0 + warp * 32 + r0 + u;
+            const uint64_t i = p0 + warp * 16 + r0 + u;
             q[u] = i < P.n ? __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax) + lane)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int row = warp * 32 + r0 + u;
+            const int row = warp * 16 + r0 + u;
             const bool valid = p0 + row < P.n;
             const float x0 = valid ? q[u].x - m4.x : 0.f, x1 = valid ? q[u].y - m4.y : 0.f;
             const float x2 = valid ? q[u].z - m4.z : 0.f, x3 = valid ? q[u].w - m4.w : 0.f;
@@ -336,8 +356,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           }
         }
       } else {
-        for (int r = 0; r < 32; ++r) {
-          const int row = warp * 32 + r;
+        for (int r = 0; r < 16; ++r) {
+          const int row = warp * 16 + r;
           const uint64_t i = p0 + row;
           const bool valid = i < P.n;
           for (int e0 = lane * 4; e0 < kslices * 8; e0 += 128) {
@@ -359,7 +379,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       {  // pull the next tile of this CTA towards L2 while the MMAs run
         const uint64_t pn = p0 + (uint64_t)gridDim.x * kTcM;
         const uint64_t row = pn + tid;
-        if (row < P.n) {
+        if (tid < kTcM && row < P.n) {
           const char* base = reinterpret_cast<const char*>(P.X + row * P.d);
           for (int b = 0; b < P.d * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
         }
@@ -442,6 +462,9 @@ __global__ void selftest_check(const float* X, uint64_t n, int d, const double* 
     double best = INFINITY;
     int bi = -1;
     double at_idx = 0;
+    const bool lo_half = top_s[i * 8] <= top_s[i * 8 + 4];
+    const int t1 = lo_half ? top_i[i * 8] : top_i[i * 8 + 4];
+    const float s1 = lo_half ? top_s[i * 8] : top_s[i * 8 + 4];
     for (uint64_t c = 0; c < k; ++c) {
       double cc = 0, xc = 0;
       for (int j = 0; j < d; ++j) {
@@ -455,7 +478,7 @@ __global__ void selftest_check(const float* X, uint64_t n, int d, const double* 
         best = S;
         bi = (int)c;
       }
-      if ((int)c == top_i[i * 4]) at_idx = S;
+      if ((int)c == t1) at_idx = S;
     }
     double xn2 = 0.0;
     for (int j = 0; j < d; ++j) {
@@ -463,9 +486,9 @@ __global__ void selftest_check(const float* X, uint64_t n, int d, const double* 
       xn2 += xv * xv;
     }
     const double scale = sqrt(xn2) * __longlong_as_double((long long)*cmax_bits) + 1e-30;
-    const double err = fabs((double)top_s[i * 4] - at_idx) / scale;
+    const double err = fabs((double)s1 - at_idx) / scale;
     atomicMax(reinterpret_cast<unsigned long long*>(worst), (unsigned long long)__double_as_longlong(err));
-    if (bi != top_i[i * 4] && best < at_idx) atomicAdd(bad, 1ull);
+    if (bi != t1 && best < at_idx) atomicAdd(bad, 1ull);
   }
 }
 
@@ -479,8 +502,8 @@ extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, double* out_host) {
   Scratch X, C, ts, ti, xn, img, c2, mu, misc;
   GEEK_TRY(X.alloc(n * d * 4, s));
   GEEK_TRY(C.alloc(k * d * 8, s));
-  GEEK_TRY(ts.alloc(n * 16, s));
-  GEEK_TRY(ti.alloc(n * 16, s));
+  GEEK_TRY(ts.alloc(n * 32, s));
+  GEEK_TRY(ti.alloc(n * 32, s));
   GEEK_TRY(xn.alloc(n * 4, s));
   GEEK_TRY(misc.alloc(32, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
