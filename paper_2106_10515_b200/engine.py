@@ -189,6 +189,25 @@ class _Timer:
         return self.t
 
 
+def route_tables(keys: torch.Tensor, n: int, comm: _Comm) -> torch.Tensor:
+    """Bucket synchronisation (engine.py:199-238): every rank holds keys
+    [m, n_local] of its contiguous shard; table j goes to rank j % G, which
+    receives [m_own, n] with the shards concatenated in id order."""
+    if not comm.on:
+        return keys
+    m, G, rank = keys.shape[0], comm.G, comm.rank
+    spans = split_data(n, G)
+    mine = [[j for j in range(m) if j % G == q] for q in range(G)]
+    own = mine[rank]
+    send = torch.cat([keys[mine[q]].reshape(-1) for q in range(G)])
+    recv_sizes = [len(own) * (hi - lo) for lo, hi in spans]
+    recv = torch.empty(sum(recv_sizes), dtype=keys.dtype, device=keys.device)
+    dist.all_to_all_single(recv, send, recv_sizes, [len(mine[q]) * keys.shape[1] for q in range(G)])
+    comm.count("BucketShard", (send.numel() - len(own) * keys.shape[1]) * keys.element_size())
+    parts = torch.split(recv, recv_sizes)
+    return torch.cat([pt.view(len(own), hi - lo) for pt, (lo, hi) in zip(parts, spans)], dim=1).contiguous()
+
+
 def _merge_groups(comm: _Comm, local: GroupSet) -> GroupSet:
     if not comm.on:
         return local
@@ -223,19 +242,8 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     with tm.stage("transform"):
         keys = project_keys(X_local, A)  # [m, n_local]
     with tm.stage("sync_buckets"):
-        if comm.on:
-            spans = split_data(n, G)
-            mine = [[j for j in range(m) if j % G == q] for q in range(G)]
-            send = torch.cat([keys[mine[q]].reshape(-1) for q in range(G)])
-            recv_sizes = [len(own) * (hi - lo) for lo, hi in spans]
-            recv = torch.empty(sum(recv_sizes), dtype=keys.dtype, device=keys.device)
-            dist.all_to_all_single(recv, send, [len(mine[q]) * keys.shape[1] for q in range(G)], recv_sizes)
-            comm.count("BucketShard", (send.numel() - len(own) * keys.shape[1]) * 8)
-            parts = torch.split(recv, recv_sizes)
-            keys_own = torch.cat([pt.view(len(own), hi - lo) for pt, (lo, hi) in zip(parts, spans)], dim=1)
-            del keys, send, recv, parts
-        else:
-            keys_own = keys
+        keys_own = route_tables(keys, n, comm)
+        del keys
         stats = {}
         codes = rank_split_codes(keys_own.contiguous(), t, stats) if own else None
         del keys_own

@@ -1,0 +1,59 @@
+"""Multi-GPU parity: run under torchrun with G ranks; the sharded NCCL engine
+must reproduce the golden single-process reference outputs exactly.
+
+    torchrun --standalone --local-addr 127.0.0.1 --nproc-per-node 2 tools/mgpu_check.py
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2106_10515_b200 as G  # noqa: E402
+from oracle import geek_oracle as O  # noqa: E402
+from tests.golden_io import groups as golden_groups, meta, npz  # noqa: E402
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    arr = npz("pipelines")
+    ok = True
+    for name in ("c06", "small", "cfg1"):
+        m = meta()["pipelines"][name]
+        _, n, d, C, sep, seed = m["spec"]
+        X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+        for g in m["runs"]:
+            if int(g) % world:
+                continue
+            cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(int(g)),
+                                   homo=G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]),
+                                   seeding=G.SeedingParams(m["K"], m["L"], min_group_size=m["delta"],
+                                                           seed=m["sseed"]))
+            out = G.run_pipeline(G.DenseData(X), cfg)
+            got = [tuple(x.members.tolist()) for x in out.seed_groups]
+            want = [tuple(x.tolist()) for x in golden_groups(arr, f"{name}_g{g}")]
+            cl = out.clustering
+            good = (got == want and np.array_equal(cl.assignment, arr[f"{name}_g{g}_labels"])
+                    and np.array_equal(cl.radii, arr[f"{name}_g{g}_radii"])
+                    and np.array_equal(np.stack([c.values for c in cl.centers]), arr[f"{name}_g{g}_centers"])
+                    and cl.objective == m["runs"][g]["objective"])
+            ok &= good
+            if rank == 0:
+                print(f"[G={world}] {name} g={g}: {'OK' if good else 'MISMATCH'} groups={len(got)} "
+                      f"bytes={out.transport_bytes}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()
