@@ -82,9 +82,12 @@ int geek_silk_invscan(const uint32_t* codes, uint64_t n, int m, uint64_t t,
 
 /* keys[j*n + i] = order-preserving uint64 image of the float64 projection
  * <x_i, A_j> (transform.py:125, engine.py:180); -0.0 folds onto +0.0 and NaN
- * onto the top key, matching np.lexsort.  dtype 0 = float32 X, 1 = float64.  */
+ * onto the top key, matching np.lexsort.  dtype 0 = float32 X, 1 = float64.
+ * `exprange` (device int[2], may be NULL; caller initialises {INT_MAX-ish,
+ * INT_MIN-ish}) receives atomic min/max of the exact-sum exponent window of
+ * X (as geek_exponent_range), fused into the same pass over X.              */
 int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
-                      uint64_t* keys, void* stream);
+                      uint64_t* keys, int* exprange, void* stream);
 
 /* Exact even rank split of every table (transform.py:95-109, engine.py:219-225):
  * codes[i*m + j] = slot of id i in table j, ties broken by id.  keys are

@@ -11,14 +11,36 @@ constexpr int kProjPts = 2;     // points per thread
 constexpr int kProjTB = 8;      // tables per pass
 constexpr int kProjTile = kProjThreads * kProjPts;
 
+// Bounds of the binary exponent window of a value as the exact-sum kernel
+// decomposes it (v = M * 2^L, |M| < 2^P; numeric.py:19-40): lo <= L, hi >= L + P.
+// Subnormals take the most negative L their format allows.
+__device__ __forceinline__ void exp_window(float v, int& lo, int& hi) {
+  const uint32_t b = __float_as_uint(v);
+  const int e = (b >> 23) & 0xFF;
+  if (e == 0xFF || (b & 0x7FFFFFFFu) == 0) return;
+  const int L = e ? e - 150 : -172;
+  lo = min(lo, L);
+  hi = max(hi, e ? e - 126 : -148);
+}
+
+__device__ __forceinline__ void exp_window(double v, int& lo, int& hi) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+  const int e = (int)((b >> 52) & 0x7FF);
+  if (e == 0x7FF || (b & 0x7FFFFFFFFFFFFFFFull) == 0) return;
+  lo = min(lo, e ? e - 1075 : -1127);
+  hi = max(hi, e ? e - 1022 : -1074);
+}
+
 template <class T>
 __global__ void __launch_bounds__(kProjThreads) project_kernel(const T* __restrict__ X, uint64_t n,
                                                                int d, const double* __restrict__ A,
-                                                               int m, uint64_t* __restrict__ keys) {
+                                                               int m, uint64_t* __restrict__ keys,
+                                                               int* exprange) {
   constexpr int kProjKT = sizeof(T) == 4 ? 32 : 16;  // dims per shared-memory tile (<= 33 KB)
   __shared__ double sA[kProjTB][kProjKT];
   __shared__ T sX[kProjKT][kProjTile + 1];
   const uint64_t tile0 = blockIdx.x * (uint64_t)kProjTile;
+  int elo = 1 << 30, ehi = -(1 << 30);
   for (int j0 = 0; j0 < m; j0 += kProjTB) {
     double acc[kProjPts][kProjTB];
 #pragma unroll
@@ -35,7 +57,9 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const T* __restri
       for (int e = threadIdx.x; e < kProjTile * kProjKT; e += kProjThreads) {
         int pt = e / kProjKT, k = e % kProjKT;
         uint64_t i = tile0 + pt;
-        sX[k][pt] = (i < n && k0 + k < d) ? X[i * d + k0 + k] : T(0);
+        const T v = (i < n && k0 + k < d) ? X[i * d + k0 + k] : T(0);
+        sX[k][pt] = v;
+        if (j0 == 0) exp_window(v, elo, ehi);  // fused exponent window (first table pass)
       }
       __syncthreads();
 #pragma unroll 8
@@ -61,6 +85,16 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const T* __restri
       }
     }
   }
+  if (exprange) {
+    for (int o = 16; o; o >>= 1) {
+      elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+      ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&exprange[0], elo);
+      atomicMax(&exprange[1], ehi);
+    }
+  }
 }
 
 template <class T>
@@ -78,16 +112,16 @@ using namespace geek;
 extern "C" {
 
 int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
-                      uint64_t* keys, void* stream) {
+                      uint64_t* keys, int* exprange, void* stream) {
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 (f32) or 1 (f64)");
   GEEK_REQUIRE(d >= 1 && m >= 1, "empty projection");
   if (n == 0) return GEEK_OK;
   unsigned grid = (unsigned)((n + kProjTile - 1) / kProjTile);
   if (dtype == 0)
-    project_kernel<float><<<grid, kProjThreads, 0, s>>>((const float*)X, n, d, A, m, keys);
+    project_kernel<float><<<grid, kProjThreads, 0, s>>>((const float*)X, n, d, A, m, keys, exprange);
   else
-    project_kernel<double><<<grid, kProjThreads, 0, s>>>((const double*)X, n, d, A, m, keys);
+    project_kernel<double><<<grid, kProjThreads, 0, s>>>((const double*)X, n, d, A, m, keys, exprange);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }

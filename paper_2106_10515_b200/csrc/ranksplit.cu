@@ -32,12 +32,19 @@ struct SplitGeom {
 __device__ __forceinline__ uint32_t coarse_of(uint64_t key, int cb) {
   return static_cast<uint32_t>(key >> (64 - cb));
 }
+#define coarse_of_key coarse_of
 
-__device__ __forceinline__ uint32_t fine_of(uint64_t key, int cb, const uint32_t* nfine,
-                                            const uint32_t* fbase, uint32_t cell) {
-  const uint32_t nf = nfine[cell];
+// cinfo[cell] = (number of fine bins, first fine bin): one 8-byte lookup
+__device__ __forceinline__ uint32_t fine_of(uint64_t key, int cb, const uint2* __restrict__ cinfo) {
+  const uint2 ci = __ldg(cinfo + coarse_of_key(key, cb));
   const uint32_t frac = static_cast<uint32_t>((key << cb) >> 32);
-  return fbase[cell] + static_cast<uint32_t>(((uint64_t)frac * nf) >> 32);
+  return ci.y + static_cast<uint32_t>(((uint64_t)frac * ci.x) >> 32);
+}
+
+__global__ void pack_cinfo_kernel(const uint32_t* nfine, const uint32_t* fbase, uint64_t total, uint2* cinfo) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
+       c += (uint64_t)gridDim.x * blockDim.x)
+    cinfo[c] = make_uint2(nfine[c], fbase[c]);
 }
 
 __global__ void coarse_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g, uint64_t stride,
@@ -61,18 +68,14 @@ __global__ void fine_layout_kernel(const uint32_t* hist, uint64_t total, uint64_
   }
 }
 
-__global__ void fine_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
-                                 const uint32_t* __restrict__ nfine, const uint32_t* __restrict__ fbase,
+__global__ void fine_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g, const uint2* __restrict__ cinfo,
                                  uint32_t* fcnt) {
   const int jb = blockIdx.y;
   const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
-  const uint32_t* nf = nfine + (uint64_t)jb * g.nc;
-  const uint32_t* fb = fbase + (uint64_t)jb * g.nc;
+  const uint2* ci = cinfo + (uint64_t)jb * g.nc;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = kj[i];
-    atomicAdd(&fcnt[fine_of(key, g.cb, nf, fb, coarse_of(key, g.cb))], 1u);
-  }
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&fcnt[fine_of(kj[i], g.cb, ci)], 1u);
 }
 
 __device__ __forceinline__ int table_of_fine(const uint32_t* tb_first, int tb, uint32_t f) {
@@ -82,33 +85,35 @@ __device__ __forceinline__ int table_of_fine(const uint32_t* tb_first, int tb, u
 }
 
 // per fine bin: rank start within its table, straddle size (0 if inside one bucket)
+// fcode[f] = the slot of every id of bin f, or GEEK_NONE when f straddles a boundary
 __global__ void straddle_kernel(SplitGeom g, const uint32_t* fcnt, const uint32_t* fstart,
-                                const uint32_t* tb_first, uint32_t nfbins, uint32_t* scnt,
+                                const uint32_t* tb_first, uint32_t nfbins, uint32_t* scnt, uint32_t* fcode,
                                 unsigned long long* stats) {
   for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nfbins;
        f += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = fcnt[f];
-    uint32_t s = 0;
-    if (c > 1) {
+    uint32_t s = 0, code = 0;
+    if (c > 0) {
       const int jb = table_of_fine(tb_first, g.tb, (uint32_t)f);
       const uint64_t r0 = (uint64_t)fstart[f] - (uint64_t)jb * g.n;
-      if (slot_of_rank(r0, g.n, g.t) != slot_of_rank(r0 + c - 1, g.n, g.t)) {
+      code = slot_of_rank(r0, g.n, g.t);
+      if (c > 1 && code != slot_of_rank(r0 + c - 1, g.n, g.t)) {
         s = c;
+        code = GEEK_NONE;
         atomicAdd(&stats[0], (unsigned long long)c);
         atomicMax(&stats[1], (unsigned long long)c);
         if (c > kLocalRankMax) atomicAdd(&stats[2], (unsigned long long)c);
       }
     }
     scnt[f] = s;
+    fcode[f] = code;
   }
 }
 
 // slot codes for ids in non-straddling bins; straddling ids are staged
 __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
-                                                    const uint32_t* __restrict__ nfine,
-                                                    const uint32_t* __restrict__ fbase,
-                                                    const uint32_t* __restrict__ fstart,
-                                                    const uint32_t* __restrict__ scnt,
+                                                    const uint2* __restrict__ cinfo,
+                                                    const uint32_t* __restrict__ fcode,
                                                     const uint32_t* __restrict__ sbase,
                                                     uint32_t* sfill, uint32_t* codes,
                                                     uint64_t* st_key, uint32_t* st_id,
@@ -118,11 +123,10 @@ __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__
     uint32_t* crow = codes + i * (uint64_t)g.m + g.c0;
     for (int jb = 0; jb < g.tb; ++jb) {
       const uint64_t key = keys[(uint64_t)(g.j0 + jb) * g.n + i];
-      const uint32_t cell = coarse_of(key, g.cb);
-      const uint32_t f = fine_of(key, g.cb, nfine + (uint64_t)jb * g.nc, fbase + (uint64_t)jb * g.nc,
-                                 cell);
-      if (scnt[f] == 0) {
-        crow[jb] = slot_of_rank((uint64_t)fstart[f] - (uint64_t)jb * g.n, g.n, g.t);
+      const uint32_t f = fine_of(key, g.cb, cinfo + (uint64_t)jb * g.nc);
+      const uint32_t code = __ldg(fcode + f);
+      if (code != GEEK_NONE) {
+        crow[jb] = code;
       } else {
         const uint32_t pos = sbase[f] + atomicAdd(&sfill[f], 1u);
         st_key[pos] = key;
@@ -203,7 +207,8 @@ __global__ void big_rank_kernel(SplitGeom g, const uint32_t* rows, const uint32_
 static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, uint64_t* stats_acc,
                             cudaStream_t s) {
   const uint64_t ncell = (uint64_t)g.tb * g.nc;
-  const uint64_t stride = g.n >= (1ull << 22) ? 8 : 1;
+  // ~2M samples per table shape the fine bins; the fine counts are exact anyway
+  const uint64_t stride = g.n > (1ull << 21) ? g.n >> 21 : 1;
   Scratch hist, nfine, fbase;
   GEEK_TRY(hist.alloc(ncell * 4, s));
   GEEK_TRY(nfine.alloc(ncell * 4, s));
@@ -222,7 +227,12 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   for (int jb = 0; jb < g.tb; ++jb)
     GEEK_CHECK_CUDA(cudaMemcpyAsync(&tbf[jb], fbase.as<uint32_t>() + (uint64_t)jb * g.nc, 4,
                                     cudaMemcpyDeviceToHost, s));
-  Scratch fcnt, fstart, scnt, sbase, sfill, tbfirst, stats;
+  Scratch fcnt, fstart, scnt, sbase, sfill, tbfirst, stats, cinfo, fcode;
+  GEEK_TRY(cinfo.alloc(ncell * 8, s));
+  GEEK_TRY(fcode.alloc(nfb * 4, s));
+  pack_cinfo_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(nfine.as<uint32_t>(), fbase.as<uint32_t>(), ncell,
+                                                         cinfo.as<uint2>());
+  GEEK_CHECK_LAUNCH();
   GEEK_TRY(fcnt.alloc(nfb * 4, s));
   GEEK_TRY(fstart.alloc(nfb * 4, s));
   GEEK_TRY(scnt.alloc(nfb * 4, s));
@@ -236,13 +246,12 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   GEEK_CHECK_CUDA(cudaMemsetAsync(sfill.ptr, 0, nfb * 4, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(stats.ptr, 0, 32, s));
   dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
-  fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, nfine.as<uint32_t>(), fbase.as<uint32_t>(),
-                                      fcnt.as<uint32_t>());
+  fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), fcnt.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
   GEEK_TRY(exclusive_scan_u32(fcnt.as<uint32_t>(), fstart.as<uint32_t>(), nfb, s));
   straddle_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
                                                       tbfirst.as<uint32_t>(), (uint32_t)nfb,
-                                                      scnt.as<uint32_t>(),
+                                                      scnt.as<uint32_t>(), fcode.as<uint32_t>(),
                                                       stats.as<unsigned long long>());
   GEEK_CHECK_LAUNCH();
   uint64_t nstage = 0;
@@ -254,9 +263,8 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   GEEK_TRY(sid.alloc(nstage * 4, s));
   GEEK_TRY(sbin.alloc(nstage * 4, s));
   codes_kernel<<<grid_for(g.n, 256, 148 * 16), 256, 0, s>>>(
-      keys, g, nfine.as<uint32_t>(), fbase.as<uint32_t>(), fstart.as<uint32_t>(), scnt.as<uint32_t>(),
-      sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes, skey.as<uint64_t>(), sid.as<uint32_t>(),
-      sbin.as<uint32_t>());
+      keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes,
+      skey.as<uint64_t>(), sid.as<uint32_t>(), sbin.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
   if (nstage) {
     resolve_kernel<<<grid_for(nstage, 256, 148 * 16), 256, 0, s>>>(

@@ -28,6 +28,71 @@ __global__ void emit_members_kernel(const uint32_t* __restrict__ codes, uint64_t
   }
 }
 
+// bit b set when bucket b belongs to at least one bin
+__global__ void binned_bitmap_kernel(const uint32_t* bb_off, uint64_t nb, uint32_t* words) {
+  const uint64_t nw = (nb + 31) / 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int k = 0; k < 32; ++k) {
+      const uint64_t b = w * 32 + k;
+      if (b < nb && bb_off[b + 1] > bb_off[b]) v |= 1u << k;
+    }
+    words[w] = v;
+  }
+}
+
+// One thread per id row: test each table's bucket against the bitmap
+// (shared memory when it fits), count the row's pairs, take a warp-aggregated
+// range of the output, then write.
+__global__ void __launch_bounds__(256) emit_rows_kernel(const uint32_t* __restrict__ codes, uint64_t n, int m,
+                                                        uint64_t t, const uint32_t* __restrict__ bb_off,
+                                                        const uint32_t* __restrict__ bb_bins,
+                                                        const uint32_t* __restrict__ gwords, uint64_t nwords,
+                                                        int smem_words, uint32_t* out_bin, uint32_t* out_id,
+                                                        uint64_t cap, unsigned long long* cursor) {
+  extern __shared__ uint32_t sw[];
+  const bool in_smem = smem_words > 0;
+  if (in_smem)
+    for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) sw[w] = gwords[w];
+  __syncthreads();
+  const uint32_t* words = in_smem ? sw : gwords;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    const uint32_t* row = codes + (valid ? i : 0) * m;
+    uint32_t cnt = 0;
+    if (valid)
+      for (int j = 0; j < m; ++j) {
+        const uint64_t b = (uint64_t)j * t + row[j];
+        if ((words[b >> 5] >> (b & 31)) & 1u) cnt += bb_off[b + 1] - bb_off[b];
+      }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    unsigned long long wbase = 0;
+    if (lane == 31) wbase = atomicAdd(cursor, (unsigned long long)total);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    unsigned long long pos = wbase + incl - cnt;
+    if (cnt)
+      for (int j = 0; j < m; ++j) {
+        const uint64_t b = (uint64_t)j * t + row[j];
+        if ((words[b >> 5] >> (b & 31)) & 1u)
+          for (uint32_t k = bb_off[b]; k < bb_off[b + 1]; ++k, ++pos)
+            if (pos < cap) {
+              out_bin[pos] = bb_bins[k];
+              out_id[pos] = static_cast<uint32_t>(i);
+            }
+      }
+  }
+}
+
 __global__ void gather_u32(const uint32_t* src, const uint32_t* perm, uint32_t* dst, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -154,12 +219,21 @@ int geek_emit_members_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t
                             const uint32_t* bb_bins, uint32_t* out_bin, uint32_t* out_id, uint64_t cap,
                             uint64_t* count_host, void* stream) {
   cudaStream_t s = as_stream(stream);
-  Scratch cur;
+  Scratch cur, bm;
   GEEK_TRY(cur.alloc(8, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(cur.ptr, 0, 8, s));
   if (n) {
-    emit_members_kernel<<<grid_for(n * (uint64_t)m, 256, 148 * 16), 256, 0, s>>>(
-        codes, n, m, t, bb_off, bb_bins, out_bin, out_id, cap, cur.as<unsigned long long>());
+    const uint64_t nb = (uint64_t)m * t, nw = (nb + 31) / 32;
+    GEEK_TRY(bm.alloc(nw * 4, s));
+    binned_bitmap_kernel<<<grid_for(nw, 256), 256, 0, s>>>(bb_off, nb, bm.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    const int smem_words = nw * 4 <= 96 * 1024 ? (int)nw : 0;
+    if (smem_words * 4 > 48 * 1024)
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(emit_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem_words * 4));
+    emit_rows_kernel<<<grid_for(n, 256, 148 * 8), 256, smem_words * 4, s>>>(
+        codes, n, m, t, bb_off, bb_bins, bm.as<uint32_t>(), nw, smem_words, out_bin, out_id, cap,
+        cur.as<unsigned long long>());
     GEEK_CHECK_LAUNCH();
   }
   unsigned long long c = 0;

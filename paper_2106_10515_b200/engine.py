@@ -240,7 +240,8 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     A = p.direction_matrix(d)
     own = [j for j in range(m) if j % G == rank]
     with tm.stage("transform"):
-        keys = project_keys(X_local, A)  # [m, n_local]
+        exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=X_local.device)
+        keys = project_keys(X_local, A, exprange)  # [m, n_local]; exponent window fused
     with tm.stage("sync_buckets"):
         keys_own = route_tables(keys, n, comm)
         del keys
@@ -260,11 +261,9 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         if groups.count == 0:
             groups = _fallback_groups(n, g, config.fallback_seed, warnings)
     with tm.stage("centers"):
-        emin, emax = exponent_range(X_local)
-        if comm.on:
-            r = torch.tensor([-emin, emax], dtype=torch.int64, device=X_local.device)
-            comm.all_reduce(r, dist.ReduceOp.MAX, "LocalCenters")
-            emin, emax = -int(r[0].item()), int(r[1].item())
+        r = torch.stack([-exprange[0], exprange[1]]).to(torch.int64)
+        comm.all_reduce(r, dist.ReduceOp.MAX, "LocalCenters")
+        emin, emax = -int(r[0].item()), int(r[1].item())
         nd = digit_count(emin, emax)
         digits = partial_sums(X_local, groups, emin, nd, row_lo)
         comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")

@@ -93,14 +93,16 @@ def even_partition_sizes(n: int, parts: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # dense
 
-def project_keys(X: torch.Tensor, A: np.ndarray) -> torch.Tensor:
-    """[m, n] order-preserving uint64 keys (int64 storage) of X @ A.T in float64."""
+def project_keys(X: torch.Tensor, A: np.ndarray, exprange: torch.Tensor = None) -> torch.Tensor:
+    """[m, n] order-preserving uint64 keys (int64 storage) of X @ A.T in float64.
+    `exprange` (int32[2] on the device, preset to (2^30, -2^30)) receives the
+    exact-sum exponent window of X from the same pass."""
     n, d = X.shape
     m = A.shape[0]
     keys = _lib.empty(max(1, m * n), torch.int64)
     Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
     _lib.call("geek_project_keys", _lib.ptr(X), _lib.dtype_code(X), n, d, _lib.ptr(Ad), m, _lib.ptr(keys),
-              _lib.stream())
+              _lib.ptr(exprange), _lib.stream())
     return keys[: m * n].view(m, n) if n else keys[:0].view(m, 0)
 
 
