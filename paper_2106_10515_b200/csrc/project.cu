@@ -97,6 +97,93 @@ __global__ void __launch_bounds__(kProjThreads) project_kernel(const T* __restri
   }
 }
 
+// Register-blocked float64 projection: a block owns 128 points and ALL m
+// tables; thread (pg, tg) accumulates 4 points x 4 tables (16 DFMA per
+// LDS.128 of x and two LDS.128 of directions).  X and A are staged through
+// shared memory in 64-dim chunks, so every X byte is read from HBM once.
+constexpr int kP2Pts = 128, kP2KC = 64;
+
+template <class T>
+__global__ void __launch_bounds__(512) project4x4_kernel(const T* __restrict__ X, uint64_t n, int d,
+                                                          const double* __restrict__ A, int m,
+                                                          uint64_t* __restrict__ keys, int* exprange) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int mg = (m + 3) / 4;                       // table groups
+  double* sA = reinterpret_cast<double*>(smraw);    // [kP2KC][mg*4] (k-major, tables adjacent)
+  float* sX = reinterpret_cast<float*>(sA + kP2KC * mg * 4);  // [kP2KC][kP2Pts + 4] (T = float)
+  double* sXd = reinterpret_cast<double*>(sA + kP2KC * mg * 4);  // (T = double)
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int pg = tid & 31, tg = tid >> 5;           // 32 point groups x mg table groups
+  const uint64_t p0 = blockIdx.x * (uint64_t)kP2Pts;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  int elo = 1 << 30, ehi = -(1 << 30);
+  const int ldx = kP2Pts + 4;
+  for (int k0 = 0; k0 < d; k0 += kP2KC) {
+    const int kc = min(kP2KC, d - k0);
+    __syncthreads();
+    for (int e = tid; e < kP2KC * mg * 4; e += nthr) {
+      const int k = e / (mg * 4), j = e - k * (mg * 4);
+      sA[e] = (k < kc && j < m) ? A[(uint64_t)j * d + k0 + k] : 0.0;
+    }
+    for (int e = tid; e < kP2Pts * kP2KC; e += nthr) {
+      const int p = e / kP2KC, k = e - p * kP2KC;  // consecutive threads: consecutive dims of a row
+      const uint64_t i = p0 + p;
+      const T v = (i < n && k < kc) ? X[i * d + k0 + k] : T(0);
+      exp_window(v, elo, ehi);
+      if (sizeof(T) == 4) sX[k * ldx + p] = (float)v;
+      else sXd[k * ldx + p] = (double)v;
+    }
+    __syncthreads();
+    if (tg < mg) {
+#pragma unroll 4
+      for (int k = 0; k < kc; ++k) {
+        double xv[4];
+        if (sizeof(T) == 4) {
+          const float4 x4 = *reinterpret_cast<const float4*>(sX + k * ldx + pg * 4);
+          xv[0] = x4.x; xv[1] = x4.y; xv[2] = x4.z; xv[3] = x4.w;
+        } else {
+          const double2 xa = *reinterpret_cast<const double2*>(sXd + k * ldx + pg * 4);
+          const double2 xb = *reinterpret_cast<const double2*>(sXd + k * ldx + pg * 4 + 2);
+          xv[0] = xa.x; xv[1] = xa.y; xv[2] = xb.x; xv[3] = xb.y;
+        }
+        const double2 aa = *reinterpret_cast<const double2*>(sA + k * mg * 4 + tg * 4);
+        const double2 ab = *reinterpret_cast<const double2*>(sA + k * mg * 4 + tg * 4 + 2);
+        const double av[4] = {aa.x, aa.y, ab.x, ab.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], av[b], acc[a][b]);
+      }
+    }
+  }
+  if (tg < mg) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = tg * 4 + b;
+      if (j >= m) break;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const uint64_t i = p0 + pg * 4 + a;
+        if (i < n) keys[(uint64_t)j * n + i] = f64_key(acc[a][b]);
+      }
+    }
+  }
+  if (exprange) {
+    for (int o = 16; o; o >>= 1) {
+      elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+      ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+    }
+    if ((tid & 31) == 0) {
+      atomicMin(&exprange[0], elo);
+      atomicMax(&exprange[1], ehi);
+    }
+  }
+}
+
 template <class T>
 __global__ void column_keys_kernel(const T* __restrict__ v, uint64_t n, uint64_t stride, uint64_t col,
                                    uint64_t* __restrict__ keys) {
@@ -117,6 +204,24 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 (f32) or 1 (f64)");
   GEEK_REQUIRE(d >= 1 && m >= 1, "empty projection");
   if (n == 0) return GEEK_OK;
+  const int mg = (m + 3) / 4;
+  if (mg <= 16) {  // register-blocked path: 32 point groups x mg table groups per block
+    const size_t smem = (size_t)kP2KC * mg * 4 * 8 + (size_t)kP2KC * (kP2Pts + 4) * (dtype == 0 ? 4 : 8);
+    const unsigned grid = (unsigned)((n + kP2Pts - 1) / kP2Pts);
+    if (dtype == 0) {
+      if (smem > 48 * 1024)
+        GEEK_CHECK_CUDA(cudaFuncSetAttribute(project4x4_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+      project4x4_kernel<float><<<grid, 32 * mg, smem, s>>>((const float*)X, n, d, A, m, keys, exprange);
+    } else {
+      if (smem > 48 * 1024)
+        GEEK_CHECK_CUDA(cudaFuncSetAttribute(project4x4_kernel<double>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      project4x4_kernel<double><<<grid, 32 * mg, smem, s>>>((const double*)X, n, d, A, m, keys, exprange);
+    }
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
   unsigned grid = (unsigned)((n + kProjTile - 1) / kProjTile);
   if (dtype == 0)
     project_kernel<float><<<grid, kProjThreads, 0, s>>>((const float*)X, n, d, A, m, keys, exprange);
