@@ -4,6 +4,8 @@
 // block through shared memory; directions stay resident in shared memory.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace geek {
 
 constexpr int kProjThreads = 128;
@@ -184,6 +186,104 @@ __global__ void __launch_bounds__(512) project4x4_kernel(const T* __restrict__ X
   }
 }
 
+// float64 projection on the DMMA tensor path (mma.sync m8n8k4 f64; FP64 on
+// sm_100 has no tcgen05 kind): 4 warps x 32 points per block, each warp holds
+// 4 x NT accumulator fragments (32 points x 8*NT tables); X (as stored) and
+// the directions are staged in 64-dim chunks, X read from HBM once.
+constexpr int kDmLdx = 136;  // 136: fragment loads are bank-conflict free
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <class T, int NT>
+__global__ void __launch_bounds__(128) project_dmma_kernel(const T* __restrict__ X, uint64_t n, int d,
+                                                           const double* __restrict__ A, int m,
+                                                           uint64_t* __restrict__ keys, int* exprange) {
+  constexpr int LDA = NT * 8 + 4;  // tables per k row (+pad)
+  constexpr int kDmKC = sizeof(T) == 4 ? 32 : 16;  // dims per chunk: static smem <= 48 KB
+  __shared__ __align__(16) T sX[kDmKC * kDmLdx];
+  __shared__ __align__(16) double sA[kDmKC * LDA];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t p0 = blockIdx.x * 128ull;
+  double acc[4][NT][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int elo = 1 << 30, ehi = -(1 << 30);
+  for (int k0 = 0; k0 < d; k0 += kDmKC) {
+    const int kc = min(kDmKC, d - k0);
+    __syncthreads();
+    // consecutive threads take consecutive points for one dim: conflict-free stores
+    for (int e = tid; e < 128 * kDmKC; e += 128) {
+      const int k = e >> 7, p = e & 127;  // kDmKC rows of 128 points
+      const uint64_t i = p0 + p;
+      const T v = (i < n && k < kc) ? X[i * d + k0 + k] : T(0);
+      exp_window(v, elo, ehi);
+      sX[k * kDmLdx + p] = v;
+    }
+    for (int e = tid; e < kDmKC * NT * 8; e += 128) {
+      const int k = e / (NT * 8), t = e - k * (NT * 8);
+      sA[k * LDA + t] = (k < kc && t < m) ? A[(uint64_t)t * d + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    const int kr = lane & 3, rr = lane >> 2;
+#pragma unroll 2
+    for (int ks = 0; ks < kDmKC; ks += 4) {
+      double a[4], b[NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (double)sX[(ks + kr) * kDmLdx + warp * 32 + i * 8 + rr];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = sA[(ks + kr) * LDA + j * 8 + rr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j], a[i], b[j]);
+    }
+  }
+  // D fragment: row (point) = lane>>2, columns (tables) 2*(lane&3) + {0,1}
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t pt = p0 + warp * 32 + i * 8 + (lane >> 2);
+    if (pt >= n) continue;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = j * 8 + (lane & 3) * 2 + h;
+        if (t < m) keys[(uint64_t)t * n + pt] = f64_key(acc[i][j][h]);
+      }
+  }
+  if (exprange) {
+    for (int o = 16; o; o >>= 1) {
+      elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+      ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+    }
+    if (lane == 0) {
+      atomicMin(&exprange[0], elo);
+      atomicMax(&exprange[1], ehi);
+    }
+  }
+}
+
+template <class T>
+static void launch_dmma(const T* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
+                        cudaStream_t s) {
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  switch ((m + 7) / 8) {
+    case 1: project_dmma_kernel<T, 1><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    case 2: project_dmma_kernel<T, 2><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    case 3: project_dmma_kernel<T, 3><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    case 4: project_dmma_kernel<T, 4><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    case 5: project_dmma_kernel<T, 5><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    case 6: project_dmma_kernel<T, 6><<<grid, 128, 0, s>>>(X, n, d, A, m, keys, er); break;
+    default: break;
+  }
+}
+
 template <class T>
 __global__ void column_keys_kernel(const T* __restrict__ v, uint64_t n, uint64_t stride, uint64_t col,
                                    uint64_t* __restrict__ keys) {
@@ -204,6 +304,12 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 (f32) or 1 (f64)");
   GEEK_REQUIRE(d >= 1 && m >= 1, "empty projection");
   if (n == 0) return GEEK_OK;
+  if (m <= 48 && !getenv("GEEK_NO_DMMA")) {  // DMMA path (up to 6 column fragments)
+    if (dtype == 0) launch_dmma<float>((const float*)X, n, d, A, m, keys, exprange, s);
+    else launch_dmma<double>((const double*)X, n, d, A, m, keys, exprange, s);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
   const int mg = (m + 3) / 4;
   if (mg <= 16) {  // register-blocked path: 32 point groups x mg table groups per block
     const size_t smem = (size_t)kP2KC * mg * 4 * 8 + (size_t)kP2KC * (kP2Pts + 4) * (dtype == 0 ? 4 : 8);
