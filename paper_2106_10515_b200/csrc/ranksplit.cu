@@ -110,6 +110,25 @@ __global__ void straddle_kernel(SplitGeom g, const uint32_t* fcnt, const uint32_
   }
 }
 
+// Coarse cells whose non-empty fine bins all map to one slot are rewritten to
+// (0, slot): codes_kernel then needs a single lookup for most ids.
+__global__ void cell_shortcut_kernel(uint2* cinfo, const uint32_t* fcnt, const uint32_t* fcode, uint64_t ncell) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < ncell;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 ci = cinfo[c];
+    uint32_t code = GEEK_NONE;
+    bool uniform = true, any = false;
+    for (uint32_t f = ci.y; f < ci.y + ci.x && uniform; ++f) {
+      if (fcnt[f] == 0) continue;
+      const uint32_t fc = fcode[f];
+      if (fc == GEEK_NONE || (any && fc != code)) uniform = false;
+      code = fc;
+      any = true;
+    }
+    if (uniform && any) cinfo[c] = make_uint2(0u, code);
+  }
+}
+
 // slot codes for ids in non-straddling bins; straddling ids are staged
 __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
                                                     const uint2* __restrict__ cinfo,
@@ -123,8 +142,14 @@ __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__
     uint32_t* crow = codes + i * (uint64_t)g.m + g.c0;
     for (int jb = 0; jb < g.tb; ++jb) {
       const uint64_t key = keys[(uint64_t)(g.j0 + jb) * g.n + i];
-      const uint32_t f = fine_of(key, g.cb, cinfo + (uint64_t)jb * g.nc);
-      const uint32_t code = __ldg(fcode + f);
+      const uint2 ci = __ldg(cinfo + (uint64_t)jb * g.nc + coarse_of(key, g.cb));
+      uint32_t f = 0, code;
+      if (ci.x == 0) {
+        code = ci.y;  // whole cell inside one bucket
+      } else {
+        f = ci.y + static_cast<uint32_t>(((uint64_t)static_cast<uint32_t>((key << g.cb) >> 32) * ci.x) >> 32);
+        code = __ldg(fcode + f);
+      }
       if (code != GEEK_NONE) {
         crow[jb] = code;
       } else {
@@ -255,6 +280,9 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
                                                       stats.as<unsigned long long>());
   GEEK_CHECK_LAUNCH();
   uint64_t nstage = 0;
+  cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(cinfo.as<uint2>(), fcnt.as<uint32_t>(),
+                                                             fcode.as<uint32_t>(), ncell);
+  GEEK_CHECK_LAUNCH();
   GEEK_TRY(exclusive_scan_u32(scnt.as<uint32_t>(), sbase.as<uint32_t>(), nfb, s, &nstage));
   unsigned long long st[4] = {0, 0, 0, 0};
   GEEK_CHECK_CUDA(cudaMemcpyAsync(st, stats.ptr, 24, cudaMemcpyDeviceToHost, s));
