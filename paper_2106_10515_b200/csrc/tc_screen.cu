@@ -202,9 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint64_t* acce = bars + 8;    // [2] accumulator drained (128 epilogue threads)
   uint64_t* afull = bars + 10;  // point tile written (128 threads)
   uint64_t* aempty = bars + 11; // point tile no longer read (MMA commit)
-  uint64_t* c2full = bars + 12; // [4] |c'|^2 of a center tile landed (TMA tx)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  float* sc2 = reinterpret_cast<float*>(bars + 18);  // [4][kTcN], buffered by center-tile count
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -218,7 +216,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     }
     mbar_init(afull, kTcEpiThreads);
     mbar_init(aempty, 1);
-    for (int b = 0; b < 4; ++b) mbar_init(&c2full[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -241,15 +238,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
       uint64_t q_issue = 0, q_mma = 0;
       auto issue = [&]() {
-        if (q_issue % nck == 0) {  // first chunk of a center tile: also stage its |c'|^2
-          // buffer g%4 was last read by the epilogue of g-4; this load is issued
-          // after the MMAs of g-2 at the earliest, which waited for that epilogue
-          // (acce of g-4)
-          const uint64_t g = q_issue / nck;
-          const int ct = (int)(g % P.nct);
-          mbar_expect_tx(&c2full[g % 4], kTcN * 4);
-          bulk_g2s(sc2 + (g % 4) * kTcN, P.c2 + (uint64_t)ct * kTcN, kTcN * 4, &c2full[g % 4]);
-        }
         const uint32_t s = (uint32_t)(q_issue % kTcStages);
         if (q_issue >= kTcStages) mbar_wait(&empty[s], (uint32_t)((q_issue / kTcStages) - 1) & 1);
         mbar_expect_tx(&full[s], kTcStageBytes);
@@ -300,12 +288,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
       const uint64_t g = (uint64_t)t * P.nct + ct;
       const int buf = (int)(g & 1);
-      mbar_wait(&c2full[g % 4], (uint32_t)((g / 4) & 1));
       mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-      const float4* c2t = reinterpret_cast<const float4*>(sc2 + (g % 4) * kTcN + ch * (kTcN / 2));
+      const float4* c2t = reinterpret_cast<const float4*>(P.c2 + (uint64_t)ct * kTcN + ch * (kTcN / 2));
 #pragma unroll 1
       for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
         float v[32];
@@ -313,7 +300,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         float mn = INFINITY;
 #pragma unroll
         for (int u = 0; u < 32; u += 4) {
-          const float4 cc = c2t[(c0 + u) / 4];  // shared-memory broadcast
+          const float4 cc = __ldg(c2t + (c0 + u) / 4);
           v[u] = cc.x - 2.f * v[u];
           v[u + 1] = cc.y - 2.f * v[u + 1];
           v[u + 2] = cc.z - 2.f * v[u + 2];
@@ -559,7 +546,7 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t
 }
 
 size_t tc_screen_smem() {
-  return (size_t)kTcABytes + kTcStages * kTcStageBytes + 18 * 8 + 4 * kTcN * 4;
+  return (size_t)kTcABytes + kTcStages * kTcStageBytes + 12 * 8 + 16;
 }
 
 int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
