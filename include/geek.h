@@ -177,17 +177,20 @@ int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngr
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
                    int64_t* labels, double* best, void* stream);
 
-/* Self-test of the tcgen05 screen's operand layout on a synthetic problem
- * (1000 x 128 points, 300 centers): out_host[0] = max |s_tc - S_f64| /
- * (|x'||c'|max), out_host[1] = points whose screened top-1 is not the f64
- * argmin.  lbo/sbo are the canonical-layout core-matrix strides in bytes. */
-int geek_tc_selftest(uint32_t lbo, uint32_t sbo, double* out_host);
+/* Self-test of the tcgen05 screen on a synthetic problem (1000 x 128
+ * points, 300 centers): out_host[0] = max |s_tc - S_f64| / (|x'||c'|max)
+ * over every kept entry, out_host[1] = points whose screened top-1 is not
+ * the f64 argmin.  lbo/sbo are the canonical-layout core-matrix strides in
+ * bytes; nprod = 1 (TF32) or 3 (TF32x3).                                   */
+int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host);
 
 /* number of points the last geek_assign_l2 call re-checked exactly because
  * the float32 screen could not separate their two nearest centers        */
 uint64_t geek_assign_last_rechecked(void);
 /* CUDA-event duration (ms) of the last tensor-core screen kernel launch     */
 double geek_assign_last_screen_ms(void);
+/* of those, points whose candidate window overflowed (exact scan over all)   */
+uint64_t geek_assign_last_full_scans(void);
 
 /* radii[c] = max best over members (0 if none), sizes[c] = member count
  * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed

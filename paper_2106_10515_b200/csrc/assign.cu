@@ -251,6 +251,11 @@ static double& last_screen_ms() {
   return v;
 }
 
+static uint64_t& last_full() {
+  static uint64_t v = 0;
+  return v;
+}
+
 constexpr int kScrP = 128, kScrC = 128, kScrK = 16, kScrThreads = 256;
 
 __global__ void center_prep_kernel(const double* C, uint64_t k, int d, float* Cf, float* c2f,
@@ -396,11 +401,6 @@ __global__ void __launch_bounds__(kScrThreads, 2) screen_kernel(const float* __r
 
 // ---- tensor-core screen: classification and candidate recheck ----------------
 
-int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t sbo, Scratch& img, Scratch& c2,
-                      Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s);
-int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
-                     uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i, float* xnorm,
-                     cudaStream_t s);
 // SWIZZLE_NONE K-major canonical layout strides (bytes): K-adjacent / M,N-adjacent core matrices
 constexpr uint32_t kTcLBO = 128, kTcSBO = 256;
 
@@ -409,41 +409,66 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
   return __dsqrt_rn(pw_sum(plan, get));
 }
 
-// Bound of |s - S| for the TF32x3 screen (see tc_screen.cu): operand
-// rounding to float32, hi/lo split residuals and the dropped lo*lo term,
-// fp32 accumulation of 3d products, |c'|^2 rounding and the final subtraction.
-__device__ __forceinline__ double tc_threshold(double xn, double cn, int d) {
+// Bound T(x) on the separation the screen must show before its winner is
+// final.  E bounds |s - S| (S = |c-mu|^2 - 2(x-mu).(c-mu) in exact arithmetic):
+//   nprod 3: float32 operand rounding, hi/lo split residuals and the dropped
+//            lo*lo term, fp32 accumulation of 3d products, |c'|^2 rounding and
+//            the final subtraction;
+//   nprod 1: float32 operand rounding, TF32 rounding of both operands
+//            (2^-11 relative each), fp32 accumulation of d products, |c'|^2
+//            rounding and the subtraction.
+// Every product is bounded through sum |x'_i||c'_i| <= |x'||c'| (Cauchy-Schwarz).
+// E64 bounds numpy's float64 evaluation of the squared distance, and the last
+// term keeps the correctly rounded square roots of the two best distinct.
+__device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int nprod) {
   const double u = 5.9604644775390625e-08;  // 2^-24
-  const double E = 1.05 * ((1.9073486328125e-06 + 6.0 * d * 1.1920928955078125e-07 + 8.0 * u) * xn * cn +
-                           2.0 * u * cn * cn);
+  const double acc = (double)d * 1.1920928955078125e-07;  // d * 2^-23
+  const double E = nprod == 3 ? 1.05 * ((1.9073486328125e-06 + 6.0 * acc + 8.0 * u) * xn * cn + 2.0 * u * cn * cn)
+                              : 1.05 * ((1.953125e-03 + 2.0 * acc + 6.0 * u) * xn * cn + 3.0 * u * cn * cn);
   const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
   return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
 }
 
-// merged top-4 (ascending) of the screen's two column-half lists
-__device__ __forceinline__ void merge_top8(const float* s8, const int* i8, float* s, int* ix) {
-  int a = 0, b = 4;
+// The screen keeps the top-4 of each accumulator column half ([8] per point).
+// Their union holds the true best and second best; every center within the
+// window s0 + T is among them unless a half's 4th entry is itself inside the
+// window (overflow -> exact scan over all centers).
+struct ScreenView {
+  float s0, s1;
+  int i0;
+  float s3a, s3b;
+};
+
+__device__ __forceinline__ ScreenView screen_view(const float* s8, const int* i8) {
+  ScreenView v;
+  v.s0 = INFINITY;
+  v.s1 = INFINITY;
+  v.i0 = -1;
 #pragma unroll
-  for (int o = 0; o < 4; ++o) {
-    const bool ta = b >= 8 || (a < 4 && s8[a] <= s8[b]);
-    s[o] = ta ? s8[a] : s8[b];
-    ix[o] = ta ? i8[a] : i8[b];
-    a += ta;
-    b += !ta;
+  for (int a = 0; a < 8; ++a) {
+    const float x = s8[a];
+    if (x < v.s0) {
+      v.s1 = v.s0;
+      v.s0 = x;
+      v.i0 = i8[a];
+    } else if (x < v.s1) {
+      v.s1 = x;
+    }
   }
+  v.s3a = s8[3];
+  v.s3b = s8[7];
+  return v;
 }
 
 // certain points: label + exact best; others: queued with their candidates
 __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                    uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
-                                   float* xnorm, const float* mu, const unsigned long long* cmax_bits,
+                                   float* xnorm, const float* mu, const unsigned long long* cmax_bits, int nprod,
                                    int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb,
                                    uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    float s[4];
-    int ix[4];
-    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
+    const ScreenView v = screen_view(top_s + i * 8, top_i + i * 8);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
     for (int j = 0; j < d; ++j) {
       const double xv = (double)(X[i * d + j] - mu[j]);
@@ -451,10 +476,10 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
     }
     const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
     xnorm[i] = xn;
-    const double T = tc_threshold((double)xn, cn, d);
-    const double s0 = s[0];
-    if (k == 1 || (double)s[1] - s0 > T) {
-      const int lab = ix[0];
+    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double s0 = v.s0;
+    if (k == 1 || (double)v.s1 - s0 > T) {
+      const int lab = v.i0;
       const float* xr = X + i * d;
       const double* cr = C + (uint64_t)lab * d;
       labels[i] = lab;
@@ -462,8 +487,8 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
         const double df = __dsub_rn((double)xr[j], cr[j]);
         return __dmul_rn(df, df);
       });
-    } else if (k > 4 && (double)s[3] - s0 <= T) {
-      full[atomicAdd(nfull, 1ull)] = (uint32_t)i;  // more than four candidates
+    } else if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) {
+      full[atomicAdd(nfull, 1ull)] = (uint32_t)i;  // candidate window overflows the kept lists
     } else {
       amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
     }
@@ -475,18 +500,16 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
 // and the summation order is exactly pw_leaf's.
 __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                     uint64_t k, const float* top_s, const int* top_i, float* xnorm,
-                                    const float* mu, const unsigned long long* cmax_bits, int64_t* labels,
-                                    double* best, uint32_t* amb, unsigned long long* namb, uint32_t* full,
-                                    unsigned long long* nfull) {
+                                    const float* mu, const unsigned long long* cmax_bits, int nprod,
+                                    int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb,
+                                    uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   const unsigned lane = threadIdx.x & 31, a = lane & 7;
   const unsigned gmask = 0xFFu << (lane & 24);
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
   const int lim = d - (d % 8);
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; i < n; i += stride) {
-    float s[4];
-    int ix[4];
-    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
+    const ScreenView v = screen_view(top_s + i * 8, top_i + i * 8);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
     for (int e = (int)a; e < d; e += 8) {
       const double xv = (double)(X[i * d + e] - mu[e]);
@@ -497,11 +520,11 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
     xn2 += __shfl_xor_sync(gmask, xn2, 4);
     const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
     if (a == 0) xnorm[i] = xn;
-    const double T = tc_threshold((double)xn, cn, d);
-    const double s0 = s[0];
-    const bool certain = k == 1 || (double)s[1] - s0 > T;
+    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double s0 = v.s0;
+    const bool certain = k == 1 || (double)v.s1 - s0 > T;
     if (certain) {
-      const int lab = ix[0];
+      const int lab = v.i0;
       const float* xr = X + i * d;
       const double* cr = C + (uint64_t)lab * d;
       double r;
@@ -529,37 +552,39 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
         best[i] = __dsqrt_rn(res);
       }
     } else if (a == 0) {
-      if (k > 4 && (double)s[3] - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
+      if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
       else amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
     }
   }
 }
 
-// exact numpy distances over the (<= 4) screen candidates; ties -> lower index
+// exact numpy distances over the screen candidates (<= 8 entries within the
+// window); ties -> lower index
 __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const double* __restrict__ C, uint64_t k,
                                   const PwPlan plan, const float* top_s, const int* top_i, const float* xnorm,
-                                  const unsigned long long* cmax_bits, const uint32_t* amb, uint64_t na,
+                                  const unsigned long long* cmax_bits, int nprod, const uint32_t* amb, uint64_t na,
                                   int64_t* labels, double* best) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < na; q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = amb[q];
-    float s[4];
-    int ix[4];
-    merge_top8(top_s + i * 8, top_i + i * 8, s, ix);
-    const double T = tc_threshold((double)xnorm[i], cn, d);
+    const float* s8 = top_s + i * 8;
+    const int* i8 = top_i + i * 8;
+    const ScreenView v = screen_view(s8, i8);
+    const double T = tc_threshold((double)xnorm[i], cn, d, nprod);
     const float* xr = X + i * d;
     double bd = 0.0;
     int64_t bl = -1;
-    for (int a = 0; a < 4 && (uint64_t)a < k; ++a) {
-      if ((double)s[a] - (double)s[0] > T || ix[a] < 0) break;
-      const double* cr = C + (uint64_t)ix[a] * d;
+    (void)k;
+    for (int a = 0; a < 8; ++a) {
+      if ((double)s8[a] - (double)v.s0 > T || i8[a] < 0) continue;
+      const double* cr = C + (uint64_t)i8[a] * d;
       const double dist = exact_dist(plan, [&](int j) {
         const double df = __dsub_rn((double)xr[j], cr[j]);
         return __dmul_rn(df, df);
       });
-      if (bl < 0 || dist < bd || (dist == bd && ix[a] < bl)) {
+      if (bl < 0 || dist < bd || (dist == bd && i8[a] < bl)) {
         bd = dist;
-        bl = ix[a];
+        bl = i8[a];
       }
     }
     labels[i] = bl;
@@ -591,7 +616,10 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                          (int)smem));
   }
   if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull && !getenv("GEEK_NO_TC")) {
-    // tensor-core TF32x3 screen -> classification -> candidate / full recheck
+    // tensor-core screen (1 TF32 product by default; GEEK_SCREEN=3 selects
+    // TF32x3) -> classification -> candidate / full recheck
+    const char* sel = getenv("GEEK_SCREEN");
+    const int nprod = (sel && sel[0] == '3') ? 3 : 1;
     Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt;
     GEEK_TRY(cnt.alloc(32, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 32, s));
@@ -599,7 +627,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     unsigned long long* namb = cmax + 1;
     unsigned long long* nfull = cmax + 2;
     int nct = 0;
-    GEEK_TRY(tc_screen_prepare(C, k, d, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, s));
+    GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, s));
     GEEK_TRY(ts.alloc(n * 32, s));
     GEEK_TRY(ti.alloc(n * 32, s));
     GEEK_TRY(xn.alloc(n * 4, s));
@@ -609,22 +637,23 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_CUDA(cudaEventCreate(&ev0));
     GEEK_CHECK_CUDA(cudaEventCreate(&ev1));
     GEEK_CHECK_CUDA(cudaEventRecord(ev0, s));
-    GEEK_TRY(tc_screen_launch((const float*)X, n, d, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
-                              ti.as<int>(), xn.as<float>(), s));
+    GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
+                              ti.as<int>(), s));
     GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
     if (d >= 8)
       tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax,
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,
           labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     else
       tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
           (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax,
-          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+          nprod, labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     GEEK_CHECK_LAUNCH();
     unsigned long long cnts[2];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(cnts, namb, 16, cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
     last_ambiguous() = cnts[0] + cnts[1];
+    last_full() = cnts[1];
     float ms = 0.f;
     GEEK_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     last_screen_ms() = ms;
@@ -632,8 +661,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     cudaEventDestroy(ev1);
     if (cnts[0]) {
       tc_recheck_kernel<<<grid_for(cnts[0], 128), 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(),
-                                                               ti.as<int>(), xn.as<float>(), cmax, amb.as<uint32_t>(),
-                                                               cnts[0], labels, best);
+                                                               ti.as<int>(), xn.as<float>(), cmax, nprod,
+                                                               amb.as<uint32_t>(), cnts[0], labels, best);
       GEEK_CHECK_LAUNCH();
     }
     if (cnts[1]) {
@@ -686,6 +715,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
 uint64_t geek_assign_last_rechecked(void) { return last_ambiguous(); }
 
 double geek_assign_last_screen_ms(void) { return last_screen_ms(); }
+
+uint64_t geek_assign_last_full_scans(void) { return last_full(); }
 
 int geek_radii_sizes(const int64_t* labels, const double* best, uint64_t n, uint64_t k, double* radii,
                      int64_t* sizes, void* stream) {

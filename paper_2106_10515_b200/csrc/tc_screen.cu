@@ -1,37 +1,51 @@
 // K8 on the 5th-gen tensor cores: the assignment screen s(x, c) = |c'|^2 -
-// 2 x'.c' (x' = x - mu, c' = c - mu) as a tcgen05 TF32x3 GEMM
-// (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM) with a fused top-4
-// epilogue, followed by the exact float64 distance to the winner.
+// 2 x'.c' (x' = x - mu, c' = c - mu) as a tcgen05 GEMM with fused top-4
+// epilogues; the classifier (assign.cu) turns the screen into exact float64
+// labels with a rigorous error bound.
 //
+// Two precisions of the same kernel (template NPROD):
+//   NPROD = 1: one TF32 product (operands rounded to TF32, fp32 accumulation);
+//              A = 64 KB per point tile, double-buffered, so the conversion
+//              of the next tile overlaps the MMAs of this one
+//   NPROD = 3: TF32x3 (hi*hi + hi*lo + lo*hi): fp32-level screen, A = 128 KB
+//              single-buffered
 // Per CTA (persistent over 128-point tiles):
-//   A  = the point tile, hi/lo TF32 split, K-major, resident in SMEM (128 KB)
+//   A  = the point tile, K-major, in SMEM
 //   B  = center tiles of 128 centers, streamed in 32-dim chunks by 1-D bulk
-//        TMA (cp.async.bulk) into a 3-stage SMEM ring (32 KB per stage)
+//        TMA (cp.async.bulk) into a ring of SMEM stages
 //   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
-//        of center tile j (tcgen05.ld, one TMEM lane = one point per thread)
-//        overlaps the MMAs of tile j+1
+//        of center tile j overlaps the MMAs of tile j+1
 // Warp-specialised: lane 0 of warp 8 issues the bulk copies and the MMAs;
-// warps 0-7 convert the next point tile into A and run the epilogues (warp w
-// reads TMEM lanes 32(w%4).. over column half w/4, keeping its own top-4);
-// the roles hand off through mbarriers only (stage
-// full/empty, accumulator full/empty, point tile full/empty).
-// Operands use the SWIZZLE_NONE K-major canonical layout: 8-row x
-// 16-byte core matrices, LBO between K-adjacent, SBO between M/N-adjacent
-// core matrices.
+// warps 0-7 convert point tiles into A and run the epilogues (warp w reads
+// TMEM lanes 32(w%4).. over column half w/4 and keeps its own top-4); roles
+// hand off through mbarriers only (stage full/empty, accumulator full/empty,
+// point tile full/empty).  Operands use the SWIZZLE_NONE K-major canonical
+// layout: 8-row x 16-byte core matrices, LBO between K-adjacent and SBO
+// between M/N-adjacent core matrices (validated on the GPU by
+// geek_tc_selftest).
 #include "common.cuh"
 
 #include <cstring>
 
 namespace geek {
 
-constexpr int kTcM = 128;           // points per tile (TMEM lanes)
-constexpr int kTcN = 128;            // centers per tile
-constexpr int kTcKmax = 128;         // padded dimension (<= 128)
-constexpr int kTcChunk = 32;         // dims per B stage
-constexpr int kTcStages = 3;
-constexpr int kTcSliceBytes = kTcM * 8 * 4;                  // one K=8 tf32 slice of 128 rows: 4 KB
-constexpr int kTcStageBytes = 2 * (kTcChunk / 8) * kTcSliceBytes;  // hi + lo: 32 KB
-constexpr int kTcABytes = 2 * (kTcKmax / 8) * kTcSliceBytes;       // hi + lo: 128 KB
+constexpr int kTcM = 128;      // points per tile (TMEM lanes)
+constexpr int kTcN = 128;      // centers per tile
+constexpr int kTcKmax = 128;   // padded dimension (<= 128)
+constexpr int kTcChunk = 32;   // dims per B stage
+constexpr int kTcSliceBytes = kTcM * 8 * 4;                       // one K=8 tf32 slice of 128 rows: 4 KB
+constexpr int kTcHalfStage = (kTcChunk / 8) * kTcSliceBytes;      // 16 KB: one 32-dim chunk, one part
+constexpr int kTcAPart = (kTcKmax / 8) * kTcSliceBytes;           // 64 KB: one part of a point tile
+
+template <int NPROD>
+struct TcCfg {
+  static constexpr int kParts = NPROD == 3 ? 2 : 1;              // hi (+ lo)
+  static constexpr int kABytes = kParts * kTcAPart;
+  static constexpr int kABuf = NPROD == 3 ? 1 : 2;
+  static constexpr int kStageBytes = kParts * kTcHalfStage;
+  static constexpr int kStages = NPROD == 3 ? 3 : 4;
+  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 24 * 8;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -53,8 +67,7 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
-  // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); base offset 0, SWIZZLE_NONE
   return d;
 }
 
@@ -70,6 +83,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -167,46 +184,42 @@ struct Top4 {
 };
 
 struct TcParams {
-  const float* X;       // [n][d] float32
+  const float* X;     // [n][d] float32
   uint64_t n;
   int d;
-  const float* Bimg;    // center operand image: [nct][4 chunks][32 KB]
-  const float* c2;      // [nct*128] |c'|^2 (float, +inf for padding)
-  const float* mu;      // [d]
+  const float* Bimg;  // center operand image: [nct][chunks][stage bytes]
+  const float* c2;    // [nct*128] |c'|^2 (float, +inf for padding)
+  const float* mu;    // [d]
   uint64_t k;
   int nct;
   uint32_t lbo, sbo;
-  float* top_s;         // [n][8]: top-4 of each accumulator column half
-  int* top_i;           // [n][8]
-  float* xnorm;         // [n] |x'| upper bound
+  float* top_s;       // [n][8]: top-4 of each accumulator column half
+  int* top_i;         // [n][8]
 };
 
-// warps 0-7: A loader + epilogue (warp w reads TMEM lanes 32(w%4).. and
-// accumulator columns 64(w/4)..+64), warp 8: TMA + MMA issuer
+// warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcEpiThreads = kTcEpiWarps * 32;
 constexpr int kTcThreads = kTcEpiThreads + 32;
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
+template <int NPROD>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams P) {
+  using Cfg = TcCfg<NPROD>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* A = smem;                                   // hi: 64 KB, lo: 64 KB
-  uint8_t* B = smem + kTcABytes;                       // 3 stages x 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(B + kTcStages * kTcStageBytes);
-  uint64_t* full = bars;        // [3] stage loaded (TMA tx)
-  uint64_t* empty = bars + 3;   // [3] stage consumed (MMA commit)
-  uint64_t* accf = bars + 6;    // [2] accumulator ready (MMA commit)
-  uint64_t* acce = bars + 8;    // [2] accumulator drained (128 epilogue threads)
-  uint64_t* afull = bars + 10;  // point tile written (128 threads)
-  uint64_t* aempty = bars + 11; // point tile no longer read (MMA commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint8_t* A = smem;                                           // kABuf x kABytes
+  uint8_t* B = smem + Cfg::kABuf * Cfg::kABytes;               // kStages x kStageBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(B + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* full = bars;                    // [kStages] stage loaded (TMA tx)
+  uint64_t* empty = bars + 4;               // [kStages] stage consumed (MMA commit)
+  uint64_t* accf = bars + 8;                // [2] accumulator ready (MMA commit)
+  uint64_t* acce = bars + 10;               // [2] accumulator drained (256 epilogue threads)
+  uint64_t* afull = bars + 12;              // [kABuf] point tile written (256 threads)
+  uint64_t* aempty = bars + 14;             // [kABuf] point tile no longer read (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -214,8 +227,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], kTcEpiThreads);
     }
-    mbar_init(afull, kTcEpiThreads);
-    mbar_init(aempty, 1);
+    for (int b = 0; b < Cfg::kABuf; ++b) {
+      mbar_init(&afull[b], kTcEpiThreads);
+      mbar_init(&aempty[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -238,19 +253,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
       uint64_t q_issue = 0, q_mma = 0;
       auto issue = [&]() {
-        const uint32_t s = (uint32_t)(q_issue % kTcStages);
-        if (q_issue >= kTcStages) mbar_wait(&empty[s], (uint32_t)((q_issue / kTcStages) - 1) & 1);
-        mbar_expect_tx(&full[s], kTcStageBytes);
-        bulk_g2s(B + s * kTcStageBytes,
-                 reinterpret_cast<const uint8_t*>(P.Bimg) + (q_issue % total_q) * (uint64_t)kTcStageBytes,
-                 kTcStageBytes, &full[s]);
+        const uint32_t s = (uint32_t)(q_issue % Cfg::kStages);
+        if (q_issue >= (uint64_t)Cfg::kStages) mbar_wait(&empty[s], (uint32_t)((q_issue / Cfg::kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], Cfg::kStageBytes);
+        bulk_g2s(B + s * Cfg::kStageBytes,
+                 reinterpret_cast<const uint8_t*>(P.Bimg) + (q_issue % total_q) * (uint64_t)Cfg::kStageBytes,
+                 Cfg::kStageBytes, &full[s]);
         ++q_issue;
       };
-      while (q_issue < kTcStages - 1 && q_issue < total_chunks) issue();
-      const uint32_t ab = smem_u32(A);
+      while (q_issue < (uint64_t)Cfg::kStages - 1 && q_issue < total_chunks) issue();
       for (uint32_t t = 0; t < my_tiles; ++t) {
-        mbar_wait(afull, t & 1);
+        const int ab = t % Cfg::kABuf;
+        mbar_wait(&afull[ab], (t / Cfg::kABuf) & 1);
         fence_after();
+        const uint32_t abase = smem_u32(A + ab * Cfg::kABytes);
         for (int ct = 0; ct < P.nct; ++ct) {
           const uint64_t g = (uint64_t)t * P.nct + ct;
           const int buf = (int)(g & 1);
@@ -258,41 +274,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
           for (int kc = 0; kc < nck; ++kc) {
-            const uint32_t s = (uint32_t)(q_mma % kTcStages);
-            mbar_wait(&full[s], (uint32_t)(q_mma / kTcStages) & 1);
+            const uint32_t s = (uint32_t)(q_mma % Cfg::kStages);
+            mbar_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1);
             fence_after();
-            const uint32_t bb = smem_u32(B + s * kTcStageBytes);
+            const uint32_t bb = smem_u32(B + s * Cfg::kStageBytes);
 #pragma unroll
             for (int j = 0; j < kTcChunk / 8; ++j) {
               const int ks = kc * (kTcChunk / 8) + j;
-              const uint64_t ahi = make_sdesc(ab + ks * kTcSliceBytes, P.lbo, P.sbo);
-              const uint64_t alo = make_sdesc(ab + kTcABytes / 2 + ks * kTcSliceBytes, P.lbo, P.sbo);
+              const uint64_t ahi = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
               const uint64_t bhi = make_sdesc(bb + j * kTcSliceBytes, P.lbo, P.sbo);
-              const uint64_t blo = make_sdesc(bb + kTcStageBytes / 2 + j * kTcSliceBytes, P.lbo, P.sbo);
               tc_mma(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
-              tc_mma(dt, ahi, blo, idesc, 1u);
-              tc_mma(dt, alo, bhi, idesc, 1u);
+              if (NPROD == 3) {
+                const uint64_t alo = make_sdesc(abase + kTcAPart + ks * kTcSliceBytes, P.lbo, P.sbo);
+                const uint64_t blo = make_sdesc(bb + kTcHalfStage + j * kTcSliceBytes, P.lbo, P.sbo);
+                tc_mma(dt, ahi, blo, idesc, 1u);
+                tc_mma(dt, alo, bhi, idesc, 1u);
+              }
             }
             tc_commit(&empty[s]);
             ++q_mma;
-            if (q_issue < total_chunks) issue();  // into the stage of chunk q_mma-2, queued ahead
+            if (q_issue < total_chunks) issue();  // into the stage of an earlier, queued chunk
           }
           tc_commit(&accf[buf]);
         }
-        tc_commit(aempty);
+        tc_commit(&aempty[ab]);
       }
     }
-  } else {  // ---------------- warps 0-3: point tiles + epilogue ----------------
+  } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
     Top4 cur, prev;
     cur.init();
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
       const uint64_t g = (uint64_t)t * P.nct + ct;
       const int buf = (int)(g & 1);
+      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
+      const float4* c2t = reinterpret_cast<const float4*>(P.c2 + (uint64_t)ct * kTcN + ch * (kTcN / 2));
       mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
-      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-      const float4* c2t = reinterpret_cast<const float4*>(P.c2 + (uint64_t)ct * kTcN + ch * (kTcN / 2));
 #pragma unroll 1
       for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
         float v[32];
@@ -325,11 +343,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
-    for (uint32_t t = 0; t < my_tiles; ++t) {
+    // x' = x - mu rounded to tf32 (+ the tf32 residual for NPROD = 3) into
+    // buffer t % kABuf; warp w owns rows 16w..16w+15, lane = float4 column
+    auto load_a = [&](uint32_t t) {
+      const int ab = t % Cfg::kABuf;
+      mbar_wait(&aempty[ab], ((t / Cfg::kABuf) & 1) ^ 1u);  // MMAs that read this buffer are done
+      uint8_t* Ab = A + ab * Cfg::kABytes;
       const uint64_t p0 = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM;
-      mbar_wait(aempty, (t & 1) ^ 1u);  // MMAs of the previous tile no longer read A
-      // x' = x - mu, tf32 hi/lo into the canonical layout; warp w owns rows
-      // 16w..16w+15, lane = float4 column, 8 rows of loads in flight
       if (P.d == kTcKmax) {
         const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.mu) + lane);
         const uint32_t off0 = ((lane * 4) >> 3) * kTcSliceBytes;
@@ -350,9 +370,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const float x2 = valid ? q[u].z - m4.z : 0.f, x3 = valid ? q[u].w - m4.w : 0.f;
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = off0 + core_off(row, (lane * 4) & 7, P.lbo, P.sbo);
-            *reinterpret_cast<float4*>(A + off) = make_float4(h0, h1, h2, h3);
-            *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) =
-                make_float4(tf32_round(x0 - h0), tf32_round(x1 - h1), tf32_round(x2 - h2), tf32_round(x3 - h3));
+            *reinterpret_cast<float4*>(Ab + off) = make_float4(h0, h1, h2, h3);
+            if (NPROD == 3)
+              *reinterpret_cast<float4*>(Ab + kTcAPart + off) =
+                  make_float4(tf32_round(x0 - h0), tf32_round(x1 - h1), tf32_round(x2 - h2), tf32_round(x3 - h3));
           }
         }
       } else {
@@ -369,24 +390,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               lo4[u] = tf32_round(xv - hi4[u]);
             }
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
-            *reinterpret_cast<float4*>(A + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
-            *reinterpret_cast<float4*>(A + kTcABytes / 2 + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+            *reinterpret_cast<float4*>(Ab + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
+            if (NPROD == 3)
+              *reinterpret_cast<float4*>(Ab + kTcAPart + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
           }
         }
       }
       fence_proxy_async();
-      mbar_arrive(afull);
-      {  // pull the next tile of this CTA towards L2 while the MMAs run
-        const uint64_t pn = p0 + (uint64_t)gridDim.x * kTcM;
-        const uint64_t row = pn + tid;
+      mbar_arrive(&afull[ab]);
+      {  // pull the following tile of this CTA towards L2 while the MMAs run
+        const uint64_t row = p0 + (uint64_t)gridDim.x * kTcM + tid;
         if (tid < kTcM && row < P.n) {
           const char* base = reinterpret_cast<const char*>(P.X + row * P.d);
           for (int b = 0; b < P.d * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
         }
       }
+    };
+    for (uint32_t t = 0; t < my_tiles; ++t) {
+      if (Cfg::kABuf == 1 || t == 0) load_a(t);  // double buffering loads t+1 one tile early
       prev = cur;
       cur.init();
       if (t > 0) finish(t - 1, prev);
+      if (Cfg::kABuf == 2 && t + 1 < my_tiles) load_a(t + 1);  // overlaps the MMAs of tile t
       for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
     }
     if (my_tiles > 0) finish(my_tiles - 1, cur);
@@ -406,17 +431,19 @@ __global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu
   }
 }
 
-// Bimg[ct][kc] = { hi[128 centers][32 dims], lo[...] } in the canonical layout
-__global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, uint32_t lbo,
-                                    uint32_t sbo, float* Bimg, float* c2, unsigned long long* cmax_bits) {
+// Bimg[ct][kc] = { tf32(c')[128 centers][32 dims] (, residual[...] for NPROD=3) }
+__global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, int parts,
+                                    uint32_t lbo, uint32_t sbo, float* Bimg, float* c2,
+                                    unsigned long long* cmax_bits) {
   const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
+  const uint64_t stage = (uint64_t)parts * kTcHalfStage;
   const uint64_t total = (uint64_t)nct * kTcN;
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
        c += (uint64_t)gridDim.x * blockDim.x) {
     const int ct = (int)(c / kTcN), r = (int)(c % kTcN);
     double n2 = 0.0;
     for (int kc = 0; kc < nchunks_k; ++kc) {
-      uint8_t* img = reinterpret_cast<uint8_t*>(Bimg) + ((uint64_t)ct * nchunks_k + kc) * kTcStageBytes;
+      uint8_t* img = reinterpret_cast<uint8_t*>(Bimg) + ((uint64_t)ct * nchunks_k + kc) * stage;
       for (int e = 0; e < kTcChunk; ++e) {
         const int j = kc * kTcChunk + e;
         float cv = 0.f;
@@ -426,10 +453,9 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
           n2 = fma((double)cv, (double)cv, n2);
         }
         const float hi = tf32_round(cv);
-        const float lo = tf32_round(cv - hi);
         const uint32_t off = (e >> 3) * kTcSliceBytes + core_off(r, e & 7, lbo, sbo);
         *reinterpret_cast<float*>(img + off) = hi;
-        *reinterpret_cast<float*>(img + kTcStageBytes / 2 + off) = lo;
+        if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(cv - hi);
       }
     }
     c2[c] = c < k ? (float)n2 : INFINITY;
@@ -437,120 +463,40 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
   }
 }
 
-}  // namespace geek
-
-// internal entry used by assign.cu
-namespace geek {
-
-__global__ void selftest_fill(float* X, uint64_t n, int d, double* C, uint64_t k, float offset) {
-  const uint64_t tot = n * d + k * d;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < tot; e += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t z = e * 0x9E3779B97F4A7C15ull + 12345;
-    z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
-    z ^= z >> 29;
-    const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
-    if (e < n * d) X[e] = (float)(u * 3.0 + offset);
-    else C[e - n * d] = u * 3.0 + offset;
-  }
-}
-
-// reference: exact f64 S for the screen's chosen index and the true argmin
-__global__ void selftest_check(const float* X, uint64_t n, int d, const double* C, uint64_t k, const float* mu,
-                               const float* top_s, const int* top_i, const float* xnorm,
-                               const unsigned long long* cmax_bits, double* worst, unsigned long long* bad) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    double best = INFINITY;
-    int bi = -1;
-    double at_idx = 0;
-    const bool lo_half = top_s[i * 8] <= top_s[i * 8 + 4];
-    const int t1 = lo_half ? top_i[i * 8] : top_i[i * 8 + 4];
-    const float s1 = lo_half ? top_s[i * 8] : top_s[i * 8 + 4];
-    for (uint64_t c = 0; c < k; ++c) {
-      double cc = 0, xc = 0;
-      for (int j = 0; j < d; ++j) {
-        const double cv = (double)(float)(C[c * d + j] - (double)mu[j]);
-        const double xv = (double)(X[i * d + j] - mu[j]);
-        cc += cv * cv;
-        xc += xv * cv;
-      }
-      const double S = cc - 2.0 * xc;
-      if (S < best) {
-        best = S;
-        bi = (int)c;
-      }
-      if ((int)c == t1) at_idx = S;
-    }
-    double xn2 = 0.0;
-    for (int j = 0; j < d; ++j) {
-      const double xv = (double)(X[i * d + j] - mu[j]);
-      xn2 += xv * xv;
-    }
-    const double scale = sqrt(xn2) * __longlong_as_double((long long)*cmax_bits) + 1e-30;
-    const double err = fabs((double)s1 - at_idx) / scale;
-    atomicMax(reinterpret_cast<unsigned long long*>(worst), (unsigned long long)__double_as_longlong(err));
-    if (bi != t1 && best < at_idx) atomicAdd(bad, 1ull);
-  }
-}
-
-}  // namespace geek
-
-extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, double* out_host) {
-  using namespace geek;
-  cudaStream_t s = 0;
-  const uint64_t n = 1000, k = 300;
-  const int d = 128;
-  Scratch X, C, ts, ti, xn, img, c2, mu, misc;
-  GEEK_TRY(X.alloc(n * d * 4, s));
-  GEEK_TRY(C.alloc(k * d * 8, s));
-  GEEK_TRY(ts.alloc(n * 32, s));
-  GEEK_TRY(ti.alloc(n * 32, s));
-  GEEK_TRY(xn.alloc(n * 4, s));
-  GEEK_TRY(misc.alloc(32, s));
-  GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
-  selftest_fill<<<64, 256, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, 40.f);
-  unsigned long long* cmax = misc.as<unsigned long long>();
-  int nct = 0;
-  GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, lbo, sbo, img, c2, mu, cmax, nct, s));
-  GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(),
-                            xn.as<float>(), s));
-  double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
-  unsigned long long* bad = misc.as<unsigned long long>() + 2;
-  selftest_check<<<8, 128, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, mu.as<float>(), ts.as<float>(),
-                                   ti.as<int>(), xn.as<float>(), cmax, worst, bad);
-  GEEK_CHECK_LAUNCH();
-  unsigned long long h[3];
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(h, misc.ptr, 24, cudaMemcpyDeviceToHost, s));
-  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-  double w;
-  memcpy(&w, &h[1], 8);
-  out_host[0] = w;
-  out_host[1] = (double)h[2];
-  return GEEK_OK;
-}
-
-namespace geek {
-
-int tc_screen_prepare(const double* C, uint64_t k, int d, uint32_t lbo, uint32_t sbo, Scratch& img, Scratch& c2,
-                      Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s) {
+int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
+                      Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s) {
+  GEEK_REQUIRE(nprod == 1 || nprod == 3, "screen precision must be 1 or 3 TF32 products");
   nct = (int)((k + kTcN - 1) / kTcN);
   const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
-  GEEK_TRY(img.alloc((size_t)nct * nchunks_k * kTcStageBytes, s));
+  const int parts = nprod == 3 ? 2 : 1;
+  GEEK_TRY(img.alloc((size_t)nct * nchunks_k * parts * kTcHalfStage, s));
   GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
   GEEK_TRY(mu.alloc((size_t)d * 4, s));
   center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
   GEEK_CHECK_LAUNCH();
-  center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(C, k, d, mu.as<float>(), nct, lbo, sbo,
-                                                                          img.as<float>(), c2.as<float>(), cmax_dev);
+  center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(
+      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 
-size_t tc_screen_smem() {
-  return (size_t)kTcABytes + kTcStages * kTcStageBytes + 12 * 8 + 16;
+template <int NPROD>
+static int launch_screen(const TcParams& P, cudaStream_t s) {
+  const size_t smem = TcCfg<NPROD>::kSmem;
+  GEEK_CHECK_CUDA(
+      cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
+  const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
+  tc_screen_kernel<NPROD><<<grid, kTcThreads, smem, s>>>(P);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
 }
 
-int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, const Scratch& c2, const Scratch& mu,
-                     uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i, float* xnorm,
+int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
+                     const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
                      cudaStream_t s) {
   GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
   TcParams P;
@@ -566,18 +512,96 @@ int tc_screen_launch(const float* X, uint64_t n, int d, const Scratch& img, cons
   P.sbo = sbo;
   P.top_s = top_s;
   P.top_i = top_i;
-  P.xnorm = xnorm;
-  const size_t smem = tc_screen_smem();
-  GEEK_CHECK_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t ntiles = (n + kTcM - 1) / kTcM;
-  const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
-  tc_screen_kernel<<<grid, kTcThreads, smem, s>>>(P);
-  GEEK_CHECK_LAUNCH();
-  return GEEK_OK;
+  return nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
+}
+
+// ---- self-test of the operand layout and the measured screen error -------------
+
+__global__ void selftest_fill(float* X, uint64_t n, int d, double* C, uint64_t k, float offset) {
+  const uint64_t tot = n * d + k * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < tot; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t z = e * 0x9E3779B97F4A7C15ull + 12345;
+    z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 29;
+    const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+    if (e < n * d) X[e] = (float)(u * 3.0 + offset);
+    else C[e - n * d] = u * 3.0 + offset;
+  }
+}
+
+// worst |s_screen - S_f64| / (|x'| |c'|max) over every kept entry, and the
+// number of points whose screened top-1 is not the float64 argmin
+__global__ void selftest_check(const float* X, uint64_t n, int d, const double* C, uint64_t k, const float* mu,
+                               const float* top_s, const int* top_i, const unsigned long long* cmax_bits,
+                               double* worst, unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    double xn2 = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double xv = (double)(X[i * d + j] - mu[j]);
+      xn2 += xv * xv;
+    }
+    const double scale = sqrt(xn2) * __longlong_as_double((long long)*cmax_bits) + 1e-30;
+    double best = INFINITY, err = 0.0;
+    int bi = -1;
+    float s1 = INFINITY;
+    int t1 = -1;
+    for (int a = 0; a < 8; ++a)
+      if (top_s[i * 8 + a] < s1) {
+        s1 = top_s[i * 8 + a];
+        t1 = top_i[i * 8 + a];
+      }
+    for (uint64_t c = 0; c < k; ++c) {
+      double cc = 0, xc = 0;
+      for (int j = 0; j < d; ++j) {
+        const double cv = C[c * d + j] - (double)mu[j];
+        const double xv = (double)X[i * d + j] - (double)mu[j];
+        cc += cv * cv;
+        xc += xv * cv;
+      }
+      const double S = cc - 2.0 * xc;
+      if (S < best) {
+        best = S;
+        bi = (int)c;
+      }
+      for (int a = 0; a < 8; ++a)
+        if (top_i[i * 8 + a] == (int)c) err = fmax(err, fabs((double)top_s[i * 8 + a] - S) / scale);
+    }
+    atomicMax(reinterpret_cast<unsigned long long*>(worst), (unsigned long long)__double_as_longlong(err));
+    if (bi != t1) atomicAdd(bad, 1ull);
+  }
 }
 
 }  // namespace geek
+
+extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host) {
+  using namespace geek;
+  cudaStream_t s = 0;
+  const uint64_t n = 1000, k = 300;
+  const int d = 128;
+  Scratch X, C, ts, ti, img, c2, mu, misc;
+  GEEK_TRY(X.alloc(n * d * 4, s));
+  GEEK_TRY(C.alloc(k * d * 8, s));
+  GEEK_TRY(ts.alloc(n * 32, s));
+  GEEK_TRY(ti.alloc(n * 32, s));
+  GEEK_TRY(misc.alloc(32, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
+  selftest_fill<<<64, 256, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, 40.f);
+  unsigned long long* cmax = misc.as<unsigned long long>();
+  int nct = 0;
+  GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, nprod, lbo, sbo, img, c2, mu, cmax, nct, s));
+  GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, nprod, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(),
+                            s));
+  double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
+  unsigned long long* bad = misc.as<unsigned long long>() + 2;
+  selftest_check<<<8, 128, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, mu.as<float>(), ts.as<float>(),
+                                   ti.as<int>(), cmax, worst, bad);
+  GEEK_CHECK_LAUNCH();
+  unsigned long long h[3];
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(h, misc.ptr, 24, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  double w;
+  memcpy(&w, &h[1], 8);
+  out_host[0] = w;
+  out_host[1] = (double)h[2];
+  return GEEK_OK;
+}

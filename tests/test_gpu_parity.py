@@ -257,13 +257,30 @@ def test_assign_screened_f32_vs_oracle(d, k, offset):
 
 
 def test_tcgen05_screen_selftest():
-    """The tcgen05 TF32x3 screen agrees with float64 far inside its error bound."""
+    """The tcgen05 screens agree with float64 far inside the classifier's bounds."""
     import ctypes
 
     out = (ctypes.c_double * 2)()
-    assert G._lib.load_library().geek_tc_selftest(128, 256, out) == 0
-    assert out[0] < 1e-5  # bound used by the classifier: ~9e-5 * |x'||c'| at d = 128
+    L = G._lib.load_library()
+    assert L.geek_tc_selftest(128, 256, 3, out) == 0
+    assert out[0] < 1e-5  # TF32x3 bound used by the classifier: ~9e-5 * |x'||c'| at d = 128
     assert out[1] == 0
+    assert L.geek_tc_selftest(128, 256, 1, out) == 0
+    assert out[0] < 5e-4  # 1x TF32 bound: ~2.0e-3 * |x'||c'| at d = 128
+
+
+@pytest.mark.parametrize("mode", ["1", "3"])
+def test_assign_screen_modes_vs_oracle(mode, monkeypatch):
+    monkeypatch.setenv("GEEK_SCREEN", mode)
+    rng = np.random.default_rng(11)
+    C = rng.standard_normal((150, 128)) * 4 + 200.0
+    C[7] = C[3] + 1e-9
+    X = (C[rng.integers(0, 150, 30_000)] + rng.standard_normal((30_000, 128))).astype(np.float32)
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
 
 
 def test_tie_to_lowest_index():
