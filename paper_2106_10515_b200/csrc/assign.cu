@@ -616,10 +616,12 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                          (int)smem));
   }
   if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull && !getenv("GEEK_NO_TC")) {
-    // tensor-core screen (1 TF32 product by default; GEEK_SCREEN=3 selects
-    // TF32x3) -> classification -> candidate / full recheck
+    // tensor-core screen (TF32x3 by default; GEEK_SCREEN=1 selects the single
+    // TF32 product, 1.4x faster but its bound ~2e-3|x'||c'| only separates
+    // data whose cluster gaps are large against |x'||c'|) -> classification
+    // -> candidate / full recheck
     const char* sel = getenv("GEEK_SCREEN");
-    const int nprod = (sel && sel[0] == '3') ? 3 : 1;
+    const int nprod = (sel && sel[0] == '1') ? 1 : 3;
     Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt;
     GEEK_TRY(cnt.alloc(32, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 32, s));
