@@ -127,6 +127,21 @@ int geek_emit_members_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t
                             uint32_t* out_bin, uint32_t* out_id, uint64_t cap,
                             uint64_t* count_host, void* stream);
 
+/* Fused emission + strict-majority vote over an id-major partition: an id's
+ * multiplicity in a bin is read off its own code row, so only winning (bin,
+ * id) pairs are written (unique, unordered).  GEEK_ERANGE when an id reaches
+ * more than 64 bins (callers fall back to the pair path).  SYNC.           */
+int geek_emit_winners_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t,
+                            const uint32_t* bb_off, const uint32_t* bb_bins, const uint32_t* bin_size,
+                            uint32_t* out_bin, uint32_t* out_id, uint64_t cap,
+                            uint64_t* count_host, void* stream);
+
+/* Winners grouped by bin, ids ascending, bins with < delta winners dropped
+ * (seeding.py:160, engine.py:281).  id_bound bounds the ids.  SYNC.        */
+int geek_group_winners(const uint32_t* win_bin, const uint32_t* win_id, uint64_t nwin, uint64_t nbins,
+                       uint64_t id_bound, uint64_t delta, uint32_t* out_bin, uint32_t* out_id,
+                       uint64_t* nout_host, void* stream);
+
 /* Strict-majority vote (seeding.py:107-114, engine.py:278-282): given (bin,
  * id) pairs (any order; a bucket listed once per bin) and bin sizes in
  * buckets, writes the winners grouped by bin with ids ascending

@@ -56,6 +56,8 @@ _SIGS = {
     "geek_group_rows": (i32, [vp, u64, i32, vp, vp, vp, vp, vp]),
     "geek_emit_members_codes": (i32, [vp, u64, i32, u64, vp, vp, vp, vp, u64, vp, vp]),
     "geek_majority_vote": (i32, [vp, vp, u64, vp, u64, u64, vp, vp, vp, vp]),
+    "geek_emit_winners_codes": (i32, [vp, u64, i32, u64, vp, vp, vp, vp, vp, u64, vp, vp]),
+    "geek_group_winners": (i32, [vp, vp, u64, u64, u64, u64, vp, vp, vp, vp]),
     "geek_pick_representatives": (i32, [vp, vp, vp, vp, u64, vp, vp]),
     "geek_sort_groups": (i32, [vp, vp, u64, vp, vp]),
     "geek_exponent_range": (i32, [vp, i32, u64, i32, vp, vp]),

@@ -93,6 +93,89 @@ __global__ void __launch_bounds__(256) emit_rows_kernel(const uint32_t* __restri
   }
 }
 
+// Strict-majority vote fused into the emission (seeding.py:107-114): an id's
+// count in a bin is the number of its m buckets that belong to the bin, all
+// visible in the id's own code row, so each (bin, id) is decided in place and
+// only the winners are written.
+constexpr int kRowBins = 64;  // bins one id can reach through its m buckets (checked)
+
+__global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __restrict__ codes, uint64_t n, int m,
+                                                           uint64_t t, const uint32_t* __restrict__ bb_off,
+                                                           const uint32_t* __restrict__ bb_bins,
+                                                           const uint32_t* __restrict__ bin_size,
+                                                           const uint32_t* __restrict__ gwords, uint64_t nwords,
+                                                           int smem_words, uint32_t* out_bin, uint32_t* out_id,
+                                                           uint64_t cap, unsigned long long* cursor,
+                                                           unsigned long long* overflow) {
+  extern __shared__ uint32_t sw[];
+  const bool in_smem = smem_words > 0;
+  if (in_smem)
+    for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) sw[w] = gwords[w];
+  __syncthreads();
+  const uint32_t* words = in_smem ? sw : gwords;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    uint32_t rb[kRowBins];
+    int nb = 0;
+    if (valid) {
+      const uint32_t* row = codes + i * m;
+      for (int j = 0; j < m; ++j) {
+        const uint64_t b = (uint64_t)j * t + row[j];
+        if ((words[b >> 5] >> (b & 31)) & 1u)
+          for (uint32_t k = bb_off[b]; k < bb_off[b + 1]; ++k) {
+            if (nb < kRowBins) rb[nb] = bb_bins[k];
+            ++nb;
+          }
+      }
+    }
+    if (nb > kRowBins) {  // cannot happen for m <= 64 with one bin per bucket and table; keep loud
+      atomicAdd(overflow, 1ull);
+      nb = kRowBins;
+    }
+    // winners: first occurrence of each bin whose multiplicity is a strict majority
+    uint32_t cnt = 0;
+    for (int a = 0; a < nb; ++a) {
+      int c = 0;
+      bool first = true;
+      for (int q = 0; q < nb; ++q) {
+        c += rb[q] == rb[a];
+        first &= !(q < a && rb[q] == rb[a]);
+      }
+      if (first && 2u * (uint32_t)c > bin_size[rb[a]]) ++cnt;
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    unsigned long long wbase = 0;
+    if (lane == 31) wbase = atomicAdd(cursor, (unsigned long long)total);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    unsigned long long pos = wbase + incl - cnt;
+    for (int a = 0; a < nb && cnt; ++a) {
+      int c = 0;
+      bool first = true;
+      for (int q = 0; q < nb; ++q) {
+        c += rb[q] == rb[a];
+        first &= !(q < a && rb[q] == rb[a]);
+      }
+      if (first && 2u * (uint32_t)c > bin_size[rb[a]]) {
+        if (pos < cap) {
+          out_bin[pos] = rb[a];
+          out_id[pos] = static_cast<uint32_t>(i);
+        }
+        ++pos;
+      }
+    }
+  }
+}
+
 __global__ void gather_u32(const uint32_t* src, const uint32_t* perm, uint32_t* dst, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -149,6 +232,13 @@ __global__ void expand_keep(const uint32_t* gstart, const uint32_t* keep, uint64
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < ng;
        r += (uint64_t)gridDim.x * blockDim.x)
     for (uint32_t e = gstart[r]; e < gstart[r + 1]; ++e) ekeep[e] = keep[r];
+}
+
+// element-parallel: element e belongs to run gidx[e] + flag[e] - 1
+__global__ void expand_keep_elems(const uint32_t* gidx, const uint32_t* flag, const uint32_t* keep, uint64_t n,
+                                  uint32_t* ekeep) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
+    ekeep[e] = keep[gidx[e] + flag[e] - 1];
 }
 
 __global__ void compact_pairs(const uint32_t* a, const uint32_t* b, const uint32_t* keep,
@@ -247,6 +337,89 @@ int geek_emit_members_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t
   return GEEK_OK;
 }
 
+int geek_emit_winners_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t, const uint32_t* bb_off,
+                            const uint32_t* bb_bins, const uint32_t* bin_size, uint32_t* out_bin, uint32_t* out_id,
+                            uint64_t cap, uint64_t* count_host, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  Scratch cur, bm;
+  GEEK_TRY(cur.alloc(16, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(cur.ptr, 0, 16, s));
+  unsigned long long* cursor = cur.as<unsigned long long>();
+  if (n) {
+    const uint64_t nb = (uint64_t)m * t, nw = (nb + 31) / 32;
+    GEEK_TRY(bm.alloc(nw * 4, s));
+    binned_bitmap_kernel<<<grid_for(nw, 256), 256, 0, s>>>(bb_off, nb, bm.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    const int smem_words = nw * 4 <= 96 * 1024 ? (int)nw : 0;
+    if (smem_words * 4 > 48 * 1024)
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(emit_winners_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem_words * 4));
+    emit_winners_kernel<<<grid_for(n, 256, 148 * 8), 256, smem_words * 4, s>>>(
+        codes, n, m, t, bb_off, bb_bins, bin_size, bm.as<uint32_t>(), nw, smem_words, out_bin, out_id, cap, cursor,
+        cursor + 1);
+    GEEK_CHECK_LAUNCH();
+  }
+  unsigned long long c[2] = {0, 0};
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(c, cursor, 16, cudaMemcpyDeviceToHost, s));
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  *count_host = c[0];
+  if (c[1]) {
+    set_error("emit_winners: %llu ids reach more than %d bins; use the pair path", c[1], kRowBins);
+    return GEEK_ERANGE;
+  }
+  if (c[0] > cap) {
+    set_error("emit_winners: %llu winners exceed capacity %llu", c[0], (unsigned long long)cap);
+    return GEEK_ERANGE;
+  }
+  return GEEK_OK;
+}
+
+int geek_group_winners(const uint32_t* win_bin, const uint32_t* win_id, uint64_t nwin, uint64_t nbins,
+                       uint64_t id_bound, uint64_t delta, uint32_t* out_bin, uint32_t* out_id, uint64_t* nout_host,
+                       void* stream) {
+  cudaStream_t s = as_stream(stream);
+  *nout_host = 0;
+  if (nwin == 0) return GEEK_OK;
+  GEEK_REQUIRE(nwin < 0xFFFFFFFFull, "too many winners");
+  const uint64_t nw = nwin;
+  Scratch perm, wb, wi, gflag, gidx, gstart, gkeep, ekeep, epos;
+  GEEK_TRY(perm.alloc(nw * 4, s));
+  GEEK_TRY(wb.alloc(nw * 4, s));
+  GEEK_TRY(wi.alloc(nw * 4, s));
+  const uint32_t* cols[2] = {win_bin, win_id};
+  const int bits[2] = {bitlen_u64(nbins ? nbins - 1 : 0) ? bitlen_u64(nbins - 1) : 1,
+                       bitlen_u64(id_bound ? id_bound - 1 : 0) ? bitlen_u64(id_bound - 1) : 1};
+  GEEK_TRY(argsort_cols(cols, 2, bits, nw, perm.as<uint32_t>(), s));
+  gather_u32<<<grid_for(nw, 256), 256, 0, s>>>(win_bin, perm.as<uint32_t>(), wb.as<uint32_t>(), nw);
+  gather_u32<<<grid_for(nw, 256), 256, 0, s>>>(win_id, perm.as<uint32_t>(), wi.as<uint32_t>(), nw);
+  GEEK_CHECK_LAUNCH();
+  // delta filter per bin (engine.py:281)
+  GEEK_TRY(gflag.alloc(nw * 4, s));
+  GEEK_TRY(gidx.alloc(nw * 4, s));
+  run_flags2<<<grid_for(nw, 256), 256, 0, s>>>(wb.as<uint32_t>(), nullptr, gflag.as<uint32_t>(), nw);
+  GEEK_CHECK_LAUNCH();
+  uint64_t ng = 0;
+  GEEK_TRY(exclusive_scan_u32(gflag.as<uint32_t>(), gidx.as<uint32_t>(), nw, s, &ng));
+  GEEK_TRY(gstart.alloc((ng + 1) * 4, s));
+  scatter_run_start<<<grid_for(nw, 256), 256, 0, s>>>(gflag.as<uint32_t>(), gidx.as<uint32_t>(),
+                                                      gstart.as<uint32_t>(), nw, ng);
+  GEEK_TRY(gkeep.alloc(ng * 4, s));
+  bin_keep_flags<<<grid_for(ng, 256), 256, 0, s>>>(gstart.as<uint32_t>(), ng, delta, gkeep.as<uint32_t>());
+  GEEK_TRY(ekeep.alloc(nw * 4, s));
+  GEEK_TRY(epos.alloc(nw * 4, s));
+  expand_keep_elems<<<grid_for(nw, 256), 256, 0, s>>>(gidx.as<uint32_t>(), gflag.as<uint32_t>(),
+                                                      gkeep.as<uint32_t>(), nw, ekeep.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nk = 0;
+  GEEK_TRY(exclusive_scan_u32(ekeep.as<uint32_t>(), epos.as<uint32_t>(), nw, s, &nk));
+  compact_pairs<<<grid_for(nw, 256), 256, 0, s>>>(wb.as<uint32_t>(), wi.as<uint32_t>(), ekeep.as<uint32_t>(),
+                                                  epos.as<uint32_t>(), nw, out_bin, out_id);
+  GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  *nout_host = nk;
+  return GEEK_OK;
+}
+
 int geek_majority_vote(const uint32_t* pair_bin, const uint32_t* pair_id, uint64_t npairs,
                        const uint32_t* bin_size, uint64_t nbins, uint64_t delta, uint32_t* win_bin,
                        uint32_t* win_id, uint64_t* nwin_host, void* stream) {
@@ -304,8 +477,8 @@ int geek_majority_vote(const uint32_t* pair_bin, const uint32_t* pair_id, uint64
   bin_keep_flags<<<grid_for(ng, 256), 256, 0, s>>>(gstart.as<uint32_t>(), ng, delta, gkeep.as<uint32_t>());
   GEEK_TRY(ekeep.alloc(nw * 4, s));
   GEEK_TRY(epos.alloc(nw * 4, s));
-  expand_keep<<<grid_for(ng, 256), 256, 0, s>>>(gstart.as<uint32_t>(), gkeep.as<uint32_t>(), ng,
-                                                ekeep.as<uint32_t>());
+  expand_keep_elems<<<grid_for(nw, 256), 256, 0, s>>>(gidx.as<uint32_t>(), gflag.as<uint32_t>(),
+                                                      gkeep.as<uint32_t>(), nw, ekeep.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
   uint64_t nk = 0;
   GEEK_TRY(exclusive_scan_u32(ekeep.as<uint32_t>(), epos.as<uint32_t>(), nw, s, &nk));

@@ -22,6 +22,7 @@ import torch
 
 from . import _lib
 from .data import Bin, Bucket, CategoricalData, CentralVector, DenseData, InvalidInput, SeedGroup, SparseData
+from .errors import EngineError
 from .hashing import PermBatch, SignatureScheme, derive_seed, set_signatures_device, csr_from_sets
 from .tables import BucketTable, GroupSet, csr_gather
 
@@ -217,6 +218,46 @@ def vote(pair_bin, pair_id, bins: Bins, delta: int):
     return GroupSet(wi.contiguous(), off), ub
 
 
+def fused_votes_codes(bins: Bins, bt: BucketTable, bucket_sizes: torch.Tensor, delta: int):
+    """Emission with the majority decided per id row (geek_emit_winners_codes),
+    then winners grouped by bin.  None if an id reaches too many bins."""
+    if bins.pair_bucket.numel() == 0:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=bins.pair_bin.device), 0
+    nb = bt.m * bt.stride
+    order = torch.argsort(bins.pair_bucket, stable=True)
+    pbk = bins.pair_bucket[order]
+    pbn = bins.pair_bin[order].to(torch.int32).contiguous()
+    cnt = torch.bincount(pbk, minlength=nb)
+    bb_off = torch.zeros(nb + 1, dtype=torch.int64, device=pbk.device)
+    torch.cumsum(cnt, 0, out=bb_off[1:])
+    bb_off = bb_off.to(torch.int32).contiguous()
+    cap = max(1, int(bucket_sizes[bins.pair_bucket].sum().item()))
+    wb = _lib.empty(cap, _lib.U32)
+    wi = _lib.empty(cap, _lib.U32)
+    count = np.zeros(1, dtype=np.uint64)
+    try:
+        _lib.call("geek_emit_winners_codes", _lib.ptr(bt.codes), bt.n, bt.m, bt.stride, _lib.ptr(bb_off),
+                  _lib.ptr(pbn), _lib.ptr(bins.bin_size.contiguous()), _lib.ptr(wb), _lib.ptr(wi), cap,
+                  _lib.hptr(count), _lib.stream())
+    except EngineError:
+        return None
+    nw = int(count[0])
+    if nw == 0:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=wb.device), 0
+    ob = _lib.empty(nw, _lib.U32)
+    oi = _lib.empty(nw, _lib.U32)
+    nk = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_group_winners", _lib.ptr(wb), _lib.ptr(wi), nw, bins.count, bt.n, int(delta), _lib.ptr(ob),
+              _lib.ptr(oi), _lib.hptr(nk), _lib.stream())
+    k = int(nk[0])
+    if k == 0:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=wb.device), nw
+    ub, c = torch.unique_consecutive(ob[:k].to(torch.int64), return_counts=True)
+    off = torch.zeros(ub.numel() + 1, dtype=torch.int64, device=wb.device)
+    torch.cumsum(c, 0, out=off[1:])
+    return GroupSet(oi[:k].contiguous(), off), ub, nw
+
+
 def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=None):
     """Every surviving vote of every SILK table (collect_votes / local_votes)
     -> (GroupSet, Bins, winning bin ids)."""
@@ -227,6 +268,15 @@ def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=N
         sizes = buckets.bucket_sizes()
     else:
         sizes = _lib.to_dev(np.array([b.members.size for b in buckets], dtype=np.int64))
+    if csr is None:
+        fused = fused_votes_codes(bins, buckets, sizes, params.min_group_size)
+        if fused is not None:
+            groups, won, nw = fused
+            if info is not None:
+                info["bins"] = bins.count
+                info["vote_winners"] = nw
+                info["raw_groups"] = groups.count
+            return groups, bins, won
     pbin, pid = membership_pairs(bins, buckets, csr, sizes)
     groups, won = vote(pbin, pid, bins, params.min_group_size)
     if info is not None:
