@@ -112,20 +112,19 @@ __global__ void straddle_kernel(SplitGeom g, const uint32_t* fcnt, const uint32_
 
 // Coarse cells whose non-empty fine bins all map to one slot are rewritten to
 // (0, slot): codes_kernel then needs a single lookup for most ids.
-__global__ void cell_shortcut_kernel(uint2* cinfo, const uint32_t* fcnt, const uint32_t* fcode, uint64_t ncell) {
+// A cell's ids occupy the rank range of its fine bins, so the cell is
+// uniform exactly when its first and last rank fall in the same slot: O(1).
+__global__ void cell_shortcut_kernel(SplitGeom g, uint2* cinfo, const uint32_t* fcnt, const uint32_t* fstart,
+                                     uint64_t ncell) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < ncell;
        c += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 ci = cinfo[c];
-    uint32_t code = GEEK_NONE;
-    bool uniform = true, any = false;
-    for (uint32_t f = ci.y; f < ci.y + ci.x && uniform; ++f) {
-      if (fcnt[f] == 0) continue;
-      const uint32_t fc = fcode[f];
-      if (fc == GEEK_NONE || (any && fc != code)) uniform = false;
-      code = fc;
-      any = true;
-    }
-    if (uniform && any) cinfo[c] = make_uint2(0u, code);
+    const uint64_t base = (c / g.nc) * g.n;  // ranks of table jb start at jb * n in fstart
+    const uint32_t fl = ci.y + ci.x - 1;
+    const uint64_t r0 = (uint64_t)fstart[ci.y] - base;
+    const uint64_t r1 = (uint64_t)fstart[fl] + fcnt[fl] - base;  // one past the last rank
+    if (r1 > r0 && slot_of_rank(r0, g.n, g.t) == slot_of_rank(r1 - 1, g.n, g.t))
+      cinfo[c] = make_uint2(0u, slot_of_rank(r0, g.n, g.t));
   }
 }
 
@@ -280,8 +279,8 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
                                                       stats.as<unsigned long long>());
   GEEK_CHECK_LAUNCH();
   uint64_t nstage = 0;
-  cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(cinfo.as<uint2>(), fcnt.as<uint32_t>(),
-                                                             fcode.as<uint32_t>(), ncell);
+  cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, cinfo.as<uint2>(), fcnt.as<uint32_t>(),
+                                                             fstart.as<uint32_t>(), ncell);
   GEEK_CHECK_LAUNCH();
   GEEK_TRY(exclusive_scan_u32(scnt.as<uint32_t>(), sbase.as<uint32_t>(), nfb, s, &nstage));
   unsigned long long st[4] = {0, 0, 0, 0};
