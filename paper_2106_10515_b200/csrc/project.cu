@@ -4,6 +4,7 @@
 // block through shared memory; directions stay resident in shared memory.
 #include "common.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace geek {
@@ -269,6 +270,151 @@ __global__ void __launch_bounds__(128) project_dmma_kernel(const T* __restrict__
   }
 }
 
+// Streaming DMMA projection for float32 X (d % 4 == 0, d <= 128): persistent
+// CTAs (two per SM) keep the transposed directions resident in SMEM and pull
+// 32-dim chunks of 128-point tiles through a 3-stage cp.async ring, so the
+// HBM stream of X overlaps the DMMAs.  The k order of the accumulation is the
+// one of project_dmma_kernel (chunks of 4 dims, ascending): same bits.
+constexpr int kPsLdp = 36;     // floats per point row of a stage: fragment loads are conflict-free
+constexpr int kPsStages = 3;
+constexpr int kPsStageFloats = 128 * kPsLdp;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __restrict__ X, uint64_t n, int d,
+                                                                const double* __restrict__ A, int m,
+                                                                uint64_t* __restrict__ keys, int* exprange) {
+  constexpr int LDA = NT * 8 + 4;
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* sA = reinterpret_cast<double*>(smem);                      // [d][LDA]
+  float* sX = reinterpret_cast<float*>(smem + (size_t)d * LDA * 8);  // [stages][128][kPsLdp]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < d * NT * 8; e += 128) {
+    const int k = e / (NT * 8), t = e - k * (NT * 8);
+    sA[k * LDA + t] = t < m ? A[(uint64_t)t * d + k] : 0.0;
+  }
+  const int nck = (d + 31) / 32;
+  const uint64_t ntiles = (n + 127) / 128;
+  const uint64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint64_t total = my_tiles * nck;
+  auto issue = [&](uint64_t q) {
+    if (q < total) {
+      const uint64_t tile = blockIdx.x + (q / nck) * gridDim.x;
+      const int kc = (int)(q % nck);
+      float* st = sX + (q % kPsStages) * kPsStageFloats;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int piece = tid + u * 128, r = piece >> 3, c4 = piece & 7;
+        const uint64_t row = tile * 128 + r;
+        const int dim = kc * 32 + c4 * 4;
+        const bool ok = row < n && dim < d;
+        cp_async16(st + r * kPsLdp + c4 * 4, ok ? X + row * d + dim : X, ok ? 16u : 0u);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  };
+#pragma unroll
+  for (int q = 0; q < kPsStages - 1; ++q) issue(q);
+  double acc[4][NT][2];
+  int elo = 1 << 30, ehi = -(1 << 30);
+  const int kr = lane & 3, rr = lane >> 2;
+  for (uint64_t q = 0; q < total; ++q) {
+    cp_async_wait<kPsStages - 2>();
+    __syncthreads();                // chunk q landed for all threads; stage (q-1) % S is free
+    issue(q + kPsStages - 1);
+    const int kc = (int)(q % nck);
+    if (kc == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    const float* st = sX + (q % kPsStages) * kPsStageFloats + (warp * 32 + rr) * kPsLdp + kr;
+    const double* sa = sA + (kc * 32 + kr) * LDA + rr;
+#pragma unroll 2
+    for (int ks = 0; ks < 32; ks += 4) {
+      double a[4], b[NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float v = st[i * 8 * kPsLdp + ks];
+        exp_window(v, elo, ehi);
+        a[i] = (double)v;
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = kc * 32 + ks < d ? sa[ks * LDA + j * 8] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j], a[i], b[j]);
+    }
+    if (kc == nck - 1) {
+      const uint64_t tile = blockIdx.x + (q / nck) * gridDim.x;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t pt = tile * 128 + warp * 32 + i * 8 + rr;
+        if (pt >= n) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int t = j * 8 + kr * 2 + h;
+            if (t < m) keys[(uint64_t)t * n + pt] = f64_key(acc[i][j][h]);
+          }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (exprange) {
+    for (int o = 16; o; o >>= 1) {
+      elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+      ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+    }
+    if (lane == 0) {
+      atomicMin(&exprange[0], elo);
+      atomicMax(&exprange[1], ehi);
+    }
+  }
+}
+
+template <int NT>
+static int launch_stream(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
+                         cudaStream_t s) {
+  const size_t smem = (size_t)d * (NT * 8 + 4) * 8 + (size_t)kPsStages * kPsStageFloats * 4;
+  GEEK_CHECK_CUDA(cudaFuncSetAttribute(project_stream_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ntiles = (n + 127) / 128;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * 2);
+  project_stream_kernel<NT><<<grid, 128, smem, s>>>(X, n, d, A, m, keys, er);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+static int launch_stream_any(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
+                             cudaStream_t s) {
+  switch ((m + 7) / 8) {
+    case 1: return launch_stream<1>(X, n, d, A, m, keys, er, s);
+    case 2: return launch_stream<2>(X, n, d, A, m, keys, er, s);
+    case 3: return launch_stream<3>(X, n, d, A, m, keys, er, s);
+    case 4: return launch_stream<4>(X, n, d, A, m, keys, er, s);
+    case 5: return launch_stream<5>(X, n, d, A, m, keys, er, s);
+    default: return launch_stream<6>(X, n, d, A, m, keys, er, s);
+  }
+}
+
 template <class T>
 static void launch_dmma(const T* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
                         cudaStream_t s) {
@@ -304,6 +450,8 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 (f32) or 1 (f64)");
   GEEK_REQUIRE(d >= 1 && m >= 1, "empty projection");
   if (n == 0) return GEEK_OK;
+  if (m <= 48 && dtype == 0 && d % 4 == 0 && d <= 128 && !getenv("GEEK_NO_DMMA") && !getenv("GEEK_NO_PSTREAM"))
+    return launch_stream_any((const float*)X, n, d, A, m, keys, exprange, s);
   if (m <= 48 && !getenv("GEEK_NO_DMMA")) {  // DMMA path (up to 6 column fragments)
     if (dtype == 0) launch_dmma<float>((const float*)X, n, d, A, m, keys, exprange, s);
     else launch_dmma<double>((const double*)X, n, d, A, m, keys, exprange, s);

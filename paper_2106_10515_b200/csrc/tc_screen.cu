@@ -5,10 +5,11 @@
 //
 // Two precisions of the same kernel (template NPROD):
 //   NPROD = 1: one TF32 product (operands rounded to TF32, fp32 accumulation);
-//              A = 64 KB per point tile, double-buffered, so the conversion
-//              of the next tile overlaps the MMAs of this one
+//              A = 64 KB per point tile, double-buffered
 //   NPROD = 3: TF32x3 (hi*hi + hi*lo + lo*hi): fp32-level screen, A = 128 KB
-//              single-buffered
+//              single-buffered, handed over per 32-dim chunk so the next
+//              tile's chunk kc is written as soon as the last MMAs reading
+//              chunk kc of this tile retire
 // Per CTA (persistent over 128-point tiles):
 //   A  = the point tile, K-major, in SMEM
 //   B  = center tiles of 128 centers, streamed in 32-dim chunks by 1-D bulk
@@ -44,7 +45,7 @@ struct TcCfg {
   static constexpr int kABuf = NPROD == 3 ? 1 : 2;
   static constexpr int kStageBytes = kParts * kTcHalfStage;
   static constexpr int kStages = NPROD == 3 ? 3 : 4;
-  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 24 * 8;
+  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 32 * 8;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -213,9 +214,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint64_t* empty = bars + 4;               // [kStages] stage consumed (MMA commit)
   uint64_t* accf = bars + 8;                // [2] accumulator ready (MMA commit)
   uint64_t* acce = bars + 10;               // [2] accumulator drained (256 epilogue threads)
-  uint64_t* afull = bars + 12;              // [kABuf] point tile written (256 threads)
-  uint64_t* aempty = bars + 14;             // [kABuf] point tile no longer read (MMA commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* afull = bars + 12;              // [kABuf][4] point-tile chunk written (256 threads)
+  uint64_t* aempty = bars + 20;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], kTcEpiThreads);
     }
-    for (int b = 0; b < Cfg::kABuf; ++b) {
+    for (int b = 0; b < Cfg::kABuf * 4; ++b) {
       mbar_init(&afull[b], kTcEpiThreads);
       mbar_init(&aempty[b], 1);
     }
@@ -241,8 +242,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nck = (P.d + kTcChunk - 1) / kTcChunk;  // B chunks per center tile
-  const int kslices = nck * (kTcChunk / 8);
+  const int nck = (P.d + kTcChunk - 1) / kTcChunk;  // 32-dim chunks (A and B)
   const uint32_t total_q = (uint32_t)P.nct * nck;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -264,8 +264,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       while (q_issue < (uint64_t)Cfg::kStages - 1 && q_issue < total_chunks) issue();
       for (uint32_t t = 0; t < my_tiles; ++t) {
         const int ab = t % Cfg::kABuf;
-        mbar_wait(&afull[ab], (t / Cfg::kABuf) & 1);
-        fence_after();
+        const uint32_t apar = (t / Cfg::kABuf) & 1;
         const uint32_t abase = smem_u32(A + ab * Cfg::kABytes);
         for (int ct = 0; ct < P.nct; ++ct) {
           const uint64_t g = (uint64_t)t * P.nct + ct;
@@ -274,6 +273,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
           for (int kc = 0; kc < nck; ++kc) {
+            if (ct == 0) {  // first use of this chunk of the point tile
+              mbar_wait(&afull[ab * 4 + kc], apar);
+              fence_after();
+            }
             const uint32_t s = (uint32_t)(q_mma % Cfg::kStages);
             mbar_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1);
             fence_after();
@@ -292,16 +295,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               }
             }
             tc_commit(&empty[s]);
+            if (ct == P.nct - 1) tc_commit(&aempty[ab * 4 + kc]);  // last read of this chunk
             ++q_mma;
             if (q_issue < total_chunks) issue();  // into the stage of an earlier, queued chunk
           }
           tc_commit(&accf[buf]);
         }
-        tc_commit(&aempty[ab]);
       }
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
-    Top4 cur, prev;
+    Top4 cur;
     cur.init();
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
       const uint64_t g = (uint64_t)t * P.nct + ct;
@@ -343,78 +346,98 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
-    // x' = x - mu rounded to tf32 (+ the tf32 residual for NPROD = 3) into
-    // buffer t % kABuf; warp w owns rows 16w..16w+15, lane = float4 column
-    auto load_a = [&](uint32_t t) {
-      const int ab = t % Cfg::kABuf;
-      mbar_wait(&aempty[ab], ((t / Cfg::kABuf) & 1) ^ 1u);  // MMAs that read this buffer are done
-      uint8_t* Ab = A + ab * Cfg::kABytes;
-      const uint64_t p0 = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM;
-      if (P.d == kTcKmax) {
-        const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.mu) + lane);
-        const uint32_t off0 = ((lane * 4) >> 3) * kTcSliceBytes;
-#pragma unroll 1
-        for (int r0 = 0; r0 < 16; r0 += 8) {
-          float4 q[8];
+    // Point tiles travel global -> registers -> SMEM.  Warp w owns rows
+    // 16w..16w+15; for chunk kc (32 dims) lane l holds rows (l&7) and
+    // (l&7)+8 at float4 columns kc*8 + (l>>3) and +4, so each 8-lane group
+    // writes one 128-byte row of core matrices (conflict-free).  The global
+    // loads of tile t+1 are issued before the epilogues of tile t and land
+    // in registers meanwhile; the SMEM writes then wait chunk by chunk for
+    // the MMAs of tile t that still read that chunk.
+    float4 q[16];
+    const int rsub = lane & 7, csub = lane >> 3;
+    auto tile_row0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + warp * 16; };
+    auto load_regs = [&](uint32_t t) {
+      const uint64_t p0 = tile_row0(t);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint64_t i = p0 + warp * 16 + r0 + u;
-            q[u] = i < P.n ? __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax) + lane)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int kc = 0; kc < 4; ++kc) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint64_t i = p0 + rsub + 8 * (p & 1);
+          const int e0 = (kc * 8 + csub + 4 * (p >> 1)) * 4;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (kc < nck && i < P.n) {
+            if (P.d == kTcKmax) {
+              v = __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax + e0));
+            } else {
+              const float* xr = P.X + i * P.d;
+              if (e0 < P.d) v.x = xr[e0];
+              if (e0 + 1 < P.d) v.y = xr[e0 + 1];
+              if (e0 + 2 < P.d) v.z = xr[e0 + 2];
+              if (e0 + 3 < P.d) v.w = xr[e0 + 3];
+            }
           }
+          q[kc * 4 + p] = v;
+        }
+      }
+      {  // pull the tile after it towards L2 while this one is in flight
+        const uint64_t row = (blockIdx.x + (uint64_t)(t + 1) * gridDim.x) * kTcM + (warp * 32 + lane) / 2;
+        if (row < P.n) {
+          const char* base = reinterpret_cast<const char*>(P.X + row * P.d) + (lane & 1) * 256;
+          for (int b = 0; b < 256 && (lane & 1) * 256 + b < P.d * 4; b += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
+        }
+      }
+    };
+    auto store_chunks = [&](uint32_t t) {
+      const int ab = t % Cfg::kABuf;
+      const uint32_t epar = ((t / Cfg::kABuf) & 1) ^ 1u;
+      uint8_t* Ab = A + ab * Cfg::kABytes;
+      const uint64_t p0 = tile_row0(t);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int row = warp * 16 + r0 + u;
-            const bool valid = p0 + row < P.n;
-            const float x0 = valid ? q[u].x - m4.x : 0.f, x1 = valid ? q[u].y - m4.y : 0.f;
-            const float x2 = valid ? q[u].z - m4.z : 0.f, x3 = valid ? q[u].w - m4.w : 0.f;
+      for (int kc = 0; kc < 4; ++kc) {
+        if (kc < nck) {
+          mbar_wait(&aempty[ab * 4 + kc], epar);  // the MMAs of the previous tile in this buffer are done
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int row = warp * 16 + rsub + 8 * (p & 1);
+            const int e0 = (kc * 8 + csub + 4 * (p >> 1)) * 4;
+            const bool valid = p0 + rsub + 8 * (p & 1) < P.n;
+            float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (P.d == kTcKmax) {
+              m4 = __ldg(reinterpret_cast<const float4*>(P.mu + e0));
+            } else {
+              if (e0 < P.d) m4.x = __ldg(P.mu + e0);
+              if (e0 + 1 < P.d) m4.y = __ldg(P.mu + e0 + 1);
+              if (e0 + 2 < P.d) m4.z = __ldg(P.mu + e0 + 2);
+              if (e0 + 3 < P.d) m4.w = __ldg(P.mu + e0 + 3);
+            }
+            const float4 x = q[kc * 4 + p];
+            const float x0 = valid ? x.x - m4.x : 0.f, x1 = valid ? x.y - m4.y : 0.f;
+            const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
-            const uint32_t off = off0 + core_off(row, (lane * 4) & 7, P.lbo, P.sbo);
+            const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
             *reinterpret_cast<float4*>(Ab + off) = make_float4(h0, h1, h2, h3);
             if (NPROD == 3)
               *reinterpret_cast<float4*>(Ab + kTcAPart + off) =
                   make_float4(tf32_round(x0 - h0), tf32_round(x1 - h1), tf32_round(x2 - h2), tf32_round(x3 - h3));
           }
-        }
-      } else {
-        for (int r = 0; r < 16; ++r) {
-          const int row = warp * 16 + r;
-          const uint64_t i = p0 + row;
-          const bool valid = i < P.n;
-          for (int e0 = lane * 4; e0 < kslices * 8; e0 += 128) {
-            float hi4[4], lo4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float xv = (valid && e0 + u < P.d) ? P.X[i * P.d + e0 + u] - __ldg(P.mu + e0 + u) : 0.f;
-              hi4[u] = tf32_round(xv);
-              lo4[u] = tf32_round(xv - hi4[u]);
-            }
-            const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
-            *reinterpret_cast<float4*>(Ab + off) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
-            if (NPROD == 3)
-              *reinterpret_cast<float4*>(Ab + kTcAPart + off) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
-          }
-        }
-      }
-      fence_proxy_async();
-      mbar_arrive(&afull[ab]);
-      {  // pull the following tile of this CTA towards L2 while the MMAs run
-        const uint64_t row = p0 + (uint64_t)gridDim.x * kTcM + tid;
-        if (tid < kTcM && row < P.n) {
-          const char* base = reinterpret_cast<const char*>(P.X + row * P.d);
-          for (int b = 0; b < P.d * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
+          fence_proxy_async();
+          mbar_arrive(&afull[ab * 4 + kc]);
         }
       }
     };
-    for (uint32_t t = 0; t < my_tiles; ++t) {
-      if (Cfg::kABuf == 1 || t == 0) load_a(t);  // double buffering loads t+1 one tile early
-      prev = cur;
-      cur.init();
-      if (t > 0) finish(t - 1, prev);
-      if (Cfg::kABuf == 2 && t + 1 < my_tiles) load_a(t + 1);  // overlaps the MMAs of tile t
-      for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
+    if (my_tiles > 0) {
+      load_regs(0);
+      store_chunks(0);
     }
-    if (my_tiles > 0) finish(my_tiles - 1, cur);
+    for (uint32_t t = 0; t < my_tiles; ++t) {
+      const bool more = t + 1 < my_tiles;
+      if (more) load_regs(t + 1);  // in flight during the epilogues below
+      for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
+      if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
+      finish(t, cur);
+      cur.init();
+    }
   }
   fence_before();
   __syncthreads();
