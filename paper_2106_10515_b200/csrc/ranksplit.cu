@@ -15,10 +15,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace geek {
 
-constexpr uint32_t kFineTarget = 32;     // ids per fine bin (G)
+// ids per fine bin (G).  256 keeps the per-bin tables of a batch of 8 tables
+// (~17 MB) L2-resident for the random lookups of fine_hist / codes; the
+// straddling bins it stages (~G per boundary) are ranked in L1-broadcast loops.
+constexpr uint32_t kFineTargetDefault = 256;
 constexpr uint32_t kLocalRankMax = 2048; // larger straddling bins take the sort path
 
 struct SplitGeom {
@@ -27,6 +31,7 @@ struct SplitGeom {
   int c0;         // code column of key table j0 in codes[i*m + c]
   int cb;         // coarse bits
   uint32_t nc;    // coarse cells per table
+  uint32_t fine_target;  // ids per fine bin
 };
 
 __device__ __forceinline__ uint32_t coarse_of(uint64_t key, int cb) {
@@ -58,12 +63,12 @@ __global__ void coarse_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom 
     atomicAdd(&h[coarse_of(kj[s * stride], g.cb)], 1u);
 }
 
-__global__ void fine_layout_kernel(const uint32_t* hist, uint64_t total, uint64_t stride,
+__global__ void fine_layout_kernel(const uint32_t* hist, uint64_t total, uint64_t stride, uint32_t target,
                                    uint32_t* nfine) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
        c += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t est = (uint64_t)hist[c] * stride;
-    uint64_t nf = (est + kFineTarget - 1) / kFineTarget;
+    uint64_t nf = (est + target - 1) / target;
     nfine[c] = static_cast<uint32_t>(nf < 1 ? 1 : (nf > (1u << 20) ? (1u << 20) : nf));
   }
 }
@@ -241,7 +246,7 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   dim3 gs(grid_for((g.n + stride - 1) / stride, 256, 148 * 8), g.tb);
   coarse_hist_kernel<<<gs, 256, 0, s>>>(keys, g, stride, hist.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
-  fine_layout_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(hist.as<uint32_t>(), ncell, stride,
+  fine_layout_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(hist.as<uint32_t>(), ncell, stride, g.fine_target,
                                                           nfine.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
   uint64_t nfb = 0;
@@ -338,7 +343,9 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   int cb = (int)std::ceil(std::log2((double)n / 16.0 + 1.0));
   g.cb = std::min(20, std::max(10, cb));
   g.nc = 1u << g.cb;
-  const double per_table = 4.0 * ((double)n / kFineTarget + 2.0 * g.nc) * 5.0;
+  g.fine_target = kFineTargetDefault;
+  if (const char* ft = getenv("GEEK_FINE_TARGET")) g.fine_target = (uint32_t)std::max(1, atoi(ft));
+  const double per_table = 4.0 * ((double)n / g.fine_target + 2.0 * g.nc) * 5.0;
   // batches of whole tables: codes rows are then written in tb-word runs
   // (8 tables = one 32-byte sector), counters stay u32 (tb * n < 2^32)
   int tb = (int)std::max(1.0, std::min((double)m, (1024.0 * (1 << 20)) / per_table));

@@ -1,7 +1,14 @@
-// K8 on the 5th-gen tensor cores: the assignment screen s(x, c) = |c'|^2 -
-// 2 x'.c' (x' = x - mu, c' = c - mu) as a tcgen05 GEMM with fused top-4
-// epilogues; the classifier (assign.cu) turns the screen into exact float64
+// K8 on the 5th-gen tensor cores: the assignment screen
+//   s(x, c) / 2 = |c'|^2 / 2 - x'.c'      (x' = x - mu, c' = c - mu)
+// as one tcgen05 GEMM per (point tile, center tile) with a fused top-4
+// epilogue; the classifier (assign.cu) turns the screen into exact float64
 // labels with a rigorous error bound.
+//
+// The |c'|^2/2 term rides in the GEMM itself: after the d/8 data slices every
+// accumulator gets one more K=8 slice whose A rows are all ones and whose B
+// rows hold |c'|^2/2 split into three TF32 parts (B holds -c' for the data
+// slices), issued last so the fp32 accumulation of the products is unchanged.
+// The epilogue is then a bare TMEM read + min scan, no per-column loads.
 //
 // Two precisions of the same kernel (template NPROD):
 //   NPROD = 1: one TF32 product (operands rounded to TF32, fp32 accumulation);
@@ -12,20 +19,24 @@
 //              chunk kc of this tile retire
 // Per CTA (persistent over 128-point tiles):
 //   A  = the point tile, K-major, in SMEM
-//   B  = center tiles of 128 centers, streamed in 32-dim chunks by 1-D bulk
-//        TMA (cp.async.bulk) into a ring of SMEM stages
+//   B  = center tiles of 128 centers, streamed in 32-dim chunks (+ the |c'|^2
+//        chunk: its B slice and the all-ones A slice) by 1-D bulk TMA
+//        (cp.async.bulk) into a ring of SMEM stages; CTA b walks the center
+//        tiles starting at tile b % nct so the L2 reads spread out
 //   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
 //        of center tile j overlaps the MMAs of tile j+1
-// Warp-specialised: lane 0 of warp 8 issues the bulk copies and the MMAs;
+// Warp-specialised: lane 0 of warp 9 streams B (bulk copies), lane 0 of
+// warp 8 issues the MMAs;
 // warps 0-7 convert point tiles into A and run the epilogues (warp w reads
 // TMEM lanes 32(w%4).. over column half w/4 and keeps its own top-4); roles
 // hand off through mbarriers only (stage full/empty, accumulator full/empty,
-// point tile full/empty).  Operands use the SWIZZLE_NONE K-major canonical
-// layout: 8-row x 16-byte core matrices, LBO between K-adjacent and SBO
-// between M/N-adjacent core matrices (validated on the GPU by
+// point-tile chunk full/empty).  Operands use the SWIZZLE_NONE K-major
+// canonical layout: 8-row x 16-byte core matrices, LBO between K-adjacent and
+// SBO between M/N-adjacent core matrices (validated on the GPU by
 // geek_tc_selftest).
 #include "common.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace geek {
@@ -33,6 +44,7 @@ namespace geek {
 constexpr int kTcM = 128;      // points per tile (TMEM lanes)
 constexpr int kTcN = 128;      // centers per tile
 constexpr int kTcKmax = 128;   // padded dimension (<= 128)
+constexpr int kTcAChunk = 32;  // dims per point-tile hand-off chunk
 constexpr int kTcChunk = 32;   // dims per B stage
 constexpr int kTcSliceBytes = kTcM * 8 * 4;                       // one K=8 tf32 slice of 128 rows: 4 KB
 constexpr int kTcHalfStage = (kTcChunk / 8) * kTcSliceBytes;      // 16 KB: one 32-dim chunk, one part
@@ -41,12 +53,24 @@ constexpr int kTcAPart = (kTcKmax / 8) * kTcSliceBytes;           // 64 KB: one 
 template <int NPROD>
 struct TcCfg {
   static constexpr int kParts = NPROD == 3 ? 2 : 1;              // hi (+ lo)
-  static constexpr int kABytes = kParts * kTcAPart;
+  // NPROD = 3 keeps the hi part of the point tile in TMEM (columns 256..383)
+  // and only the lo part in SMEM: the SMEM this frees deepens the B ring
+  static constexpr bool kATmem = NPROD == 3;
+  static constexpr int kABytes = kTcAPart;
   static constexpr int kABuf = NPROD == 3 ? 1 : 2;
   static constexpr int kStageBytes = kParts * kTcHalfStage;
-  static constexpr int kStages = NPROD == 3 ? 3 : 4;
-  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 32 * 8;
+  static constexpr int kStages = NPROD == 3 ? 5 : 4;
+  static constexpr uint32_t kTmemCols = kATmem ? 512 : 256;
+  static constexpr uint32_t kTmemA = 256;                        // first column of the TMEM A operand
+  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
 };
+
+// bytes of one center tile in the operand image: data chunks + the |c'|^2
+// chunk (B slice with |c'|^2/2, then the all-ones A slice)
+constexpr int kTcC2Bytes = 2 * kTcSliceBytes;
+__host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts) {
+  return (uint64_t)((d + kTcChunk - 1) / kTcChunk) * parts * kTcHalfStage + kTcC2Bytes;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -121,6 +145,29 @@ __device__ __forceinline__ void tc_mma(uint32_t dtmem, uint64_t adesc, uint64_t 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
+// A operand from TMEM (M rows = lanes, one tf32 per 32-bit column)
+__device__ __forceinline__ void tc_mma_ta(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -140,6 +187,26 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tc_ld32_async(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// pins the registers of an async TMEM load after tc_wait_ld (no instruction)
+__device__ __forceinline__ void tc_regs_ready(float* v) {
+  asm volatile("" : "+f"(v[0]),"+f"(v[1]),"+f"(v[2]),"+f"(v[3]),"+f"(v[4]),"+f"(v[5]),"+f"(v[6]),"+f"(v[7]),"+f"(v[8]),"+f"(v[9]),"+f"(v[10]),"+f"(v[11]),"+f"(v[12]),"+f"(v[13]),"+f"(v[14]),"+f"(v[15]),"+f"(v[16]),"+f"(v[17]),"+f"(v[18]),"+f"(v[19]),"+f"(v[20]),"+f"(v[21]),"+f"(v[22]),"+f"(v[23]),"+f"(v[24]),"+f"(v[25]),"+f"(v[26]),"+f"(v[27]),"+f"(v[28]),"+f"(v[29]),"+f"(v[30]),"+f"(v[31]) :: "memory");
 }
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -188,20 +255,20 @@ struct TcParams {
   const float* X;     // [n][d] float32
   uint64_t n;
   int d;
-  const float* Bimg;  // center operand image: [nct][chunks][stage bytes]
-  const float* c2;    // [nct*128] |c'|^2 (float, +inf for padding)
+  const float* Bimg;  // center operand image: [nct][data chunks + |c'|^2 slice]
   const float* mu;    // [d]
   uint64_t k;
   int nct;
   uint32_t lbo, sbo;
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
+  int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcEpiThreads = kTcEpiWarps * 32;
-constexpr int kTcThreads = kTcEpiThreads + 32;
+constexpr int kTcThreads = kTcEpiThreads + 64;  // + MMA warp + TMA warp
 
 template <int NPROD>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams P) {
@@ -210,13 +277,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint8_t* A = smem;                                           // kABuf x kABytes
   uint8_t* B = smem + Cfg::kABuf * Cfg::kABytes;               // kStages x kStageBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(B + Cfg::kStages * Cfg::kStageBytes);
-  uint64_t* full = bars;                    // [kStages] stage loaded (TMA tx)
-  uint64_t* empty = bars + 4;               // [kStages] stage consumed (MMA commit)
-  uint64_t* accf = bars + 8;                // [2] accumulator ready (MMA commit)
-  uint64_t* acce = bars + 10;               // [2] accumulator drained (256 epilogue threads)
-  uint64_t* afull = bars + 12;              // [kABuf][4] point-tile chunk written (256 threads)
-  uint64_t* aempty = bars + 20;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  uint64_t* full = bars;                    // [8] stage loaded (TMA tx)
+  uint64_t* empty = bars + 8;               // [8] stage consumed (MMA commit)
+  uint64_t* accf = bars + 16;               // [2] accumulator ready (MMA commit)
+  uint64_t* acce = bars + 18;               // [2] accumulator drained (256 epilogue threads)
+  uint64_t* afull = bars + 20;              // [kABuf][4] point-tile chunk written (256 threads)
+  uint64_t* aempty = bars + 28;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
+  static_assert(Cfg::kStages <= 8 && Cfg::kABuf <= 2, "barrier map");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -235,33 +303,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nck = (P.d + kTcChunk - 1) / kTcChunk;  // 32-dim chunks (A and B)
-  const uint32_t total_q = (uint32_t)P.nct * nck;
+  const int nck = (P.d + kTcAChunk - 1) / kTcAChunk;  // 32-dim point-tile chunks
+  const int nbk = (P.d + kTcChunk - 1) / kTcChunk;    // B chunks per center tile
+  const uint32_t qct = (uint32_t)nbk + 1;              // + the |c'|^2 slice
+  const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts);
+  const uint32_t total_q = (uint32_t)P.nct * qct;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
-  if (warp == kTcEpiWarps) {
-    if (lane == 0) {  // ---------------- producer + MMA issuer ----------------
-      const uint32_t idesc = make_idesc(kTcM, kTcN);
+  if (warp == kTcEpiWarps + 1) {
+    if (lane == 0) {  // ---------------- TMA producer: the B ring ----------------
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
-      uint64_t q_issue = 0, q_mma = 0;
-      auto issue = [&]() {
-        const uint32_t s = (uint32_t)(q_issue % Cfg::kStages);
-        if (q_issue >= (uint64_t)Cfg::kStages) mbar_wait(&empty[s], (uint32_t)((q_issue / Cfg::kStages) - 1) & 1);
-        mbar_expect_tx(&full[s], Cfg::kStageBytes);
+      for (uint64_t q = 0; q < total_chunks; ++q) {
+        const uint32_t s = (uint32_t)(q % Cfg::kStages);
+        if (q >= (uint64_t)Cfg::kStages) mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+        const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
+        const uint32_t ct = (cq + blockIdx.x) % (uint32_t)P.nct;  // CTAs start on different center tiles
+        const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
+        mbar_expect_tx(&full[s], bytes);
         bulk_g2s(B + s * Cfg::kStageBytes,
-                 reinterpret_cast<const uint8_t*>(P.Bimg) + (q_issue % total_q) * (uint64_t)Cfg::kStageBytes,
-                 Cfg::kStageBytes, &full[s]);
-        ++q_issue;
+                 reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes, bytes,
+                 &full[s]);
+      }
+    }
+  } else if (warp == kTcEpiWarps) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      const uint32_t idesc = make_idesc(kTcM, kTcN);
+      uint64_t q_mma = 0;
+      auto next_stage = [&]() -> uint32_t {
+        const uint32_t s = (uint32_t)(q_mma % Cfg::kStages);
+        mbar_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1);
+        fence_after();
+        return s;
       };
-      while (q_issue < (uint64_t)Cfg::kStages - 1 && q_issue < total_chunks) issue();
+      auto stage_done = [&](uint32_t s) {
+        tc_commit(&empty[s]);
+        ++q_mma;
+      };
       for (uint32_t t = 0; t < my_tiles; ++t) {
         const int ab = t % Cfg::kABuf;
         const uint32_t apar = (t / Cfg::kABuf) & 1;
@@ -272,32 +358,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           mbar_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u);
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
-          for (int kc = 0; kc < nck; ++kc) {
+          for (int kc = 0; kc < nbk; ++kc) {
+            const int ac = kc;  // point-tile chunk
             if (ct == 0) {  // first use of this chunk of the point tile
-              mbar_wait(&afull[ab * 4 + kc], apar);
+              mbar_wait(&afull[ab * 4 + ac], apar);
               fence_after();
             }
-            const uint32_t s = (uint32_t)(q_mma % Cfg::kStages);
-            mbar_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1);
-            fence_after();
+            const uint32_t s = next_stage();
             const uint32_t bb = smem_u32(B + s * Cfg::kStageBytes);
 #pragma unroll
             for (int j = 0; j < kTcChunk / 8; ++j) {
               const int ks = kc * (kTcChunk / 8) + j;
-              const uint64_t ahi = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
+              if (P.prof == 2) continue;
               const uint64_t bhi = make_sdesc(bb + j * kTcSliceBytes, P.lbo, P.sbo);
-              tc_mma(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
-              if (NPROD == 3) {
-                const uint64_t alo = make_sdesc(abase + kTcAPart + ks * kTcSliceBytes, P.lbo, P.sbo);
+              if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
+                const uint32_t ahi = tmem + Cfg::kTmemA + ks * 8;
+                const uint64_t alo = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
                 const uint64_t blo = make_sdesc(bb + kTcHalfStage + j * kTcSliceBytes, P.lbo, P.sbo);
-                tc_mma(dt, ahi, blo, idesc, 1u);
+                tc_mma_ta(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
+                tc_mma_ta(dt, ahi, blo, idesc, 1u);
                 tc_mma(dt, alo, bhi, idesc, 1u);
+              } else {
+                tc_mma(dt, make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo), bhi, idesc, (kc | j) ? 1u : 0u);
               }
             }
-            tc_commit(&empty[s]);
-            if (ct == P.nct - 1) tc_commit(&aempty[ab * 4 + kc]);  // last read of this chunk
-            ++q_mma;
-            if (q_issue < total_chunks) issue();  // into the stage of an earlier, queued chunk
+            if (ct == P.nct - 1) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
+            stage_done(s);
+          }
+          {  // |c'|^2 / 2, added last
+            const uint32_t s = next_stage();
+            const uint32_t sb = smem_u32(B + s * Cfg::kStageBytes);
+            if (P.prof != 2)
+              tc_mma(dt, make_sdesc(sb + kTcSliceBytes, P.lbo, P.sbo), make_sdesc(sb, P.lbo, P.sbo), idesc, 1u);
+            stage_done(s);
           }
           tc_commit(&accf[buf]);
         }
@@ -310,28 +403,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const uint64_t g = (uint64_t)t * P.nct + ct;
       const int buf = (int)(g & 1);
       const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
-      const float4* c2t = reinterpret_cast<const float4*>(P.c2 + (uint64_t)ct * kTcN + ch * (kTcN / 2));
       mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-#pragma unroll 1
-      for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
-        float v[32];
-        tc_ld32(trow + c0, v);
-        float mn = INFINITY;
+      if (P.prof != 1) {
+        float v[64];
+        tc_ld32_async(trow, v);       // both halves in flight, one wait
+        tc_ld32_async(trow + 32, v + 32);
+        tc_wait_ld();
+        tc_regs_ready(v);
+        tc_regs_ready(v + 32);
 #pragma unroll
-        for (int u = 0; u < 32; u += 4) {
-          const float4 cc = __ldg(c2t + (c0 + u) / 4);
-          v[u] = cc.x - 2.f * v[u];
-          v[u + 1] = cc.y - 2.f * v[u + 1];
-          v[u + 2] = cc.z - 2.f * v[u + 2];
-          v[u + 3] = cc.w - 2.f * v[u + 3];
-          mn = fminf(mn, fminf(fminf(v[u], v[u + 1]), fminf(v[u + 2], v[u + 3])));
-        }
-        if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
-          const int cbase = ct * kTcN + ch * (kTcN / 2) + c0;
+        for (int h = 0; h < 2; ++h) {
+          float mn = v[h * 32];
 #pragma unroll
-          for (int u = 0; u < 32; ++u) top.push(v[u], cbase + u);
+          for (int u = 1; u < 32; ++u) mn = fminf(mn, v[h * 32 + u]);
+          if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
+            const int cbase = (int)((ct + blockIdx.x) % P.nct) * kTcN + ch * (kTcN / 2) + h * 32;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) top.push(v[h * 32 + u], cbase + u);
+          }
         }
       }
       fence_before();
@@ -340,30 +431,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     auto finish = [&](uint32_t t, Top4& top) {
       epilogue(t, P.nct - 1, top);
       const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + (warp & 3) * 32 + lane;
-      if (i < P.n) {  // two column halves -> [n][8]; the classifier merges them
+      if (i < P.n) {  // two column halves -> [n][8] of s = 2 * (s / 2) (exact); the classifier merges them
         const int h = (warp >> 2) * 4;
-        *reinterpret_cast<float4*>(P.top_s + i * 8 + h) = make_float4(top.s[0], top.s[1], top.s[2], top.s[3]);
+        *reinterpret_cast<float4*>(P.top_s + i * 8 + h) =
+            make_float4(2.f * top.s[0], 2.f * top.s[1], 2.f * top.s[2], 2.f * top.s[3]);
         *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
-    // Point tiles travel global -> registers -> SMEM.  Warp w owns rows
-    // 16w..16w+15; for chunk kc (32 dims) lane l holds rows (l&7) and
-    // (l&7)+8 at float4 columns kc*8 + (l>>3) and +4, so each 8-lane group
-    // writes one 128-byte row of core matrices (conflict-free).  The global
-    // loads of tile t+1 are issued before the epilogues of tile t and land
-    // in registers meanwhile; the SMEM writes then wait chunk by chunk for
-    // the MMAs of tile t that still read that chunk.
+    // Point tiles travel global -> registers -> A.  The global loads of tile
+    // t+1 are issued before the epilogues of tile t and land in registers
+    // meanwhile; the A writes then wait chunk by chunk (32 dims) for the MMAs
+    // of tile t that still read that chunk.
+    //   SMEM A (NPROD = 1): warp w owns rows 16w..16w+15; for chunk kc lane l
+    //     holds rows (l&7) and (l&7)+8 at float4 columns kc*8 + (l>>3) and +4,
+    //     so each 8-lane group writes one 128-byte row of core matrices.
+    //   TMEM A (NPROD = 3): thread l of warp w owns row 32(w%4)+l (its TMEM
+    //     lane) and dims kc*32 + 16(w/4) .. +15 of every chunk: the hi part
+    //     goes to TMEM with one tcgen05.st, the lo part to the SMEM K-major tile.
     float4 q[16];
     const int rsub = lane & 7, csub = lane >> 3;
-    auto tile_row0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + warp * 16; };
+    auto tile_p0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM; };
+    auto slot_of = [&](int kc, int p, int& row, int& e0) {
+      if (Cfg::kATmem) {
+        row = (warp & 3) * 32 + lane;
+        e0 = kc * 32 + (warp >> 2) * 16 + 4 * p;
+      } else {
+        row = warp * 16 + rsub + 8 * (p & 1);
+        e0 = (kc * 8 + csub + 4 * (p >> 1)) * 4;
+      }
+    };
     auto load_regs = [&](uint32_t t) {
-      const uint64_t p0 = tile_row0(t);
+      const uint64_t p0 = tile_p0(t);
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const uint64_t i = p0 + rsub + 8 * (p & 1);
-          const int e0 = (kc * 8 + csub + 4 * (p >> 1)) * 4;
+          int row, e0;
+          slot_of(kc, p, row, e0);
+          const uint64_t i = p0 + row;
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
           if (kc < nck && i < P.n) {
             if (P.d == kTcKmax) {
@@ -380,7 +485,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         }
       }
       {  // pull the tile after it towards L2 while this one is in flight
-        const uint64_t row = (blockIdx.x + (uint64_t)(t + 1) * gridDim.x) * kTcM + (warp * 32 + lane) / 2;
+        const uint64_t row = tile_p0(t + 1) + (warp * 32 + lane) / 2;
         if (row < P.n) {
           const char* base = reinterpret_cast<const char*>(P.X + row * P.d) + (lane & 1) * 256;
           for (int b = 0; b < 256 && (lane & 1) * 256 + b < P.d * 4; b += 128)
@@ -392,16 +497,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const int ab = t % Cfg::kABuf;
       const uint32_t epar = ((t / Cfg::kABuf) & 1) ^ 1u;
       uint8_t* Ab = A + ab * Cfg::kABytes;
-      const uint64_t p0 = tile_row0(t);
+      const uint64_t p0 = tile_p0(t);
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         if (kc < nck) {
-          mbar_wait(&aempty[ab * 4 + kc], epar);  // the MMAs of the previous tile in this buffer are done
+          mbar_wait(&aempty[ab * 4 + kc], epar);  // the MMAs of the previous tile on this chunk are done
+          if (Cfg::kATmem) fence_after();
+          float hi[16];
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
-            const int row = warp * 16 + rsub + 8 * (p & 1);
-            const int e0 = (kc * 8 + csub + 4 * (p >> 1)) * 4;
-            const bool valid = p0 + rsub + 8 * (p & 1) < P.n;
+            int row, e0;
+            slot_of(kc, p, row, e0);
+            const bool valid = p0 + row < P.n;
             float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
             if (P.d == kTcKmax) {
               m4 = __ldg(reinterpret_cast<const float4*>(P.mu + e0));
@@ -416,10 +523,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
-            *reinterpret_cast<float4*>(Ab + off) = make_float4(h0, h1, h2, h3);
-            if (NPROD == 3)
-              *reinterpret_cast<float4*>(Ab + kTcAPart + off) =
+            if (P.prof == 3) continue;
+            if (Cfg::kATmem) {
+              hi[4 * p] = h0;
+              hi[4 * p + 1] = h1;
+              hi[4 * p + 2] = h2;
+              hi[4 * p + 3] = h3;
+              *reinterpret_cast<float4*>(Ab + off) =
                   make_float4(tf32_round(x0 - h0), tf32_round(x1 - h1), tf32_round(x2 - h2), tf32_round(x3 - h3));
+            } else {
+              *reinterpret_cast<float4*>(Ab + off) = make_float4(h0, h1, h2, h3);
+            }
+          }
+          if (Cfg::kATmem) {
+            if (P.prof != 3)
+              tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + kc * 32 + (warp >> 2) * 16, hi);
+            tc_wait_st();
+            fence_before();
           }
           fence_proxy_async();
           mbar_arrive(&afull[ab * 4 + kc]);
@@ -441,7 +561,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   }
   fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
 }
 
 // ---- center operand image ------------------------------------------------
@@ -454,19 +574,24 @@ __global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu
   }
 }
 
-// Bimg[ct][kc] = { tf32(c')[128 centers][32 dims] (, residual[...] for NPROD=3) }
+// Bimg[ct] = { chunk kc: tf32(-c')[128 centers][32 dims] (, residual[...] for
+// NPROD=3) ..., then the |c'|^2/2 slice: [128 centers][8] = (p1, p2, p3, 0...)
+// with p1 + p2 + p3 = |c'|^2/2 to ~33 bits (+inf for padding centers), then
+// the all-ones A slice that multiplies it }
 __global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, int parts,
                                     uint32_t lbo, uint32_t sbo, float* Bimg, float* c2,
                                     unsigned long long* cmax_bits) {
   const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
   const uint64_t stage = (uint64_t)parts * kTcHalfStage;
+  const uint64_t ct_bytes = tc_ct_bytes(d, parts);
   const uint64_t total = (uint64_t)nct * kTcN;
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
        c += (uint64_t)gridDim.x * blockDim.x) {
     const int ct = (int)(c / kTcN), r = (int)(c % kTcN);
+    uint8_t* base = reinterpret_cast<uint8_t*>(Bimg) + (uint64_t)ct * ct_bytes;
     double n2 = 0.0;
     for (int kc = 0; kc < nchunks_k; ++kc) {
-      uint8_t* img = reinterpret_cast<uint8_t*>(Bimg) + ((uint64_t)ct * nchunks_k + kc) * stage;
+      uint8_t* img = base + (uint64_t)kc * stage;
       for (int e = 0; e < kTcChunk; ++e) {
         const int j = kc * kTcChunk + e;
         float cv = 0.f;
@@ -475,11 +600,25 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
           cv = (float)dv;
           n2 = fma((double)cv, (double)cv, n2);
         }
-        const float hi = tf32_round(cv);
+        const float hi = tf32_round(-cv);
         const uint32_t off = (e >> 3) * kTcSliceBytes + core_off(r, e & 7, lbo, sbo);
         *reinterpret_cast<float*>(img + off) = hi;
-        if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(cv - hi);
+        if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(-cv - hi);
       }
+    }
+    uint8_t* cs = base + (uint64_t)nchunks_k * stage;
+    float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c < k) {
+      const double h = 0.5 * n2;
+      p[0] = tf32_round((float)h);
+      p[1] = tf32_round((float)(h - (double)p[0]));
+      p[2] = tf32_round((float)(h - (double)p[0] - (double)p[1]));
+    } else {
+      p[0] = INFINITY;
+    }
+    for (int e = 0; e < 8; ++e) {
+      *reinterpret_cast<float*>(cs + core_off(r, e, lbo, sbo)) = p[e];
+      *reinterpret_cast<float*>(cs + kTcSliceBytes + core_off(r, e, lbo, sbo)) = 1.f;  // all-ones A slice
     }
     c2[c] = c < k ? (float)n2 : INFINITY;
     if (c < k) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(n2) * (1.0 + 1e-6)));
@@ -490,9 +629,8 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s) {
   GEEK_REQUIRE(nprod == 1 || nprod == 3, "screen precision must be 1 or 3 TF32 products");
   nct = (int)((k + kTcN - 1) / kTcN);
-  const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
   const int parts = nprod == 3 ? 2 : 1;
-  GEEK_TRY(img.alloc((size_t)nct * nchunks_k * parts * kTcHalfStage, s));
+  GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts), s));
   GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
   GEEK_TRY(mu.alloc((size_t)d * 4, s));
   center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
@@ -527,7 +665,6 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.n = n;
   P.d = d;
   P.Bimg = img.as<float>();
-  P.c2 = c2.as<float>();
   P.mu = mu.as<float>();
   P.k = k;
   P.nct = nct;
@@ -535,6 +672,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.sbo = sbo;
   P.top_s = top_s;
   P.top_i = top_i;
+  P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   return nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
 }
 

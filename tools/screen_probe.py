@@ -1,0 +1,34 @@
+"""Time the tensor-core assignment screen alone at the bench size under the
+GEEK_SCREEN_PROF knobs (0 normal, 1 no epilogue math, 2 no MMAs, 3 no A
+writes).  Usage: python tools/screen_probe.py [n] [k]."""
+import os
+import subprocess
+import sys
+
+if os.environ.get("_PROBE_CHILD"):
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2106_10515_b200 import _lib as L
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+    k = int(sys.argv[2]) if len(sys.argv) > 2 else 963
+    d = 128
+    g = torch.Generator(device="cuda").manual_seed(0)
+    C = torch.randn(k, d, device="cuda", dtype=torch.float64, generator=g) * 10
+    X = torch.empty(n, d, device="cuda", dtype=torch.float32)
+    for i in range(0, n, 10_000_000):
+        j = min(n, i + 10_000_000)
+        lab = torch.randint(0, k, (j - i,), device="cuda", generator=g)
+        X[i:j] = (C[lab] + torch.randn(j - i, d, device="cuda", dtype=torch.float64, generator=g)).float()
+    labels = torch.empty(n, dtype=torch.int64, device="cuda")
+    best = torch.empty(n, dtype=torch.float64, device="cuda")
+    ms = []
+    for it in range(4):
+        L.call("geek_assign_l2", L.ptr(X), 0, n, d, L.ptr(C), k, L.ptr(labels), L.ptr(best), L.stream())
+        torch.cuda.synchronize()
+        ms.append(L.load_library().geek_assign_last_screen_ms())
+    print(f"mode={os.environ.get('GEEK_SCREEN_PROF','0')} nprod={os.environ.get('GEEK_SCREEN','3')} "
+          f"screen_ms={min(ms[1:]):.2f} all={['%.2f' % v for v in ms]}", flush=True)
+else:
+    for mode in ["0", "1", "2", "3"]:
+        env = dict(os.environ, _PROBE_CHILD="1", GEEK_SCREEN_PROF=mode, GEEK_SCREEN_ONLY="1")
+        subprocess.run([sys.executable, __file__] + sys.argv[1:], env=env, check=False)
