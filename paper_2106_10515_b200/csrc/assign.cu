@@ -129,6 +129,58 @@ __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restr
   }
 }
 
+// Exact argmin for the few points whose screen window overflowed: one block
+// per point, threads over centers (first index wins ties, as np.argmin).
+constexpr int kFsThreads = 256;
+__global__ void __launch_bounds__(kFsThreads) full_scan_kernel(const float* __restrict__ X, int d,
+                                                               const double* __restrict__ C, uint64_t k,
+                                                               const PwPlan plan, const uint32_t* idx,
+                                                               int64_t* labels, double* best) {
+  extern __shared__ double sx[];  // [d]
+  __shared__ double rd[kFsThreads / 32];
+  __shared__ long long rl[kFsThreads / 32];
+  const uint64_t i = idx[blockIdx.x];
+  for (int j = threadIdx.x; j < d; j += kFsThreads) sx[j] = (double)X[i * d + j];
+  __syncthreads();
+  double bd = INFINITY;
+  long long bl = -1;
+  for (uint64_t c = threadIdx.x; c < k; c += kFsThreads) {
+    const double* cr = C + c * d;
+    const double dist = __dsqrt_rn(pw_sum(plan, [&](int j) {
+      const double df = __dsub_rn(sx[j], cr[j]);
+      return __dmul_rn(df, df);
+    }));
+    if (bl < 0 || dist < bd) {
+      bd = dist;
+      bl = (long long)c;
+    }
+  }
+  // lexicographic (dist, index) minimum over the block
+  for (int o = 16; o; o >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const long long ol = __shfl_xor_sync(0xffffffffu, bl, o);
+    if (ol >= 0 && (bl < 0 || od < bd || (od == bd && ol < bl))) {
+      bd = od;
+      bl = ol;
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    rd[w] = bd;
+    rl[w] = bl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int v = 1; v < kFsThreads / 32; ++v)
+      if (rl[v] >= 0 && (bl < 0 || rd[v] < bd || (rd[v] == bd && rl[v] < bl))) {
+        bd = rd[v];
+        bl = rl[v];
+      }
+    labels[i] = bl;
+    best[i] = bd;
+  }
+}
+
 __global__ void radii_sizes_kernel(const int64_t* labels, const double* best, uint64_t n, double* radii,
                                    int64_t* sizes) {
   // warp-aggregated: ids are cluster-contiguous, so a warp mostly shares a label
@@ -679,8 +731,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
       GEEK_CHECK_LAUNCH();
     }
     if (cnts[1]) {
-      assign_l2_kernel<float><<<(unsigned)((cnts[1] + kAsgThreads - 1) / kAsgThreads), kAsgThreads, smem, s>>>(
-          (const float*)X, cnts[1], d, C, k, plan, labels, best, full.as<uint32_t>());
+      full_scan_kernel<<<(unsigned)cnts[1], kFsThreads, sizeof(double) * d, s>>>(
+          (const float*)X, d, C, k, plan, full.as<uint32_t>(), labels, best);
       GEEK_CHECK_LAUNCH();
     }
     return GEEK_OK;

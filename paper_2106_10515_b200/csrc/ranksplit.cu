@@ -73,14 +73,28 @@ __global__ void fine_layout_kernel(const uint32_t* hist, uint64_t total, uint64_
   }
 }
 
-__global__ void fine_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g, const uint2* __restrict__ cinfo,
-                                 uint32_t* fcnt) {
+// 4 ids per thread per round: the key -> cell -> counter chains of
+// independent ids overlap instead of exposing three latencies each
+__global__ void __launch_bounds__(256) fine_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                                        const uint2* __restrict__ cinfo, uint32_t* fcnt) {
   const int jb = blockIdx.y;
   const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
   const uint2* ci = cinfo + (uint64_t)jb * g.nc;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(&fcnt[fine_of(kj[i], g.cb, ci)], 1u);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < g.n; i0 += 4 * stride) {
+    uint64_t key[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) key[u] = i0 + u * stride < g.n ? __ldg(kj + i0 + u * stride) : 0ull;
+    uint2 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + coarse_of(key[u], g.cb));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * stride < g.n) {
+        const uint32_t frac = static_cast<uint32_t>((key[u] << g.cb) >> 32);
+        atomicAdd(&fcnt[c[u].y + static_cast<uint32_t>(((uint64_t)frac * c[u].x) >> 32)], 1u);
+      }
+  }
 }
 
 __device__ __forceinline__ int table_of_fine(const uint32_t* tb_first, int tb, uint32_t f) {
@@ -133,7 +147,11 @@ __global__ void cell_shortcut_kernel(SplitGeom g, uint2* cinfo, const uint32_t* 
   }
 }
 
-// slot codes for ids in non-straddling bins; straddling ids are staged
+// slot codes for ids in non-straddling bins; straddling ids are staged (their
+// code word is written as GEEK_NONE here and fixed by resolve / big_rank).
+// Tables go in groups of 8 with the three dependent loads (key, cell,
+// fine-bin code) issued group-wide, and each id's 8 codes leave as one
+// 32-byte row segment when the row layout allows it.
 __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
                                                     const uint2* __restrict__ cinfo,
                                                     const uint32_t* __restrict__ fcode,
@@ -141,26 +159,42 @@ __global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__
                                                     uint32_t* sfill, uint32_t* codes,
                                                     uint64_t* st_key, uint32_t* st_id,
                                                     uint32_t* st_bin) {
+  const bool vec = (g.m % 4) == 0 && (g.c0 % 4) == 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t* crow = codes + i * (uint64_t)g.m + g.c0;
-    for (int jb = 0; jb < g.tb; ++jb) {
-      const uint64_t key = keys[(uint64_t)(g.j0 + jb) * g.n + i];
-      const uint2 ci = __ldg(cinfo + (uint64_t)jb * g.nc + coarse_of(key, g.cb));
-      uint32_t f = 0, code;
-      if (ci.x == 0) {
-        code = ci.y;  // whole cell inside one bucket
-      } else {
-        f = ci.y + static_cast<uint32_t>(((uint64_t)static_cast<uint32_t>((key << g.cb) >> 32) * ci.x) >> 32);
-        code = __ldg(fcode + f);
+    for (int jb0 = 0; jb0 < g.tb; jb0 += 8) {
+      uint64_t key[8];
+      uint2 ci[8];
+      uint32_t f[8], code[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        key[u] = jb0 + u < g.tb ? __ldg(keys + (uint64_t)(g.j0 + jb0 + u) * g.n + i) : 0ull;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        ci[u] = jb0 + u < g.tb ? __ldg(cinfo + (uint64_t)(jb0 + u) * g.nc + coarse_of(key[u], g.cb))
+                               : make_uint2(0u, 0u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        f[u] = ci[u].y + static_cast<uint32_t>(((uint64_t)static_cast<uint32_t>((key[u] << g.cb) >> 32) * ci[u].x) >> 32);
+        code[u] = ci[u].x == 0 ? ci[u].y : __ldg(fcode + f[u]);  // (0, slot): whole cell inside one bucket
       }
-      if (code != GEEK_NONE) {
-        crow[jb] = code;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (jb0 + u < g.tb && code[u] == GEEK_NONE) {
+          const uint32_t pos = sbase[f[u]] + atomicAdd(&sfill[f[u]], 1u);
+          st_key[pos] = key[u];
+          st_id[pos] = static_cast<uint32_t>(i);
+          st_bin[pos] = f[u];
+        }
+      if (vec && jb0 + 8 <= g.tb) {
+        uint4* dst = reinterpret_cast<uint4*>(crow + jb0);
+        dst[0] = make_uint4(code[0], code[1], code[2], code[3]);
+        dst[1] = make_uint4(code[4], code[5], code[6], code[7]);
       } else {
-        const uint32_t pos = sbase[f] + atomicAdd(&sfill[f], 1u);
-        st_key[pos] = key;
-        st_id[pos] = static_cast<uint32_t>(i);
-        st_bin[pos] = f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (jb0 + u < g.tb) crow[jb0 + u] = code[u];
       }
     }
   }
@@ -341,7 +375,11 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   g.t = t;
   g.m = static_cast<int>(code_stride);
   int cb = (int)std::ceil(std::log2((double)n / 16.0 + 1.0));
-  g.cb = std::min(20, std::max(10, cb));
+  // 16 coarse bits (sign, exponent, 4 mantissa bits: 1/16-octave cells) keep
+  // the per-cell tables of a 16-table batch at 8 MB: the random lookups of
+  // fine_hist / codes stay in L2 next to the key stream
+  g.cb = std::min(16, std::max(10, cb));
+  if (const char* e = getenv("GEEK_COARSE_BITS")) g.cb = std::min(24, std::max(8, atoi(e)));
   g.nc = 1u << g.cb;
   g.fine_target = kFineTargetDefault;
   if (const char* ft = getenv("GEEK_FINE_TARGET")) g.fine_target = (uint32_t)std::max(1, atoi(ft));
