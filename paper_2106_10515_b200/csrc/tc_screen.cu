@@ -12,11 +12,10 @@
 //
 // Two precisions of the same kernel (template NPROD):
 //   NPROD = 1: one TF32 product (operands rounded to TF32, fp32 accumulation);
-//              A = 64 KB per point tile, double-buffered
-//   NPROD = 3: TF32x3 (hi*hi + hi*lo + lo*hi): fp32-level screen, A = 128 KB
-//              single-buffered, handed over per 32-dim chunk so the next
-//              tile's chunk kc is written as soon as the last MMAs reading
-//              chunk kc of this tile retire
+//              A = 64 KB per point tile in SMEM
+//   NPROD = 3: TF32x3 (hi*hi + hi*lo + lo*hi): fp32-level screen; the hi part
+//              of the point tile lives in TMEM, the lo part (64 KB) in SMEM
+// Point tiles are double-buffered and handed over per 32-dim chunk.
 // Per CTA (persistent over 128-point tiles):
 //   A  = the point tile, K-major, in SMEM
 //   B  = center tiles of 128 centers, streamed in 32-dim chunks (+ the |c'|^2
@@ -57,11 +56,11 @@ struct TcCfg {
   // and only the lo part in SMEM: the SMEM this frees deepens the B ring
   static constexpr bool kATmem = NPROD == 3;
   static constexpr int kABytes = kTcAPart;
-  static constexpr int kABuf = NPROD == 3 ? 1 : 2;
+  static constexpr int kABuf = 2;                                // point tiles double-buffered
   static constexpr int kStageBytes = kParts * kTcHalfStage;
-  static constexpr int kStages = NPROD == 3 ? 5 : 4;
+  static constexpr int kStages = NPROD == 3 ? 3 : 4;
   static constexpr uint32_t kTmemCols = kATmem ? 512 : 256;
-  static constexpr uint32_t kTmemA = 256;                        // first column of the TMEM A operand
+  static constexpr uint32_t kTmemA = 256;                        // TMEM A operand: buffer b at 256 + 128 b
   static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
 };
 
@@ -209,6 +208,18 @@ __device__ __forceinline__ void tc_regs_ready(float* v) {
   asm volatile("" : "+f"(v[0]),"+f"(v[1]),"+f"(v[2]),"+f"(v[3]),"+f"(v[4]),"+f"(v[5]),"+f"(v[6]),"+f"(v[7]),"+f"(v[8]),"+f"(v[9]),"+f"(v[10]),"+f"(v[11]),"+f"(v[12]),"+f"(v[13]),"+f"(v[14]),"+f"(v[15]),"+f"(v[16]),"+f"(v[17]),"+f"(v[18]),"+f"(v[19]),"+f"(v[20]),"+f"(v[21]),"+f"(v[22]),"+f"(v[23]),"+f"(v[24]),"+f"(v[25]),"+f"(v[26]),"+f"(v[27]),"+f"(v[28]),"+f"(v[29]),"+f"(v[30]),"+f"(v[31]) :: "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -319,8 +330,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
+  // The producer and MMA warps run their loops warp-wide (so addresses and
+  // descriptors stay warp-uniform) and issue through one elected lane.
   if (warp == kTcEpiWarps + 1) {
-    if (lane == 0) {  // ---------------- TMA producer: the B ring ----------------
+    const bool leader = elect_one();
+    {  // ---------------- TMA producer: the B ring ----------------
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
       for (uint64_t q = 0; q < total_chunks; ++q) {
         const uint32_t s = (uint32_t)(q % Cfg::kStages);
@@ -328,14 +342,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
         const uint32_t ct = (cq + blockIdx.x) % (uint32_t)P.nct;  // CTAs start on different center tiles
         const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
-        mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(B + s * Cfg::kStageBytes,
-                 reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes, bytes,
-                 &full[s]);
+        if (leader) {
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(B + s * Cfg::kStageBytes,
+                   reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes, bytes,
+                   &full[s]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == kTcEpiWarps) {
-    if (lane == 0) {  // ---------------- MMA issuer ----------------
+    const bool leader = elect_one();
+    {  // ---------------- MMA issuer ----------------
       const uint32_t idesc = make_idesc(kTcM, kTcN);
       uint64_t q_mma = 0;
       auto next_stage = [&]() -> uint32_t {
@@ -345,7 +363,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         return s;
       };
       auto stage_done = [&](uint32_t s) {
-        tc_commit(&empty[s]);
+        if (leader) tc_commit(&empty[s]);
+        __syncwarp();
         ++q_mma;
       };
       for (uint32_t t = 0; t < my_tiles; ++t) {
@@ -372,27 +391,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               if (P.prof == 2) continue;
               const uint64_t bhi = make_sdesc(bb + j * kTcSliceBytes, P.lbo, P.sbo);
               if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
-                const uint32_t ahi = tmem + Cfg::kTmemA + ks * 8;
+                const uint32_t ahi = tmem + Cfg::kTmemA + ab * 128 + ks * 8;
                 const uint64_t alo = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
                 const uint64_t blo = make_sdesc(bb + kTcHalfStage + j * kTcSliceBytes, P.lbo, P.sbo);
-                tc_mma_ta(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
-                tc_mma_ta(dt, ahi, blo, idesc, 1u);
-                tc_mma(dt, alo, bhi, idesc, 1u);
+                if (leader) {
+                  tc_mma_ta(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
+                  tc_mma_ta(dt, ahi, blo, idesc, 1u);
+                  tc_mma(dt, alo, bhi, idesc, 1u);
+                }
               } else {
-                tc_mma(dt, make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo), bhi, idesc, (kc | j) ? 1u : 0u);
+                const uint64_t a = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
+                if (leader) tc_mma(dt, a, bhi, idesc, (kc | j) ? 1u : 0u);
               }
             }
-            if (ct == P.nct - 1) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
+            if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
           {  // |c'|^2 / 2, added last
             const uint32_t s = next_stage();
             const uint32_t sb = smem_u32(B + s * Cfg::kStageBytes);
-            if (P.prof != 2)
-              tc_mma(dt, make_sdesc(sb + kTcSliceBytes, P.lbo, P.sbo), make_sdesc(sb, P.lbo, P.sbo), idesc, 1u);
+            const uint64_t a1 = make_sdesc(sb + kTcSliceBytes, P.lbo, P.sbo), b1 = make_sdesc(sb, P.lbo, P.sbo);
+            if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
             stage_done(s);
           }
-          tc_commit(&accf[buf]);
+          if (leader) tc_commit(&accf[buf]);
+          __syncwarp();
         }
       }
     }
@@ -537,7 +560,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           }
           if (Cfg::kATmem) {
             if (P.prof != 3)
-              tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + kc * 32 + (warp >> 2) * 16, hi);
+              tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 32 + (warp >> 2) * 16,
+                      hi);
             tc_wait_st();
             fence_before();
           }
