@@ -612,6 +612,80 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
   }
 }
 
+// tc_classify8_kernel with 2 lanes per point and 16-byte loads (d % 8 == 0,
+// 8 <= d <= 128): lane h keeps numpy's accumulators r[4h..4h+3] (elements
+// e with e % 8 in [4h, 4h+4)), forms (r[4h]+r[4h+1]) + (r[4h+2]+r[4h+3])
+// locally and one xor-shuffle adds the other half: numpy's pairwise tree.
+__global__ void __launch_bounds__(256) tc_classify2_kernel(
+    const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C, uint64_t k,
+    const float* __restrict__ top_s, const int* __restrict__ top_i, float* xnorm, const float* __restrict__ mu,
+    const unsigned long long* cmax_bits, int nprod, int64_t* labels, double* best, uint32_t* amb,
+    unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
+  const double cn = __longlong_as_double((long long)*cmax_bits);
+  const unsigned lane = threadIdx.x & 31, h = lane & 1;
+  const unsigned pmask = 3u << (lane & 30);
+  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+  const int nu = d / 8;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 1; i < n; i += stride) {
+    const ScreenView v = screen_view(top_s + i * 8, top_i + i * 8);
+    const float4* xr = reinterpret_cast<const float4*>(X + i * d);
+    const float4* m4 = reinterpret_cast<const float4*>(mu);
+    double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
+    for (int u = 0; u < nu; ++u) {
+      const float4 x = __ldg(xr + 2 * u + h), m = __ldg(m4 + 2 * u + h);
+      const double a0 = (double)(x.x - m.x), a1 = (double)(x.y - m.y);
+      const double a2 = (double)(x.z - m.z), a3 = (double)(x.w - m.w);
+      xn2 = fma(a0, a0, xn2);
+      xn2 = fma(a1, a1, xn2);
+      xn2 = fma(a2, a2, xn2);
+      xn2 = fma(a3, a3, xn2);
+    }
+    xn2 += __shfl_xor_sync(pmask, xn2, 1);
+    const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
+    if (h == 0) xnorm[i] = xn;
+    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double s0 = v.s0;
+    if (k == 1 || (double)v.s1 - s0 > T) {
+      const int lab = v.i0;
+      const double2* cr = reinterpret_cast<const double2*>(C + (uint64_t)lab * d);
+      double r0, r1, r2, r3;
+      {
+        const float4 x = __ldg(xr + h);
+        const double2 c01 = __ldg(cr + 2 * h), c23 = __ldg(cr + 2 * h + 1);
+        double df = __dsub_rn((double)x.x, c01.x);
+        r0 = __dmul_rn(df, df);
+        df = __dsub_rn((double)x.y, c01.y);
+        r1 = __dmul_rn(df, df);
+        df = __dsub_rn((double)x.z, c23.x);
+        r2 = __dmul_rn(df, df);
+        df = __dsub_rn((double)x.w, c23.y);
+        r3 = __dmul_rn(df, df);
+      }
+      for (int u = 1; u < nu; ++u) {
+        const float4 x = __ldg(xr + 2 * u + h);
+        const double2 c01 = __ldg(cr + 4 * u + 2 * h), c23 = __ldg(cr + 4 * u + 2 * h + 1);
+        double df = __dsub_rn((double)x.x, c01.x);
+        r0 = __dadd_rn(r0, __dmul_rn(df, df));
+        df = __dsub_rn((double)x.y, c01.y);
+        r1 = __dadd_rn(r1, __dmul_rn(df, df));
+        df = __dsub_rn((double)x.z, c23.x);
+        r2 = __dadd_rn(r2, __dmul_rn(df, df));
+        df = __dsub_rn((double)x.w, c23.y);
+        r3 = __dadd_rn(r3, __dmul_rn(df, df));
+      }
+      const double t = __dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3));
+      const double res = __dadd_rn(t, __shfl_xor_sync(pmask, t, 1));
+      if (h == 0) {
+        labels[i] = lab;
+        best[i] = __dsqrt_rn(res);
+      }
+    } else if (h == 0) {
+      if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
+      else amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
+    }
+  }
+}
+
 // exact numpy distances over the screen candidates (<= 8 entries within the
 // window); ties -> lower index
 __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const double* __restrict__ C, uint64_t k,
@@ -643,6 +717,65 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const doub
     }
     labels[i] = bl;
     best[i] = bd;
+  }
+}
+
+// tc_recheck_kernel with 8 lanes per point (8 <= d <= 128): lane a keeps
+// numpy's accumulator r[a]; the xor butterfly gives every lane the same,
+// numpy-ordered total (IEEE addition is commutative), so all lanes agree.
+__global__ void tc_recheck8_kernel(const float* __restrict__ X, int d, const double* __restrict__ C,
+                                   const float* __restrict__ top_s, const int* __restrict__ top_i,
+                                   const float* __restrict__ xnorm, const unsigned long long* cmax_bits, int nprod,
+                                   const uint32_t* __restrict__ amb, uint64_t na, int64_t* labels, double* best) {
+  const double cn = __longlong_as_double((long long)*cmax_bits);
+  const unsigned lane = threadIdx.x & 31, a = lane & 7;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
+  const int lim = d - (d % 8);
+  for (uint64_t q = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3; q < na; q += stride) {
+    const uint64_t i = amb[q];
+    const float* s8 = top_s + i * 8;
+    const int* i8 = top_i + i * 8;
+    const ScreenView v = screen_view(s8, i8);
+    const double T = tc_threshold((double)xnorm[i], cn, d, nprod);
+    const float* xr = X + i * d;
+    double xv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) xv[u] = 8 * u + (int)a < lim ? (double)__ldg(xr + 8 * u + a) : 0.0;
+    double bd = 0.0;
+    long long bl = -1;
+    for (int c8 = 0; c8 < 8; ++c8) {
+      const int ci = i8[c8];
+      if ((double)s8[c8] - (double)v.s0 > T || ci < 0) continue;
+      const double* cr = C + (uint64_t)ci * d;
+      double r;
+      {
+        const double df = __dsub_rn(xv[0], __ldg(cr + a));
+        r = __dmul_rn(df, df);
+      }
+#pragma unroll
+      for (int u = 1; u < 16; ++u)
+        if (8 * u < lim) {
+          const double df = __dsub_rn(xv[u], __ldg(cr + 8 * u + a));
+          r = __dadd_rn(r, __dmul_rn(df, df));
+        }
+      const double p1 = __dadd_rn(r, __shfl_xor_sync(gmask, r, 1));
+      const double p2 = __dadd_rn(p1, __shfl_xor_sync(gmask, p1, 2));
+      double res = __dadd_rn(p2, __shfl_xor_sync(gmask, p2, 4));
+      for (int e = lim; e < d; ++e) {
+        const double df = __dsub_rn((double)xr[e], cr[e]);
+        res = __dadd_rn(res, __dmul_rn(df, df));
+      }
+      const double dist = __dsqrt_rn(res);
+      if (bl < 0 || dist < bd || (dist == bd && ci < bl)) {
+        bd = dist;
+        bl = ci;
+      }
+    }
+    if (a == 0) {
+      labels[i] = bl;
+      best[i] = bd;
+    }
   }
 }
 
@@ -705,7 +838,11 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
       cudaEventDestroy(ev1);
       return GEEK_OK;
     }
-    if (d >= 8)
+    if (d % 8 == 0 && d <= 128)
+      tc_classify2_kernel<<<grid_for(n * 2, 256, 148 * 16), 256, 0, s>>>(
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,
+          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+    else if (d >= 8)
       tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
           (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,
           labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
@@ -724,7 +861,12 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     last_screen_ms() = ms;
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    if (cnts[0]) {
+    if (cnts[0] && d >= 8) {
+      tc_recheck8_kernel<<<grid_for(cnts[0] * 8, 256, 148 * 16), 256, 0, s>>>(
+          (const float*)X, d, C, ts.as<float>(), ti.as<int>(), xn.as<float>(), cmax, nprod, amb.as<uint32_t>(),
+          cnts[0], labels, best);
+      GEEK_CHECK_LAUNCH();
+    } else if (cnts[0]) {
       tc_recheck_kernel<<<grid_for(cnts[0], 128), 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(),
                                                                ti.as<int>(), xn.as<float>(), cmax, nprod,
                                                                amb.as<uint32_t>(), cnts[0], labels, best);

@@ -271,7 +271,8 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
                             cudaStream_t s) {
   const uint64_t ncell = (uint64_t)g.tb * g.nc;
   // ~2M samples per table shape the fine bins; the fine counts are exact anyway
-  const uint64_t stride = g.n > (1ull << 21) ? g.n >> 21 : 1;
+  const int sbits = getenv("GEEK_SAMPLE_BITS") ? atoi(getenv("GEEK_SAMPLE_BITS")) : 18;
+  const uint64_t stride = g.n > (1ull << sbits) ? g.n >> sbits : 1;
   Scratch hist, nfine, fbase;
   GEEK_TRY(hist.alloc(ncell * 4, s));
   GEEK_TRY(nfine.alloc(ncell * 4, s));
@@ -388,6 +389,10 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   // (8 tables = one 32-byte sector), counters stay u32 (tb * n < 2^32)
   int tb = (int)std::max(1.0, std::min((double)m, (1024.0 * (1 << 20)) / per_table));
   tb = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)tb, 0xFFFFFFF0ull / n));
+  // at most 16 tables per batch: the cell and fine-bin tables of a batch
+  // (~30 MB at n = 1e8) stay L2-resident for the random lookups
+  const int tb_cap = getenv("GEEK_SPLIT_TB") ? std::max(1, atoi(getenv("GEEK_SPLIT_TB"))) : 16;
+  tb = std::min(tb, tb_cap);
   if (tb >= 8 && tb < m) tb -= tb % 8;
   uint64_t acc[4] = {0, 0, 0, 0};
   for (int j0 = 0; j0 < m; j0 += tb) {

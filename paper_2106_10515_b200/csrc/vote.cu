@@ -126,7 +126,11 @@ __global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __res
         const uint64_t b = (uint64_t)j * t + row[j];
         if ((words[b >> 5] >> (b & 31)) & 1u)
           for (uint32_t k = bb_off[b]; k < bb_off[b + 1]; ++k) {
-            if (nb < kRowBins) rb[nb] = bb_bins[k];
+            const uint32_t bin = bb_bins[k];
+            // an id's count in a bin is at most m (one bucket per table): bins
+            // of 2m or more buckets can never be won by anyone
+            if (bin_size[bin] >= 2u * (uint32_t)m) continue;
+            if (nb < kRowBins) rb[nb] = bin;
             ++nb;
           }
       }
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __res
     // winners: first occurrence of each bin whose multiplicity is a strict majority
     uint32_t cnt = 0;
     for (int a = 0; a < nb; ++a) {
+      if (2u * (uint32_t)nb <= bin_size[rb[a]]) continue;  // count <= nb cannot be a strict majority
       int c = 0;
       bool first = true;
       for (int q = 0; q < nb; ++q) {
@@ -159,6 +164,7 @@ __global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __res
     wbase = __shfl_sync(0xffffffffu, wbase, 31);
     unsigned long long pos = wbase + incl - cnt;
     for (int a = 0; a < nb && cnt; ++a) {
+      if (2u * (uint32_t)nb <= bin_size[rb[a]]) continue;
       int c = 0;
       bool first = true;
       for (int q = 0; q < nb; ++q) {
