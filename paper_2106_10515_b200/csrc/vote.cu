@@ -99,40 +99,80 @@ __global__ void __launch_bounds__(256) emit_rows_kernel(const uint32_t* __restri
 // only the winners are written.
 constexpr int kRowBins = 64;  // bins one id can reach through its m buckets (checked)
 
-__global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __restrict__ codes, uint64_t n, int m,
-                                                           uint64_t t, const uint32_t* __restrict__ bb_off,
-                                                           const uint32_t* __restrict__ bb_bins,
-                                                           const uint32_t* __restrict__ bin_size,
-                                                           const uint32_t* __restrict__ gwords, uint64_t nwords,
-                                                           int smem_words, uint32_t* out_bin, uint32_t* out_id,
-                                                           uint64_t cap, unsigned long long* cursor,
-                                                           unsigned long long* overflow) {
-  extern __shared__ uint32_t sw[];
-  const bool in_smem = smem_words > 0;
-  if (in_smem)
-    for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) sw[w] = gwords[w];
-  __syncthreads();
-  const uint32_t* words = in_smem ? sw : gwords;
-  const unsigned lane = threadIdx.x & 31;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
-    const uint64_t i = base + lane;
-    const bool valid = i < n;
-    uint32_t rb[kRowBins];
+// per bucket: (first entry, entries) of its bin list; per entry: (bin, size),
+// with bins of 2m or more buckets dropped -- an id's count in a bin is at most
+// m (one bucket per table), so nobody can win them
+__global__ void pack_bins_kernel(const uint32_t* bb_off, const uint32_t* bb_bins, const uint32_t* bin_size,
+                                 uint64_t nbk, int m, uint2* pack, uint2* ent, uint32_t* words) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbk; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lo = bb_off[b], hi = bb_off[b + 1];
+    uint32_t c = 0;
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t bin = bb_bins[k], sz = bin_size[bin];
+      if (sz < 2u * (uint32_t)m) ent[lo + c++] = make_uint2(bin, sz);
+    }
+    pack[b] = make_uint2(lo, c);
+    if (c) atomicOr(&words[b >> 5], 1u << (b & 31));
+  }
+}
+
+// One block = 256 consecutive ids: their code rows (contiguous, id-major) are
+// staged in SMEM with coalesced 16-byte loads; each thread then walks its row
+// from SMEM with the winnable-bin bitmap in SMEM too.
+constexpr int kEwThreads = 256;
+__global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
+    const uint32_t* __restrict__ codes, uint64_t n, int m, uint64_t t, const uint2* __restrict__ pack,
+    const uint2* __restrict__ ent, const uint32_t* __restrict__ gwords, uint64_t nwords, int smem_words,
+    uint32_t* out_bin, uint32_t* out_id, uint64_t cap, unsigned long long* cursor, unsigned long long* overflow) {
+  extern __shared__ uint32_t sm[];
+  const int ld = m + 1;
+  uint32_t* srow = sm;                     // [256][m+1]
+  uint32_t* sw = sm + kEwThreads * ld;     // bitmap
+  const int tid = threadIdx.x;
+  if (smem_words > 0)
+    for (uint64_t w = tid; w < nwords; w += kEwThreads) sw[w] = gwords[w];
+  const uint32_t* words = smem_words > 0 ? sw : gwords;
+  const unsigned lane = tid & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)kEwThreads; base < n; base += (uint64_t)gridDim.x * kEwThreads) {
+    const int rows = (int)(n - base < (uint64_t)kEwThreads ? n - base : (uint64_t)kEwThreads);
+    __syncthreads();  // previous rows consumed (and the bitmap is in)
+    const uint32_t* src = codes + base * m;
+    if ((m & 3) == 0) {
+      const int n4 = rows * m / 4;
+      for (int e4 = tid; e4 < n4; e4 += kEwThreads) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + e4);
+        const int e = 4 * e4, r = e / m, j = e - r * m;
+        uint32_t* d = srow + r * ld + j;
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+      }
+    } else {
+      for (int e = tid; e < rows * m; e += kEwThreads) {
+        const int r = e / m;
+        srow[r * ld + (e - r * m)] = __ldg(src + e);
+      }
+    }
+    __syncthreads();
+    const uint64_t i = base + tid;
+    uint32_t rb[kRowBins], rs[kRowBins];
     int nb = 0;
-    if (valid) {
-      const uint32_t* row = codes + i * m;
+    if (tid < rows) {
+      const uint32_t* row = srow + tid * ld;
       for (int j = 0; j < m; ++j) {
         const uint64_t b = (uint64_t)j * t + row[j];
-        if ((words[b >> 5] >> (b & 31)) & 1u)
-          for (uint32_t k = bb_off[b]; k < bb_off[b + 1]; ++k) {
-            const uint32_t bin = bb_bins[k];
-            // an id's count in a bin is at most m (one bucket per table): bins
-            // of 2m or more buckets can never be won by anyone
-            if (bin_size[bin] >= 2u * (uint32_t)m) continue;
-            if (nb < kRowBins) rb[nb] = bin;
+        if ((words[b >> 5] >> (b & 31)) & 1u) {
+          const uint2 pk = __ldg(pack + b);
+          for (uint32_t k = 0; k < pk.y; ++k) {
+            const uint2 e = __ldg(ent + pk.x + k);
+            if (nb < kRowBins) {
+              rb[nb] = e.x;
+              rs[nb] = e.y;
+            }
             ++nb;
           }
+        }
       }
     }
     if (nb > kRowBins) {  // cannot happen for m <= 64 with one bin per bucket and table; keep loud
@@ -140,17 +180,19 @@ __global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __res
       nb = kRowBins;
     }
     // winners: first occurrence of each bin whose multiplicity is a strict majority
-    uint32_t cnt = 0;
-    for (int a = 0; a < nb; ++a) {
-      if (2u * (uint32_t)nb <= bin_size[rb[a]]) continue;  // count <= nb cannot be a strict majority
+    auto is_winner = [&](int a) -> bool {
+      if (2u * (uint32_t)nb <= rs[a]) return false;  // count <= nb cannot be a strict majority
       int c = 0;
       bool first = true;
       for (int q = 0; q < nb; ++q) {
-        c += rb[q] == rb[a];
-        first &= !(q < a && rb[q] == rb[a]);
+        const bool eq = rb[q] == rb[a];
+        c += eq;
+        first &= !(q < a && eq);
       }
-      if (first && 2u * (uint32_t)c > bin_size[rb[a]]) ++cnt;
-    }
+      return first && 2u * (uint32_t)c > rs[a];
+    };
+    uint32_t cnt = 0;
+    for (int a = 0; a < nb; ++a) cnt += is_winner(a);
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -164,14 +206,7 @@ __global__ void __launch_bounds__(256) emit_winners_kernel(const uint32_t* __res
     wbase = __shfl_sync(0xffffffffu, wbase, 31);
     unsigned long long pos = wbase + incl - cnt;
     for (int a = 0; a < nb && cnt; ++a) {
-      if (2u * (uint32_t)nb <= bin_size[rb[a]]) continue;
-      int c = 0;
-      bool first = true;
-      for (int q = 0; q < nb; ++q) {
-        c += rb[q] == rb[a];
-        first &= !(q < a && rb[q] == rb[a]);
-      }
-      if (first && 2u * (uint32_t)c > bin_size[rb[a]]) {
+      if (is_winner(a)) {
         if (pos < cap) {
           out_bin[pos] = rb[a];
           out_id[pos] = static_cast<uint32_t>(i);
@@ -347,22 +382,31 @@ int geek_emit_winners_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t
                             const uint32_t* bb_bins, const uint32_t* bin_size, uint32_t* out_bin, uint32_t* out_id,
                             uint64_t cap, uint64_t* count_host, void* stream) {
   cudaStream_t s = as_stream(stream);
-  Scratch cur, bm;
+  Scratch cur, bm, pk, en;
   GEEK_TRY(cur.alloc(16, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(cur.ptr, 0, 16, s));
   unsigned long long* cursor = cur.as<unsigned long long>();
   if (n) {
+    GEEK_REQUIRE(m <= 256, "emit_winners: m = %d tables per row exceeds 256", m);
     const uint64_t nb = (uint64_t)m * t, nw = (nb + 31) / 32;
+    uint32_t nent = 0;
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(&nent, bb_off + nb, 4, cudaMemcpyDeviceToHost, s));
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
     GEEK_TRY(bm.alloc(nw * 4, s));
-    binned_bitmap_kernel<<<grid_for(nw, 256), 256, 0, s>>>(bb_off, nb, bm.as<uint32_t>());
+    GEEK_TRY(pk.alloc(nb * 8, s));
+    GEEK_TRY(en.alloc((size_t)(nent ? nent : 1) * 8, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(bm.ptr, 0, nw * 4, s));
+    pack_bins_kernel<<<grid_for(nb, 256), 256, 0, s>>>(bb_off, bb_bins, bin_size, nb, m, pk.as<uint2>(),
+                                                       en.as<uint2>(), bm.as<uint32_t>());
     GEEK_CHECK_LAUNCH();
-    const int smem_words = nw * 4 <= 96 * 1024 ? (int)nw : 0;
-    if (smem_words * 4 > 48 * 1024)
-      GEEK_CHECK_CUDA(cudaFuncSetAttribute(emit_winners_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           smem_words * 4));
-    emit_winners_kernel<<<grid_for(n, 256, 148 * 8), 256, smem_words * 4, s>>>(
-        codes, n, m, t, bb_off, bb_bins, bin_size, bm.as<uint32_t>(), nw, smem_words, out_bin, out_id, cap, cursor,
-        cursor + 1);
+    const size_t fixed = (size_t)4 * kEwThreads * (m + 1);
+    const int smem_words = fixed + nw * 4 <= 160 * 1024 ? (int)nw : 0;
+    const size_t smem = fixed + (size_t)smem_words * 4;
+    GEEK_CHECK_CUDA(
+        cudaFuncSetAttribute(emit_winners_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    emit_winners_kernel<<<(unsigned)std::min<uint64_t>((n + kEwThreads - 1) / kEwThreads, 148 * 8), kEwThreads,
+                          smem, s>>>(codes, n, m, t, pk.as<uint2>(), en.as<uint2>(), bm.as<uint32_t>(), nw,
+                                     smem_words, out_bin, out_id, cap, cursor, cursor + 1);
     GEEK_CHECK_LAUNCH();
   }
   unsigned long long c[2] = {0, 0};
