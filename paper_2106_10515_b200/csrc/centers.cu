@@ -195,6 +195,17 @@ static void launch_sums(const void* X, uint64_t nrows, int d, uint64_t row_lo, c
 
 using namespace geek;
 
+namespace geek {
+// exact exponent window of float32 values into out[0..1] (atomically merged)
+int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStream_t s) {
+  if (total) {
+    exponent_range_kernel<float><<<grid_for(total, 256, 148 * 8), 256, 0, s>>>(X, total, out);
+    GEEK_CHECK_LAUNCH();
+  }
+  return GEEK_OK;
+}
+}  // namespace geek
+
 extern "C" {
 
 int geek_exponent_range(const void* X, int dtype, uint64_t n, int d, int* out_host, void* stream) {

@@ -180,6 +180,7 @@ int argsort_cols(const uint32_t* const* cols, int ncols, const int* bits, uint64
 int bitlen_u64(uint64_t v);
 
 // tensor-core assignment screen (tc_screen.cu)
+int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStream_t s);
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s);
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,

@@ -294,7 +294,8 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int NT>
 __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __restrict__ X, uint64_t n, int d,
                                                                 const double* __restrict__ A, int m,
-                                                                uint64_t* __restrict__ keys, int* exprange) {
+                                                                uint64_t* __restrict__ keys, int* exprange,
+                                                                unsigned* nonfinite) {
   constexpr int LDA = NT * 8 + 4;
   extern __shared__ __align__(16) uint8_t smem[];
   double* sA = reinterpret_cast<double*>(smem);                      // [d][LDA]
@@ -327,7 +328,11 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
   for (int q = 0; q < kPsStages - 1; ++q) issue(q);
   double acc[4][NT][2];
-  int elo = 1 << 30, ehi = -(1 << 30);
+  // exponent window from the extreme |x| bit patterns (4 integer ops per
+  // element): the exponent field of the smallest nonzero and of the largest
+  // |x| give exp_window's bounds; a non-finite value sends the caller to the
+  // exact per-element pass instead
+  uint32_t amax = 0u, amin = 0xFFFFFFFFu;
   const int kr = lane & 3, rr = lane >> 2;
   for (uint64_t q = 0; q < total; ++q) {
     cp_async_wait<kPsStages - 2>();
@@ -348,7 +353,9 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float v = st[i * 8 * kPsLdp + ks];
-        exp_window(v, elo, ehi);
+        const uint32_t ab = __float_as_uint(v) & 0x7FFFFFFFu;
+        amax = max(amax, ab);
+        amin = min(amin, ab - 1u);  // 0 wraps to the top: zeros never count
         a[i] = (double)v;
       }
 #pragma unroll
@@ -376,20 +383,25 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
   }
   cp_async_wait<0>();
   if (exprange) {
-    for (int o = 16; o; o >>= 1) {
-      elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
-      ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
-    }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    amin = __reduce_min_sync(0xffffffffu, amin);
     if (lane == 0) {
-      atomicMin(&exprange[0], elo);
-      atomicMax(&exprange[1], ehi);
+      if (amax >= 0x7F800000u) atomicOr(nonfinite, 1u);
+      if (amin != 0xFFFFFFFFu) {
+        const int e = (int)(((amin + 1u) >> 23) & 0xFF);
+        atomicMin(&exprange[0], e ? e - 150 : -172);
+      }
+      if (amax != 0u) {
+        const int e = (int)((amax >> 23) & 0xFF);
+        atomicMax(&exprange[1], e ? e - 126 : -148);
+      }
     }
   }
 }
 
 template <int NT>
 static int launch_stream(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
-                         cudaStream_t s) {
+                         unsigned* nf, cudaStream_t s) {
   const size_t smem = (size_t)d * (NT * 8 + 4) * 8 + (size_t)kPsStages * kPsStageFloats * 4;
   GEEK_CHECK_CUDA(cudaFuncSetAttribute(project_stream_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
@@ -398,21 +410,35 @@ static int launch_stream(const float* X, uint64_t n, int d, const double* A, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t ntiles = (n + 127) / 128;
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * 2);
-  project_stream_kernel<NT><<<grid, 128, smem, s>>>(X, n, d, A, m, keys, er);
+  project_stream_kernel<NT><<<grid, 128, smem, s>>>(X, n, d, A, m, keys, er, nf);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 
 static int launch_stream_any(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
                              cudaStream_t s) {
-  switch ((m + 7) / 8) {
-    case 1: return launch_stream<1>(X, n, d, A, m, keys, er, s);
-    case 2: return launch_stream<2>(X, n, d, A, m, keys, er, s);
-    case 3: return launch_stream<3>(X, n, d, A, m, keys, er, s);
-    case 4: return launch_stream<4>(X, n, d, A, m, keys, er, s);
-    case 5: return launch_stream<5>(X, n, d, A, m, keys, er, s);
-    default: return launch_stream<6>(X, n, d, A, m, keys, er, s);
+  Scratch flag;
+  unsigned* nf = nullptr;
+  if (er) {
+    GEEK_TRY(flag.alloc(4, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, s));
+    nf = flag.as<unsigned>();
   }
+  switch ((m + 7) / 8) {
+    case 1: GEEK_TRY(launch_stream<1>(X, n, d, A, m, keys, er, nf, s)); break;
+    case 2: GEEK_TRY(launch_stream<2>(X, n, d, A, m, keys, er, nf, s)); break;
+    case 3: GEEK_TRY(launch_stream<3>(X, n, d, A, m, keys, er, nf, s)); break;
+    case 4: GEEK_TRY(launch_stream<4>(X, n, d, A, m, keys, er, nf, s)); break;
+    case 5: GEEK_TRY(launch_stream<5>(X, n, d, A, m, keys, er, nf, s)); break;
+    default: GEEK_TRY(launch_stream<6>(X, n, d, A, m, keys, er, nf, s)); break;
+  }
+  if (er) {  // a non-finite value: redo the window exactly, value by value
+    unsigned h = 0;
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(&h, nf, 4, cudaMemcpyDeviceToHost, s));
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (h) GEEK_TRY(exponent_range_f32_device(X, n * (uint64_t)d, er, s));
+  }
+  return GEEK_OK;
 }
 
 template <class T>
