@@ -152,7 +152,7 @@ __global__ void cell_shortcut_kernel(SplitGeom g, uint2* cinfo, const uint32_t* 
 // Tables go in groups of 8 with the three dependent loads (key, cell,
 // fine-bin code) issued group-wide, and each id's 8 codes leave as one
 // 32-byte row segment when the row layout allows it.
-__global__ void __launch_bounds__(256) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+__global__ void __launch_bounds__(256, 4) codes_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
                                                     const uint2* __restrict__ cinfo,
                                                     const uint32_t* __restrict__ fcode,
                                                     const uint32_t* __restrict__ sbase,
