@@ -35,6 +35,7 @@
 // geek_tc_selftest).
 #include "common.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -85,6 +86,8 @@ __device__ __forceinline__ float tf32_round(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+
+__device__ __forceinline__ uint64_t desc_of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -273,7 +276,9 @@ struct TcParams {
   uint32_t lbo, sbo;
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
-  int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes
+  int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes,
+                      // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
+  unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
@@ -342,7 +347,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
         const uint32_t ct = (cq + blockIdx.x) % (uint32_t)P.nct;  // CTAs start on different center tiles
         const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
-        if (leader) {
+        if (leader && P.prof == 6 && q >= (uint64_t)Cfg::kStages) {
+          mbar_arrive(&full[s]);  // profiling: keep the stale stage, no L2 traffic
+        } else if (leader) {
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(B + s * Cfg::kStageBytes,
                    reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes, bytes,
@@ -356,9 +363,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     {  // ---------------- MMA issuer ----------------
       const uint32_t idesc = make_idesc(kTcM, kTcN);
       uint64_t q_mma = 0;
+      long long w_full = 0, w_acce = 0, w_afull = 0;
+      const long long t_start = clock64();
+      auto timed_wait = [&](uint64_t* bar, uint32_t par, long long& acc) {
+        if (P.dbg) {
+          const long long c0 = clock64();
+          mbar_wait(bar, par);
+          acc += clock64() - c0;
+        } else {
+          mbar_wait(bar, par);
+        }
+      };
       auto next_stage = [&]() -> uint32_t {
         const uint32_t s = (uint32_t)(q_mma % Cfg::kStages);
-        mbar_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1);
+        timed_wait(&full[s], (uint32_t)(q_mma / Cfg::kStages) & 1, w_full);
         fence_after();
         return s;
       };
@@ -367,41 +385,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         __syncwarp();
         ++q_mma;
       };
+      const uint64_t d0 = make_sdesc(smem_u32(B), P.lbo, P.sbo);
+      const uint32_t b_lo32 = (uint32_t)d0, d_hi32 = (uint32_t)(d0 >> 32);
+      const uint32_t a_lo32 = (uint32_t)make_sdesc(smem_u32(A), P.lbo, P.sbo);
       for (uint32_t t = 0; t < my_tiles; ++t) {
         const int ab = t % Cfg::kABuf;
         const uint32_t apar = (t / Cfg::kABuf) & 1;
-        const uint32_t abase = smem_u32(A + ab * Cfg::kABytes);
         for (int ct = 0; ct < P.nct; ++ct) {
           const uint64_t g = (uint64_t)t * P.nct + ct;
           const int buf = (int)(g & 1);
-          mbar_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u);
+          timed_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u, w_acce);
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
           for (int kc = 0; kc < nbk; ++kc) {
             const int ac = kc;  // point-tile chunk
             if (ct == 0) {  // first use of this chunk of the point tile
-              mbar_wait(&afull[ab * 4 + ac], apar);
+              timed_wait(&afull[ab * 4 + ac], apar, w_afull);
               fence_after();
             }
             const uint32_t s = next_stage();
-            const uint32_t bb = smem_u32(B + s * Cfg::kStageBytes);
+            // descriptors differ from the stage / tile bases by constant
+            // address offsets (the 14-bit address field never carries)
+            const uint32_t blo32 = b_lo32 + ((s * Cfg::kStageBytes) >> 4);
+            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * 4 * kTcSliceBytes) >> 4);
+            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * 32;
+            if (leader && P.prof != 2) {
 #pragma unroll
-            for (int j = 0; j < kTcChunk / 8; ++j) {
-              const int ks = kc * (kTcChunk / 8) + j;
-              if (P.prof == 2) continue;
-              const uint64_t bhi = make_sdesc(bb + j * kTcSliceBytes, P.lbo, P.sbo);
-              if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
-                const uint32_t ahi = tmem + Cfg::kTmemA + ab * 128 + ks * 8;
-                const uint64_t alo = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
-                const uint64_t blo = make_sdesc(bb + kTcHalfStage + j * kTcSliceBytes, P.lbo, P.sbo);
-                if (leader) {
-                  tc_mma_ta(dt, ahi, bhi, idesc, (kc | j) ? 1u : 0u);
-                  tc_mma_ta(dt, ahi, blo, idesc, 1u);
+              for (int j = 0; j < kTcChunk / 8; ++j) {
+                const uint64_t bhi = desc_of(blo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
+                const uint32_t acc = (kc | j) ? 1u : 0u;
+                if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
+                  const uint64_t blo = desc_of(blo32 + ((kTcHalfStage + j * kTcSliceBytes) >> 4), d_hi32);
+                  const uint64_t alo = desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
+                  tc_mma_ta(dt, at + j * 8, bhi, idesc, acc);
+                  tc_mma_ta(dt, at + j * 8, blo, idesc, 1u);
                   tc_mma(dt, alo, bhi, idesc, 1u);
+                } else {
+                  tc_mma(dt, desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32), bhi, idesc, acc);
                 }
-              } else {
-                const uint64_t a = make_sdesc(abase + ks * kTcSliceBytes, P.lbo, P.sbo);
-                if (leader) tc_mma(dt, a, bhi, idesc, (kc | j) ? 1u : 0u);
               }
             }
             if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
@@ -418,6 +439,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           __syncwarp();
         }
       }
+      if (P.dbg && leader) {
+        P.dbg[blockIdx.x * 4 + 0] = (unsigned long long)w_full;
+        P.dbg[blockIdx.x * 4 + 1] = (unsigned long long)w_acce;
+        P.dbg[blockIdx.x * 4 + 2] = (unsigned long long)w_afull;
+        P.dbg[blockIdx.x * 4 + 3] = (unsigned long long)(clock64() - t_start);
+      }
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
     Top4 cur;
@@ -429,7 +456,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-      if (P.prof != 1) {
+      if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3)) {
         float v[64];
         tc_ld32_async(trow, v);       // both halves in flight, one wait
         tc_ld32_async(trow + 32, v + 32);
@@ -546,7 +573,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
-            if (P.prof == 3) continue;
+            if (P.prof == 3 || P.prof >= 5) continue;
             if (Cfg::kATmem) {
               hi[4 * p] = h0;
               hi[4 * p + 1] = h1;
@@ -559,7 +586,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             }
           }
           if (Cfg::kATmem) {
-            if (P.prof != 3)
+            if (P.prof != 3 && P.prof < 5)
               tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 32 + (warp >> 2) * 16,
                       hi);
             tc_wait_st();
@@ -697,7 +724,29 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.top_s = top_s;
   P.top_i = top_i;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
-  return nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
+  P.dbg = nullptr;
+  Scratch dbg;
+  if (getenv("GEEK_SCREEN_DBG")) {
+    GEEK_TRY(dbg.alloc(148 * 4 * 8 * 2, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 4 * 8 * 2, s));
+    P.dbg = dbg.as<unsigned long long>();
+  }
+  const int st = nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
+  if (st == GEEK_OK && P.dbg) {  // diagnostics: where the MMA warp waits
+    unsigned long long h[148 * 4];
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+    double f = 0, a = 0, af = 0, tot = 0;
+    for (int b = 0; b < 148; ++b) {
+      f += h[4 * b];
+      a += h[4 * b + 1];
+      af += h[4 * b + 2];
+      tot += h[4 * b + 3];
+    }
+    fprintf(stderr, "[screen dbg] MMA warp cycles: total %.3g, wait B %.1f%%, wait acc %.1f%%, wait A %.1f%%\n", tot / 148,
+            100 * f / tot, 100 * a / tot, 100 * af / tot);
+  }
+  return st;
 }
 
 // ---- self-test of the operand layout and the measured screen error -------------

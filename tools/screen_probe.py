@@ -29,6 +29,6 @@ if os.environ.get("_PROBE_CHILD"):
     print(f"mode={os.environ.get('GEEK_SCREEN_PROF','0')} nprod={os.environ.get('GEEK_SCREEN','3')} "
           f"screen_ms={min(ms[1:]):.2f} all={['%.2f' % v for v in ms]}", flush=True)
 else:
-    for mode in ["0", "1", "2", "3"]:
+    for mode in os.environ.get("PROBE_MODES", "0,1,2,3").split(","):
         env = dict(os.environ, _PROBE_CHILD="1", GEEK_SCREEN_PROF=mode, GEEK_SCREEN_ONLY="1")
         subprocess.run([sys.executable, __file__] + sys.argv[1:], env=env, check=False)
