@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="geek", choices=["geek", "reference"])
     ap.add_argument("--n", type=int, default=100_000_000)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=50_000)
+    ap.add_argument("--cpu-sample", type=int, default=20_000)
     return ap.parse_args()
 
 
