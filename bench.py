@@ -247,14 +247,23 @@ def main():
         sec = info["screen_ms"] / 1e3
         kk = info.get("centers", ngroups)
         flops = 2.0 * (hi - lo) * kk * P["d"]
-        kpad = -(-kk // 128) * 128
+        nct = -(-kk // 128)
+        kexec = 128 * (nct - 1) + -(-(kk - 128 * (nct - 1)) // 16) * 16  # last tile at N = valid rounded to 16
+        nl = hi - lo
+        exec_flops = 2.0 * nl * kexec * (3 * P["d"] + 8)  # 3 TF32 products + the |c'|^2 slice
         roof = dict(kernel="tc_screen_kernel", bound="tensor", achieved=flops / sec / 1e12, unit="TFLOP/s",
-                    peak=peaks.get("bf16_tflops", 1590.0), traffic=None,
-                    peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS; TF32 dense is half of it)",
-                    executed_tf32_tflops=3 * 2.0 * (hi - lo) * kpad * P["d"] / sec / 1e12,
+                    peak=peaks.get("bf16_tflops", 1590.0),
+                    # dram read + write per launch from `ncu --set full` (profiles/r1_kernels.md: 51.24 GB
+                    # + 6.40 GB at n = 1e8), scaled to this rank's points; = the algorithmic X + top-list bytes
+                    traffic=57.64e9 * nl / 1e8,
+                    peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); tcgen05 kind::tf32 runs at "
+                                "half of it: 1066 TFLOP/s measured by tools/tc_rate.cu",
+                    executed_tf32_tflops=exec_flops / sec / 1e12,
+                    executed_frac_of_tf32_peak=exec_flops / sec / 1e12 / 1066.0,
                     kernel_ms=info["screen_ms"],
-                    note=f"algorithmic flops 2*n*k*d with k={kk}, d={P['d']} per launch; the kernel executes "
-                         f"3 TF32 products (hi*hi, hi*lo, lo*hi) over k padded to {kpad}")
+                    note=f"achieved = algorithmic flops 2*n*k*d (k={kk}, d={P['d']}) per launch / CUDA-event time; "
+                         f"the kernel executes 3 TF32 products (hi*hi, hi*lo, lo*hi) over k padded to {kexec} plus "
+                         f"the |c'|^2 K-slice, for exact float64 labels after the recheck")
         roof["frac"] = roof["achieved"] / roof["peak"]
     elif "geek_project_keys" in calls:
         dom = "geek_project_keys"
