@@ -273,6 +273,7 @@ struct TcParams {
   const float* mu;    // [d]
   uint64_t k;
   int nct;
+  int nlast;          // MMA N of the last center tile (its valid centers rounded up to 16)
   uint32_t lbo, sbo;
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   } else if (warp == kTcEpiWarps) {
     const bool leader = elect_one();
     {  // ---------------- MMA issuer ----------------
-      const uint32_t idesc = make_idesc(kTcM, kTcN);
+      const uint32_t idesc_full = make_idesc(kTcM, kTcN), idesc_last = make_idesc(kTcM, P.nlast);
       uint64_t q_mma = 0;
       long long w_full = 0, w_acce = 0, w_afull = 0;
       const long long t_start = clock64();
@@ -397,6 +398,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           timed_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u, w_acce);
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
+          // the last center tile runs with N = its valid centers rounded up to 16
+          const uint32_t idesc = (int)((ct + blockIdx.x) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
           for (int kc = 0; kc < nbk; ++kc) {
             const int ac = kc;  // point-tile chunk
             if (ct == 0) {  // first use of this chunk of the point tile
@@ -463,13 +466,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         tc_wait_ld();
         tc_regs_ready(v);
         tc_regs_ready(v + 32);
+        const int cta = (int)((ct + blockIdx.x) % P.nct);
+        if (cta == P.nct - 1) {  // columns past the last tile's MMA width hold stale sums
+#pragma unroll
+          for (int u = 0; u < 64; ++u)
+            if (ch * (kTcN / 2) + u >= P.nlast) v[u] = INFINITY;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float mn = v[h * 32];
 #pragma unroll
           for (int u = 1; u < 32; ++u) mn = fminf(mn, v[h * 32 + u]);
           if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
-            const int cbase = (int)((ct + blockIdx.x) % P.nct) * kTcN + ch * (kTcN / 2) + h * 32;
+            const int cbase = cta * kTcN + ch * (kTcN / 2) + h * 32;
 #pragma unroll
             for (int u = 0; u < 32; ++u) top.push(v[h * 32 + u], cbase + u);
           }
@@ -719,6 +728,11 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.mu = mu.as<float>();
   P.k = k;
   P.nct = nct;
+  {
+    const uint64_t last = k - (uint64_t)(nct - 1) * kTcN;  // 1..128 valid centers
+    P.nlast = (int)((last + 15) / 16 * 16);
+    if (getenv("GEEK_SCREEN_FULLN")) P.nlast = kTcN;
+  }
   P.lbo = lbo;
   P.sbo = sbo;
   P.top_s = top_s;
