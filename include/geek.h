@@ -89,6 +89,17 @@ int geek_silk_invscan(const uint32_t* codes, uint64_t n, int m, uint64_t t,
 int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
                       uint64_t* keys, int* exprange, void* stream);
 
+/* geek_project_keys for a shard of rows [row_lo, row_lo + n) of an ntot-row
+ * job, with the bucket synchronisation fused in (engine.py:199-238): the key
+ * of table j is stored straight into owner rank j % G's buffer,
+ * dst_host[j % G][(j / G) * ntot + row_lo + i] -- device pointers that may be
+ * peer (NVLink) mappings, e.g. a symmetric-memory buffer.  float32 X only,
+ * d % 4 == 0, d <= 128, m <= 48, G <= 8.  The caller orders the ranks'
+ * writes against the owners' reads (barrier before and after).             */
+int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
+                             uint64_t* const* dst_host, int G, uint64_t ntot, uint64_t row_lo, int* exprange,
+                             void* stream);
+
 /* Exact even rank split of every table (transform.py:95-109, engine.py:219-225):
  * codes[i*m + j] = slot of id i in table j, ties broken by id.  keys are
  * [m][n] as produced by geek_project_keys (or any order-preserving image).

@@ -50,6 +50,7 @@ _SIGS = {
     "geek_set_minhash": (i32, [vp, i32, vp, vp, vp, u64, vp, vp]),
     "geek_silk_invscan": (i32, [vp, u64, i32, u64, vp, i32, vp, vp, vp, vp, vp]),
     "geek_project_keys": (i32, [vp, i32, u64, i32, vp, i32, vp, vp, vp]),
+    "geek_project_keys_routed": (i32, [vp, i32, u64, i32, vp, i32, vp, i32, u64, u64, vp, vp]),
     "geek_rank_split": (i32, [vp, u64, i32, u64, vp, vp, vp]),
     "geek_rank_split_strided": (i32, [vp, u64, u64, vp, u64, u64, vp]),
     "geek_column_keys": (i32, [vp, i32, u64, u64, u64, vp, vp]),

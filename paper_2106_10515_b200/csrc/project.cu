@@ -291,10 +291,22 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Where table t's key of local point p goes: dst[t % G] + (t / G) * ntot +
+// row_lo + p.  G = 1 is the local [m][n] array; G > 1 stores every key
+// straight into its owner rank's buffer (peer memory over NVLink), which is
+// the bucket synchronisation of engine.py:199-238 without a separate
+// all-to-all.
+constexpr int kMaxKeyDst = 8;
+struct KeyDst {
+  uint64_t* ptr[kMaxKeyDst];
+  int G;
+  uint64_t ntot, row_lo;
+};
+
 template <int NT>
 __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __restrict__ X, uint64_t n, int d,
                                                                 const double* __restrict__ A, int m,
-                                                                uint64_t* __restrict__ keys, int* exprange,
+                                                                const KeyDst dst, int* exprange,
                                                                 unsigned* nonfinite) {
   constexpr int LDA = NT * 8 + 4;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -334,6 +346,14 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
   // exact per-element pass instead
   uint32_t amax = 0u, amin = 0xFFFFFFFFu;
   const int kr = lane & 3, rr = lane >> 2;
+  uint64_t* kdst[NT][2];  // this thread's tables (D fragment columns)
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = j * 8 + kr * 2 + h;
+      kdst[j][h] = t < m ? dst.ptr[t % dst.G] + (uint64_t)(t / dst.G) * dst.ntot + dst.row_lo : nullptr;
+    }
   for (uint64_t q = 0; q < total; ++q) {
     cp_async_wait<kPsStages - 2>();
     __syncthreads();                // chunk q landed for all threads; stage (q-1) % S is free
@@ -376,7 +396,7 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int t = j * 8 + kr * 2 + h;
-            if (t < m) keys[(uint64_t)t * n + pt] = f64_key(acc[i][j][h]);
+            if (t < m) kdst[j][h][pt] = f64_key(acc[i][j][h]);
           }
       }
     }
@@ -400,7 +420,7 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 }
 
 template <int NT>
-static int launch_stream(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
+static int launch_stream(const float* X, uint64_t n, int d, const double* A, int m, const KeyDst& dst, int* er,
                          unsigned* nf, cudaStream_t s) {
   const size_t smem = (size_t)d * (NT * 8 + 4) * 8 + (size_t)kPsStages * kPsStageFloats * 4;
   GEEK_CHECK_CUDA(cudaFuncSetAttribute(project_stream_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -410,13 +430,13 @@ static int launch_stream(const float* X, uint64_t n, int d, const double* A, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t ntiles = (n + 127) / 128;
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * 2);
-  project_stream_kernel<NT><<<grid, 128, smem, s>>>(X, n, d, A, m, keys, er, nf);
+  project_stream_kernel<NT><<<grid, 128, smem, s>>>(X, n, d, A, m, dst, er, nf);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 
-static int launch_stream_any(const float* X, uint64_t n, int d, const double* A, int m, uint64_t* keys, int* er,
-                             cudaStream_t s) {
+static int launch_stream_any(const float* X, uint64_t n, int d, const double* A, int m, const KeyDst& keys,
+                             int* er, cudaStream_t s) {
   Scratch flag;
   unsigned* nf = nullptr;
   if (er) {
@@ -477,7 +497,14 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
   GEEK_REQUIRE(d >= 1 && m >= 1, "empty projection");
   if (n == 0) return GEEK_OK;
   if (m <= 48 && dtype == 0 && d % 4 == 0 && d <= 128 && !getenv("GEEK_NO_DMMA") && !getenv("GEEK_NO_PSTREAM"))
-    return launch_stream_any((const float*)X, n, d, A, m, keys, exprange, s);
+  {
+    KeyDst dst{};
+    dst.ptr[0] = keys;
+    dst.G = 1;
+    dst.ntot = n;
+    dst.row_lo = 0;
+    return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
+  }
   if (m <= 48 && !getenv("GEEK_NO_DMMA")) {  // DMMA path (up to 6 column fragments)
     if (dtype == 0) launch_dmma<float>((const float*)X, n, d, A, m, keys, exprange, s);
     else launch_dmma<double>((const double*)X, n, d, A, m, keys, exprange, s);
@@ -509,6 +536,24 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
     project_kernel<double><<<grid, kProjThreads, 0, s>>>((const double*)X, n, d, A, m, keys, exprange);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
+}
+
+int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
+                             uint64_t* const* dst_host, int G, uint64_t ntot, uint64_t row_lo, int* exprange,
+                             void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(G >= 1 && G <= kMaxKeyDst, "routed projection supports 1..%d owners", kMaxKeyDst);
+  GEEK_REQUIRE(dtype == 0 && d % 4 == 0 && d >= 4 && d <= 128 && m >= 1 && m <= 48,
+               "routed projection needs float32 rows, d %% 4 == 0, d <= 128, m <= 48");
+  GEEK_REQUIRE(row_lo + n <= ntot, "rows [%llu, %llu) outside the %llu-row key arrays",
+               (unsigned long long)row_lo, (unsigned long long)(row_lo + n), (unsigned long long)ntot);
+  if (n == 0) return GEEK_OK;
+  KeyDst dst{};
+  for (int q = 0; q < G; ++q) dst.ptr[q] = dst_host[q];
+  dst.G = G;
+  dst.ntot = ntot;
+  dst.row_lo = row_lo;
+  return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
 }
 
 int geek_column_keys(const void* values, int dtype, uint64_t n, uint64_t stride, uint64_t col,

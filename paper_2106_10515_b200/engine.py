@@ -189,6 +189,55 @@ class _Timer:
         return self.t
 
 
+_SYMM = {}
+_ROUTED_OFF = [bool(__import__('os').environ.get('GEEK_NO_ROUTED'))]
+
+
+def _symm_keys(comm: _Comm, rows: int, cols: int, device):
+    """Symmetric-memory int64 [rows, cols] buffer mapped on every rank (cached
+    per shape; one live at a time)."""
+    key = (comm.G, rows, cols, device.index)
+    ent = _SYMM.get(key)
+    if ent is None:
+        import torch.distributed._symmetric_memory as symm
+        group = dist.group.WORLD
+        try:
+            symm.enable_symm_mem_for_group(group.group_name)
+        except Exception:  # already enabled / not needed on this torch
+            pass
+        _SYMM.clear()
+        buf = symm.empty((rows, cols), dtype=torch.int64, device=device)
+        handle = symm.rendezvous(buf, group)
+        ent = (buf, handle)
+        _SYMM[key] = ent
+    return ent
+
+
+def _routable(X: torch.Tensor, m: int, G: int) -> bool:
+    return (X.is_cuda and X.dtype == torch.float32 and X.shape[1] % 4 == 0 and 4 <= X.shape[1] <= 128
+            and 1 <= m <= 48 and G <= 8)
+
+
+def project_routed(X_local: torch.Tensor, A: np.ndarray, n: int, row_lo: int, comm: _Comm,
+                   exprange: torch.Tensor) -> torch.Tensor:
+    """Projection with the bucket synchronisation fused in (engine.py:199-238):
+    every rank stores the key of table j for its rows straight into owner
+    j % G's symmetric buffer over NVLink (geek_project_keys_routed), so no
+    all-to-all follows.  Returns this rank's [m_own, n] keys."""
+    m, G = A.shape[0], comm.G
+    n_local, d = X_local.shape
+    buf, handle = _symm_keys(comm, -(-m // G), n, X_local.device)
+    ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)
+    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    handle.barrier()  # every owner is done with the previous job's keys
+    _lib.call("geek_project_keys_routed", _lib.ptr(X_local), _lib.dtype_code(X_local), n_local, d, _lib.ptr(Ad),
+              m, _lib.hptr(ptrs), G, n, row_lo, _lib.ptr(exprange), _lib.stream())
+    handle.barrier()  # all keys of this rank's tables have landed
+    comm.count("BucketShard", n_local * m * 8 * (G - 1) // G)
+    own = len([j for j in range(m) if j % G == comm.rank])
+    return buf[:own]
+
+
 def route_tables(keys: torch.Tensor, n: int, comm: _Comm) -> torch.Tensor:
     """Bucket synchronisation (engine.py:199-238): every rank holds keys
     [m, n_local] of its contiguous shard; table j goes to rank j % G, which
@@ -239,12 +288,21 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     tm = _Timer()
     A = p.direction_matrix(d)
     own = [j for j in range(m) if j % G == rank]
+    keys_own = None
     with tm.stage("transform"):
         exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=X_local.device)
-        keys = project_keys(X_local, A, exprange)  # [m, n_local]; exponent window fused
+        if comm.on and _routable(X_local, m, G) and not _ROUTED_OFF[0]:
+            try:
+                keys_own = project_routed(X_local, A, n, row_lo, comm, exprange)
+            except Exception as exc:  # no peer mappings here: the all-to-all path below
+                _ROUTED_OFF[0] = True
+                warnings.append(f"routed projection unavailable ({exc}); using all_to_all")
+        if keys_own is None:
+            keys = project_keys(X_local, A, exprange)  # [m, n_local]; exponent window fused
     with tm.stage("sync_buckets"):
-        keys_own = route_tables(keys, n, comm)
-        del keys
+        if keys_own is None:
+            keys_own = route_tables(keys, n, comm)
+            del keys
         stats = {}
         codes = rank_split_codes(keys_own.contiguous(), t, stats) if own else None
         del keys_own

@@ -49,6 +49,32 @@ def main():
             if rank == 0:
                 print(f"[G={world}] {name} g={g}: {'OK' if good else 'MISMATCH'} groups={len(got)} "
                       f"bytes={out.transport_bytes}", flush=True)
+    # float32 rows take the routed projection (keys stored into the owners'
+    # symmetric buffers); checked against the oracle on the float32 values
+    for name in ("c06", "small"):
+        m = meta()["pipelines"][name]
+        _, n, d, C, sep, seed = m["spec"]
+        X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+        X = X.astype(np.float32)
+        for g in m["runs"]:
+            if int(g) % world:
+                continue
+            cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(int(g)),
+                                   homo=G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]),
+                                   seeding=G.SeedingParams(m["K"], m["L"], min_group_size=m["delta"],
+                                                           seed=m["sseed"]))
+            out = G.run_pipeline(G.DenseData(X), cfg)
+            ref = O.pipeline_dense(X.astype(np.float64), m["m"], m["t"], m["tseed"], m["K"], m["L"], m["delta"],
+                                   m["sseed"], g=int(g))
+            got = [tuple(x.members.tolist()) for x in out.seed_groups]
+            want = [tuple(np.asarray(x.members if hasattr(x, "members") else x).tolist()) for x in ref["groups"]]
+            good = (got == want and np.array_equal(out.clustering.assignment, ref["labels"])
+                    and np.array_equal(out.clustering.radii, ref["radii"]))
+            ok &= good
+            if rank == 0:
+                print(f"[G={world}] {name} f32 g={g}: {'OK' if good else 'MISMATCH'} groups={len(got)} "
+                      f"bytes={out.transport_bytes} warnings={out.warnings if hasattr(out, 'warnings') else ''}",
+                      flush=True)
     dist.barrier()
     dist.destroy_process_group()
     if not ok:
