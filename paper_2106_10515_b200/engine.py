@@ -257,6 +257,92 @@ def route_tables(keys: torch.Tensor, n: int, comm: _Comm) -> torch.Tensor:
     return torch.cat([pt.view(len(own), hi - lo) for pt, (lo, hi) in zip(parts, spans)], dim=1).contiguous()
 
 
+def _pw_leaf(vals) -> float:
+    """numpy's pairwise_sum on <= 128 doubles (loops_utils.h: 8 accumulators)."""
+    n = len(vals)
+    if n < 8:
+        res = 0.0
+        for v in vals:
+            res += v
+        return res
+    r = list(vals[:8])
+    i = 8
+    while i < n - n % 8:
+        for j in range(8):
+            r[j] += vals[i + j]
+        i += 8
+    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+    while i < n:
+        res += vals[i]
+        i += 1
+    return res
+
+
+def sharded_pairwise_sum(best: torch.Tensor, n: int, row_lo: int, comm: _Comm) -> float:
+    """numpy's pairwise sum of the n-element array whose rows [row_lo, row_lo +
+    len(best)) this rank holds, without gathering it: every rank sums the
+    maximal subtrees of numpy's recursion (n2 = n/2 rounded down to a multiple
+    of 8) that lie inside its rows on the device, ships those values plus the
+    elements of leaf blocks that cross a shard boundary, and the top of the
+    tree is evaluated identically on every rank."""
+    lo, hi = row_lo, row_lo + best.numel()
+    nodes, elems = [], []
+
+    def walk(a, m):
+        if a >= hi or a + m <= lo or m == 0:
+            return
+        if lo <= a and a + m <= hi:
+            nodes.append((a, m))
+            return
+        if m <= 128:  # a leaf block crossing a shard boundary: ship its elements
+            elems.append((max(a, lo), min(a + m, hi)))
+            return
+        m2 = m // 2
+        m2 -= m2 % 8
+        walk(a, m2)
+        walk(a + m2, m - m2)
+
+    walk(0, n)
+    vals = [pairwise_sum(best[a - lo:a - lo + m]) for a, m in nodes]
+    node_t = torch.tensor([[a, m] for a, m in nodes], dtype=torch.int64).reshape(-1, 2)
+    node_v = torch.cat(vals) if vals else torch.zeros(0, dtype=torch.float64, device=best.device)
+    el_idx = [i for a, b in elems for i in range(a, b)]
+    el_v = best[torch.tensor([i - lo for i in el_idx], dtype=torch.int64, device=best.device)] if el_idx else \
+        torch.zeros(0, dtype=torch.float64, device=best.device)
+    # ship (start, len, value) of the nodes and (index, value) of the elements
+    packed = torch.cat([node_t.to(best.device).view(torch.float64).reshape(-1), node_v,
+                        torch.tensor(el_idx, dtype=torch.int64, device=best.device).view(torch.float64), el_v])
+    header = torch.tensor([len(nodes), len(el_idx)], dtype=torch.int64, device=best.device).view(torch.float64)
+    allv = comm.all_gather_var(torch.cat([header, packed]), "Assignments").cpu()
+    known, points = {}, {}
+    pos = 0
+    while pos < allv.numel():
+        nn, ne = allv[pos:pos + 2].view(torch.int64).tolist()
+        pos += 2
+        nt = allv[pos:pos + 2 * nn].view(torch.int64).view(-1, 2).tolist()
+        pos += 2 * nn
+        nv = allv[pos:pos + nn].tolist()
+        pos += nn
+        ei = allv[pos:pos + ne].view(torch.int64).tolist()
+        pos += ne
+        ev = allv[pos:pos + ne].tolist()
+        pos += ne
+        for (a, m), v in zip(nt, nv):
+            known[(a, m)] = v
+        points.update(zip(ei, ev))
+
+    def evaluate(a, m):
+        if (a, m) in known:
+            return known[(a, m)]
+        if m <= 128:
+            return _pw_leaf([points[i] for i in range(a, a + m)])
+        m2 = m // 2
+        m2 -= m2 % 8
+        return evaluate(a, m2) + evaluate(a + m2, m - m2)
+
+    return evaluate(0, n)
+
+
 def _merge_groups(comm: _Comm, local: GroupSet) -> GroupSet:
     if not comm.on:
         return local
@@ -335,9 +421,10 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         radii, sizes = radii_sizes(labels, best, groups.count)
         comm.all_reduce(radii.view(torch.int64), dist.ReduceOp.MAX, "Assignments")
         comm.all_reduce(sizes, dist.ReduceOp.SUM, "Assignments")
-        best_all = comm.all_gather_var(best, "Assignments")
-        obj = pairwise_sum(best_all)
-        del best_all
+        if comm.on:
+            obj = torch.tensor([sharded_pairwise_sum(best, n, row_lo, comm)], dtype=torch.float64)
+        else:
+            obj = pairwise_sum(best)
     timings = tm.finish()
     sizes_h = groups.sizes().cpu().numpy()
 

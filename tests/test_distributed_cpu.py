@@ -1,6 +1,7 @@
 """Multi-process plumbing of the engine on CPU (gloo, world_size 2): table
 routing to owners (engine.py:199-238), seed-group all-gather (engine.py:285-295),
-the float64 radii MAX reduction over bit patterns and the variable-size gather.
+the float64 radii MAX reduction over bit patterns, the variable-size gather and
+the sharded numpy-order pairwise sum of the objective.
 The kernels themselves need a GPU; these tests cover the host-side exchange
 logic that the NCCL runs use unchanged."""
 
@@ -52,7 +53,17 @@ def _worker(rank, world, port, n, m, q):
         ok_radii = radii.tolist() == [0.5, 2.0 + world - 1, 1e-300 * world, 0.0]
         v = comm.all_gather_var(torch.arange(rank + 2, dtype=torch.float64), "Assignments")
         ok_gather = v.tolist() == [float(x) for r in range(world) for x in range(r + 2)]
-        q.put((rank, ok_route, ok_merge, ok_radii, ok_gather, dict(comm.bytes)))
+        # objective: numpy's pairwise sum of the sharded best distances, exact
+        import paper_2106_10515_b200.engine as E
+        E.pairwise_sum = lambda t: torch.tensor([float(np.add.reduce(t.numpy()))], dtype=torch.float64)
+        ok_pw = True
+        for npts in (5, 130, 1000, 20_011):
+            vals = np.random.default_rng(npts).standard_normal(npts) * 10.0 ** np.random.default_rng(1).integers(
+                -8, 8, npts)
+            plo, phi = split_data(npts, world)[rank]
+            got_pw = E.sharded_pairwise_sum(torch.from_numpy(vals[plo:phi].copy()), npts, plo, comm)
+            ok_pw &= got_pw == float(np.add.reduce(vals))
+        q.put((rank, ok_route, ok_merge, ok_radii, ok_gather and ok_pw, dict(comm.bytes)))
     finally:
         dist.destroy_process_group()
 
