@@ -194,7 +194,7 @@ def main():
     clk = clocks.stop()
     calls = timer.ms_by_name()
     info = dict(out.info)
-    stage = {k: round(v / (args.warmup + args.steps), 4) for k, v in out.timings.items()}
+    stage = {k: round(v, 4) for k, v in out.timings.items()}  # CUDA-event stage times of the last step
     k_star, ngroups = out.k_star, len(out.seed_groups) if n <= 10**6 else out._groups.count
 
     # ---- launches per step (torch profiler / CUPTI, untimed) ------------------
@@ -208,6 +208,11 @@ def main():
         launches = sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "geek::" in e.name)
         if os.environ.get("GEEK_PROFILE") and rank == 0:
             print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=45), file=sys.stderr)
+        if os.environ.get("GEEK_TRACE") and rank == 0:  # CPU + GPU timeline of one step (chrome trace)
+            with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as tr:
+                step(X)
+                torch.cuda.synchronize()
+            tr.export_chrome_trace(os.environ["GEEK_TRACE"])
     except Exception as exc:  # profiler unavailable: leave null
         print(f"[bench] launch count unavailable: {exc}", file=sys.stderr)
 

@@ -124,42 +124,46 @@ def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Ten
     table-major, then in sorted (owner, signature) order."""
     nb = sig.shape[1]
     dev = sig.device
-    tables = range(L) if tables is None else tables
-    width = K + (1 if owner is not None else 0)
-    bits = ([max(1, int(int(owner.max().item())).bit_length())] if owner is not None and nb else []) + \
-        [max(1, int(universe - 1).bit_length())] * K
-    bits = np.array(bits, dtype=np.int32)
-    perm = _lib.empty(max(1, nb), _lib.U32)
-    gid = _lib.empty(max(1, nb), _lib.U32)
-    pb, pn, bs, bt, bsig = [], [], [], [], []
-    base = 0
-    for st in tables:
-        cols = ([owner] if owner is not None else []) + [sig[st * K + j] for j in range(K)]
-        rows = torch.stack(cols, dim=1).contiguous()
-        ng = np.zeros(1, dtype=np.uint64)
-        _lib.call("geek_group_rows", _lib.ptr(rows), nb, width, _lib.hptr(bits), _lib.ptr(perm), _lib.ptr(gid),
-                  _lib.hptr(ng), _lib.stream())
-        g = gid[:nb].to(torch.int64)
-        counts = torch.bincount(g, minlength=int(ng[0]))
-        binned = counts >= 2
-        nbins = int(binned.sum().item())
-        if nbins == 0:
-            continue
-        newid = torch.cumsum(binned.to(torch.int64), 0) - 1 + base
-        sel = binned[g]
-        pb.append(perm[:nb].to(torch.int64)[sel])
-        pn.append(newid[g][sel])
-        bs.append(counts[binned].to(torch.int32))
-        bt.append(np.full(nbins, st, dtype=np.int64))
-        first = torch.ones_like(sel)
-        first[1:] = g[1:] != g[:-1]
-        bsig.append(rows[perm[:nb].to(torch.int64)[sel & first]][:, -K:])
-        base += nbins
-    if not pb:
+    tables = list(range(L) if tables is None else tables)
+    nt = len(tables)
+    if nb == 0 or nt == 0:
         z = torch.zeros(0, dtype=torch.int64, device=dev)
         return Bins(z, z, torch.zeros(0, dtype=torch.int32, device=dev), np.zeros(0, np.int64),
                     torch.zeros((0, K), dtype=torch.int32, device=dev))
-    return Bins(torch.cat(pb), torch.cat(pn), torch.cat(bs), np.concatenate(bt), torch.cat(bsig))
+    # all SILK tables in one group-by: rows (table, owner, signature), the
+    # table column most significant, so groups come out table-major
+    width = K + 1 + (1 if owner is not None else 0)
+    bits = [max(1, int(nt - 1).bit_length())] + \
+        ([max(1, int(int(owner.max().item())).bit_length())] if owner is not None else []) + \
+        [max(1, int(universe - 1).bit_length())] * K
+    bits = np.array(bits, dtype=np.int32)
+    tcol = torch.arange(nt, dtype=torch.int32, device=dev).repeat_interleave(nb)
+    cols = [tcol]
+    if owner is not None:
+        cols.append(owner.to(torch.int32).repeat(nt))
+    idx = torch.tensor([st * K for st in tables], dtype=torch.int64, device=dev)
+    for j in range(K):
+        cols.append(sig.index_select(0, idx + j).reshape(-1).to(torch.int32))
+    rows = torch.stack(cols, dim=1).contiguous()
+    nr = nt * nb
+    perm = _lib.empty(nr, _lib.U32)
+    gid = _lib.empty(nr, _lib.U32)
+    ng = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_group_rows", _lib.ptr(rows), nr, width, _lib.hptr(bits), _lib.ptr(perm), _lib.ptr(gid),
+              _lib.hptr(ng), _lib.stream())
+    g = gid.to(torch.int64)
+    counts = torch.bincount(g, minlength=int(ng[0]))
+    binned = counts >= 2
+    newid = torch.cumsum(binned.to(torch.int64), 0) - 1
+    sel = binned[g]
+    p64 = perm.to(torch.int64)
+    psel = p64[sel]
+    first = torch.ones_like(sel)
+    first[1:] = g[1:] != g[:-1]
+    heads = p64[sel & first]
+    bt = torch.tensor(tables, dtype=torch.int64, device=dev)[rows[heads, 0].to(torch.int64)]
+    return Bins(psel % nb, newid[g][sel], counts[binned].to(torch.int32), bt.cpu().numpy(),
+                rows[heads][:, -K:])
 
 
 # ---------------------------------------------------------------------------
