@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     {  // ---------------- MMA issuer ----------------
       const uint32_t idesc_full = make_idesc(kTcM, kTcN), idesc_last = make_idesc(kTcM, P.nlast);
       uint64_t q_mma = 0;
-      long long w_full = 0, w_acce = 0, w_afull = 0;
+      long long w_full = 0, w_acce = 0, w_afull = 0, w_issue = 0;
       const long long t_start = clock64();
       auto timed_wait = [&](uint64_t* bar, uint32_t par, long long& acc) {
         if (P.dbg) {
@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const uint32_t blo32 = b_lo32 + ((s * Cfg::kStageBytes) >> 4);
             const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * 4 * kTcSliceBytes) >> 4);
             const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * 32;
+            const long long c_is = P.dbg ? clock64() : 0;
             if (leader && P.prof != 2) {
 #pragma unroll
               for (int j = 0; j < kTcChunk / 8; ++j) {
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
                 }
               }
             }
+            if (P.dbg) w_issue += clock64() - c_is;
             if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
@@ -443,10 +445,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         }
       }
       if (P.dbg && leader) {
-        P.dbg[blockIdx.x * 4 + 0] = (unsigned long long)w_full;
-        P.dbg[blockIdx.x * 4 + 1] = (unsigned long long)w_acce;
-        P.dbg[blockIdx.x * 4 + 2] = (unsigned long long)w_afull;
-        P.dbg[blockIdx.x * 4 + 3] = (unsigned long long)(clock64() - t_start);
+        P.dbg[blockIdx.x * 8 + 0] = (unsigned long long)w_full;
+        P.dbg[blockIdx.x * 8 + 1] = (unsigned long long)w_acce;
+        P.dbg[blockIdx.x * 8 + 2] = (unsigned long long)w_afull;
+        P.dbg[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
+        P.dbg[blockIdx.x * 8 + 4] = (unsigned long long)w_issue;
       }
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
@@ -747,18 +750,21 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   }
   const int st = nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
   if (st == GEEK_OK && P.dbg) {  // diagnostics: where the MMA warp waits
-    unsigned long long h[148 * 4];
+    unsigned long long h[148 * 8];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-    double f = 0, a = 0, af = 0, tot = 0;
+    double f = 0, a = 0, af = 0, tot = 0, is = 0;
     for (int b = 0; b < 148; ++b) {
-      f += h[4 * b];
-      a += h[4 * b + 1];
-      af += h[4 * b + 2];
-      tot += h[4 * b + 3];
+      f += h[8 * b];
+      a += h[8 * b + 1];
+      af += h[8 * b + 2];
+      tot += h[8 * b + 3];
+      is += h[8 * b + 4];
     }
-    fprintf(stderr, "[screen dbg] MMA warp cycles: total %.3g, wait B %.1f%%, wait acc %.1f%%, wait A %.1f%%\n", tot / 148,
-            100 * f / tot, 100 * a / tot, 100 * af / tot);
+    fprintf(stderr,
+            "[screen dbg] MMA warp cycles: total %.3g, wait B %.1f%%, wait acc %.1f%%, wait A %.1f%%, issuing the "
+            "12 MMAs of a chunk %.1f%%\n",
+            tot / 148, 100 * f / tot, 100 * a / tot, 100 * af / tot, 100 * is / tot);
   }
   return st;
 }
