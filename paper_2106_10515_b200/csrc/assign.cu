@@ -619,8 +619,8 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
 __global__ void __launch_bounds__(256) tc_classify2_kernel(
     const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C, uint64_t k,
     const float* __restrict__ top_s, const int* __restrict__ top_i, float* xnorm, const float* __restrict__ mu,
-    const unsigned long long* cmax_bits, int nprod, int64_t* labels, double* best, uint32_t* amb,
-    unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
+    const double* __restrict__ xpart, const unsigned long long* cmax_bits, int nprod, int64_t* labels, double* best,
+    uint32_t* amb, unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   const unsigned lane = threadIdx.x & 31, h = lane & 1;
   const unsigned pmask = 3u << (lane & 30);
@@ -631,7 +631,9 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
     const float4* xr = reinterpret_cast<const float4*>(X + i * d);
     const float4* m4 = reinterpret_cast<const float4*>(mu);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
-    for (int u = 0; u < nu; ++u) {
+    if (xpart) {       // summed by the screen while it converted the point tile
+      xn2 = h == 0 ? __ldg(xpart + 2 * i) : __ldg(xpart + 2 * i + 1);
+    } else for (int u = 0; u < nu; ++u) {
       const float4 x = __ldg(xr + 2 * u + h), m = __ldg(m4 + 2 * u + h);
       const double a0 = (double)(x.x - m.x), a1 = (double)(x.y - m.y);
       const double a2 = (double)(x.z - m.z), a3 = (double)(x.w - m.w);
@@ -641,7 +643,8 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
       xn2 = fma(a3, a3, xn2);
     }
     xn2 += __shfl_xor_sync(pmask, xn2, 1);
-    const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
+    // the screen's partial sums are fp32 (relative error <= 64 u = 3.8e-6)
+    const float xn = (float)(sqrt(xn2) * (xpart ? 1.0 + 1e-5 : 1.0 + 1e-6));
     if (h == 0) xnorm[i] = xn;
     const double T = tc_threshold((double)xn, cn, d, nprod);
     const double s0 = v.s0;
@@ -826,8 +829,12 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_CUDA(cudaEventCreate(&ev0));
     GEEK_CHECK_CUDA(cudaEventCreate(&ev1));
     GEEK_CHECK_CUDA(cudaEventRecord(ev0, s));
+    // TF32x3 screen also leaves |x'|^2 per row half for the 2-lane classifier
+    Scratch xp;
+    const bool use_xp = nprod == 3 && d % 8 == 0 && d <= 128;
+    if (use_xp) GEEK_TRY(xp.alloc(n * 16, s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
-                              ti.as<int>(), s));
+                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, s));
     GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
     if (getenv("GEEK_SCREEN_ONLY")) {  // profiling hook: time the screen alone (labels are not written)
       GEEK_CHECK_CUDA(cudaEventSynchronize(ev1));
@@ -840,8 +847,9 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     }
     if (d % 8 == 0 && d <= 128)
       tc_classify2_kernel<<<grid_for(n * 2, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,
-          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(),
+          use_xp ? xp.as<double>() : nullptr, cmax, nprod, labels, best, amb.as<uint32_t>(), namb,
+          full.as<uint32_t>(), nfull);
     else if (d >= 8)
       tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
           (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,

@@ -185,7 +185,7 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s);
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     cudaStream_t s);
+                     double* xpart, cudaStream_t s);
 
 __global__ void iota_u32(uint32_t* p, uint64_t n);
 __global__ void fill_u32(uint32_t* p, uint32_t v, uint64_t n);

@@ -277,6 +277,7 @@ struct TcParams {
   uint32_t lbo, sbo;
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
+  double* xpart;      // [n][2] (NPROD = 3, may be null): |x'|^2 over each half of the dims, for the classifier
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
@@ -560,6 +561,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const uint32_t epar = ((t / Cfg::kABuf) & 1) ^ 1u;
       uint8_t* Ab = A + ab * Cfg::kABytes;
       const uint64_t p0 = tile_p0(t);
+      float xs[4] = {0.f, 0.f, 0.f, 0.f};  // |x'|^2 over this thread's half of the row's dims (kATmem layout)
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         if (kc < nck) {
@@ -585,6 +587,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
+            if (Cfg::kATmem) {
+              // fp32, four independent chains: relative error <= 64 u (the
+              // classifier inflates |x'| by 1e-5 for it)
+              xs[p] = fmaf(x0, x0, xs[p]);
+              xs[p] = fmaf(x1, x1, xs[p]);
+              xs[p] = fmaf(x2, x2, xs[p]);
+              xs[p] = fmaf(x3, x3, xs[p]);
+            }
             if (P.prof == 3 || P.prof >= 5) continue;
             if (Cfg::kATmem) {
               hi[4 * p] = h0;
@@ -607,6 +617,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           fence_proxy_async();
           mbar_arrive(&afull[ab * 4 + kc]);
         }
+      }
+      if (Cfg::kATmem && P.xpart) {
+        const uint64_t i = p0 + (warp & 3) * 32 + lane;
+        if (i < P.n) P.xpart[i * 2 + (warp >> 2)] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
       }
     };
     if (my_tiles > 0) {
@@ -721,7 +735,7 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
 
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     cudaStream_t s) {
+                     double* xpart, cudaStream_t s) {
   GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
   TcParams P;
   P.X = X;
@@ -740,6 +754,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.sbo = sbo;
   P.top_s = top_s;
   P.top_i = top_i;
+  P.xpart = nprod == 3 ? xpart : nullptr;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   P.dbg = nullptr;
   Scratch dbg;
@@ -843,7 +858,7 @@ extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* o
   unsigned long long* cmax = misc.as<unsigned long long>();
   int nct = 0;
   GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, nprod, lbo, sbo, img, c2, mu, cmax, nct, s));
-  GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, nprod, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(),
+  GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, nprod, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(), nullptr,
                             s));
   double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
   unsigned long long* bad = misc.as<unsigned long long>() + 2;
