@@ -160,19 +160,30 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
     int nb = 0;
     if (tid < rows) {
       const uint32_t* row = srow + tid * ld;
-      for (int j = 0; j < m; ++j) {
-        const uint64_t b = (uint64_t)j * t + row[j];
-        if ((words[b >> 5] >> (b & 31)) & 1u) {
-          const uint2 pk = __ldg(pack + b);
-          for (uint32_t k = 0; k < pk.y; ++k) {
-            const uint2 e = __ldg(ent + pk.x + k);
+      // 8 tables at a time: their bucket lists and first entries are
+      // fetched together instead of as one dependent chain per table
+      for (int j0 = 0; j0 < m; j0 += 8) {
+        uint2 pk[8], e0[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          pk[u] = make_uint2(0u, 0u);
+          if (j0 + u < m) {
+            const uint64_t b = (uint64_t)(j0 + u) * t + row[j0 + u];
+            if ((words[b >> 5] >> (b & 31)) & 1u) pk[u] = __ldg(pack + b);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e0[u] = pk[u].y ? __ldg(ent + pk[u].x) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          for (uint32_t k = 0; k < pk[u].y; ++k) {
+            const uint2 e = k == 0 ? e0[u] : __ldg(ent + pk[u].x + k);
             if (nb < kRowBins) {
               rb[nb] = e.x;
               rs[nb] = e.y;
             }
             ++nb;
           }
-        }
       }
     }
     if (nb > kRowBins) {  // cannot happen for m <= 64 with one bin per bucket and table; keep loud

@@ -186,6 +186,13 @@ def membership_pairs(bins: Bins, buckets, csr, bucket_sizes: torch.Tensor):
     order = torch.argsort(bins.pair_bucket, stable=True)
     pbk = bins.pair_bucket[order]
     pbn = bins.pair_bin[order].to(torch.int32).contiguous()
+    # an id's count in a bin is at most the number of distinct tables among the
+    # bin's buckets (one bucket per table per id): bins with 2 * that <= |bin|
+    # cannot be won by anyone, so their memberships are not emitted at all
+    key = pbn.to(torch.int64) * bt.m + pbk // bt.stride
+    dt = torch.bincount(torch.unique(key) // bt.m, minlength=bins.count)
+    keep = (2 * dt > bins.bin_size.to(torch.int64))[pbn.to(torch.int64)]
+    pbk, pbn = pbk[keep], pbn[keep].contiguous()
     cnt = torch.bincount(pbk, minlength=nb)
     bb_off = torch.zeros(nb + 1, dtype=torch.int64, device=pbk.device)
     torch.cumsum(cnt, 0, out=bb_off[1:])
@@ -231,6 +238,13 @@ def fused_votes_codes(bins: Bins, bt: BucketTable, bucket_sizes: torch.Tensor, d
     order = torch.argsort(bins.pair_bucket, stable=True)
     pbk = bins.pair_bucket[order]
     pbn = bins.pair_bin[order].to(torch.int32).contiguous()
+    # an id's count in a bin is at most the number of distinct tables among the
+    # bin's buckets (one bucket per table per id): bins with 2 * that <= |bin|
+    # cannot be won by anyone, so their memberships are not emitted at all
+    key = pbn.to(torch.int64) * bt.m + pbk // bt.stride
+    dt = torch.bincount(torch.unique(key) // bt.m, minlength=bins.count)
+    keep = (2 * dt > bins.bin_size.to(torch.int64))[pbn.to(torch.int64)]
+    pbk, pbn = pbk[keep], pbn[keep].contiguous()
     cnt = torch.bincount(pbk, minlength=nb)
     bb_off = torch.zeros(nb + 1, dtype=torch.int64, device=pbk.device)
     torch.cumsum(cnt, 0, out=bb_off[1:])
