@@ -393,3 +393,37 @@ def test_mixed_pipeline_golden(g):
     assert np.array_equal(out.clustering.assignment, arr[f"mx_g{g}_labels"])
     assert np.array_equal(out.clustering.radii, arr[f"mx_g{g}_radii"])
     assert out.clustering.objective == m["runs"][str(g)]["objective"]
+
+
+@pytest.mark.parametrize("owners", [2, 3, 8])
+def test_routed_projection_layout(owners):
+    """geek_project_keys_routed (the fused bucket synchronisation) writes the
+    same keys as geek_project_keys, table j of rows [lo, hi) at owner j % G,
+    row (j / G), columns lo..hi of an ntot-row array -- checked on one GPU
+    with ordinary device buffers standing in for the owners' peer mappings."""
+    from paper_2106_10515_b200 import _lib
+    from paper_2106_10515_b200.transform import project_keys
+    rng = np.random.default_rng(owners)
+    ntot, lo, hi, d, m = 5003, 1201, 4090, 32, 21
+    X = rng.standard_normal((ntot, d)).astype(np.float32)
+    A = rng.standard_normal((m, d))
+    ref = project_keys(_lib.to_dev(X), A).cpu().numpy()
+    bufs = [torch.full((-(-m // owners), ntot), -1, dtype=torch.int64, device="cuda") for _ in range(owners)]
+    ptrs = np.array([b.data_ptr() for b in bufs], dtype=np.uint64)
+    er = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device="cuda")
+    Xs = _lib.to_dev(X[lo:hi])
+    _lib.call("geek_project_keys_routed", _lib.ptr(Xs), 0, hi - lo, d, _lib.ptr(_lib.to_dev(A)), m, _lib.hptr(ptrs),
+              owners, ntot, lo, _lib.ptr(er), _lib.stream())
+    torch.cuda.synchronize()
+    for j in range(m):
+        got = bufs[j % owners][j // owners].cpu().numpy()
+        assert np.array_equal(got[lo:hi], ref[j, lo:hi]), j
+        assert (got[:lo] == -1).all() and (got[hi:] == -1).all(), j
+    O_lo, O_hi = [], []  # exp_window of every nonzero value (project.cu)
+    for v in X[lo:hi].ravel():
+        if v != 0:
+            e = (int(np.float32(v).view(np.uint32)) >> 23) & 0xFF
+            O_lo.append(e - 150 if e else -172)
+            O_hi.append(e - 126 if e else -148)
+    want = np.array([min(O_lo), max(O_hi)], dtype=np.int32)
+    assert np.array_equal(er.cpu().numpy(), want)
