@@ -57,12 +57,15 @@ struct TcCfg {
   // and only the lo part in SMEM: the SMEM this frees deepens the B ring
   static constexpr bool kATmem = NPROD == 3;
   static constexpr int kABytes = kTcAPart;
-  static constexpr int kABuf = 2;                                // point tiles double-buffered
+  // NPROD = 1: point tiles double-buffered; NPROD = 3: single-buffered, the
+  // SMEM goes to the resident |c'|^2 slices instead (chunked hand-off keeps
+  // the tile switch short)
+  static constexpr int kABuf = NPROD == 3 ? 1 : 2;
   static constexpr int kStageBytes = kParts * kTcHalfStage;
   static constexpr int kStages = NPROD == 3 ? 3 : 4;
   static constexpr uint32_t kTmemCols = kATmem ? 512 : 256;
   static constexpr uint32_t kTmemA = 256;                        // TMEM A operand: buffer b at 256 + 128 b
-  static constexpr size_t kSmem = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
+  static constexpr size_t kSmemFixed = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
 };
 
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
@@ -278,6 +281,7 @@ struct TcParams {
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
   double* xpart;      // [n][2] (NPROD = 3, may be null): |x'|^2 over each half of the dims, for the classifier
+  int c2res;          // 1: the |c'|^2/2 slices of all center tiles (+ the ones slice) stay in SMEM
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
@@ -294,14 +298,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                           // kABuf x kABytes
   uint8_t* B = smem + Cfg::kABuf * Cfg::kABytes;               // kStages x kStageBytes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(B + Cfg::kStages * Cfg::kStageBytes);
+  uint8_t* C2 = B + Cfg::kStages * Cfg::kStageBytes;           // resident: ones slice, then one slice per tile
+  const uint32_t c2bytes = P.c2res ? (uint32_t)(P.nct + 1) * kTcSliceBytes : 0u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(C2 + c2bytes);
   uint64_t* full = bars;                    // [8] stage loaded (TMA tx)
   uint64_t* empty = bars + 8;               // [8] stage consumed (MMA commit)
   uint64_t* accf = bars + 16;               // [2] accumulator ready (MMA commit)
   uint64_t* acce = bars + 18;               // [2] accumulator drained (256 epilogue threads)
   uint64_t* afull = bars + 20;              // [kABuf][4] point-tile chunk written (256 threads)
   uint64_t* aempty = bars + 28;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
+  uint64_t* c2full = bars + 36;             // resident |c'|^2 slices loaded (TMA tx)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
   static_assert(Cfg::kStages <= 8 && Cfg::kABuf <= 2, "barrier map");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -318,6 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       mbar_init(&afull[b], kTcEpiThreads);
       mbar_init(&aempty[b], 1);
     }
+    mbar_init(c2full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   const uint32_t tmem = *tmem_slot;
   const int nck = (P.d + kTcAChunk - 1) / kTcAChunk;  // 32-dim point-tile chunks
   const int nbk = (P.d + kTcChunk - 1) / kTcChunk;    // B chunks per center tile
-  const uint32_t qct = (uint32_t)nbk + 1;              // + the |c'|^2 slice
+  const uint32_t qct = (uint32_t)nbk + (P.c2res ? 0u : 1u);  // + the |c'|^2 slice when it is not resident
   const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts);
   const uint32_t total_q = (uint32_t)P.nct * qct;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
@@ -342,6 +350,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   if (warp == kTcEpiWarps + 1) {
     const bool leader = elect_one();
     {  // ---------------- TMA producer: the B ring ----------------
+      if (P.c2res && my_tiles > 0) {  // the |c'|^2 slices, once
+        if (leader) {
+          mbar_expect_tx(c2full, c2bytes);
+          const uint8_t* img = reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)nbk * Cfg::kStageBytes;
+          bulk_g2s(C2, img + kTcSliceBytes, kTcSliceBytes, c2full);  // the all-ones A slice
+          for (int ct = 0; ct < P.nct; ++ct)
+            bulk_g2s(C2 + (ct + 1) * kTcSliceBytes, img + (uint64_t)ct * ct_bytes, kTcSliceBytes, c2full);
+        }
+        __syncwarp();
+      }
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
       for (uint64_t q = 0; q < total_chunks; ++q) {
         const uint32_t s = (uint32_t)(q % Cfg::kStages);
@@ -434,7 +452,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
-          {  // |c'|^2 / 2, added last
+          if (P.c2res) {  // |c'|^2 / 2, added last, from the resident slices
+            if (t == 0 && ct == 0) {
+              mbar_wait(c2full, 0);
+              fence_after();
+            }
+            const uint32_t cta = (uint32_t)((ct + blockIdx.x) % P.nct);
+            const uint64_t a1 = make_sdesc(smem_u32(C2), P.lbo, P.sbo);
+            const uint64_t b1 = make_sdesc(smem_u32(C2) + (cta + 1) * kTcSliceBytes, P.lbo, P.sbo);
+            if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
+            __syncwarp();
+          } else {  // |c'|^2 / 2, added last, through the ring
             const uint32_t s = next_stage();
             const uint32_t sb = smem_u32(B + s * Cfg::kStageBytes);
             const uint64_t a1 = make_sdesc(sb + kTcSliceBytes, P.lbo, P.sbo), b1 = make_sdesc(sb, P.lbo, P.sbo);
@@ -720,7 +748,7 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
 
 template <int NPROD>
 static int launch_screen(const TcParams& P, cudaStream_t s) {
-  const size_t smem = TcCfg<NPROD>::kSmem;
+  const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)(P.nct + 1) * kTcSliceBytes : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -756,6 +784,10 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.top_i = top_i;
   P.xpart = nprod == 3 ? xpart : nullptr;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
+  // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
+  P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)(nct + 1) * kTcSliceBytes <= 227 * 1024
+                ? 1 : 0;
+  if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
   P.dbg = nullptr;
   Scratch dbg;
   if (getenv("GEEK_SCREEN_DBG")) {
