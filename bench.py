@@ -208,11 +208,12 @@ def main():
         launches = sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "geek::" in e.name)
         if os.environ.get("GEEK_PROFILE") and rank == 0:
             print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=45), file=sys.stderr)
-        if os.environ.get("GEEK_TRACE") and rank == 0:  # CPU + GPU timeline of one step (chrome trace)
+        if os.environ.get("GEEK_TRACE"):  # CPU + GPU timeline of one step (all ranks step; rank 0 exports)
             with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as tr:
                 step(X)
                 torch.cuda.synchronize()
-            tr.export_chrome_trace(os.environ["GEEK_TRACE"])
+            if rank == 0:
+                tr.export_chrome_trace(os.environ["GEEK_TRACE"])
     except Exception as exc:  # profiler unavailable: leave null
         print(f"[bench] launch count unavailable: {exc}", file=sys.stderr)
 
