@@ -88,7 +88,8 @@ class ClockSampler:
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+            ids = [f"--id={self.idx}"] if self.idx is not None else []
+            self.proc = subprocess.Popen(["nvidia-smi", *ids, f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
@@ -178,8 +179,11 @@ def main():
         out = step(X)
     barrier()
     # ---- timed region: resident data --------------------------------------
-    clocks = ClockSampler(local)
-    clocks.start()
+    # one sampler for the job: rank 0 polls every GPU of the node (an
+    # nvidia-smi per rank perturbs the timed steps)
+    clocks = ClockSampler(local if world == 1 else None)
+    if rank == 0:
+        clocks.start()
     timer = _lib.CallTimer()
     _lib.set_call_timer(timer)
     barrier()
