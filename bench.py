@@ -226,17 +226,15 @@ def main():
     if not args.no_e2e:
         Xh = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
         Xh.copy_(X)
-        del X
-        torch.cuda.empty_cache()
-        lab_h = None
+        Xd = X  # the device buffer the inputs are copied into every step
+        lab_h = torch.empty(hi - lo, dtype=torch.int64, pin_memory=True)
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            Xd = Xh.to("cuda", non_blocking=True)
+            Xd.copy_(Xh, non_blocking=True)  # host -> device, pinned
             o = step(Xd)
-            lab_h = o.labels_device.to("cpu")
-            del Xd
+            lab_h.copy_(o.labels_device, non_blocking=True)  # labels device -> host, pinned
         f1.record()
         barrier()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
