@@ -98,7 +98,27 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
  * writes against the owners' reads (barrier before and after).             */
 int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
                              uint64_t* const* dst_host, int G, uint64_t ntot, uint64_t row_lo, int* exprange,
-                             void* stream);
+                             const uint32_t* fine_cinfo, int cb, uint32_t* fine_cnt, void* stream);
+/* ...and with fine_cnt != NULL it also performs the rank split's fine-bin
+ * count of every key it writes: fine_cnt[f] += 1 for f = the key's fine bin
+ * under fine_cinfo (uint2 [m][2^cb] from geek_fine_layout, global bins).    */
+
+/* Precounted rank split (the fine histogram comes from the projection):
+ *  geek_split_plan     coarse bits and sample stride of an n-key split;
+ *  geek_coarse_hist    hist[j][cell] += sample keys [m][ns] (caller zeroes);
+ *                      the sample is rows 0, stride, 2*stride, ... of the job;
+ *  geek_fine_layout    fine bins of every cell from hist: cinfo (uint2
+ *                      [m][2^cb] = {bins, first global bin}), toff[m+1] =
+ *                      first global bin of each table, *nfb_host = total;
+ *  geek_rank_split_counted  geek_rank_split of keys [m][n] given the tables'
+ *                      hist rows [m][2^cb] and their fine counts concatenated
+ *                      in table order.  SYNC.                               */
+int geek_split_plan(uint64_t n, int* cb_out, uint64_t* stride_out);
+int geek_coarse_hist(const uint64_t* keys, uint64_t ns, int m, int cb, uint32_t* hist, void* stream);
+int geek_fine_layout(const uint32_t* hist, int m, uint64_t n, uint32_t* cinfo, uint32_t* toff, uint64_t* nfb_host,
+                     void* stream);
+int geek_rank_split_counted(const uint64_t* keys, uint64_t n, int m, uint64_t t, const uint32_t* hist,
+                            const uint32_t* fcnt, uint32_t* codes, uint64_t* stats_host, void* stream);
 
 /* Exact even rank split of every table (transform.py:95-109, engine.py:219-225):
  * codes[i*m + j] = slot of id i in table j, ties broken by id.  keys are

@@ -50,7 +50,11 @@ _SIGS = {
     "geek_set_minhash": (i32, [vp, i32, vp, vp, vp, u64, vp, vp]),
     "geek_silk_invscan": (i32, [vp, u64, i32, u64, vp, i32, vp, vp, vp, vp, vp]),
     "geek_project_keys": (i32, [vp, i32, u64, i32, vp, i32, vp, vp, vp]),
-    "geek_project_keys_routed": (i32, [vp, i32, u64, i32, vp, i32, vp, i32, u64, u64, vp, vp]),
+    "geek_project_keys_routed": (i32, [vp, i32, u64, i32, vp, i32, vp, i32, u64, u64, vp, vp, i32, vp, vp]),
+    "geek_split_plan": (i32, [u64, vp, vp]),
+    "geek_coarse_hist": (i32, [vp, u64, i32, i32, vp, vp]),
+    "geek_fine_layout": (i32, [vp, i32, u64, vp, vp, vp, vp]),
+    "geek_rank_split_counted": (i32, [vp, u64, i32, u64, vp, vp, vp, vp, vp]),
     "geek_rank_split": (i32, [vp, u64, i32, u64, vp, vp, vp]),
     "geek_rank_split_strided": (i32, [vp, u64, u64, vp, u64, u64, vp]),
     "geek_column_keys": (i32, [vp, i32, u64, u64, u64, vp, vp]),

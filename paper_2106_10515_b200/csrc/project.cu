@@ -301,6 +301,12 @@ struct KeyDst {
   uint64_t* ptr[kMaxKeyDst];
   int G;
   uint64_t ntot, row_lo;
+  // optional fused fine-bin histogram of the rank split (fine_hist_kernel's
+  // count, done here while the key is in a register): cinfo [m][2^cb] of
+  // (fine bins, first global fine bin) per coarse cell, counters fcnt
+  const uint2* cinfo;
+  uint32_t* fcnt;
+  int cb;
 };
 
 template <int NT>
@@ -396,7 +402,15 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int t = j * 8 + kr * 2 + h;
-            if (t < m) kdst[j][h][pt] = f64_key(acc[i][j][h]);
+            if (t < m) {
+              const uint64_t key = f64_key(acc[i][j][h]);
+              kdst[j][h][pt] = key;
+              if (dst.fcnt) {
+                const uint2 ci = __ldg(dst.cinfo + ((uint64_t)t << dst.cb) + (uint32_t)(key >> (64 - dst.cb)));
+                const uint32_t frac = static_cast<uint32_t>((key << dst.cb) >> 32);
+                atomicAdd(dst.fcnt + ci.y + static_cast<uint32_t>(((uint64_t)frac * ci.x) >> 32), 1u);
+              }
+            }
           }
       }
     }
@@ -503,6 +517,9 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
     dst.G = 1;
     dst.ntot = n;
     dst.row_lo = 0;
+    dst.cinfo = nullptr;
+    dst.fcnt = nullptr;
+    dst.cb = 0;
     return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
   }
   if (m <= 48 && !getenv("GEEK_NO_DMMA")) {  // DMMA path (up to 6 column fragments)
@@ -540,7 +557,7 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
 
 int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
                              uint64_t* const* dst_host, int G, uint64_t ntot, uint64_t row_lo, int* exprange,
-                             void* stream) {
+                             const uint32_t* fine_cinfo, int cb, uint32_t* fine_cnt, void* stream) {
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(G >= 1 && G <= kMaxKeyDst, "routed projection supports 1..%d owners", kMaxKeyDst);
   GEEK_REQUIRE(dtype == 0 && d % 4 == 0 && d >= 4 && d <= 128 && m >= 1 && m <= 48,
@@ -553,6 +570,10 @@ int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const 
   dst.G = G;
   dst.ntot = ntot;
   dst.row_lo = row_lo;
+  GEEK_REQUIRE(!fine_cnt || (fine_cinfo && cb >= 1 && cb <= 24), "fused fine counts need the cell layout");
+  dst.cinfo = reinterpret_cast<const uint2*>(fine_cinfo);
+  dst.fcnt = fine_cnt;
+  dst.cb = cb;
   return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
 }
 

@@ -267,20 +267,48 @@ __global__ void big_rank_kernel(SplitGeom g, const uint32_t* rows, const uint32_
   }
 }
 
-static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, uint64_t* stats_acc,
-                            cudaStream_t s) {
-  const uint64_t ncell = (uint64_t)g.tb * g.nc;
-  // ~2M samples per table shape the fine bins; the fine counts are exact anyway
+// coarse-histogram sample stride: ~2^18 keys per table shape the fine bins
+// (the fine counts are exact anyway)
+static uint64_t sample_stride(uint64_t n) {
   const int sbits = getenv("GEEK_SAMPLE_BITS") ? atoi(getenv("GEEK_SAMPLE_BITS")) : 18;
-  const uint64_t stride = g.n > (1ull << sbits) ? g.n >> sbits : 1;
+  return n > (1ull << sbits) ? n >> sbits : 1;
+}
+
+static int coarse_bits(uint64_t n) {
+  // 16 coarse bits (sign, exponent, 4 mantissa bits: 1/16-octave cells) keep
+  // the per-cell tables of a 16-table batch at 8 MB: the random lookups of
+  // fine_hist / codes stay in L2 next to the key stream
+  const int cb = (int)std::ceil(std::log2((double)n / 16.0 + 1.0));
+  int c = std::min(16, std::max(10, cb));
+  if (const char* e = getenv("GEEK_COARSE_BITS")) c = std::min(24, std::max(8, atoi(e)));
+  return c;
+}
+
+static uint32_t fine_target() {
+  uint32_t f = kFineTargetDefault;
+  if (const char* ft = getenv("GEEK_FINE_TARGET")) f = (uint32_t)std::max(1, atoi(ft));
+  return f;
+}
+
+// hist_in / fcnt_in (may be null): this batch's coarse sample histogram
+// [tb][nc] and exact fine-bin counts, computed elsewhere (the projection
+// counts fine bins as it writes keys); *nfb_out = fine bins of the batch
+static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, uint64_t* stats_acc,
+                            const uint32_t* hist_in, const uint32_t* fcnt_in, uint64_t* nfb_out, cudaStream_t s) {
+  const uint64_t ncell = (uint64_t)g.tb * g.nc;
+  const uint64_t stride = sample_stride(g.n);
   Scratch hist, nfine, fbase;
   GEEK_TRY(hist.alloc(ncell * 4, s));
   GEEK_TRY(nfine.alloc(ncell * 4, s));
   GEEK_TRY(fbase.alloc(ncell * 4, s));
-  GEEK_CHECK_CUDA(cudaMemsetAsync(hist.ptr, 0, ncell * 4, s));
-  dim3 gs(grid_for((g.n + stride - 1) / stride, 256, 148 * 8), g.tb);
-  coarse_hist_kernel<<<gs, 256, 0, s>>>(keys, g, stride, hist.as<uint32_t>());
-  GEEK_CHECK_LAUNCH();
+  if (hist_in) {
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(hist.ptr, hist_in, ncell * 4, cudaMemcpyDeviceToDevice, s));
+  } else {
+    GEEK_CHECK_CUDA(cudaMemsetAsync(hist.ptr, 0, ncell * 4, s));
+    dim3 gs(grid_for((g.n + stride - 1) / stride, 256, 148 * 8), g.tb);
+    coarse_hist_kernel<<<gs, 256, 0, s>>>(keys, g, stride, hist.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  }
   fine_layout_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(hist.as<uint32_t>(), ncell, stride, g.fine_target,
                                                           nfine.as<uint32_t>());
   GEEK_CHECK_LAUNCH();
@@ -306,12 +334,16 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   GEEK_TRY(stats.alloc(32, s));
   GEEK_CHECK_CUDA(cudaStreamSynchronize(s));  // tbf is host memory
   GEEK_CHECK_CUDA(cudaMemcpyAsync(tbfirst.ptr, tbf.data(), g.tb * 4, cudaMemcpyHostToDevice, s));
-  GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(sfill.ptr, 0, nfb * 4, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(stats.ptr, 0, 32, s));
-  dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
-  fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), fcnt.as<uint32_t>());
-  GEEK_CHECK_LAUNCH();
+  if (fcnt_in) {
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(fcnt.ptr, fcnt_in, nfb * 4, cudaMemcpyDeviceToDevice, s));
+  } else {
+    GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
+    dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
+    fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), fcnt.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  }
   GEEK_TRY(exclusive_scan_u32(fcnt.as<uint32_t>(), fstart.as<uint32_t>(), nfb, s));
   straddle_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
                                                       tbfirst.as<uint32_t>(), (uint32_t)nfb,
@@ -359,6 +391,7 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
     GEEK_CHECK_LAUNCH();
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
   }
+  if (nfb_out) *nfb_out = nfb;
   stats_acc[0] += nfb;
   stats_acc[1] += nstage;
   stats_acc[2] = std::max<uint64_t>(stats_acc[2], st[1]);
@@ -367,7 +400,8 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
 }
 
 static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
-                           uint64_t code_stride, uint64_t col, uint64_t* stats_host, cudaStream_t s) {
+                           uint64_t code_stride, uint64_t col, uint64_t* stats_host, cudaStream_t s,
+                           const uint32_t* hist_in = nullptr, const uint32_t* fcnt_in = nullptr) {
   GEEK_REQUIRE(t >= 1 && t <= n, "cannot split %llu objects into %llu buckets",
                (unsigned long long)n, (unsigned long long)t);
   GEEK_REQUIRE(n < 0xFFFFFFFFull, "n must be < 2^32");
@@ -375,15 +409,9 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   g.n = n;
   g.t = t;
   g.m = static_cast<int>(code_stride);
-  int cb = (int)std::ceil(std::log2((double)n / 16.0 + 1.0));
-  // 16 coarse bits (sign, exponent, 4 mantissa bits: 1/16-octave cells) keep
-  // the per-cell tables of a 16-table batch at 8 MB: the random lookups of
-  // fine_hist / codes stay in L2 next to the key stream
-  g.cb = std::min(16, std::max(10, cb));
-  if (const char* e = getenv("GEEK_COARSE_BITS")) g.cb = std::min(24, std::max(8, atoi(e)));
+  g.cb = coarse_bits(n);
   g.nc = 1u << g.cb;
-  g.fine_target = kFineTargetDefault;
-  if (const char* ft = getenv("GEEK_FINE_TARGET")) g.fine_target = (uint32_t)std::max(1, atoi(ft));
+  g.fine_target = fine_target();
   const double per_table = 4.0 * ((double)n / g.fine_target + 2.0 * g.nc) * 5.0;
   // batches of whole tables: codes rows are then written in tb-word runs
   // (8 tables = one 32-byte sector), counters stay u32 (tb * n < 2^32)
@@ -395,15 +423,33 @@ static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, 
   tb = std::min(tb, tb_cap);
   if (tb >= 8 && tb < m) tb -= tb % 8;
   uint64_t acc[4] = {0, 0, 0, 0};
+  uint64_t foff = 0;  // fine counts of the batches so far (precounted path)
   for (int j0 = 0; j0 < m; j0 += tb) {
     g.j0 = j0;
     g.c0 = static_cast<int>(col) + j0;
     g.tb = std::min(tb, m - j0);
-    GEEK_TRY(rank_split_batch(keys, g, codes, acc, s));
+    uint64_t nfb = 0;
+    GEEK_TRY(rank_split_batch(keys, g, codes, acc, hist_in ? hist_in + (uint64_t)j0 * g.nc : nullptr,
+                              fcnt_in ? fcnt_in + foff : nullptr, &nfb, s));
+    foff += nfb;
   }
   if (stats_host)
     for (int i = 0; i < 4; ++i) stats_host[i] = acc[i];
   return GEEK_OK;
+}
+
+// hist[t][cell] += counts of the sample keys [m][ns] (every key counted)
+__global__ void sample_hist_kernel(const uint64_t* __restrict__ keys, uint64_t ns, int cb, uint32_t nc,
+                                   uint32_t* hist) {
+  const int t = blockIdx.y;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[(uint64_t)t * nc + coarse_of(keys[(uint64_t)t * ns + i], cb)], 1u);
+}
+
+__global__ void table_offsets_kernel(const uint32_t* fbase, int m, uint32_t nc, uint64_t nfb, uint32_t* toff) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) toff[t] = fbase[(uint64_t)t * nc];
+  if (t == m) toff[m] = (uint32_t)nfb;
 }
 
 }  // namespace geek
@@ -422,6 +468,55 @@ int geek_rank_split_strided(const uint64_t* keys, uint64_t n, uint64_t t, uint32
                             uint64_t stride, uint64_t col, void* stream) {
   GEEK_REQUIRE(col < stride, "column outside stride");
   return rank_split_impl(keys, n, 1, t, codes, stride, col, nullptr, as_stream(stream));
+}
+
+
+int geek_split_plan(uint64_t n, int* cb_out, uint64_t* stride_out) {
+  GEEK_REQUIRE(n >= 1, "empty split");
+  if (cb_out) *cb_out = coarse_bits(n);
+  if (stride_out) *stride_out = sample_stride(n);
+  return GEEK_OK;
+}
+
+int geek_coarse_hist(const uint64_t* keys, uint64_t ns, int m, int cb, uint32_t* hist, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(m >= 1 && cb >= 1 && cb <= 24, "bad coarse histogram shape");
+  if (ns == 0) return GEEK_OK;
+  dim3 gs(grid_for(ns, 256, 148 * 8), m);
+  sample_hist_kernel<<<gs, 256, 0, s>>>(keys, ns, cb, 1u << cb, hist);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_fine_layout(const uint32_t* hist, int m, uint64_t n, uint32_t* cinfo, uint32_t* toff, uint64_t* nfb_host,
+                     void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const int cb = coarse_bits(n);
+  const uint64_t nc = 1ull << cb, ncell = (uint64_t)m * nc;
+  Scratch nfine, fbase;
+  GEEK_TRY(nfine.alloc(ncell * 4, s));
+  GEEK_TRY(fbase.alloc(ncell * 4, s));
+  fine_layout_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(hist, ncell, sample_stride(n), fine_target(),
+                                                          nfine.as<uint32_t>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nfb = 0;
+  GEEK_TRY(exclusive_scan_u32(nfine.as<uint32_t>(), fbase.as<uint32_t>(), ncell, s, &nfb));
+  GEEK_REQUIRE(nfb < 0x7FFFFFF0ull, "too many fine bins");
+  pack_cinfo_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(nfine.as<uint32_t>(), fbase.as<uint32_t>(), ncell,
+                                                         reinterpret_cast<uint2*>(cinfo));
+  GEEK_CHECK_LAUNCH();
+  table_offsets_kernel<<<1, m + 1 > 1024 ? 1024 : m + 1, 0, s>>>(fbase.as<uint32_t>(), m, (uint32_t)nc, nfb, toff);
+  GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (nfb_host) *nfb_host = nfb;
+  return GEEK_OK;
+}
+
+int geek_rank_split_counted(const uint64_t* keys, uint64_t n, int m, uint64_t t, const uint32_t* hist,
+                            const uint32_t* fcnt, uint32_t* codes, uint64_t* stats_host, void* stream) {
+  GEEK_REQUIRE(m >= 1 && m <= 1023, "need 1..1023 tables");
+  GEEK_REQUIRE(hist && fcnt, "precounted split needs the sample histogram and the fine counts");
+  return rank_split_impl(keys, n, m, t, codes, (uint64_t)m, 0, stats_host, as_stream(stream), hist, fcnt);
 }
 
 }  // extern "C"

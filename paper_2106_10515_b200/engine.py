@@ -191,6 +191,7 @@ class _Timer:
 
 _SYMM = {}
 _ROUTED_OFF = [bool(__import__('os').environ.get('GEEK_NO_ROUTED'))]
+_FUSED_COUNTS = bool(__import__('os').environ.get('GEEK_FUSED_COUNTS'))
 
 
 def _symm_keys(comm: _Comm, rows: int, cols: int, device):
@@ -231,11 +232,80 @@ def project_routed(X_local: torch.Tensor, A: np.ndarray, n: int, row_lo: int, co
     Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
     handle.barrier()  # every owner is done with the previous job's keys
     _lib.call("geek_project_keys_routed", _lib.ptr(X_local), _lib.dtype_code(X_local), n_local, d, _lib.ptr(Ad),
-              m, _lib.hptr(ptrs), G, n, row_lo, _lib.ptr(exprange), _lib.stream())
+              m, _lib.hptr(ptrs), G, n, row_lo, _lib.ptr(exprange), None, 0, None, _lib.stream())
     handle.barrier()  # all keys of this rank's tables have landed
     comm.count("BucketShard", n_local * m * 8 * (G - 1) // G)
     own = len([j for j in range(m) if j % G == comm.rank])
     return buf[:own]
+
+
+def project_counted(X_local: torch.Tensor, A: np.ndarray, n: int, row_lo: int, comm: _Comm,
+                    exprange: torch.Tensor, own):
+    """Projection with the rank split's fine-bin histogram fused in.  The
+    coarse cell histogram comes from the split's own sample rows (0, stride,
+    2*stride, ... of the job: each rank projects the sample rows it holds,
+    the histograms are summed), so every rank derives the same fine-bin
+    layout (geek_fine_layout); the projection then counts every key into its
+    fine bin as it stores it (G > 1: into the owner's symmetric buffer), the
+    counts are summed over ranks, and the owners split their tables with
+    geek_rank_split_counted -- no second pass over the keys for the histogram.
+    Returns (keys_own [m_own, n], (hist_own, fcnt_own))."""
+    m, G = A.shape[0], comm.G
+    n_local, d = X_local.shape
+    dev = X_local.device
+    cb, stride = np.zeros(1, dtype=np.int32), np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_split_plan", n, _lib.hptr(cb), _lib.hptr(stride))
+    cb, stride = int(cb[0]), int(stride[0])
+    nc = 1 << cb
+    first = -(-row_lo // stride) * stride
+    idx = torch.arange(first, row_lo + n_local, stride, device=dev) - row_lo
+    hist = torch.zeros(m * nc, dtype=torch.int32, device=dev)
+    if idx.numel():
+        ks = project_keys(X_local.index_select(0, idx).contiguous(), A)
+        _lib.call("geek_coarse_hist", _lib.ptr(ks), ks.shape[1], m, cb, _lib.ptr(hist), _lib.stream())
+        del ks
+    comm.all_reduce(hist, dist.ReduceOp.SUM, "BucketShard")
+    cinfo = _lib.empty(m * nc * 2, torch.int32)
+    toff = _lib.empty(m + 1, torch.int32)
+    nfb = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_fine_layout", _lib.ptr(hist), m, n, _lib.ptr(cinfo), _lib.ptr(toff), _lib.hptr(nfb),
+              _lib.stream())
+    fcnt = torch.zeros(max(1, int(nfb[0])), dtype=torch.int32, device=dev)
+    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    if G > 1:
+        buf, handle = _symm_keys(comm, -(-m // G), n, dev)
+        ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)
+        handle.barrier()  # every owner is done with the previous job's keys
+        _lib.call("geek_project_keys_routed", _lib.ptr(X_local), 0, n_local, d, _lib.ptr(Ad), m, _lib.hptr(ptrs),
+                  G, n, row_lo, _lib.ptr(exprange), _lib.ptr(cinfo), cb, _lib.ptr(fcnt), _lib.stream())
+        handle.barrier()  # all keys of this rank's tables have landed
+        comm.count("BucketShard", n_local * m * 8 * (G - 1) // G)
+        keys_own = buf[:len(own)]
+        comm.all_reduce(fcnt, dist.ReduceOp.SUM, "BucketShard")
+    else:
+        keys = _lib.empty(max(1, m * n), torch.int64)
+        ptrs = np.array([keys.data_ptr()], dtype=np.uint64)
+        _lib.call("geek_project_keys_routed", _lib.ptr(X_local), 0, n_local, d, _lib.ptr(Ad), m, _lib.hptr(ptrs),
+                  1, n, 0, _lib.ptr(exprange), _lib.ptr(cinfo), cb, _lib.ptr(fcnt), _lib.stream())
+        keys_own = keys[: m * n].view(m, n)
+    if len(own) == m:
+        return keys_own, (hist, fcnt)
+    toff_h = toff.cpu().numpy().astype(np.int64)
+    hist_own = hist.view(m, nc)[torch.tensor(own, dtype=torch.int64, device=dev)].contiguous()
+    fcnt_own = torch.cat([fcnt[toff_h[j]:toff_h[j + 1]] for j in own]) if own else fcnt[:0]
+    return keys_own, (hist_own, fcnt_own.contiguous())
+
+
+def rank_split_counted(keys: torch.Tensor, t: int, hist: torch.Tensor, fcnt: torch.Tensor, stats=None):
+    m, n = keys.shape
+    codes = _lib.empty(max(1, n * m), _lib.U32)
+    st = np.zeros(4, dtype=np.uint64)
+    _lib.call("geek_rank_split_counted", _lib.ptr(keys), n, m, t, _lib.ptr(hist), _lib.ptr(fcnt), _lib.ptr(codes),
+              _lib.hptr(st), _lib.stream())
+    if stats is not None:
+        stats.update(fine_bins=int(st[0]), straddling=int(st[1]), max_straddle_bin=int(st[2]),
+                     sorted_fallback=int(st[3]))
+    return codes[: n * m].view(n, m)
 
 
 def route_tables(keys: torch.Tensor, n: int, comm: _Comm) -> torch.Tensor:
@@ -374,15 +444,20 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     tm = _Timer()
     A = p.direction_matrix(d)
     own = [j for j in range(m) if j % G == rank]
-    keys_own = None
+    keys_own, counted = None, None
     with tm.stage("transform"):
         exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=X_local.device)
-        if comm.on and _routable(X_local, m, G) and not _ROUTED_OFF[0]:
+        if _routable(X_local, m, G) and not _ROUTED_OFF[0] and (comm.on or _FUSED_COUNTS):
             try:
-                keys_own = project_routed(X_local, A, n, row_lo, comm, exprange)
+                if _FUSED_COUNTS:  # measured slower on B200 (the counts stall the DMMA warps); kept opt-in
+                    keys_own, counted = project_counted(X_local, A, n, row_lo, comm, exprange, own)
+                else:
+                    keys_own = project_routed(X_local, A, n, row_lo, comm, exprange)
             except Exception as exc:  # no peer mappings here: the all-to-all path below
                 _ROUTED_OFF[0] = True
-                warnings.append(f"routed projection unavailable ({exc}); using all_to_all")
+                keys_own, counted = None, None
+                exprange.copy_(torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32))
+                warnings.append(f"fused projection unavailable ({exc}); using all_to_all")
         if keys_own is None:
             keys = project_keys(X_local, A, exprange)  # [m, n_local]; exponent window fused
     with tm.stage("sync_buckets"):
@@ -390,8 +465,13 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
             keys_own = route_tables(keys, n, comm)
             del keys
         stats = {}
-        codes = rank_split_codes(keys_own.contiguous(), t, stats) if own else None
-        del keys_own
+        if not own:
+            codes = None
+        elif counted is not None:
+            codes = rank_split_counted(keys_own, t, counted[0], counted[1], stats)
+        else:
+            codes = rank_split_codes(keys_own.contiguous(), t, stats)
+        del keys_own, counted
         info["rank_split"] = stats
     with tm.stage("seeding"):
         if own:

@@ -413,7 +413,7 @@ def test_routed_projection_layout(owners):
     er = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device="cuda")
     Xs = _lib.to_dev(X[lo:hi])
     _lib.call("geek_project_keys_routed", _lib.ptr(Xs), 0, hi - lo, d, _lib.ptr(_lib.to_dev(A)), m, _lib.hptr(ptrs),
-              owners, ntot, lo, _lib.ptr(er), _lib.stream())
+              owners, ntot, lo, _lib.ptr(er), None, 0, None, _lib.stream())
     torch.cuda.synchronize()
     for j in range(m):
         got = bufs[j % owners][j // owners].cpu().numpy()
@@ -427,3 +427,26 @@ def test_routed_projection_layout(owners):
             O_hi.append(e - 126 if e else -148)
     want = np.array([min(O_lo), max(O_hi)], dtype=np.int32)
     assert np.array_equal(er.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,t", [(50_000, 997), (120_000, 3), (7_000, 7_000)])
+def test_counted_split_equals_split(n, t):
+    """Fine-bin counts fused into the projection (geek_project_keys_routed with
+    a layout from geek_fine_layout) + geek_rank_split_counted give the same
+    bucket codes as the two-pass geek_rank_split on the same keys."""
+    from paper_2106_10515_b200 import _lib
+    from paper_2106_10515_b200.engine import _Comm, project_counted
+    from paper_2106_10515_b200.transform import rank_split_codes
+    rng = np.random.default_rng(n)
+    d, m = 64, 9
+    X = _lib.to_dev(rng.standard_normal((n, d)).astype(np.float32))
+    X[: n // 10] = X[0]  # a block of identical points: ties broken by id
+    A = rng.standard_normal((m, d))
+    er = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device="cuda")
+    keys, (hist, fcnt) = project_counted(X, A, n, 0, _Comm(), er, list(range(m)))
+    st = {}
+    from paper_2106_10515_b200.engine import rank_split_counted
+    got = rank_split_counted(keys, t, hist, fcnt, st).cpu().numpy()
+    want = rank_split_codes(keys.contiguous(), t).cpu().numpy()
+    assert np.array_equal(got, want)
+    assert int(fcnt.sum().item()) == n * m
