@@ -226,14 +226,17 @@ def main():
     if not args.no_e2e:
         Xh = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
         Xh.copy_(X)
-        Xd = X  # the device buffer the inputs are copied into every step
+        del X, out
+        torch.cuda.empty_cache()
         lab_h = torch.empty(hi - lo, dtype=torch.int64, pin_memory=True)
+        step(Xh)  # warm the engine's device row buffer
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            Xd.copy_(Xh, non_blocking=True)  # host -> device, pinned
-            o = step(Xd)
+            # the public API on pinned host rows: the engine copies them to the
+            # GPU in chunks (each projected as it lands), the labels come back
+            o = step(Xh)
             lab_h.copy_(o.labels_device, non_blocking=True)  # labels device -> host, pinned
         f1.record()
         barrier()

@@ -308,6 +308,64 @@ def rank_split_counted(keys: torch.Tensor, t: int, hist: torch.Tensor, fcnt: tor
     return codes[: n * m].view(n, m)
 
 
+_XBUF = {}
+_COPY_STREAM = []
+
+
+def _stream_host_rows(X_host: torch.Tensor, A: np.ndarray, n: int, row_lo: int, comm: _Comm,
+                      exprange: torch.Tensor, own, chunks: int = 8):
+    """Host rows (pinned for overlap) -> this GPU, projected chunk by chunk as
+    they land: the host-to-device copy of chunk c+1 runs on a copy stream
+    while chunk c is projected (keys stored locally, or straight into the
+    owners' symmetric buffers when G > 1).  Returns (X_device, keys_own or
+    None when the shape takes the unfused path)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m, G = A.shape[0], comm.G
+    n_local, d = X_host.shape
+    key = (tuple(X_host.shape), X_host.dtype, dev.index)
+    X_dev = _XBUF.get(key)
+    if X_dev is None:
+        _XBUF.clear()
+        X_dev = torch.empty(X_host.shape, dtype=X_host.dtype, device=dev)
+        _XBUF[key] = X_dev
+    fused = (X_host.dtype == torch.float32 and d % 4 == 0 and 4 <= d <= 128 and 1 <= m <= 48 and G <= 8
+             and not _ROUTED_OFF[0] and n_local > 0)
+    main = torch.cuda.current_stream()
+    if not fused:
+        X_dev.copy_(X_host, non_blocking=True)
+        return X_dev, None
+    if not _COPY_STREAM:
+        _COPY_STREAM.append(torch.cuda.Stream())
+    cs = _COPY_STREAM[0]
+    cs.wait_stream(main)  # the previous job's kernels are done with X_dev
+    step = -(-(-(-n_local // chunks)) // 128) * 128
+    spans = [(a, min(n_local, a + step)) for a in range(0, n_local, step)]
+    events = []
+    with torch.cuda.stream(cs):
+        for a, b in spans:
+            X_dev[a:b].copy_(X_host[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    if G > 1:
+        buf, handle = _symm_keys(comm, -(-m // G), n, dev)
+        ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)
+        handle.barrier()  # every owner is done with the previous job's keys
+    else:
+        keys = _lib.empty(max(1, m * n), torch.int64)
+        ptrs = np.array([keys.data_ptr()], dtype=np.uint64)
+    for (a, b), ev in zip(spans, events):
+        main.wait_event(ev)
+        _lib.call("geek_project_keys_routed", _lib.ptr(X_dev[a:b]), 0, b - a, d, _lib.ptr(Ad), m, _lib.hptr(ptrs),
+                  G, n, row_lo + a, _lib.ptr(exprange), None, 0, None, _lib.stream())
+    if G > 1:
+        handle.barrier()  # all keys of this rank's tables have landed
+        comm.count("BucketShard", n_local * m * 8 * (G - 1) // G)
+        return X_dev, buf[:len(own)]
+    return X_dev, keys[: m * n].view(m, n)
+
+
 def route_tables(keys: torch.Tensor, n: int, comm: _Comm) -> torch.Tensor:
     """Bucket synchronisation (engine.py:199-238): every rank holds keys
     [m, n_local] of its contiguous shard; table j goes to rank j % G, which
@@ -446,8 +504,11 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     own = [j for j in range(m) if j % G == rank]
     keys_own, counted = None, None
     with tm.stage("transform"):
-        exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=X_local.device)
-        if _routable(X_local, m, G) and not _ROUTED_OFF[0] and (comm.on or _FUSED_COUNTS):
+        exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32,
+                                device=torch.device("cuda", torch.cuda.current_device()))
+        if not X_local.is_cuda:  # host rows: copied in chunks, each projected as it lands
+            X_local, keys_own = _stream_host_rows(X_local, A, n, row_lo, comm, exprange, own)
+        if keys_own is None and _routable(X_local, m, G) and not _ROUTED_OFF[0] and (comm.on or _FUSED_COUNTS):
             try:
                 if _FUSED_COUNTS:  # measured slower on B200 (the counts stall the DMMA warps); kept opt-in
                     keys_own, counted = project_counted(X_local, A, n, row_lo, comm, exprange, own)
@@ -605,8 +666,9 @@ def run_pipeline(data, config: PipelineConfig) -> PipelineResult:
 
 
 def run_pipeline_shard(X_local: torch.Tensor, n: int, config: PipelineConfig) -> PipelineResult:
-    """Dense pipeline where each rank already holds its contiguous shard
-    (rows split_data(n, G)[rank]) on its own GPU."""
+    """Dense pipeline where each rank holds its contiguous shard (rows
+    split_data(n, G)[rank]), on its GPU or in (pinned) host memory -- host
+    rows are streamed to the GPU in chunks that are projected as they land."""
     comm = _Comm()
     lo, hi = split_data(n, comm.G)[comm.rank]
     if X_local.shape[0] != hi - lo:

@@ -450,3 +450,19 @@ def test_counted_split_equals_split(n, t):
     want = rank_split_codes(keys.contiguous(), t).cpu().numpy()
     assert np.array_equal(got, want)
     assert int(fcnt.sum().item()) == n * m
+
+
+def test_host_rows_streamed_equal_device_rows():
+    """run_pipeline_shard on pinned host rows (chunked H2D, each chunk projected
+    as it lands) gives the same result as on device rows."""
+    m = meta()["pipelines"]["cfg1"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    X = X.astype(np.float32)
+    cfg = dense_config(m, 1)
+    dev = G.run_pipeline_shard(torch.from_numpy(X).cuda(), n, cfg)
+    host = G.run_pipeline_shard(torch.from_numpy(X).pin_memory(), n, cfg)
+    assert keys(dev.seed_groups) == keys(host.seed_groups)
+    assert np.array_equal(dev.clustering.assignment, host.clustering.assignment)
+    assert np.array_equal(dev.clustering.radii, host.clustering.radii)
+    assert dev.clustering.objective == host.clustering.objective
