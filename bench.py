@@ -194,7 +194,13 @@ def main():
     e1.record()
     barrier()
     _lib.set_call_timer(None)
-    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    my_ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(my_ms * args.steps) / args.steps
+    rank_ms = [my_ms]
+    if world > 1:
+        allt = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(allt, torch.tensor([my_ms], dtype=torch.float64, device="cuda"))
+        rank_ms = [round(float(x.item()), 3) for x in allt]
     clk = clocks.stop()
     calls = timer.ms_by_name()
     info = dict(out.info)
@@ -306,7 +312,7 @@ def main():
                                 l2="inputs 51 GB >> 126 MB L2; no flush needed"),
                     e2e=e2e, gpu_launches=(launches * args.steps if launches is not None else None),
                     clocks=clk, roofline=roof, cpu_baseline=cpu,
-                    stages_s=stage, k_star=k_star, seed_groups=ngroups,
+                    stages_s=stage, rank_ms_per_step=rank_ms, k_star=k_star, seed_groups=ngroups,
                     calls_ms={k: round(v[0] / v[1], 3) for k, v in sorted(calls.items(), key=lambda kv: -kv[1][0])},
                     info=info)
         print(json.dumps(line), flush=True)

@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(128) project_dmma_kernel(const T* __restrict__
 constexpr int kPsLdp = 36;     // floats per point row of a stage: fragment loads are conflict-free
 constexpr int kPsStages = 3;
 constexpr int kPsStageFloats = 128 * kPsLdp;
+constexpr int kPsKeyLd = 34;   // u64 per table row of the per-warp key tile (16-byte aligned rows)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
@@ -297,10 +298,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // the bucket synchronisation of engine.py:199-238 without a separate
 // all-to-all.
 constexpr int kMaxKeyDst = 8;
+constexpr int kMaxKeyTables = 48;
 struct KeyDst {
   uint64_t* ptr[kMaxKeyDst];
   int G;
   uint64_t ntot, row_lo;
+  uint64_t* tptr[kMaxKeyTables];  // table t's row-0 address for this shard (host-computed)
+  int vec16;                      // every tptr is 16-byte aligned: 16-byte stores
   // optional fused fine-bin histogram of the rank split (fine_hist_kernel's
   // count, done here while the key is in a register): cinfo [m][2^cb] of
   // (fine bins, first global fine bin) per coarse cell, counters fcnt
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
   extern __shared__ __align__(16) uint8_t smem[];
   double* sA = reinterpret_cast<double*>(smem);                      // [d][LDA]
   float* sX = reinterpret_cast<float*>(smem + (size_t)d * LDA * 8);  // [stages][128][kPsLdp]
+  uint64_t* sK = reinterpret_cast<uint64_t*>(sX + kPsStages * kPsStageFloats);  // [4 warps][8][kPsKeyLd]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < d * NT * 8; e += 128) {
     const int k = e / (NT * 8), t = e - k * (NT * 8);
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int t = j * 8 + kr * 2 + h;
-      kdst[j][h] = t < m ? dst.ptr[t % dst.G] + (uint64_t)(t / dst.G) * dst.ntot + dst.row_lo : nullptr;
+      kdst[j][h] = t < m ? dst.tptr[t] : nullptr;
     }
   for (uint64_t q = 0; q < total; ++q) {
     cp_async_wait<kPsStages - 2>();
@@ -391,7 +396,33 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma884(acc[i][j], a[i], b[j]);
     }
-    if (kc == nck - 1) {
+    if (kc == nck - 1 && dst.vec16 && !dst.fcnt) {
+      // keys leave as 16-byte stores that make 256-byte runs per table: the
+      // warp's 32 points x 8 tables of one column group are transposed
+      // through a per-warp SMEM tile (NVLink-friendly when the owner is a peer)
+      const uint64_t tile = blockIdx.x + (q / nck) * gridDim.x;
+      uint64_t* sw = sK + warp * 8 * kPsKeyLd;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) sw[(kr * 2 + h) * kPsKeyLd + i * 8 + rr] = f64_key(acc[i][j][h]);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int tl = 2 * k + (lane >> 4), t = j * 8 + tl, qp = lane & 15;
+          const uint64_t pt0 = tile * 128 + warp * 32 + 2 * qp;
+          if (t < m && pt0 < n) {
+            const uint64_t k0 = sw[tl * kPsKeyLd + 2 * qp], k1 = sw[tl * kPsKeyLd + 2 * qp + 1];
+            uint64_t* dp = dst.tptr[t] + pt0;
+            if (pt0 + 1 < n) *reinterpret_cast<ulonglong2*>(dp) = make_ulonglong2(k0, k1);
+            else dp[0] = k0;
+          }
+        }
+      }
+    } else if (kc == nck - 1) {
       const uint64_t tile = blockIdx.x + (q / nck) * gridDim.x;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -433,10 +464,18 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
   }
 }
 
+static void fill_table_ptrs(KeyDst& dst, int m) {
+  dst.vec16 = 1;
+  for (int t = 0; t < kMaxKeyTables; ++t) {
+    dst.tptr[t] = t < m ? dst.ptr[t % dst.G] + (uint64_t)(t / dst.G) * dst.ntot + dst.row_lo : nullptr;
+    if (t < m && (reinterpret_cast<uintptr_t>(dst.tptr[t]) & 15)) dst.vec16 = 0;
+  }
+}
+
 template <int NT>
 static int launch_stream(const float* X, uint64_t n, int d, const double* A, int m, const KeyDst& dst, int* er,
                          unsigned* nf, cudaStream_t s) {
-  const size_t smem = (size_t)d * (NT * 8 + 4) * 8 + (size_t)kPsStages * kPsStageFloats * 4;
+  const size_t smem = (size_t)d * (NT * 8 + 4) * 8 + (size_t)kPsStages * kPsStageFloats * 4 + 4 * 8 * kPsKeyLd * 8;
   GEEK_CHECK_CUDA(cudaFuncSetAttribute(project_stream_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
   int sms = 148, dev = 0;
@@ -520,6 +559,7 @@ int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double*
     dst.cinfo = nullptr;
     dst.fcnt = nullptr;
     dst.cb = 0;
+    fill_table_ptrs(dst, m);
     return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
   }
   if (m <= 48 && !getenv("GEEK_NO_DMMA")) {  // DMMA path (up to 6 column fragments)
@@ -574,6 +614,7 @@ int geek_project_keys_routed(const void* X, int dtype, uint64_t n, int d, const 
   dst.cinfo = reinterpret_cast<const uint2*>(fine_cinfo);
   dst.fcnt = fine_cnt;
   dst.cb = cb;
+  fill_table_ptrs(dst, m);
   return launch_stream_any((const float*)X, n, d, A, m, dst, exprange, s);
 }
 
