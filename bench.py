@@ -270,9 +270,9 @@ def main():
         exec_flops = 2.0 * nl * kexec * (3 * P["d"] + 8)  # 3 TF32 products + the |c'|^2 slice
         roof = dict(kernel="tc_screen_kernel", bound="tensor", achieved=flops / sec / 1e12, unit="TFLOP/s",
                     peak=peaks.get("bf16_tflops", 1590.0),
-                    # dram read + write per launch from `ncu --set full` (profiles/r1_kernels.md: 51.24 GB
-                    # + 6.40 GB at n = 1e8), scaled to this rank's points; = the algorithmic X + top-list bytes
-                    traffic=57.64e9 * nl / 1e8,
+                    # dram read + write per launch from `ncu --set full` (profiles/r1_kernels.md: 51.23 GB
+                    # + 8.00 GB at n = 1e8), scaled to this rank's points; = the algorithmic X + top-list + |x'|^2 bytes
+                    traffic=59.23e9 * nl / 1e8,
                     peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); tcgen05 kind::tf32 runs at "
                                 "half of it: 1066 TFLOP/s measured by tools/tc_rate.cu",
                     executed_tf32_tflops=exec_flops / sec / 1e12,

@@ -198,7 +198,7 @@ void run(int sms, int ce = 0) {
   cudaFree(d);
 }
 
-int main() {
+int main_mix() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<128, true>(sms);
@@ -206,4 +206,128 @@ int main() {
   run_mix(sms, 2, 1, 5);
   run_mix(sms, 2, 1, 6);
   return 0;
+}
+
+// the screen's B-ring protocol without data: S stages, a producer warp that
+// waits "empty" (MMA commit) and arrives "full", an MMA warp that waits
+// "full", issues one chunk (12 MMAs) and commits "empty"
+template <int S, int H>
+__global__ void __launch_bounds__(128, 1) ring_kernel(int chunks) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t full[S], empty[S], done, accf[2], acce[2];
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < (64 * 1024 + 96 * 1024) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < S; ++q) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[q])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[q])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&done)));
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&accf[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 64;" ::"r"(su32(&acce[b])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  const int warp = threadIdx.x >> 5;
+  const int cts = chunks / 4;  // 4 chunks per accumulator tile
+  uint32_t pred;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+  if (warp == 1) {  // producer
+    for (int q = 0; q < chunks; ++q) {
+      const int s = q % S;
+      if (q >= S)
+        asm volatile("{\n.reg .pred p;\nWE: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WE;\n}\n" ::"r"(
+                         su32(&empty[s])), "r"(((q / S) - 1) & 1) : "memory");
+      if (pred) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+      __syncwarp();
+    }
+  } else if (warp >= 2) {  // epilogue stand-ins: wait for an accumulator, hand it back
+    if (H)
+      for (int g = 0; g < cts; ++g) {
+        const int b = g & 1;
+        asm volatile("{\n.reg .pred p;\nWA: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WA;\n}\n" ::"r"(
+                         su32(&accf[b])), "r"((g >> 1) & 1) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acce[b])) : "memory");
+      }
+  } else if (warp == 0) {  // MMA issuer
+    const uint32_t id = idesc(128, 128);
+    const uint32_t alo = su32(sm), bb = su32(sm + 64 * 1024);
+    for (int q = 0; q < chunks; ++q) {
+      const int s = q % S;
+      const int g = q / 4, b = g & 1;
+      if (H && (q & 3) == 0) {
+        asm volatile("{\n.reg .pred p;\nWB: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WB;\n}\n" ::"r"(
+                         su32(&acce[b])), "r"(((g >> 1) & 1) ^ 1) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      const uint32_t dacc = tmem + (H ? b * 128 : 0);
+      asm volatile("{\n.reg .pred p;\nWF: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WF;\n}\n" ::"r"(
+                       su32(&full[s])), "r"((q / S) & 1) : "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (pred) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t bhi = sdesc(bb + (s % 3) * 32768 + j * 4096), blo = sdesc(bb + (s % 3) * 32768 + 16384 + j * 4096);
+          const uint64_t a = sdesc(alo + ((q & 3) * 4 + j) * 4096);
+          const uint32_t at = tmem + 256 + ((q & 3) * 4 + j) * 8;
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dacc), "r"(at), "l"(bhi), "r"(id));
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dacc), "r"(at), "l"(blo), "r"(id));
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dacc), "l"(a), "l"(bhi), "r"(id));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&empty[s])) : "memory");
+        if (H && (q & 3) == 3)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&accf[b])) : "memory");
+      }
+      __syncwarp();
+    }
+    if (pred) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&done)) : "memory");
+    __syncwarp();
+    asm volatile("{\n.reg .pred p;\nWD: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WD;\n}\n" ::"r"(su32(&done)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int S, int H>
+void run_ring(int sms) {
+  const int chunks = 20000, smem = 160 * 1024 + 1024;
+  cudaFuncSetAttribute(ring_kernel<S, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  ring_kernel<S, H><<<sms, 128, smem>>>(100);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  ring_kernel<S, H><<<sms, 128, smem>>>(chunks);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * 128 * 128 * 8 * 12.0 * chunks * sms;
+  printf("ring stages=%d handshake=%d: %.1f TFLOP/s (%.2f ms) err=%s\n", S, H, flops / ms / 1e9, ms, cudaGetErrorString(err));
+}
+
+int main_ring() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run_ring<3, 0>(sms);
+  run_ring<3, 1>(sms);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'r') return main_ring();
+  return main_mix();
 }
