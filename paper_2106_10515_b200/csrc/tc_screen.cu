@@ -131,6 +131,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// the epilogue warps' waits: try_wait with a suspend-time hint, so a waiting
+// warp sleeps until the phase completes instead of re-polling the barrier
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x100000)
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -281,6 +295,7 @@ struct TcParams {
   float* top_s;       // [n][8]: top-4 of each accumulator column half
   int* top_i;         // [n][8]
   double* xpart;      // [n][2] (NPROD = 3, may be null): |x'|^2 over each half of the dims, for the classifier
+  int sleepwait;      // epilogue warps wait with a suspend-time hint
   int c2res;          // 1: the |c'|^2/2 slices of all center tiles (+ the ones slice) stay in SMEM
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
@@ -304,8 +319,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint64_t* full = bars;                    // [8] stage loaded (TMA tx)
   uint64_t* empty = bars + 8;               // [8] stage consumed (MMA commit)
   uint64_t* accf = bars + 16;               // [2] accumulator ready (MMA commit)
-  uint64_t* acce = bars + 18;               // [2] accumulator drained (256 epilogue threads)
-  uint64_t* afull = bars + 20;              // [kABuf][4] point-tile chunk written (256 threads)
+  uint64_t* acce = bars + 18;               // [2] accumulator drained (one arrival per epilogue warp)
+  uint64_t* afull = bars + 20;              // [kABuf][4] point-tile chunk written (one arrival per warp)
   uint64_t* aempty = bars + 28;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
   uint64_t* c2full = bars + 36;             // resident |c'|^2 slices loaded (TMA tx)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
@@ -319,10 +334,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], kTcEpiThreads);
+      mbar_init(&acce[b], kTcEpiWarps);  // one arrival per epilogue warp
     }
     for (int b = 0; b < Cfg::kABuf * 4; ++b) {
-      mbar_init(&afull[b], kTcEpiThreads);
+      mbar_init(&afull[b], kTcEpiWarps);
       mbar_init(&aempty[b], 1);
     }
     mbar_init(c2full, 1);
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     {  // ---------------- MMA issuer ----------------
       const uint32_t idesc_full = make_idesc(kTcM, kTcN), idesc_last = make_idesc(kTcM, P.nlast);
       uint64_t q_mma = 0;
-      long long w_full = 0, w_acce = 0, w_afull = 0, w_issue = 0;
+      long long w_full = 0, w_acce = 0, w_afull = 0, w_issue = 0, w_c2 = 0, w_accf = 0, w_done = 0;
       const long long t_start = clock64();
       auto timed_wait = [&](uint64_t* bar, uint32_t par, long long& acc) {
         if (P.dbg) {
@@ -452,6 +467,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
+          const long long c_c2 = P.dbg ? clock64() : 0;
           if (P.c2res) {  // |c'|^2 / 2, added last, from the resident slices
             if (t == 0 && ct == 0) {
               mbar_wait(c2full, 0);
@@ -469,8 +485,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
             stage_done(s);
           }
+          const long long c_af = P.dbg ? clock64() : 0;
+          if (P.dbg) w_c2 += c_af - c_c2;
           if (leader) tc_commit(&accf[buf]);
           __syncwarp();
+          if (P.dbg) w_accf += clock64() - c_af;
         }
       }
       if (P.dbg && leader) {
@@ -479,16 +498,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         P.dbg[blockIdx.x * 8 + 2] = (unsigned long long)w_afull;
         P.dbg[blockIdx.x * 8 + 3] = (unsigned long long)(clock64() - t_start);
         P.dbg[blockIdx.x * 8 + 4] = (unsigned long long)w_issue;
+        P.dbg[blockIdx.x * 8 + 5] = (unsigned long long)w_c2;
+        P.dbg[blockIdx.x * 8 + 6] = (unsigned long long)w_accf;
       }
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
+    const bool getenv_sleep = P.sleepwait != 0;
     Top4 cur;
     cur.init();
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
       const uint64_t g = (uint64_t)t * P.nct + ct;
       const int buf = (int)(g & 1);
       const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
-      mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
+      if (getenv_sleep) mbar_wait_sleep(&accf[buf], (uint32_t)((g >> 1) & 1));
+      else mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
       if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3)) {
@@ -517,7 +540,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         }
       }
       fence_before();
-      mbar_arrive(&acce[buf]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[buf]);  // the warp's TMEM reads are all done
     };
     auto finish = [&](uint32_t t, Top4& top) {
       epilogue(t, P.nct - 1, top);
@@ -593,7 +617,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         if (kc < nck) {
-          mbar_wait(&aempty[ab * 4 + kc], epar);  // the MMAs of the previous tile on this chunk are done
+          if (getenv_sleep) mbar_wait_sleep(&aempty[ab * 4 + kc], epar);  // the MMAs of the previous tile on this chunk are done
+          else mbar_wait(&aempty[ab * 4 + kc], epar);
           if (Cfg::kATmem) fence_after();
           float hi[16];
 #pragma unroll
@@ -643,7 +668,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             fence_before();
           }
           fence_proxy_async();
-          mbar_arrive(&afull[ab * 4 + kc]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[ab * 4 + kc]);  // the warp's A writes are all done
         }
       }
       if (Cfg::kATmem && P.xpart) {
@@ -788,6 +814,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)(nct + 1) * kTcSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
+  P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? 1 : 0;
   P.dbg = nullptr;
   Scratch dbg;
   if (getenv("GEEK_SCREEN_DBG")) {
@@ -800,18 +827,20 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
     unsigned long long h[148 * 8];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-    double f = 0, a = 0, af = 0, tot = 0, is = 0;
+    double f = 0, a = 0, af = 0, tot = 0, is = 0, c2 = 0, cf = 0;
     for (int b = 0; b < 148; ++b) {
       f += h[8 * b];
       a += h[8 * b + 1];
       af += h[8 * b + 2];
       tot += h[8 * b + 3];
       is += h[8 * b + 4];
+      c2 += h[8 * b + 5];
+      cf += h[8 * b + 6];
     }
     fprintf(stderr,
             "[screen dbg] MMA warp cycles: total %.3g, wait B %.1f%%, wait acc %.1f%%, wait A %.1f%%, issuing the "
-            "12 MMAs of a chunk %.1f%%\n",
-            tot / 148, 100 * f / tot, 100 * a / tot, 100 * af / tot, 100 * is / tot);
+            "12 MMAs of a chunk %.1f%%, |c'|^2 block %.1f%%, accumulator commit %.1f%%\n",
+            tot / 148, 100 * f / tot, 100 * a / tot, 100 * af / tot, 100 * is / tot, 100 * c2 / tot, 100 * cf / tot);
   }
   return st;
 }

@@ -1,6 +1,6 @@
 """Time the tensor-core assignment screen alone at the bench size under the
 GEEK_SCREEN_PROF knobs (0 normal, 1 no epilogue math, 2 no MMAs, 3 no A
-writes).  Usage: python tools/screen_probe.py [n] [k]."""
+writes).  Usage: python tools/screen_probe.py [n] [k] [d]."""
 import os
 import subprocess
 import sys
@@ -11,7 +11,7 @@ if os.environ.get("_PROBE_CHILD"):
     from paper_2106_10515_b200 import _lib as L
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 963
-    d = 128
+    d = int(sys.argv[3]) if len(sys.argv) > 3 else 128
     g = torch.Generator(device="cuda").manual_seed(0)
     C = torch.randn(k, d, device="cuda", dtype=torch.float64, generator=g) * 10
     X = torch.empty(n, d, device="cuda", dtype=torch.float32)
