@@ -131,7 +131,6 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
   const int tid = threadIdx.x;
   if (smem_words > 0)
     for (uint64_t w = tid; w < nwords; w += kEwThreads) sw[w] = gwords[w];
-  const uint32_t* words = smem_words > 0 ? sw : gwords;
   const unsigned lane = tid & 31;
   for (uint64_t base = blockIdx.x * (uint64_t)kEwThreads; base < n; base += (uint64_t)gridDim.x * kEwThreads) {
     const int rows = (int)(n - base < (uint64_t)kEwThreads ? n - base : (uint64_t)kEwThreads);
@@ -162,14 +161,16 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
       const uint32_t* row = srow + tid * ld;
       // 8 tables at a time: their bucket lists and first entries are
       // fetched together instead of as one dependent chain per table
+      const uint32_t t32 = (uint32_t)t;  // m * t < 2^32 (checked by the caller)
       for (int j0 = 0; j0 < m; j0 += 8) {
         uint2 pk[8], e0[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           pk[u] = make_uint2(0u, 0u);
           if (j0 + u < m) {
-            const uint64_t b = (uint64_t)(j0 + u) * t + row[j0 + u];
-            if ((words[b >> 5] >> (b & 31)) & 1u) pk[u] = __ldg(pack + b);
+            const uint32_t b = (uint32_t)(j0 + u) * t32 + row[j0 + u];
+            const uint32_t w = smem_words > 0 ? sw[b >> 5] : __ldg(gwords + (b >> 5));
+            if ((w >> (b & 31)) & 1u) pk[u] = __ldg(pack + b);
           }
         }
 #pragma unroll
@@ -400,6 +401,7 @@ int geek_emit_winners_codes(const uint32_t* codes, uint64_t n, int m, uint64_t t
   if (n) {
     GEEK_REQUIRE(m <= 256, "emit_winners: m = %d tables per row exceeds 256", m);
     const uint64_t nb = (uint64_t)m * t, nw = (nb + 31) / 32;
+    GEEK_REQUIRE(nb < 0xFFFFFFFFull, "emit_winners: %llu buckets exceed 32-bit indexing", (unsigned long long)nb);
     uint32_t nent = 0;
     GEEK_CHECK_CUDA(cudaMemcpyAsync(&nent, bb_off + nb, 4, cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
