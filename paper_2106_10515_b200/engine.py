@@ -33,8 +33,9 @@ from .hashing import DophReducer, derive_seed
 from .numeric import digit_count, exponent_range, mode_counts, partial_sums, round_means, sparse_counts
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
-from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, discretize_numeric,
-                        even_partition_sizes, project_keys, rank_split_codes, signature_bucket_codes)
+from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
+                        discretize_numeric, even_partition_sizes, project_keys, rank_split_codes,
+                        signature_bucket_codes)
 
 __all__ = ["EngineError", "WorkerConfig", "PipelineConfig", "PipelineResult", "split_data", "run_pipeline"]
 
@@ -229,7 +230,7 @@ def project_routed(X_local: torch.Tensor, A: np.ndarray, n: int, row_lo: int, co
     n_local, d = X_local.shape
     buf, handle = _symm_keys(comm, -(-m // G), n, X_local.device)
     ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)
-    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    Ad = directions_device(A)
     handle.barrier()  # every owner is done with the previous job's keys
     _lib.call("geek_project_keys_routed", _lib.ptr(X_local), _lib.dtype_code(X_local), n_local, d, _lib.ptr(Ad),
               m, _lib.hptr(ptrs), G, n, row_lo, _lib.ptr(exprange), None, 0, None, _lib.stream())
@@ -271,7 +272,7 @@ def project_counted(X_local: torch.Tensor, A: np.ndarray, n: int, row_lo: int, c
     _lib.call("geek_fine_layout", _lib.ptr(hist), m, n, _lib.ptr(cinfo), _lib.ptr(toff), _lib.hptr(nfb),
               _lib.stream())
     fcnt = torch.zeros(max(1, int(nfb[0])), dtype=torch.int32, device=dev)
-    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    Ad = directions_device(A)
     if G > 1:
         buf, handle = _symm_keys(comm, -(-m // G), n, dev)
         ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)
@@ -347,7 +348,7 @@ def _stream_host_rows(X_host: torch.Tensor, A: np.ndarray, n: int, row_lo: int, 
             ev = torch.cuda.Event()
             ev.record(cs)
             events.append(ev)
-    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    Ad = directions_device(A)
     if G > 1:
         buf, handle = _symm_keys(comm, -(-m // G), n, dev)
         ptrs = np.array([int(p) for p in handle.buffer_ptrs], dtype=np.uint64)

@@ -24,6 +24,9 @@ __all__ = ["HomoTransformParams", "MinhashTransformParams", "even_partition_size
            "discretize_numeric", "transform_hetero", "transform_sparse"]
 
 
+_DIRECTIONS = {}
+
+
 @dataclass(frozen=True)
 class HomoTransformParams:
     """m projection tables split into t even buckets (transform.py:35-60)."""
@@ -57,7 +60,12 @@ class HomoTransformParams:
             if self.directions.shape[1] != dim:
                 raise InvalidInput(f"dimension mismatch: directions have {self.directions.shape[1]}, data {dim}")
             return self.directions
-        return np.stack([self.projection(j, dim).direction for j in range(self.num_tables)])
+        key = (self.seed, self.num_tables, dim)
+        A = _DIRECTIONS.get(key)
+        if A is None:  # the reference's PCG64 draws, once per (seed, tables, dim)
+            A = np.stack([self.projection(j, dim).direction for j in range(self.num_tables)])
+            _DIRECTIONS[key] = A
+        return A
 
 
 @dataclass(frozen=True)
@@ -93,6 +101,23 @@ def even_partition_sizes(n: int, parts: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # dense
 
+_DIRS = {}
+
+
+def directions_device(A: np.ndarray) -> torch.Tensor:
+    """The float64 direction matrix on the current device, cached by content
+    (the same job's directions are re-used every call)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    key = (A.shape, hash(A.tobytes()), torch.cuda.current_device())
+    t = _DIRS.get(key)
+    if t is None:
+        if len(_DIRS) > 8:
+            _DIRS.clear()
+        t = _lib.to_dev(A)
+        _DIRS[key] = t
+    return t
+
+
 def project_keys(X: torch.Tensor, A: np.ndarray, exprange: torch.Tensor = None) -> torch.Tensor:
     """[m, n] order-preserving uint64 keys (int64 storage) of X @ A.T in float64.
     `exprange` (int32[2] on the device, preset to (2^30, -2^30)) receives the
@@ -100,7 +125,7 @@ def project_keys(X: torch.Tensor, A: np.ndarray, exprange: torch.Tensor = None) 
     n, d = X.shape
     m = A.shape[0]
     keys = _lib.empty(max(1, m * n), torch.int64)
-    Ad = _lib.to_dev(np.ascontiguousarray(A, dtype=np.float64))
+    Ad = directions_device(A)
     _lib.call("geek_project_keys", _lib.ptr(X), _lib.dtype_code(X), n, d, _lib.ptr(Ad), m, _lib.ptr(keys),
               _lib.ptr(exprange), _lib.stream())
     return keys[: m * n].view(m, n) if n else keys[:0].view(m, 0)
