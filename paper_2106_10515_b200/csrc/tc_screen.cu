@@ -18,11 +18,11 @@
 // Point tiles are double-buffered and handed over per 32-dim chunk.
 // Per CTA (persistent over 128-point tiles):
 //   A  = the point tile, K-major, in SMEM
-//   B  = center tiles of 128 centers, streamed in 32-dim chunks (+ the |c'|^2
+//   B  = center tiles of 192 centers, streamed in 16-dim chunks (+ the |c'|^2
 //        chunk: its B slice and the all-ones A slice) by 1-D bulk TMA
 //        (cp.async.bulk) into a ring of SMEM stages; CTA b walks the center
 //        tiles starting at tile b % nct so the L2 reads spread out
-//   D  = two 128x128 fp32 accumulators in TMEM (256 columns): the epilogue
+//   D  = two 128x192 fp32 accumulators in TMEM (384 columns): the epilogue
 //        of center tile j overlaps the MMAs of tile j+1
 // Warp-specialised: lane 0 of warp 9 streams B (bulk copies), lane 0 of
 // warp 8 issues the MMAs;
@@ -42,18 +42,19 @@
 namespace geek {
 
 constexpr int kTcM = 128;      // points per tile (TMEM lanes)
-constexpr int kTcN = 128;      // centers per tile
+constexpr int kTcN = 192;      // centers per tile (2 x 192 accumulator columns + 128 A columns = all of TMEM)
 constexpr int kTcKmax = 128;   // padded dimension (<= 128)
 constexpr int kTcAChunk = 32;  // dims per point-tile hand-off chunk
-constexpr int kTcChunk = 32;   // dims per B stage
-constexpr int kTcSliceBytes = kTcM * 8 * 4;                       // one K=8 tf32 slice of 128 rows: 4 KB
-constexpr int kTcHalfStage = (kTcChunk / 8) * kTcSliceBytes;      // 16 KB: one 32-dim chunk, one part
+constexpr int kTcChunk = 16;   // dims per B stage
+constexpr int kTcSliceBytes = kTcM * 8 * 4;                       // one K=8 tf32 slice of the 128 A rows: 4 KB
+constexpr int kTcBSliceBytes = kTcN * 8 * 4;                      // one K=8 tf32 slice of the B rows: 6 KB
+constexpr int kTcHalfStage = (kTcChunk / 8) * kTcBSliceBytes;     // one 16-dim B chunk, one part
 constexpr int kTcAPart = (kTcKmax / 8) * kTcSliceBytes;           // 64 KB: one part of a point tile
 
 template <int NPROD>
 struct TcCfg {
   static constexpr int kParts = NPROD == 3 ? 2 : 1;              // hi (+ lo)
-  // NPROD = 3 keeps the hi part of the point tile in TMEM (columns 256..383)
+  // NPROD = 3 keeps the hi part of the point tile in TMEM (columns 384..511)
   // and only the lo part in SMEM: the SMEM this frees deepens the B ring
   static constexpr bool kATmem = NPROD == 3;
   static constexpr int kABytes = kTcAPart;
@@ -62,15 +63,15 @@ struct TcCfg {
   // the tile switch short)
   static constexpr int kABuf = NPROD == 3 ? 1 : 2;
   static constexpr int kStageBytes = kParts * kTcHalfStage;
-  static constexpr int kStages = NPROD == 3 ? 3 : 4;
-  static constexpr uint32_t kTmemCols = kATmem ? 512 : 256;
-  static constexpr uint32_t kTmemA = 256;                        // TMEM A operand: buffer b at 256 + 128 b
+  static constexpr int kStages = 4;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kTmemA = 2 * kTcN;                   // TMEM A operand after the two accumulators
   static constexpr size_t kSmemFixed = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
 };
 
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
 // chunk (B slice with |c'|^2/2, then the all-ones A slice)
-constexpr int kTcC2Bytes = 2 * kTcSliceBytes;
+constexpr int kTcC2Bytes = kTcBSliceBytes + kTcSliceBytes;  // |c'|^2 B slice, then the all-ones A slice
 __host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts) {
   return (uint64_t)((d + kTcChunk - 1) / kTcChunk) * parts * kTcHalfStage + kTcC2Bytes;
 }
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint8_t* A = smem;                                           // kABuf x kABytes
   uint8_t* B = smem + Cfg::kABuf * Cfg::kABytes;               // kStages x kStageBytes
   uint8_t* C2 = B + Cfg::kStages * Cfg::kStageBytes;           // resident: ones slice, then one slice per tile
-  const uint32_t c2bytes = P.c2res ? (uint32_t)(P.nct + 1) * kTcSliceBytes : 0u;
+  const uint32_t c2bytes = P.c2res ? (uint32_t)(kTcSliceBytes + P.nct * kTcBSliceBytes) : 0u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(C2 + c2bytes);
   uint64_t* full = bars;                    // [8] stage loaded (TMA tx)
   uint64_t* empty = bars + 8;               // [8] stage consumed (MMA commit)
@@ -369,9 +370,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         if (leader) {
           mbar_expect_tx(c2full, c2bytes);
           const uint8_t* img = reinterpret_cast<const uint8_t*>(P.Bimg) + (uint64_t)nbk * Cfg::kStageBytes;
-          bulk_g2s(C2, img + kTcSliceBytes, kTcSliceBytes, c2full);  // the all-ones A slice
+          bulk_g2s(C2, img + kTcBSliceBytes, kTcSliceBytes, c2full);  // the all-ones A slice
           for (int ct = 0; ct < P.nct; ++ct)
-            bulk_g2s(C2 + (ct + 1) * kTcSliceBytes, img + (uint64_t)ct * ct_bytes, kTcSliceBytes, c2full);
+            bulk_g2s(C2 + kTcSliceBytes + ct * kTcBSliceBytes, img + (uint64_t)ct * ct_bytes, kTcBSliceBytes, c2full);
         }
         __syncwarp();
       }
@@ -435,8 +436,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           // the last center tile runs with N = its valid centers rounded up to 16
           const uint32_t idesc = (int)((ct + blockIdx.x) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
           for (int kc = 0; kc < nbk; ++kc) {
-            const int ac = kc;  // point-tile chunk
-            if (ct == 0) {  // first use of this chunk of the point tile
+            const int ac = kc * kTcChunk / kTcAChunk;  // point-tile chunk holding these dims
+            if (ct == 0 && (kc * kTcChunk) % kTcAChunk == 0) {  // first use of this chunk of the point tile
               timed_wait(&afull[ab * 4 + ac], apar, w_afull);
               fence_after();
             }
@@ -444,16 +445,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             // descriptors differ from the stage / tile bases by constant
             // address offsets (the 14-bit address field never carries)
             const uint32_t blo32 = b_lo32 + ((s * Cfg::kStageBytes) >> 4);
-            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * 4 * kTcSliceBytes) >> 4);
-            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * 32;
+            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * (kTcChunk / 8) * kTcSliceBytes) >> 4);
+            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * kTcChunk;
             const long long c_is = P.dbg ? clock64() : 0;
             if (leader && P.prof != 2) {
 #pragma unroll
               for (int j = 0; j < kTcChunk / 8; ++j) {
-                const uint64_t bhi = desc_of(blo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
+                const uint64_t bhi = desc_of(blo32 + ((j * kTcBSliceBytes) >> 4), d_hi32);
                 const uint32_t acc = (kc | j) ? 1u : 0u;
                 if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
-                  const uint64_t blo = desc_of(blo32 + ((kTcHalfStage + j * kTcSliceBytes) >> 4), d_hi32);
+                  const uint64_t blo = desc_of(blo32 + ((kTcHalfStage + j * kTcBSliceBytes) >> 4), d_hi32);
                   const uint64_t alo = desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
                   tc_mma_ta(dt, at + j * 8, bhi, idesc, acc);
                   tc_mma_ta(dt, at + j * 8, blo, idesc, 1u);
@@ -464,7 +465,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               }
             }
             if (P.dbg) w_issue += clock64() - c_is;
-            if (ct == P.nct - 1 && leader) tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
+            if (ct == P.nct - 1 && leader && (((kc + 1) * kTcChunk) % kTcAChunk == 0 || kc == nbk - 1))
+              tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
           const long long c_c2 = P.dbg ? clock64() : 0;
@@ -475,13 +477,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             }
             const uint32_t cta = (uint32_t)((ct + blockIdx.x) % P.nct);
             const uint64_t a1 = make_sdesc(smem_u32(C2), P.lbo, P.sbo);
-            const uint64_t b1 = make_sdesc(smem_u32(C2) + (cta + 1) * kTcSliceBytes, P.lbo, P.sbo);
+            const uint64_t b1 = make_sdesc(smem_u32(C2) + kTcSliceBytes + cta * kTcBSliceBytes, P.lbo, P.sbo);
             if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
             __syncwarp();
           } else {  // |c'|^2 / 2, added last, through the ring
             const uint32_t s = next_stage();
             const uint32_t sb = smem_u32(B + s * Cfg::kStageBytes);
-            const uint64_t a1 = make_sdesc(sb + kTcSliceBytes, P.lbo, P.sbo), b1 = make_sdesc(sb, P.lbo, P.sbo);
+            const uint64_t a1 = make_sdesc(sb + kTcBSliceBytes, P.lbo, P.sbo), b1 = make_sdesc(sb, P.lbo, P.sbo);
             if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
             stage_done(s);
           }
@@ -515,27 +517,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
       if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3)) {
-        float v[64];
-        tc_ld32_async(trow, v);       // both halves in flight, one wait
-        tc_ld32_async(trow + 32, v + 32);
-        tc_wait_ld();
-        tc_regs_ready(v);
-        tc_regs_ready(v + 32);
         const int cta = (int)((ct + blockIdx.x) % P.nct);
-        if (cta == P.nct - 1) {  // columns past the last tile's MMA width hold stale sums
+        const bool last = cta == P.nct - 1;  // columns past the last tile's MMA width hold stale sums
+#pragma unroll 1
+        for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
+          float v[32];
+          tc_ld32_async(trow + c0, v);
+          tc_wait_ld();
+          tc_regs_ready(v);
+          if (last) {
 #pragma unroll
-          for (int u = 0; u < 64; ++u)
-            if (ch * (kTcN / 2) + u >= P.nlast) v[u] = INFINITY;
-        }
+            for (int u = 0; u < 32; ++u)
+              if (ch * (kTcN / 2) + c0 + u >= P.nlast) v[u] = INFINITY;
+          }
+          float mn = v[0];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float mn = v[h * 32];
-#pragma unroll
-          for (int u = 1; u < 32; ++u) mn = fminf(mn, v[h * 32 + u]);
+          for (int u = 1; u < 32; ++u) mn = fminf(mn, v[u]);
           if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
-            const int cbase = cta * kTcN + ch * (kTcN / 2) + h * 32;
+            const int cbase = cta * kTcN + ch * (kTcN / 2) + c0;
 #pragma unroll
-            for (int u = 0; u < 32; ++u) top.push(v[h * 32 + u], cbase + u);
+            for (int u = 0; u < 32; ++u) top.push(v[u], cbase + u);
           }
         }
       }
@@ -732,7 +733,7 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
           n2 = fma((double)cv, (double)cv, n2);
         }
         const float hi = tf32_round(-cv);
-        const uint32_t off = (e >> 3) * kTcSliceBytes + core_off(r, e & 7, lbo, sbo);
+        const uint32_t off = (e >> 3) * kTcBSliceBytes + core_off(r, e & 7, lbo, sbo);
         *reinterpret_cast<float*>(img + off) = hi;
         if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(-cv - hi);
       }
@@ -749,7 +750,7 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
     }
     for (int e = 0; e < 8; ++e) {
       *reinterpret_cast<float*>(cs + core_off(r, e, lbo, sbo)) = p[e];
-      *reinterpret_cast<float*>(cs + kTcSliceBytes + core_off(r, e, lbo, sbo)) = 1.f;  // all-ones A slice
+      if (r < kTcM) *reinterpret_cast<float*>(cs + kTcBSliceBytes + core_off(r, e, lbo, sbo)) = 1.f;  // all-ones A slice
     }
     c2[c] = c < k ? (float)n2 : INFINITY;
     if (c < k) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(n2) * (1.0 + 1e-6)));
@@ -774,7 +775,7 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
 
 template <int NPROD>
 static int launch_screen(const TcParams& P, cudaStream_t s) {
-  const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)(P.nct + 1) * kTcSliceBytes : 0);
+  const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -800,7 +801,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.k = k;
   P.nct = nct;
   {
-    const uint64_t last = k - (uint64_t)(nct - 1) * kTcN;  // 1..128 valid centers
+    const uint64_t last = k - (uint64_t)(nct - 1) * kTcN;  // 1..kTcN valid centers
     P.nlast = (int)((last + 15) / 16 * 16);
     if (getenv("GEEK_SCREEN_FULLN")) P.nlast = kTcN;
   }
@@ -811,7 +812,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.xpart = nprod == 3 ? xpart : nullptr;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)(nct + 1) * kTcSliceBytes <= 227 * 1024
+  P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
   P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? 1 : 0;
