@@ -283,6 +283,20 @@ struct Top4 {
   }
 };
 
+// v[u] for a lane-dependent u without local memory: a 5-level select tree
+__device__ __forceinline__ float pick32(const float (&v)[32], int u) {
+  float w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) w[j] = (u & 1) ? v[2 * j + 1] : v[2 * j];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = (u & 2) ? w[2 * j + 1] : w[2 * j];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w[j] = (u & 4) ? w[2 * j + 1] : w[2 * j];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) w[j] = (u & 8) ? w[2 * j + 1] : w[2 * j];
+  return (u & 16) ? w[1] : w[0];
+}
+
 struct TcParams {
   const float* X;     // [n][d] float32
   uint64_t n;
@@ -298,7 +312,8 @@ struct TcParams {
   double* xpart;      // [n][2] (NPROD = 3, may be null): |x'|^2 over each half of the dims, for the classifier
   int sleepwait;      // epilogue warps wait with a suspend-time hint
   int c2res;          // 1: the |c'|^2/2 slices of all center tiles (+ the ones slice) stay in SMEM
-  int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes,
+  int pushcut;        // candidates per lane above which a round walks every column (GEEK_SCREEN_PUSHCUT)
+  int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes, 8 = no top-4 inserts,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
 };
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       else mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-      if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3)) {
+      if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3) || P.prof == 8) {
         const int cta = (int)((ct + blockIdx.x) % P.nct);
         const bool last = cta == P.nct - 1;  // columns past the last tile's MMA width hold stale sums
 #pragma unroll 1
@@ -533,10 +548,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           float mn = v[0];
 #pragma unroll
           for (int u = 1; u < 32; ++u) mn = fminf(mn, v[u]);
-          if (mn < top.s[3]) {  // most center tiles hold no candidate: one compare per 32
+          // warp-uniform branch (the votes below need every lane); a lane
+          // without a candidate has m = 0 and its pushes are no-ops
+          if (__any_sync(0xffffffffu, mn < top.s[3]) && P.prof != 8) {
             const int cbase = cta * kTcN + ch * (kTcN / 2) + c0;
+            const float thr = top.s[3];
+            uint32_t m = 0;
 #pragma unroll
-            for (int u = 0; u < 32; ++u) top.push(v[u], cbase + u);
+            for (int u = 0; u < 32; ++u) m |= v[u] < thr ? 1u << u : 0u;
+            if (__any_sync(0xffffffffu, __popc(m) > P.pushcut)) {  // a young list: walk every column
+#pragma unroll
+              for (int u = 0; u < 32; ++u) top.push(v[u], cbase + u);
+            } else {  // a few candidates: pull each out by its column (same order as the walk)
+              while (m) {
+                const int u = __ffs(m) - 1;
+                m &= m - 1;
+                top.push(pick32(v, u), cbase + u);
+              }
+            }
           }
         }
       }
@@ -649,7 +678,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               xs[p] = fmaf(x2, x2, xs[p]);
               xs[p] = fmaf(x3, x3, xs[p]);
             }
-            if (P.prof == 3 || P.prof >= 5) continue;
+            if (P.prof == 3 || (P.prof >= 5 && P.prof <= 7)) continue;
             if (Cfg::kATmem) {
               hi[4 * p] = h0;
               hi[4 * p + 1] = h1;
@@ -810,6 +839,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.top_s = top_s;
   P.top_i = top_i;
   P.xpart = nprod == 3 ? xpart : nullptr;
+  P.pushcut = getenv("GEEK_SCREEN_PUSHCUT") ? atoi(getenv("GEEK_SCREEN_PUSHCUT")) : 12;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
   P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
