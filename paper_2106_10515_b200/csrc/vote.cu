@@ -101,7 +101,9 @@ constexpr int kRowBins = 64;  // bins one id can reach through its m buckets (ch
 
 // per bucket: (first entry, entries) of its bin list; per entry: (bin, size),
 // with bins of 2m or more buckets dropped -- an id's count in a bin is at most
-// m (one bucket per table), so nobody can win them
+// m (one bucket per table), so nobody can win them.  A bucket with exactly one
+// entry carries it inline as (bin, size | kPackOne): one dependent load less.
+constexpr uint32_t kPackOne = 0x80000000u;
 __global__ void pack_bins_kernel(const uint32_t* bb_off, const uint32_t* bb_bins, const uint32_t* bin_size,
                                  uint64_t nbk, int m, uint2* pack, uint2* ent, uint32_t* words) {
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbk; b += (uint64_t)gridDim.x * blockDim.x) {
@@ -111,7 +113,7 @@ __global__ void pack_bins_kernel(const uint32_t* bb_off, const uint32_t* bb_bins
       const uint32_t bin = bb_bins[k], sz = bin_size[bin];
       if (sz < 2u * (uint32_t)m) ent[lo + c++] = make_uint2(bin, sz);
     }
-    pack[b] = make_uint2(lo, c);
+    pack[b] = c == 1 ? make_uint2(ent[lo].x, ent[lo].y | kPackOne) : make_uint2(lo, c);
     if (c) atomicOr(&words[b >> 5], 1u << (b & 31));
   }
 }
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
     const uint64_t i = base + tid;
     uint32_t rb[kRowBins], rs[kRowBins];
     int nb = 0;
+    const uint32_t* bm = smem_words > 0 ? sw : gwords;  // winnable-bucket bitmap (SMEM when it fits)
     if (tid < rows) {
       const uint32_t* row = srow + tid * ld;
       // 8 tables at a time: their bucket lists and first entries are
@@ -169,15 +172,18 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
           pk[u] = make_uint2(0u, 0u);
           if (j0 + u < m) {
             const uint32_t b = (uint32_t)(j0 + u) * t32 + row[j0 + u];
-            const uint32_t w = smem_words > 0 ? sw[b >> 5] : __ldg(gwords + (b >> 5));
+            const uint32_t w = bm[b >> 5];
             if ((w >> (b & 31)) & 1u) pk[u] = __ldg(pack + b);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) e0[u] = pk[u].y ? __ldg(ent + pk[u].x) : make_uint2(0u, 0u);
+        for (int u = 0; u < 8; ++u)
+          e0[u] = (pk[u].y & kPackOne) ? make_uint2(pk[u].x, pk[u].y & ~kPackOne)
+                  : pk[u].y            ? __ldg(ent + pk[u].x)
+                                       : make_uint2(0u, 0u);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          for (uint32_t k = 0; k < pk[u].y; ++k) {
+          for (uint32_t k = 0, ne = (pk[u].y & kPackOne) ? 1u : pk[u].y; k < ne; ++k) {
             const uint2 e = k == 0 ? e0[u] : __ldg(ent + pk[u].x + k);
             if (nb < kRowBins) {
               rb[nb] = e.x;
