@@ -122,6 +122,10 @@ __global__ void pack_bins_kernel(const uint32_t* bb_off, const uint32_t* bb_bins
 // staged in SMEM with coalesced 16-byte loads; each thread then walks its row
 // from SMEM with the winnable-bin bitmap in SMEM too.
 constexpr int kEwThreads = 256;
+#ifndef GEEK_EW_GROUP
+#define GEEK_EW_GROUP 8
+#endif
+constexpr int kEwGroup = GEEK_EW_GROUP;  // tables whose bucket words are fetched together
 __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
     const uint32_t* __restrict__ codes, uint64_t n, int m, uint64_t t, const uint2* __restrict__ pack,
     const uint2* __restrict__ ent, const uint32_t* __restrict__ gwords, uint64_t nwords, int smem_words,
@@ -165,10 +169,10 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
       // 8 tables at a time: their bucket lists and first entries are
       // fetched together instead of as one dependent chain per table
       const uint32_t t32 = (uint32_t)t;  // m * t < 2^32 (checked by the caller)
-      for (int j0 = 0; j0 < m; j0 += 8) {
-        uint2 pk[8], e0[8];
+      for (int j0 = 0; j0 < m; j0 += kEwGroup) {
+        uint2 pk[kEwGroup], e0[kEwGroup];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kEwGroup; ++u) {
           pk[u] = make_uint2(0u, 0u);
           if (j0 + u < m) {
             const uint32_t b = (uint32_t)(j0 + u) * t32 + row[j0 + u];
@@ -177,12 +181,12 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kEwGroup; ++u)
           e0[u] = (pk[u].y & kPackOne) ? make_uint2(pk[u].x, pk[u].y & ~kPackOne)
                   : pk[u].y            ? __ldg(ent + pk[u].x)
                                        : make_uint2(0u, 0u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kEwGroup; ++u)
           for (uint32_t k = 0, ne = (pk[u].y & kPackOne) ? 1u : pk[u].y; k < ne; ++k) {
             const uint2 e = k == 0 ? e0[u] : __ldg(ent + pk[u].x + k);
             if (nb < kRowBins) {
