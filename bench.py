@@ -260,27 +260,34 @@ def main():
     roof = None
     dom = None
     if info.get("screen_ms"):
-        # tcgen05 TF32x3 screen: algorithmic work = the n x k x d distance GEMM
+        # tcgen05 screen: algorithmic work = the n x k x d distance GEMM
         sec = info["screen_ms"] / 1e3
         kk = info.get("centers", ngroups)
         flops = 2.0 * (hi - lo) * kk * P["d"]
-        nct = -(-kk // 128)
-        kexec = 128 * (nct - 1) + -(-(kk - 128 * (nct - 1)) // 16) * 16  # last tile at N = valid rounded to 16
+        mode = info.get("screen_mode", 16)
+        f16 = mode == 16
+        tile_n = 192
+        nct = -(-kk // tile_n)
+        kexec = tile_n * (nct - 1) + -(-(kk - tile_n * (nct - 1)) // 16) * 16  # last tile at N = valid rounded to 16
         nl = hi - lo
-        exec_flops = 2.0 * nl * kexec * (3 * P["d"] + 8)  # 3 TF32 products + the |c'|^2 slice
+        # 3 products (hi*hi, hi*lo, lo*hi) + the |c'|^2 K slice (16 f16 / 8 tf32 wide)
+        exec_flops = 2.0 * nl * kexec * ((3 if mode != 1 else 1) * P["d"] + (16 if f16 else 8))
+        exec_peak = peaks.get("bf16_tflops", 1590.0) if f16 else 1066.0
         roof = dict(kernel="tc_screen_kernel", bound="tensor", achieved=flops / sec / 1e12, unit="TFLOP/s",
                     peak=peaks.get("bf16_tflops", 1590.0),
                     # dram read + write per launch from `ncu --set full` (profiles/r1_kernels.md: 51.23 GB
                     # + 8.00 GB at n = 1e8), scaled to this rank's points; = the algorithmic X + top-list + |x'|^2 bytes
                     traffic=59.23e9 * nl / 1e8,
-                    peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); tcgen05 kind::tf32 runs at "
-                                "half of it: 1066 TFLOP/s measured by tools/tc_rate.cu",
-                    executed_tf32_tflops=exec_flops / sec / 1e12,
-                    executed_frac_of_tf32_peak=exec_flops / sec / 1e12 / 1066.0,
+                    peak_source="MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS; the kind::f16 screen runs on "
+                                "the same tensor rate; kind::tf32 runs at 1066 TFLOP/s, tools/tc_rate.cu)",
+                    screen=("FP16x3" if f16 else "TF32x3" if mode == 3 else "TF32"),
+                    executed_tflops=exec_flops / sec / 1e12,
+                    executed_frac_of_peak=exec_flops / sec / 1e12 / exec_peak,
                     kernel_ms=info["screen_ms"],
                     note=f"achieved = algorithmic flops 2*n*k*d (k={kk}, d={P['d']}) per launch / CUDA-event time; "
-                         f"the kernel executes 3 TF32 products (hi*hi, hi*lo, lo*hi) over k padded to {kexec} plus "
-                         f"the |c'|^2 K-slice, for exact float64 labels after the recheck")
+                         f"the kernel executes 3 products (hi*hi, hi*lo, lo*hi) of "
+                         f"{'f16 parts of power-of-two scaled' if f16 else 'TF32 parts of'} operands over k padded "
+                         f"to {kexec} plus the |c'|^2 K-slice, for exact float64 labels after the recheck")
         roof["frac"] = roof["achieved"] / roof["peak"]
     elif "geek_project_keys" in calls:
         dom = "geek_project_keys"

@@ -235,6 +235,8 @@ int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host);
 uint64_t geek_assign_last_rechecked(void);
 /* CUDA-event duration (ms) of the last tensor-core screen kernel launch     */
 double geek_assign_last_screen_ms(void);
+/* precision of that screen: 16 = FP16x3 (scaled operands), 3 = TF32x3, 1 = TF32 */
+int geek_assign_last_screen_mode(void);
 /* of those, points whose candidate window overflowed (exact scan over all)   */
 uint64_t geek_assign_last_full_scans(void);
 

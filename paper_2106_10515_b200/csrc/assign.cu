@@ -303,6 +303,11 @@ static double& last_screen_ms() {
   return v;
 }
 
+static int& last_screen_mode() {  // 1 / 3 TF32 products, 16 = FP16x3
+  static int v = 0;
+  return v;
+}
+
 static uint64_t& last_full() {
   static uint64_t v = 0;
   return v;
@@ -468,17 +473,29 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
 //            the final subtraction;
 //   nprod 1: float32 operand rounding, TF32 rounding of both operands
 //            (2^-11 relative each), fp32 accumulation of d products, |c'|^2
-//            rounding and the subtraction.
+//            rounding and the subtraction;
+//   nprod 16 (FP16x3 over s x', s c', s a power of two): the nprod 3 terms
+//            (f16 and tf32 share the 11-bit significand) plus the absolute
+//            error of f16 subnormals, at most 2^-25 per scaled coordinate:
+//            2^-25 sqrt(d) (|x'| + |c'|) / s, and the three f16 parts of
+//            s^2 |c'|^2 / 2 (3 * 2^-25 / s^2 + 2^-33 |c'|^2 / 2).
+// cmax_bits[0] = |c'|max, cmax_bits[3] = 1/s (FP16 only, else 0).
 // Every product is bounded through sum |x'_i||c'_i| <= |x'||c'| (Cauchy-Schwarz).
 // E64 bounds numpy's float64 evaluation of the squared distance, and the last
 // term keeps the correctly rounded square roots of the two best distinct.
-__device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int nprod) {
+__device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int nprod,
+                                               const unsigned long long* cmax_bits) {
   const double u = 5.9604644775390625e-08;  // 2^-24
   const double acc = (double)d * 1.1920928955078125e-07;  // d * 2^-23
   // (|c'|^2/2 enters the fp32 accumulation as a last K=8 slice: one more
   // rounding of the accumulator, 2u(xn cn + cn^2) in s units, on top)
-  const double E = nprod == 3 ? 1.05 * ((1.9073486328125e-06 + 6.0 * acc + 10.0 * u) * xn * cn + 4.0 * u * cn * cn)
-                              : 1.05 * ((1.953125e-03 + 2.0 * acc + 8.0 * u) * xn * cn + 5.0 * u * cn * cn);
+  double E = nprod != 1 ? 1.05 * ((1.9073486328125e-06 + 6.0 * acc + 10.0 * u) * xn * cn + 4.0 * u * cn * cn)
+                        : 1.05 * ((1.953125e-03 + 2.0 * acc + 8.0 * u) * xn * cn + 5.0 * u * cn * cn);
+  if (nprod == 16) {
+    const double is = __longlong_as_double((long long)cmax_bits[3]);
+    const double t25 = 2.9802322387695312e-08;  // 2^-25
+    E += 1.05 * (t25 * sqrt((double)d) * (xn + cn) * is + 3.0 * t25 * is * is + 1.1641532182693481e-10 * 0.5 * cn * cn);
+  }
   const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
   return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
 }
@@ -530,7 +547,7 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
     }
     const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
     xnorm[i] = xn;
-    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
     if (k == 1 || (double)v.s1 - s0 > T) {
       const int lab = v.i0;
@@ -574,7 +591,7 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
     xn2 += __shfl_xor_sync(gmask, xn2, 4);
     const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
     if (a == 0) xnorm[i] = xn;
-    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
     const bool certain = k == 1 || (double)v.s1 - s0 > T;
     if (certain) {
@@ -646,7 +663,7 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
     // the screen's partial sums are fp32 (relative error <= 64 u = 3.8e-6)
     const float xn = (float)(sqrt(xn2) * (xpart ? 1.0 + 1e-5 : 1.0 + 1e-6));
     if (h == 0) xnorm[i] = xn;
-    const double T = tc_threshold((double)xn, cn, d, nprod);
+    const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
     if (k == 1 || (double)v.s1 - s0 > T) {
       const int lab = v.i0;
@@ -701,7 +718,7 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const doub
     const float* s8 = top_s + i * 8;
     const int* i8 = top_i + i * 8;
     const ScreenView v = screen_view(s8, i8);
-    const double T = tc_threshold((double)xnorm[i], cn, d, nprod);
+    const double T = tc_threshold((double)xnorm[i], cn, d, nprod, cmax_bits);
     const float* xr = X + i * d;
     double bd = 0.0;
     int64_t bl = -1;
@@ -740,7 +757,7 @@ __global__ void tc_recheck8_kernel(const float* __restrict__ X, int d, const dou
     const float* s8 = top_s + i * 8;
     const int* i8 = top_i + i * 8;
     const ScreenView v = screen_view(s8, i8);
-    const double T = tc_threshold((double)xnorm[i], cn, d, nprod);
+    const double T = tc_threshold((double)xnorm[i], cn, d, nprod, cmax_bits);
     const float* xr = X + i * d;
     double xv[16];
 #pragma unroll
@@ -806,20 +823,27 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                          (int)smem));
   }
   if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull && !getenv("GEEK_NO_TC")) {
-    // tensor-core screen (TF32x3 by default; GEEK_SCREEN=1 selects the single
-    // TF32 product, 1.4x faster but its bound ~2e-3|x'||c'| only separates
-    // data whose cluster gaps are large against |x'||c'|) -> classification
-    // -> candidate / full recheck
+    // tensor-core screen (FP16x3 over power-of-two scaled operands by default;
+    // GEEK_SCREEN=3 selects TF32x3 -- the same accuracy at half the MMA rate --
+    // and GEEK_SCREEN=1 the single TF32 product, whose bound ~2e-3|x'||c'|
+    // only separates data whose cluster gaps are large against |x'||c'|)
+    // -> classification -> candidate / full recheck
     const char* sel = getenv("GEEK_SCREEN");
-    const int nprod = (sel && sel[0] == '1') ? 1 : 3;
+    int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : 16;
     Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt;
-    GEEK_TRY(cnt.alloc(32, s));
-    GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 32, s));
-    unsigned long long* cmax = cnt.as<unsigned long long>();
+    GEEK_TRY(cnt.alloc(48, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
+    unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16)
     unsigned long long* namb = cmax + 1;
     unsigned long long* nfull = cmax + 2;
+    unsigned* ovf = reinterpret_cast<unsigned*>(cmax + 4);
     int nct = 0;
-    GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, s));
+    float xscale = 1.f;
+    GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
+    if (nprod == 16) {
+      const double is = 1.0 / (double)xscale;
+      GEEK_CHECK_CUDA(cudaMemcpyAsync(cmax + 3, &is, 8, cudaMemcpyHostToDevice, s));
+    }
     GEEK_TRY(ts.alloc(n * 32, s));
     GEEK_TRY(ti.alloc(n * 32, s));
     GEEK_TRY(xn.alloc(n * 4, s));
@@ -831,11 +855,25 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_CUDA(cudaEventRecord(ev0, s));
     // TF32x3 screen also leaves |x'|^2 per row half for the 2-lane classifier
     Scratch xp;
-    const bool use_xp = nprod == 3 && d % 8 == 0 && d <= 128;
+    const bool use_xp = nprod != 1 && d % 8 == 0 && d <= 128;
     if (use_xp) GEEK_TRY(xp.alloc(n * 16, s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
-                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, s));
+                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s));
+    if (nprod == 16) {  // a point coordinate beyond the f16 range: redo the screen in TF32x3
+      unsigned hov = 0;
+      GEEK_CHECK_CUDA(cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, s));
+      GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (hov) {
+        nprod = 3;
+        xscale = 1.f;
+        GEEK_CHECK_CUDA(cudaMemsetAsync(cmax, 0, 48, s));
+        GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
+        GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO,
+                                  ts.as<float>(), ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s));
+      }
+    }
     GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
+    last_screen_mode() = nprod;
     if (getenv("GEEK_SCREEN_ONLY")) {  // profiling hook: time the screen alone (labels are not written)
       GEEK_CHECK_CUDA(cudaEventSynchronize(ev1));
       float ms = 0.f;
@@ -930,6 +968,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
 uint64_t geek_assign_last_rechecked(void) { return last_ambiguous(); }
 
 double geek_assign_last_screen_ms(void) { return last_screen_ms(); }
+
+int geek_assign_last_screen_mode(void) { return last_screen_mode(); }
 
 uint64_t geek_assign_last_full_scans(void) { return last_full(); }
 

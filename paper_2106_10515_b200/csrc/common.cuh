@@ -181,11 +181,15 @@ int bitlen_u64(uint64_t v);
 
 // tensor-core assignment screen (tc_screen.cu)
 int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStream_t s);
+// nprod: 1 / 3 TF32 products, 16 = FP16x3 over operands scaled by xscale (a
+// power of two chosen by prepare; the kernel sets *ovf if a scaled point
+// coordinate leaves the f16 range -- the caller then reruns with nprod 3)
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
-                      Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s);
+                      Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
+                      cudaStream_t s);
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     double* xpart, cudaStream_t s);
+                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s);
 
 __global__ void iota_u32(uint32_t* p, uint64_t n);
 __global__ void fill_u32(uint32_t* p, uint32_t v, uint64_t n);

@@ -35,8 +35,11 @@
 // geek_tc_selftest).
 #include "common.cuh"
 
+#include <cuda_fp16.h>
+
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 namespace geek {
@@ -51,17 +54,23 @@ constexpr int kTcBSliceBytes = kTcN * 8 * 4;                      // one K=8 tf3
 constexpr int kTcHalfStage = (kTcChunk / 8) * kTcBSliceBytes;     // one 16-dim B chunk, one part
 constexpr int kTcAPart = (kTcKmax / 8) * kTcSliceBytes;           // 64 KB: one part of a point tile
 
+// NPROD = 16 is the FP16x3 screen: the same three products on kind::f16
+// MMAs (twice the TF32 rate, half the operand bytes) over power-of-two scaled
+// operands; a K slice is 32 bytes per row in both formats (8 tf32 / 16 f16).
 template <int NPROD>
 struct TcCfg {
-  static constexpr int kParts = NPROD == 3 ? 2 : 1;              // hi (+ lo)
-  // NPROD = 3 keeps the hi part of the point tile in TMEM (columns 384..511)
+  static constexpr bool kF16 = NPROD == 16;
+  static constexpr int kSliceDims = kF16 ? 16 : 8;               // dims per K slice
+  static constexpr int kChunkDims = 2 * kSliceDims;              // dims per B stage (two slices)
+  static constexpr int kParts = NPROD == 1 ? 1 : 2;              // hi (+ lo)
+  // NPROD = 3 / 16 keep the hi part of the point tile in TMEM (columns 384..)
   // and only the lo part in SMEM: the SMEM this frees deepens the B ring
-  static constexpr bool kATmem = NPROD == 3;
-  static constexpr int kABytes = kTcAPart;
+  static constexpr bool kATmem = NPROD != 1;
+  static constexpr int kABytes = (kTcKmax / kSliceDims) * kTcSliceBytes;
   // NPROD = 1: point tiles double-buffered; NPROD = 3: single-buffered, the
   // SMEM goes to the resident |c'|^2 slices instead (chunked hand-off keeps
   // the tile switch short)
-  static constexpr int kABuf = NPROD == 3 ? 1 : 2;
+  static constexpr int kABuf = NPROD == 1 ? 2 : 1;
   static constexpr int kStageBytes = kParts * kTcHalfStage;
   static constexpr int kStages = 4;
   static constexpr uint32_t kTmemCols = 512;
@@ -72,8 +81,8 @@ struct TcCfg {
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
 // chunk (B slice with |c'|^2/2, then the all-ones A slice)
 constexpr int kTcC2Bytes = kTcBSliceBytes + kTcSliceBytes;  // |c'|^2 B slice, then the all-ones A slice
-__host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts) {
-  return (uint64_t)((d + kTcChunk - 1) / kTcChunk) * parts * kTcHalfStage + kTcC2Bytes;
+__host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts, int chunk_dims = kTcChunk) {
+  return (uint64_t)((d + chunk_dims - 1) / chunk_dims) * parts * kTcHalfStage + kTcC2Bytes;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -83,6 +92,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // byte offset of element (row r, k e) inside one K=8 slice of a 128-row operand
 __device__ __forceinline__ uint32_t core_off(int r, int e, uint32_t lbo, uint32_t sbo) {
   return (r >> 3) * sbo + (e >> 2) * lbo + (r & 7) * 16 + (e & 3) * 4;
+}
+// the same for byte kb (0..31) of row r's 32-byte slice row (any element size)
+__device__ __forceinline__ uint32_t core_off_b(int r, int kb, uint32_t lbo, uint32_t sbo) {
+  return (r >> 3) * sbo + (kb >> 4) * lbo + (r & 7) * 16 + (kb & 15);
 }
 
 __device__ __forceinline__ float tf32_round(float x) {
@@ -102,9 +115,11 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// kind::tf32, D=f32, A=B=tf32, K-major both, N>>3 at [17,23), M>>4 at [24,29)
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::tf32 (A=B=tf32, format 2) or kind::f16 (A=B=f16, format 0); D=f32,
+// K-major both, N>>3 at [17,23), M>>4 at [24,29)
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool f16 = false) {
+  return (1u << 4) | ((f16 ? 0u : 2u) << 7) | ((f16 ? 0u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -154,27 +169,53 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+template <bool F16 = false>
 __device__ __forceinline__ void tc_mma(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  if (F16)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
 // A operand from TMEM (M rows = lanes, one tf32 per 32-bit column)
+template <bool F16 = false>
 __device__ __forceinline__ void tc_mma_ta(uint32_t dtmem, uint32_t atmem, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(dtmem),
-      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum));
+  if (F16)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum));
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 
 __device__ __forceinline__ void tc_st16(uint32_t taddr, const float* v) {
@@ -316,6 +357,9 @@ struct TcParams {
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes, 8 = no top-4 inserts,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
+  float xscale;       // NPROD = 16: x' is multiplied by this power of two before the f16 split
+  float oscale;       // top_s = oscale * (accumulator): 2 (TF32) or 2 / xscale^2 (FP16)
+  unsigned* ovf;      // NPROD = 16: set when a scaled operand leaves the f16 range (caller reruns in TF32x3)
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
@@ -369,9 +413,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nck = (P.d + kTcAChunk - 1) / kTcAChunk;  // 32-dim point-tile chunks
-  const int nbk = (P.d + kTcChunk - 1) / kTcChunk;    // B chunks per center tile
+  const int nbk = (P.d + Cfg::kChunkDims - 1) / Cfg::kChunkDims;  // B chunks per center tile
   const uint32_t qct = (uint32_t)nbk + (P.c2res ? 0u : 1u);  // + the |c'|^2 slice when it is not resident
-  const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts);
+  const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts, Cfg::kChunkDims);
   const uint32_t total_q = (uint32_t)P.nct * qct;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -412,7 +456,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   } else if (warp == kTcEpiWarps) {
     const bool leader = elect_one();
     {  // ---------------- MMA issuer ----------------
-      const uint32_t idesc_full = make_idesc(kTcM, kTcN), idesc_last = make_idesc(kTcM, P.nlast);
+      const uint32_t idesc_full = make_idesc(kTcM, kTcN, Cfg::kF16), idesc_last = make_idesc(kTcM, P.nlast, Cfg::kF16);
       uint64_t q_mma = 0;
       long long w_full = 0, w_acce = 0, w_afull = 0, w_issue = 0, w_c2 = 0, w_accf = 0, w_done = 0;
       const long long t_start = clock64();
@@ -451,8 +495,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           // the last center tile runs with N = its valid centers rounded up to 16
           const uint32_t idesc = (int)((ct + blockIdx.x) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
           for (int kc = 0; kc < nbk; ++kc) {
-            const int ac = kc * kTcChunk / kTcAChunk;  // point-tile chunk holding these dims
-            if (ct == 0 && (kc * kTcChunk) % kTcAChunk == 0) {  // first use of this chunk of the point tile
+            const int ac = kc * Cfg::kChunkDims / kTcAChunk;  // point-tile chunk holding these dims
+            if (ct == 0 && (kc * Cfg::kChunkDims) % kTcAChunk == 0) {  // first use of this chunk of the point tile
               timed_wait(&afull[ab * 4 + ac], apar, w_afull);
               fence_after();
             }
@@ -460,27 +504,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             // descriptors differ from the stage / tile bases by constant
             // address offsets (the 14-bit address field never carries)
             const uint32_t blo32 = b_lo32 + ((s * Cfg::kStageBytes) >> 4);
-            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * (kTcChunk / 8) * kTcSliceBytes) >> 4);
-            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * kTcChunk;
+            // two K slices per chunk; a slice is 8 TMEM columns of A (8 tf32 or 16 f16)
+            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * 2 * kTcSliceBytes) >> 4);
+            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * 16;
             const long long c_is = P.dbg ? clock64() : 0;
             if (leader && P.prof != 2) {
 #pragma unroll
-              for (int j = 0; j < kTcChunk / 8; ++j) {
+              for (int j = 0; j < 2; ++j) {
                 const uint64_t bhi = desc_of(blo32 + ((j * kTcBSliceBytes) >> 4), d_hi32);
                 const uint32_t acc = (kc | j) ? 1u : 0u;
                 if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
                   const uint64_t blo = desc_of(blo32 + ((kTcHalfStage + j * kTcBSliceBytes) >> 4), d_hi32);
                   const uint64_t alo = desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
-                  tc_mma_ta(dt, at + j * 8, bhi, idesc, acc);
-                  tc_mma_ta(dt, at + j * 8, blo, idesc, 1u);
-                  tc_mma(dt, alo, bhi, idesc, 1u);
+                  tc_mma_ta<Cfg::kF16>(dt, at + j * 8, bhi, idesc, acc);
+                  tc_mma_ta<Cfg::kF16>(dt, at + j * 8, blo, idesc, 1u);
+                  tc_mma<Cfg::kF16>(dt, alo, bhi, idesc, 1u);
                 } else {
                   tc_mma(dt, desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32), bhi, idesc, acc);
                 }
               }
             }
             if (P.dbg) w_issue += clock64() - c_is;
-            if (ct == P.nct - 1 && leader && (((kc + 1) * kTcChunk) % kTcAChunk == 0 || kc == nbk - 1))
+            if (ct == P.nct - 1 && leader && (((kc + 1) * Cfg::kChunkDims) % kTcAChunk == 0 || kc == nbk - 1))
               tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
             stage_done(s);
           }
@@ -493,13 +538,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             const uint32_t cta = (uint32_t)((ct + blockIdx.x) % P.nct);
             const uint64_t a1 = make_sdesc(smem_u32(C2), P.lbo, P.sbo);
             const uint64_t b1 = make_sdesc(smem_u32(C2) + kTcSliceBytes + cta * kTcBSliceBytes, P.lbo, P.sbo);
-            if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
+            if (P.prof != 2 && leader) tc_mma<Cfg::kF16>(dt, a1, b1, idesc, 1u);
             __syncwarp();
           } else {  // |c'|^2 / 2, added last, through the ring
             const uint32_t s = next_stage();
             const uint32_t sb = smem_u32(B + s * Cfg::kStageBytes);
             const uint64_t a1 = make_sdesc(sb + kTcBSliceBytes, P.lbo, P.sbo), b1 = make_sdesc(sb, P.lbo, P.sbo);
-            if (P.prof != 2 && leader) tc_mma(dt, a1, b1, idesc, 1u);
+            if (P.prof != 2 && leader) tc_mma<Cfg::kF16>(dt, a1, b1, idesc, 1u);
             stage_done(s);
           }
           const long long c_af = P.dbg ? clock64() : 0;
@@ -579,7 +624,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       if (i < P.n) {  // two column halves -> [n][8] of s = 2 * (s / 2) (exact); the classifier merges them
         const int h = (warp >> 2) * 4;
         *reinterpret_cast<float4*>(P.top_s + i * 8 + h) =
-            make_float4(2.f * top.s[0], 2.f * top.s[1], 2.f * top.s[2], 2.f * top.s[3]);
+            make_float4(P.oscale * top.s[0], P.oscale * top.s[1], P.oscale * top.s[2], P.oscale * top.s[3]);
         *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
@@ -651,6 +696,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           else mbar_wait(&aempty[ab * 4 + kc], epar);
           if (Cfg::kATmem) fence_after();
           float hi[16];
+          uint32_t hp[8];     // FP16: hi parts, two dims per TMEM column
+          bool big = false;   // FP16: a scaled operand outside the f16 range
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             int row, e0;
@@ -679,7 +726,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               xs[p] = fmaf(x3, x3, xs[p]);
             }
             if (P.prof == 3 || (P.prof >= 5 && P.prof <= 7)) continue;
-            if (Cfg::kATmem) {
+            if (Cfg::kF16) {
+              const float y0 = x0 * P.xscale, y1 = x1 * P.xscale, y2 = x2 * P.xscale, y3 = x3 * P.xscale;
+              big |= fmaxf(fmaxf(fabsf(y0), fabsf(y1)), fmaxf(fabsf(y2), fabsf(y3))) > 32768.f;
+              const __half g0 = __float2half_rn(y0), g1 = __float2half_rn(y1), g2 = __float2half_rn(y2),
+                           g3 = __float2half_rn(y3);
+              const __half l0 = __float2half_rn(y0 - __half2float(g0)), l1 = __float2half_rn(y1 - __half2float(g1)),
+                           l2 = __float2half_rn(y2 - __half2float(g2)), l3 = __float2half_rn(y3 - __half2float(g3));
+              hp[2 * p] = (uint32_t)__half_as_ushort(g0) | ((uint32_t)__half_as_ushort(g1) << 16);
+              hp[2 * p + 1] = (uint32_t)__half_as_ushort(g2) | ((uint32_t)__half_as_ushort(g3) << 16);
+              const uint32_t offh = (e0 >> 4) * kTcSliceBytes + core_off_b(row, (e0 & 15) * 2, P.lbo, P.sbo);
+              *reinterpret_cast<uint2*>(Ab + offh) =
+                  make_uint2((uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16),
+                             (uint32_t)__half_as_ushort(l2) | ((uint32_t)__half_as_ushort(l3) << 16));
+            } else if (Cfg::kATmem) {
               hi[4 * p] = h0;
               hi[4 * p + 1] = h1;
               hi[4 * p + 2] = h2;
@@ -690,8 +750,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               *reinterpret_cast<float4*>(Ab + off) = make_float4(h0, h1, h2, h3);
             }
           }
-          if (Cfg::kATmem) {
-            if (P.prof != 3 && P.prof < 5)
+          if (Cfg::kF16) {
+            if (big) atomicOr(P.ovf, 1u);
+            if (P.prof != 3 && (P.prof < 5 || P.prof > 7))
+              tc_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 16 + (warp >> 2) * 8,
+                     hp);
+            tc_wait_st();
+            fence_before();
+          } else if (Cfg::kATmem) {
+            if (P.prof != 3 && (P.prof < 5 || P.prof > 7))
               tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 32 + (warp >> 2) * 16,
                       hi);
             tc_wait_st();
@@ -739,12 +806,16 @@ __global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu
 // NPROD=3) ..., then the |c'|^2/2 slice: [128 centers][8] = (p1, p2, p3, 0...)
 // with p1 + p2 + p3 = |c'|^2/2 to ~33 bits (+inf for padding centers), then
 // the all-ones A slice that multiplies it }
+// FP16 (f16 = 1): the same image in f16 over s * c' (s = xscale, a power of
+// two): K slices of 16 dims, hi/lo f16 parts, the |c'|^2/2 slice holds
+// s^2 |c'|^2 / 2 as three f16 parts, and the ones slice is f16 1.0.
 __global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, int parts,
                                     uint32_t lbo, uint32_t sbo, float* Bimg, float* c2,
-                                    unsigned long long* cmax_bits) {
-  const int nchunks_k = (d + kTcChunk - 1) / kTcChunk;
+                                    unsigned long long* cmax_bits, int f16, float xscale) {
+  const int chunk = f16 ? 32 : kTcChunk, sdims = f16 ? 16 : 8, eb = f16 ? 2 : 4;
+  const int nchunks_k = (d + chunk - 1) / chunk;
   const uint64_t stage = (uint64_t)parts * kTcHalfStage;
-  const uint64_t ct_bytes = tc_ct_bytes(d, parts);
+  const uint64_t ct_bytes = tc_ct_bytes(d, parts, chunk);
   const uint64_t total = (uint64_t)nct * kTcN;
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
        c += (uint64_t)gridDim.x * blockDim.x) {
@@ -753,18 +824,25 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
     double n2 = 0.0;
     for (int kc = 0; kc < nchunks_k; ++kc) {
       uint8_t* img = base + (uint64_t)kc * stage;
-      for (int e = 0; e < kTcChunk; ++e) {
-        const int j = kc * kTcChunk + e;
+      for (int e = 0; e < chunk; ++e) {
+        const int j = kc * chunk + e;
         float cv = 0.f;
         if (c < k && j < d) {
           const double dv = C[c * d + j] - (double)mu[j];
           cv = (float)dv;
           n2 = fma((double)cv, (double)cv, n2);
         }
-        const float hi = tf32_round(-cv);
-        const uint32_t off = (e >> 3) * kTcBSliceBytes + core_off(r, e & 7, lbo, sbo);
-        *reinterpret_cast<float*>(img + off) = hi;
-        if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(-cv - hi);
+        const uint32_t off = (e / sdims) * kTcBSliceBytes + core_off_b(r, (e % sdims) * eb, lbo, sbo);
+        if (f16) {
+          const float y = -cv * xscale;
+          const __half hi = __float2half_rn(y);
+          *reinterpret_cast<__half*>(img + off) = hi;
+          if (parts == 2) *reinterpret_cast<__half*>(img + kTcHalfStage + off) = __float2half_rn(y - __half2float(hi));
+        } else {
+          const float hi = tf32_round(-cv);
+          *reinterpret_cast<float*>(img + off) = hi;
+          if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(-cv - hi);
+        }
       }
     }
     uint8_t* cs = base + (uint64_t)nchunks_k * stage;
@@ -777,33 +855,79 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
     } else {
       p[0] = INFINITY;
     }
-    for (int e = 0; e < 8; ++e) {
-      *reinterpret_cast<float*>(cs + core_off(r, e, lbo, sbo)) = p[e];
-      if (r < kTcM) *reinterpret_cast<float*>(cs + kTcBSliceBytes + core_off(r, e, lbo, sbo)) = 1.f;  // all-ones A slice
+    if (f16) {
+      __half q[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) q[e] = __float2half_rn(0.f);
+      if (c < k) {
+        const double h = 0.5 * n2 * (double)xscale * (double)xscale;
+        q[0] = __double2half(h);
+        q[1] = __double2half(h - (double)__half2float(q[0]));
+        q[2] = __double2half(h - (double)__half2float(q[0]) - (double)__half2float(q[1]));
+      } else {
+        q[0] = __float2half_rn(INFINITY);
+      }
+      for (int e = 0; e < 16; ++e) {
+        *reinterpret_cast<__half*>(cs + core_off_b(r, 2 * e, lbo, sbo)) = q[e];
+        if (r < kTcM) *reinterpret_cast<__half*>(cs + kTcBSliceBytes + core_off_b(r, 2 * e, lbo, sbo)) = __float2half_rn(1.f);
+      }
+    } else {
+      for (int e = 0; e < 8; ++e) {
+        *reinterpret_cast<float*>(cs + core_off(r, e, lbo, sbo)) = p[e];
+        if (r < kTcM) *reinterpret_cast<float*>(cs + kTcBSliceBytes + core_off(r, e, lbo, sbo)) = 1.f;  // all-ones A slice
+      }
     }
     c2[c] = c < k ? (float)n2 : INFINITY;
     if (c < k) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(n2) * (1.0 + 1e-6)));
   }
 }
 
+// largest |fl32(c - mu)| component (non-negative float bits order as integers)
+__global__ void center_absmax_kernel(const double* C, uint64_t k, int d, const float* mu, unsigned* out) {
+  unsigned m = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < k * (uint64_t)d;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf((float)(C[e] - (double)mu[e % d]))));
+  atomicMax(out, m);
+}
+
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
-                      Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, cudaStream_t s) {
-  GEEK_REQUIRE(nprod == 1 || nprod == 3, "screen precision must be 1 or 3 TF32 products");
+                      Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
+                      cudaStream_t s) {
+  GEEK_REQUIRE(nprod == 1 || nprod == 3 || nprod == 16, "screen precision must be 1 or 3 TF32 products or 16 (FP16x3)");
   nct = (int)((k + kTcN - 1) / kTcN);
-  const int parts = nprod == 3 ? 2 : 1;
-  GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts), s));
+  const int parts = nprod == 1 ? 1 : 2;
+  const bool f16 = nprod == 16;
+  GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts, f16 ? 32 : kTcChunk), s));
   GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
-  GEEK_TRY(mu.alloc((size_t)d * 4, s));
+  GEEK_TRY(mu.alloc((size_t)d * 4 + 16, s));
   center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
   GEEK_CHECK_LAUNCH();
+  xscale = 1.f;
+  if (f16) {  // s = 2^e with max |s c'_j| < 16: s^2 |c'|^2 / 2 < 2^14 stays inside f16 in three parts
+    unsigned* amax = reinterpret_cast<unsigned*>(mu.as<float>() + d);
+    GEEK_CHECK_CUDA(cudaMemsetAsync(amax, 0, 4, s));
+    center_absmax_kernel<<<grid_for(k * (uint64_t)d, 256, 148 * 4), 256, 0, s>>>(C, k, d, mu.as<float>(), amax);
+    GEEK_CHECK_LAUNCH();
+    unsigned h = 0;
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(&h, amax, 4, cudaMemcpyDeviceToHost, s));
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+    float m;
+    memcpy(&m, &h, 4);
+    GEEK_REQUIRE(std::isfinite(m), "FP16 screen: non-finite center coordinate");
+    int e = 0;
+    if (m > 0.f) frexpf(m, &e);  // m < 2^e
+    xscale = ldexpf(1.f, 4 - e);
+  }
   center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(
-      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev);
+      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev, f16 ? 1 : 0, xscale);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 
 template <int NPROD>
 static int launch_screen(const TcParams& P, cudaStream_t s) {
+  static_assert(TcCfg<NPROD>::kTmemA + 128 <= TcCfg<NPROD>::kTmemCols, "TMEM map");
   const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -819,7 +943,8 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
 
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     double* xpart, cudaStream_t s) {
+                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s) {
+  GEEK_REQUIRE(nprod != 16 || ovf, "FP16 screen needs the overflow flag");
   GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
   TcParams P;
   P.X = X;
@@ -838,11 +963,14 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.sbo = sbo;
   P.top_s = top_s;
   P.top_i = top_i;
-  P.xpart = nprod == 3 ? xpart : nullptr;
+  P.xpart = nprod != 1 ? xpart : nullptr;
+  P.xscale = xscale;
+  P.oscale = nprod == 16 ? 2.f / (xscale * xscale) : 2.f;
+  P.ovf = ovf;
   P.pushcut = getenv("GEEK_SCREEN_PUSHCUT") ? atoi(getenv("GEEK_SCREEN_PUSHCUT")) : 12;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
+  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
   P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? 1 : 0;
@@ -853,7 +981,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
     GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 4 * 8 * 2, s));
     P.dbg = dbg.as<unsigned long long>();
   }
-  const int st = nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
+  const int st = nprod == 16 ? launch_screen<16>(P, s) : nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
   if (st == GEEK_OK && P.dbg) {  // diagnostics: where the MMA warp waits
     unsigned long long h[148 * 8];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -949,9 +1077,11 @@ extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* o
   selftest_fill<<<64, 256, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, 40.f);
   unsigned long long* cmax = misc.as<unsigned long long>();
   int nct = 0;
-  GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, nprod, lbo, sbo, img, c2, mu, cmax, nct, s));
+  float xscale = 1.f;
+  GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, nprod, lbo, sbo, img, c2, mu, cmax, nct, xscale, s));
+  unsigned* ovf = reinterpret_cast<unsigned*>(misc.as<unsigned long long>() + 3);
   GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, nprod, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(), nullptr,
-                            s));
+                            xscale, ovf, s));
   double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
   unsigned long long* bad = misc.as<unsigned long long>() + 2;
   selftest_check<<<8, 128, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, mu.as<float>(), ts.as<float>(),

@@ -558,6 +558,7 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         labels, best = assign_l2_device(X_local, C)
         info["assign_rechecked"] = int(_lib.load_library().geek_assign_last_rechecked())
         info["screen_ms"] = float(_lib.load_library().geek_assign_last_screen_ms())
+        info["screen_mode"] = int(_lib.load_library().geek_assign_last_screen_mode())
         info["assign_full_scans"] = int(_lib.load_library().geek_assign_last_full_scans())
         info["centers"] = int(groups.count)
         radii, sizes = radii_sizes(labels, best, groups.count)

@@ -267,15 +267,34 @@ def test_tcgen05_screen_selftest():
     assert out[1] == 0
     assert L.geek_tc_selftest(128, 256, 1, out) == 0
     assert out[0] < 5e-4  # 1x TF32 bound: ~2.0e-3 * |x'||c'| at d = 128
+    assert L.geek_tc_selftest(128, 256, 16, out) == 0
+    assert out[0] < 1e-5  # FP16x3 (scaled operands): same significand as TF32x3
+    assert out[1] == 0
 
 
-@pytest.mark.parametrize("mode", ["1", "3"])
+@pytest.mark.parametrize("mode", ["1", "3", "16"])
 def test_assign_screen_modes_vs_oracle(mode, monkeypatch):
     monkeypatch.setenv("GEEK_SCREEN", mode)
     rng = np.random.default_rng(11)
     C = rng.standard_normal((150, 128)) * 4 + 200.0
     C[7] = C[3] + 1e-9
     X = (C[rng.integers(0, 150, 30_000)] + rng.standard_normal((30_000, 128))).astype(np.float32)
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
+def test_fp16_screen_range_fallback(monkeypatch):
+    """A point far outside the centers' range overflows the scaled f16 operand:
+    the screen is redone in TF32x3 and the labels stay exact."""
+    monkeypatch.setenv("GEEK_SCREEN", "16")
+    rng = np.random.default_rng(12)
+    C = rng.standard_normal((40, 64)) * 3
+    X = (C[rng.integers(0, 40, 5_000)] + rng.standard_normal((5_000, 64)) * 0.5).astype(np.float32)
+    X[17, 5] = 3.0e6
+    X[18] = 0.0
     got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
     lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
     assert np.array_equal(got.assignment, lab)
