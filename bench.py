@@ -88,7 +88,9 @@ class ClockSampler:
 
     def start(self):
         try:
-            ids = [f"--id={self.idx}"] if self.idx is not None else []
+            # one GPU, or the node's first `world` GPUs (local rank r drives GPU r; idle GPUs
+            # of a larger box would drag the median down)
+            ids = [f"--id={self.idx}"] if isinstance(self.idx, int) else [f"--id={','.join(map(str, self.idx))}"]
             self.proc = subprocess.Popen(["nvidia-smi", *ids, f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -181,7 +183,7 @@ def main():
     # ---- timed region: resident data --------------------------------------
     # one sampler for the job: rank 0 polls every GPU of the node (an
     # nvidia-smi per rank perturbs the timed steps)
-    clocks = ClockSampler(local if world == 1 else None)
+    clocks = ClockSampler(local if world == 1 else list(range(int(os.environ.get("LOCAL_WORLD_SIZE", world)))))
     if rank == 0:
         clocks.start()
     timer = _lib.CallTimer()
