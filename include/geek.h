@@ -219,7 +219,9 @@ int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngr
 
 /* Nearest center by float64 direct-difference distance with numpy's pairwise
  * summation order and first-index ties (assignment.py:54-62, :95-99):
- * labels[i], best[i] = distance.  C is [k][d] float64.                      */
+ * labels[i], best[i] = distance.  C is [k][d] float64.  float32 X with
+ * d <= 128 and k >= 4 goes through the tcgen05 screen (FP16x3; env
+ * GEEK_SCREEN=3 / 1 selects TF32x3 / TF32) and an exact float64 recheck.     */
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
                    int64_t* labels, double* best, void* stream);
 
@@ -227,7 +229,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
  * points, 300 centers): out_host[0] = max |s_tc - S_f64| / (|x'||c'|max)
  * over every kept entry, out_host[1] = points whose screened top-1 is not
  * the f64 argmin.  lbo/sbo are the canonical-layout core-matrix strides in
- * bytes; nprod = 1 (TF32) or 3 (TF32x3).                                   */
+ * bytes; nprod = 1 (TF32), 3 (TF32x3) or 16 (FP16x3 over power-of-two
+ * scaled operands, the default screen of geek_assign_l2).                  */
 int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host);
 
 /* number of points the last geek_assign_l2 call re-checked exactly because
@@ -235,10 +238,10 @@ int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host);
 uint64_t geek_assign_last_rechecked(void);
 /* CUDA-event duration (ms) of the last tensor-core screen kernel launch     */
 double geek_assign_last_screen_ms(void);
-/* precision of that screen: 16 = FP16x3 (scaled operands), 3 = TF32x3, 1 = TF32 */
-int geek_assign_last_screen_mode(void);
 /* of those, points whose candidate window overflowed (exact scan over all)   */
 uint64_t geek_assign_last_full_scans(void);
+/* precision of that screen: 16 = FP16x3 (scaled operands), 3 = TF32x3, 1 = TF32 */
+int geek_assign_last_screen_mode(void);
 
 /* radii[c] = max best over members (0 if none), sizes[c] = member count
  * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed

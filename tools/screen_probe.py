@@ -26,7 +26,7 @@ if os.environ.get("_PROBE_CHILD"):
         L.call("geek_assign_l2", L.ptr(X), 0, n, d, L.ptr(C), k, L.ptr(labels), L.ptr(best), L.stream())
         torch.cuda.synchronize()
         ms.append(L.load_library().geek_assign_last_screen_ms())
-    print(f"mode={os.environ.get('GEEK_SCREEN_PROF','0')} nprod={os.environ.get('GEEK_SCREEN','3')} "
+    print(f"mode={os.environ.get('GEEK_SCREEN_PROF','0')} screen={os.environ.get('GEEK_SCREEN','16')} "
           f"screen_ms={min(ms[1:]):.2f} all={['%.2f' % v for v in ms]}", flush=True)
 else:
     for mode in os.environ.get("PROBE_MODES", "0,1,2,3").split(","):
