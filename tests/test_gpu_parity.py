@@ -286,6 +286,25 @@ def test_assign_screen_modes_vs_oracle(mode, monkeypatch):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("d", [100, 24, 9])
+def test_fp16_screen_ragged_dims_and_tiny_coordinates(d, monkeypatch):
+    """FP16x3 at dims that are not a multiple of the 16-dim K slice, with
+    coordinates spanning ~9 orders of magnitude (scaled lo parts underflow to
+    f16 subnormals: the bound's absolute term covers them)."""
+    monkeypatch.setenv("GEEK_SCREEN", "16")
+    rng = np.random.default_rng(100 + d)
+    C = rng.standard_normal((90, d)) * 500.0
+    C[:, : d // 3] *= 1e-6
+    C[11] = C[5] + 1e-7
+    X = (C[rng.integers(0, 90, 8_000)] + rng.standard_normal((8_000, d)) * 20.0).astype(np.float32)
+    X[:, : d // 3] = (rng.standard_normal((8_000, d // 3)) * 1e-4).astype(np.float32)
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
 def test_fp16_screen_range_fallback(monkeypatch):
     """A point far outside the centers' range overflows the scaled f16 operand:
     the screen is redone in TF32x3 and the labels stay exact."""
