@@ -729,16 +729,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             if (Cfg::kF16) {
               const float y0 = x0 * P.xscale, y1 = x1 * P.xscale, y2 = x2 * P.xscale, y3 = x3 * P.xscale;
               big |= fmaxf(fmaxf(fabsf(y0), fabsf(y1)), fmaxf(fabsf(y2), fabsf(y3))) > 32768.f;
-              const __half g0 = __float2half_rn(y0), g1 = __float2half_rn(y1), g2 = __float2half_rn(y2),
-                           g3 = __float2half_rn(y3);
-              const __half l0 = __float2half_rn(y0 - __half2float(g0)), l1 = __float2half_rn(y1 - __half2float(g1)),
-                           l2 = __float2half_rn(y2 - __half2float(g2)), l3 = __float2half_rn(y3 - __half2float(g3));
-              hp[2 * p] = (uint32_t)__half_as_ushort(g0) | ((uint32_t)__half_as_ushort(g1) << 16);
-              hp[2 * p + 1] = (uint32_t)__half_as_ushort(g2) | ((uint32_t)__half_as_ushort(g3) << 16);
+              // packed conversions: element 2j in the low half (the K-major f16 order)
+              const __half2 g01 = __floats2half2_rn(y0, y1), g23 = __floats2half2_rn(y2, y3);
+              const float2 b01 = __half22float2(g01), b23 = __half22float2(g23);
+              const __half2 l01 = __floats2half2_rn(y0 - b01.x, y1 - b01.y);
+              const __half2 l23 = __floats2half2_rn(y2 - b23.x, y3 - b23.y);
+              hp[2 * p] = *reinterpret_cast<const uint32_t*>(&g01);
+              hp[2 * p + 1] = *reinterpret_cast<const uint32_t*>(&g23);
               const uint32_t offh = (e0 >> 4) * kTcSliceBytes + core_off_b(row, (e0 & 15) * 2, P.lbo, P.sbo);
               *reinterpret_cast<uint2*>(Ab + offh) =
-                  make_uint2((uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16),
-                             (uint32_t)__half_as_ushort(l2) | ((uint32_t)__half_as_ushort(l3) << 16));
+                  make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
             } else if (Cfg::kATmem) {
               hi[4 * p] = h0;
               hi[4 * p + 1] = h1;
