@@ -284,6 +284,26 @@ int geek_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, uint64
                        uint64_t row_lo, uint64_t universe, const uint32_t* flat,
                        const uint64_t* offsets, uint64_t ngroups, int64_t* counts, void* stream);
 
+/* ---- refinement passes (assignment.py:110-170, engine.py:519-537) ------ */
+
+/* Exact digit column sums keyed by label: digits[(labels[i]*d + c)*nd + q]
+ * += row i's column c in base-2^32 digits relative to 2^emin (the
+ * geek_exact_sums representation; ADDED to, so shards reduce by addition).
+ * Rows stream once, coalesced; labels outside [0, k) are skipped.  ASYNC.   */
+int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64_t* labels, uint64_t k,
+                    int emin, int nd, int64_t* digits, void* stream);
+
+/* counts[(labels[i]*d + c)*cs + codes[i*d + c]] += 1 (categorical modes of
+ * the current clusters, assignment.py:122-126).  ASYNC.                      */
+int geek_label_mode_counts(const int32_t* codes, uint64_t nrows, int d, const int64_t* labels, uint64_t k,
+                           uint64_t cs, int64_t* counts, void* stream);
+
+/* counts[labels[i]*universe + e] += 1 for every e in set i (sparse modes of
+ * the current clusters, assignment.py:127-131).  ASYNC.                      */
+int geek_label_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, uint64_t nrows,
+                             const int64_t* labels, uint64_t k, uint64_t universe, int64_t* counts,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

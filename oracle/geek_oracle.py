@@ -440,8 +440,8 @@ def local_votes(tables_buckets, K, L, delta, seed, n, pinned=None):
 
 
 def pipeline_dense(X, m, t, tseed, K, L, delta, sseed, g=1, dedup_tables=1,
-                   dirs=None, pinned=None, dedup_pinned=None, fallback_seed=0):
-    """run_pipeline for transform_kind='dense', metric='euclidean', passes=0.
+                   dirs=None, pinned=None, dedup_pinned=None, fallback_seed=0, passes=0):
+    """run_pipeline for transform_kind='dense', metric='euclidean'.
 
     Returns dict(groups, centers, labels, best, radii, objective, warnings).
     """
@@ -463,8 +463,46 @@ def pipeline_dense(X, m, t, tseed, K, L, delta, sseed, g=1, dedup_tables=1,
         groups = [np.array([p], dtype=np.int64) for p in picks]
     centers = np.stack([exact_mean(X[gm]) for gm in groups])
     lab, best, radii, obj = assign_l2(X, centers)
-    return dict(groups=groups, centers=centers, labels=lab, best=best,
-                radii=radii, objective=obj, warnings=warnings)
+    out = dict(groups=groups, centers=centers, labels=lab, best=best,
+               radii=radii, objective=obj, warnings=warnings)
+    if passes:  # _refine_distributed (engine.py:519-537); exact sums make it g-independent
+        out.update(refine_dense(X, lab, centers.shape[0], passes))
+    return out
+
+
+# --------------------------------------------------------------------------
+# refinement passes (assignment.py:110-170, engine.py:519-537)
+
+def centers_from_labels(X: np.ndarray, labels: np.ndarray, k: int):
+    """Exact centroids of the non-empty clusters in label order
+    (assignment.py:110-127); -> (centers [k', d], sizes [k'])."""
+    X = np.asarray(X, dtype=np.float64)
+    rows = [np.flatnonzero(labels == j) for j in range(k)]
+    rows = [r for r in rows if r.size]
+    return np.stack([exact_mean(X[r]) for r in rows]), np.array([r.size for r in rows], dtype=np.int64)
+
+
+def refine_dense(X: np.ndarray, labels: np.ndarray, k: int, passes: int):
+    """refine(data, clustering, 'euclidean', passes) (assignment.py:157-170):
+    -> dict(centers, sizes, labels, best, radii, objective) of the last pass."""
+    out = None
+    for _ in range(passes):
+        C, sizes = centers_from_labels(X, labels, k)
+        labels, best, radii, obj = assign_l2(X, C)
+        k = C.shape[0]
+        out = dict(centers=C, sizes=sizes, labels=labels, best=best, radii=radii, objective=obj)
+    return out
+
+
+def modes_from_labels(codes: np.ndarray, code_space: int, labels: np.ndarray, k: int) -> np.ndarray:
+    """Categorical modes of the non-empty clusters (assignment.py:122-126)."""
+    return np.stack([mode_of(codes[labels == j], code_space) for j in range(k) if (labels == j).any()])
+
+
+def sparse_modes_from_labels(sets, universe: int, labels: np.ndarray, k: int) -> np.ndarray:
+    """Sparse strict-majority modes of the non-empty clusters (assignment.py:127-131)."""
+    return np.stack([sparse_mode([sets[i] for i in np.flatnonzero(labels == j)], universe)
+                     for j in range(k) if (labels == j).any()])
 
 
 # --------------------------------------------------------------------------

@@ -123,12 +123,34 @@ def distance_matrix(data, centers, metric, rows=None) -> np.ndarray:
 
 
 def _centers_from_assignment(data, assignment, k) -> list:
-    from .seeding import seeds_to_centers
-    from .data import SeedGroup
+    """One central vector per non-empty cluster, in label order
+    (assignment.py:110-137).  The members of cluster j are the rows labelled
+    j, so the statistics come from one pass over the rows keyed by label
+    (geek_label_sums / geek_label_mode_counts / geek_label_sparse_counts)
+    instead of materialised member lists."""
+    from .numeric import digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, \
+        round_means
 
-    assignment = np.asarray(assignment)
-    groups = [SeedGroup(np.flatnonzero(assignment == j)) for j in range(k) if (assignment == j).any()]
-    return seeds_to_centers(groups, data)
+    labels = _lib.to_dev(np.ascontiguousarray(assignment, dtype=np.int64))
+    zero = _lib.zeros(max(1, labels.numel()), torch.float64)
+    _, sizes = radii_sizes(labels, zero[: labels.numel()], k)
+    keep = torch.nonzero(sizes > 0).flatten()
+    counts = sizes[keep].contiguous()
+    w = counts.cpu().numpy()
+    if isinstance(data, DenseData):
+        X = data.device_vectors()
+        emin, emax = exponent_range(X)
+        nd = digit_count(emin, emax)
+        C = round_means(label_sums(X, labels, k, emin, nd)[keep].contiguous(), counts, emin, nd).cpu().numpy()
+        return [CentralVector("centroid", C[i], int(w[i])) for i in range(len(w))]
+    if isinstance(data, CategoricalData):
+        cnt = label_mode_counts(data.device_codes(), data.code_space, labels, k)[keep]
+        M = torch.argmax(cnt, dim=2).to(torch.int32).cpu().numpy()  # ties: smallest code
+    else:
+        flat, off = data.csr()
+        cnt = label_sparse_counts(flat, off, data.n, data.universe, labels, k)[keep]
+        M = (2 * cnt > counts[:, None]).to(torch.int32).cpu().numpy()
+    return [CentralVector("mode", M[i], int(w[i])) for i in range(len(w))]
 
 
 def squared_objective(data, clustering: Clustering, metric: str) -> float:

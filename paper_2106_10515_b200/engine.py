@@ -30,7 +30,8 @@ from .assignment import assign_cat_device, assign_l2_device, assign_sparse_devic
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
-from .numeric import digit_count, exponent_range, mode_counts, partial_sums, round_means, sparse_counts
+from .numeric import (digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, mode_counts,
+                      partial_sums, round_means, sparse_counts)
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
 from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
@@ -561,19 +562,36 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         info["screen_mode"] = int(_lib.load_library().geek_assign_last_screen_mode())
         info["assign_full_scans"] = int(_lib.load_library().geek_assign_last_full_scans())
         info["centers"] = int(groups.count)
-        radii, sizes = radii_sizes(labels, best, groups.count)
+    weights = groups.sizes()
+
+    def reduce_assignment(labels, best, k):
+        radii, sizes = radii_sizes(labels, best, k)
         comm.all_reduce(radii.view(torch.int64), dist.ReduceOp.MAX, "Assignments")
         comm.all_reduce(sizes, dist.ReduceOp.SUM, "Assignments")
         if comm.on:
             obj = torch.tensor([sharded_pairwise_sum(best, n, row_lo, comm)], dtype=torch.float64)
         else:
             obj = pairwise_sum(best)
+        return radii, sizes, obj
+
+    with tm.stage("assign"):
+        radii, sizes, obj = reduce_assignment(labels, best, groups.count)
+    for _ in range(config.passes):  # _refine_distributed (engine.py:519-537)
+        with tm.stage("centers"):
+            digits = label_sums(X_local, labels, C.shape[0], emin, nd)
+            comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
+            keep = torch.nonzero(sizes > 0).flatten()  # empty clusters are dropped
+            weights = sizes[keep].contiguous()
+            C = round_means(digits[keep].contiguous(), weights, emin, nd)
+        with tm.stage("assign"):
+            labels, best = assign_l2_device(X_local, C)
+            radii, sizes, obj = reduce_assignment(labels, best, C.shape[0])
     timings = tm.finish()
-    sizes_h = groups.sizes().cpu().numpy()
+    sizes_h = weights.cpu().numpy()
 
     def centers():
         Ch = C.cpu().numpy()
-        return [CentralVector("centroid", Ch[i], int(sizes_h[i])) for i in range(groups.count)]
+        return [CentralVector("centroid", Ch[i], int(sizes_h[i])) for i in range(Ch.shape[0])]
 
     gather = (lambda: comm.all_gather_var(labels, "Assignments")) if comm.on else None
     return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings,
@@ -634,12 +652,30 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
             labels, best = assign_sparse_device(flat, off, n, data.universe, M)
         radii, sizes = radii_sizes(labels, best, groups.count)
         obj = pairwise_sum(best)
+    weights = groups.sizes()
+    for _ in range(config.passes):  # _refine_distributed (engine.py:519-537) on one device
+        with tm.stage("centers"):
+            keep = torch.nonzero(sizes > 0).flatten()
+            weights = sizes[keep].contiguous()
+            if isinstance(data, CategoricalData):
+                cnt = label_mode_counts(data.device_codes(), data.code_space, labels, M.shape[0])[keep]
+                M = torch.argmax(cnt, dim=2).to(torch.int32)
+            else:
+                cnt = label_sparse_counts(flat, off, n, data.universe, labels, M.shape[0])[keep]
+                M = (2 * cnt > weights[:, None]).to(torch.int32)
+        with tm.stage("assign"):
+            if isinstance(data, CategoricalData):
+                labels, best = assign_cat_device(data.device_codes(), M)
+            else:
+                labels, best = assign_sparse_device(flat, off, n, data.universe, M)
+            radii, sizes = radii_sizes(labels, best, M.shape[0])
+            obj = pairwise_sum(best)
     timings = tm.finish()
-    sizes_h = groups.sizes().cpu().numpy()
+    sizes_h = weights.cpu().numpy()
 
     def centers():
         Mh = M.cpu().numpy()
-        return [CentralVector("mode", Mh[i], int(sizes_h[i])) for i in range(groups.count)]
+        return [CentralVector("mode", Mh[i], int(sizes_h[i])) for i in range(Mh.shape[0])]
 
     return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings, {}, warnings,
                           info)
@@ -650,8 +686,8 @@ def run_pipeline(data, config: PipelineConfig) -> PipelineResult:
 
     Under an initialised torch.distributed group of G ranks every rank calls
     this with the full dataset (or use run_pipeline_shard with its own rows)."""
-    if config.passes:
-        raise EngineError("stage setup: refinement passes are not part of the one-pass hot path")
+    if config.passes < 0:
+        raise EngineError("stage setup: passes must be >= 0")
     comm = _Comm()
     if config.transform_kind == "dense":
         if not isinstance(data, DenseData):

@@ -93,6 +93,36 @@ def sparse_centers(data: SparseData, groups: GroupSet) -> torch.Tensor:
     return (2 * cnt > groups.sizes()[:, None]).to(torch.int32)
 
 
+# ---- refinement: statistics keyed by the current labels (assignment.py:110-137) ----
+
+def label_sums(X: torch.Tensor, labels: torch.Tensor, k: int, emin: int, nd: int) -> torch.Tensor:
+    """int64 [k, d, nd] exact digit sums of the rows with each label (one
+    coalesced pass over X; shards add their partials exactly)."""
+    d = X.shape[1]
+    digits = _lib.zeros(max(1, k * d * nd), torch.int64)
+    if k and X.shape[0]:
+        _lib.call("geek_label_sums", _lib.ptr(X), _lib.dtype_code(X), X.shape[0], d, _lib.ptr(labels.contiguous()),
+                  k, emin, nd, _lib.ptr(digits), _lib.stream())
+    return digits[: k * d * nd].view(k, d, nd)
+
+
+def label_mode_counts(codes: torch.Tensor, code_space: int, labels: torch.Tensor, k: int) -> torch.Tensor:
+    n, d = codes.shape
+    if k * d * code_space > (1 << 31):
+        raise InvalidInput("mode statistics too large for dense counting")
+    cnt = _lib.zeros(max(1, k * d * code_space), torch.int64)
+    _lib.call("geek_label_mode_counts", _lib.ptr(codes), n, d, _lib.ptr(labels.contiguous()), k, code_space,
+              _lib.ptr(cnt), _lib.stream())
+    return cnt[: k * d * code_space].view(k, d, code_space)
+
+
+def label_sparse_counts(flat, off, n: int, universe: int, labels: torch.Tensor, k: int) -> torch.Tensor:
+    cnt = _lib.zeros(max(1, k * universe), torch.int64)
+    _lib.call("geek_label_sparse_counts", _lib.ptr(flat), _lib.ptr(off), n, _lib.ptr(labels.contiguous()), k,
+              universe, _lib.ptr(cnt), _lib.stream())
+    return cnt[: k * universe].view(k, universe)
+
+
 # ---- reference API (numeric.py:19-51) -----------------------------------------
 
 def exact_centroid(vectors) -> np.ndarray:

@@ -23,3 +23,8 @@ def groups(arr, prefix):
 
 def csr(flat, off):
     return [flat[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+
+
+def refine_meta():
+    with open(os.path.join(GOLDEN, "refine.json")) as f:
+        return json.load(f)

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle import geek_oracle as O
-from tests.golden_io import csr, groups as golden_groups, meta, npz
+from tests.golden_io import csr, groups as golden_groups, meta, npz, refine_meta
 
 pytestmark = pytest.mark.gpu
 
@@ -504,3 +504,97 @@ def test_host_rows_streamed_equal_device_rows():
     assert np.array_equal(dev.clustering.assignment, host.clustering.assignment)
     assert np.array_equal(dev.clustering.radii, host.clustering.radii)
     assert dev.clustering.objective == host.clustering.objective
+
+
+# ---- refinement passes (assignment.py:157-170, engine.py:519-537) ----------
+
+def _check_refined(cl, arr, rm, name):
+    assert np.array_equal(np.stack([c.values for c in cl.centers]), arr[f"{name}_centers"]), name
+    assert np.array_equal(np.array([c.weight for c in cl.centers]), arr[f"{name}_weights"]), name
+    assert np.array_equal(cl.assignment, arr[f"{name}_labels"]), name
+    assert np.array_equal(cl.radii, arr[f"{name}_radii"]), name
+    assert cl.objective == rm[name]["objective"], name
+    assert cl.k_star == rm[name]["k_star"], name
+
+
+def test_refine_c08_golden():
+    """geek_label_sums / geek_label_mode_counts + assignment against the
+    reference's refine() outputs, bit for bit."""
+    arr, rm = npz("refine"), refine_meta()
+    rng = np.random.default_rng(80)
+    dense = G.DenseData(rng.standard_normal((10_000, 16)))
+    cents = [G.CentralVector("centroid", rng.standard_normal(16)) for _ in range(200)]
+    c0 = G.assign(dense, cents, "euclidean")
+    assert G.refine(dense, c0, "euclidean", 0) is c0
+    for p in (1, 2):
+        _check_refined(G.refine(dense, c0, "euclidean", p), arr, rm, f"c08_p{p}")
+    codes = rng.integers(0, 8, (10_000, 9)).astype(np.int32)
+    modes = [G.CentralVector("mode", rng.integers(0, 8, 9).astype(np.int32)) for _ in range(200)]
+    cat = G.CategoricalData(codes, code_space=8)
+    c0 = G.assign(cat, modes, "jaccard")
+    _check_refined(G.refine(cat, c0, "jaccard", 2), arr, rm, "c08cat_p2")
+
+
+def test_refine_label_sums_ragged():
+    """Label-keyed exact sums equal the member-list sums (geek_exact_sums) on
+    shuffled labels, a float32 input, coordinates over many binades, d not a
+    multiple of 32 and an empty cluster."""
+    from paper_2106_10515_b200 import _lib, numeric
+    from paper_2106_10515_b200.tables import GroupSet
+    rng = np.random.default_rng(5)
+    n, d, k = 4099, 45, 37
+    X = (rng.standard_normal((n, d)) * np.exp2(rng.integers(-30, 30, (n, d)))).astype(np.float32)
+    X[rng.random((n, d)) < 0.05] = 0.0
+    lab = rng.integers(0, k, n)
+    lab[lab == 7] = 8  # cluster 7 empty
+    Xd = _lib.to_dev(X)
+    emin, emax = numeric.exponent_range(Xd)
+    nd = numeric.digit_count(emin, emax)
+    got = numeric.label_sums(Xd, _lib.to_dev(lab.astype(np.int64)), k, emin, nd)
+    want = numeric.partial_sums(Xd, GroupSet.from_host([np.flatnonzero(lab == j) for j in range(k)]), emin, nd)
+    C1 = numeric.round_means(got, torch.bincount(_lib.to_dev(lab), minlength=k), emin, nd).cpu().numpy()
+    C2 = numeric.round_means(want, torch.bincount(_lib.to_dev(lab), minlength=k), emin, nd).cpu().numpy()
+    assert np.array_equal(C1, C2)
+    for j in (0, 13, 36):
+        assert np.array_equal(C1[j], O.exact_mean(X[lab == j].astype(np.float64)))
+
+
+@pytest.mark.parametrize("g", [1, 2])
+def test_refine_pipeline_golden(g):
+    m = meta()["pipelines"]["small"]
+    arr, rm = npz("refine"), refine_meta()
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    cfg = dense_config(m, g)
+    cfg.passes = 2
+    for x in (X, X.astype(np.float32)):
+        out = G.run_pipeline(G.DenseData(x), cfg)
+        if x.dtype == np.float32:  # different data: the oracle on the f32 values
+            ref = O.pipeline_dense(x.astype(np.float64), m["m"], m["t"], m["tseed"], m["K"], m["L"], m["delta"],
+                                   m["sseed"], g=g, passes=2)
+            assert np.array_equal(out.clustering.assignment, ref["labels"])
+            assert np.array_equal(np.stack([c.values for c in out.clustering.centers]), ref["centers"])
+            assert out.clustering.objective == ref["objective"]
+        else:
+            _check_refined(out.clustering, arr, rm, f"small_p2_g{g}")
+
+
+def test_refine_pipeline_c06_sparse_mixed_golden():
+    arr, rm = npz("refine"), refine_meta()
+    m = meta()["pipelines"]["c06"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    cfg = dense_config(m, 1)
+    cfg.passes = 3
+    _check_refined(G.run_pipeline(G.DenseData(X), cfg).clustering, arr, rm, "c06_p3_g1")
+    parr = npz("pipelines")
+    data = G.SparseData(csr(parr["sp_flat"], parr["sp_off"]), 20_000)
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="sparse", workers=G.WorkerConfig(1),
+                           minhash=G.MinhashTransformParams(3, 6, seed=4, target_dims=400),
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=5), passes=2)
+    _check_refined(G.run_pipeline(data, cfg).clustering, arr, rm, "sp_p2_g1")
+    data = G.MixedData(parr["mx_num"], parr["mx_cat"])
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="mixed", workers=G.WorkerConfig(1),
+                           minhash=G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16),
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9), passes=2)
+    _check_refined(G.run_pipeline(data, cfg).clustering, arr, rm, "mx_p2_g1")

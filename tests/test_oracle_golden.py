@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import geek_oracle as O
-from tests.golden_io import csr, groups, meta, npz
+from tests.golden_io import csr, groups, meta, npz, refine_meta
 
 WORKED = [  # pkg/tests/conftest.py:23-41
     (0, 0, [0, 1, 3]), (0, 1, [2, 4, 5]), (1, 0, [0, 1, 3, 4]), (1, 1, [5]),
@@ -148,3 +148,45 @@ def test_cfg1_pipeline_golden_g8():
     assert keys(out["groups"]) == keys(groups(arr, "cfg1_g8"))
     assert np.array_equal(out["labels"], arr["cfg1_g8_labels"])
     assert np.array_equal(out["radii"], arr["cfg1_g8_radii"])
+
+
+def test_refine_c08_golden():
+    """refine(..., passes) on the c08 inputs (assignment.py:157-170) against
+    the reference's own outputs (tests/golden/make_refine_golden.py)."""
+    arr, rm = npz("refine"), refine_meta()
+    rng = np.random.default_rng(80)
+    X = rng.standard_normal((10_000, 16))
+    C = np.stack([rng.standard_normal(16) for _ in range(200)])
+    lab, _, _, _ = O.assign_l2(X, C)
+    for p in (1, 2):
+        out = O.refine_dense(X, lab, 200, p)
+        assert np.array_equal(out["centers"], arr[f"c08_p{p}_centers"])
+        assert np.array_equal(out["sizes"], arr[f"c08_p{p}_weights"])
+        assert np.array_equal(out["labels"], arr[f"c08_p{p}_labels"])
+        assert np.array_equal(out["radii"], arr[f"c08_p{p}_radii"])
+        assert out["objective"] == rm[f"c08_p{p}"]["objective"]
+    codes = rng.integers(0, 8, (10_000, 9)).astype(np.int32)
+    modes = np.stack([rng.integers(0, 8, 9).astype(np.int32) for _ in range(200)])
+    lab, *_ = O.assign_generic(lambda a, b: O.cat_distances(codes[a:b], modes), 10_000, 200)
+    for _ in range(2):
+        modes = O.modes_from_labels(codes, 8, lab, modes.shape[0])
+        lab, _, radii, obj = O.assign_generic(lambda a, b: O.cat_distances(codes[a:b], modes), 10_000,
+                                              modes.shape[0])
+    assert np.array_equal(modes, arr["c08cat_p2_centers"])
+    assert np.array_equal(lab, arr["c08cat_p2_labels"])
+    assert np.array_equal(radii, arr["c08cat_p2_radii"])
+    assert obj == rm["c08cat_p2"]["objective"]
+
+
+def test_refine_pipeline_golden():
+    """run_pipeline(passes=2) (engine.py:464-465, :519-537) at g = 1 and 2."""
+    m = meta()["pipelines"]["small"]
+    arr, rm = npz("refine"), refine_meta()
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    for g in (1, 2):
+        out = O.pipeline_dense(X, m["m"], m["t"], m["tseed"], m["K"], m["L"], m["delta"], m["sseed"], g=g, passes=2)
+        assert np.array_equal(out["centers"], arr[f"small_p2_g{g}_centers"])
+        assert np.array_equal(out["labels"], arr[f"small_p2_g{g}_labels"])
+        assert np.array_equal(out["radii"], arr[f"small_p2_g{g}_radii"])
+        assert out["objective"] == rm[f"small_p2_g{g}"]["objective"]
