@@ -304,6 +304,15 @@ int geek_label_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, 
                              const int64_t* labels, uint64_t k, uint64_t universe, int64_t* counts,
                              void* stream);
 
+/* ---- ingestion (io.py:21-48) -------------------------------------------- */
+
+/* Strip nrec .fvecs (elem_bytes 4) / .bvecs (elem_bytes 1) records of
+ * dimension d from device memory `raw` into float32 out[nrec][d];
+ * *bad_rec (device, caller-initialised to UINT64_MAX) is lowered to the
+ * first record whose 4-byte prefix is not d.  ASYNC.                       */
+int geek_unpack_vecs(const void* raw, uint64_t nrec, int d, int elem_bytes, float* out, uint64_t* bad_rec,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

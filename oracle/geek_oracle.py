@@ -506,6 +506,31 @@ def sparse_modes_from_labels(sets, universe: int, labels: np.ndarray, k: int) ->
 
 
 # --------------------------------------------------------------------------
+# vector files (io.py:21-48)
+
+def read_vecs(raw: bytes, bvecs: bool):
+    """Parse .fvecs / .bvecs bytes -> float64 [n][d], or the reference's
+    FormatError message as a string (io.py:21-48)."""
+    raw = np.frombuffer(raw, dtype=np.uint8)
+    if raw.size == 0:
+        return np.empty((0, 0))
+    if raw.size < 4:
+        return "truncated record at byte 0"
+    d = int(raw[:4].view("<i4")[0])
+    if d <= 0:
+        return "non-positive dimension at byte 0"
+    dt = np.dtype("<u1") if bvecs else np.dtype("<f4")
+    record = 4 + d * dt.itemsize
+    if raw.size % record:
+        return f"truncated record at byte {(raw.size // record) * record}"
+    table = raw.reshape(-1, record)
+    dims = table[:, :4].copy().view("<i4").ravel()
+    if (dims != d).any():
+        return f"inconsistent dimension at byte {int(np.flatnonzero(dims != d)[0]) * record}"
+    return table[:, 4:].copy().view(dt).astype(np.float64)
+
+
+# --------------------------------------------------------------------------
 # synthetic data (synth.py:39-104), used to make parity inputs
 
 def spread_means(k, dim, separation, rng):

@@ -7,3 +7,7 @@ class InvalidInput(ValueError):
 
 class EngineError(RuntimeError):
     """A pipeline stage or device call failed; the message names the stage."""
+
+
+class FormatError(ValueError):
+    """Malformed or truncated file payload (serialize.py:28)."""

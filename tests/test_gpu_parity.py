@@ -598,3 +598,41 @@ def test_refine_pipeline_c06_sparse_mixed_golden():
                            minhash=G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16),
                            seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9), passes=2)
     _check_refined(G.run_pipeline(data, cfg).clustering, arr, rm, "mx_p2_g1")
+
+
+# ---- vector-file ingestion (io.py:21-62) ------------------------------------
+
+@pytest.mark.parametrize("ext", ["fvecs", "bvecs"])
+def test_read_vecs_golden_and_errors(ext, tmp_path):
+    from paper_2106_10515_b200.io import FormatError, read_fvecs
+    from tests.golden_io import GOLDEN
+    import os
+    got = read_fvecs(os.path.join(GOLDEN, f"io_small.{ext}"))
+    assert got.vectors.is_cuda and got.vectors.dtype == torch.float32
+    assert np.array_equal(got.host_f64(), npz("io")[ext])
+    # many chunks (a few records each), errors past the first chunk
+    rng = np.random.default_rng(3)
+    n, d = 1001, 13
+    elem, dt = (1, "<u1") if ext == "bvecs" else (4, "<f4")
+    body = (rng.integers(0, 256, (n, d)) if ext == "bvecs" else rng.standard_normal((n, d))).astype(dt)
+    rec = np.empty((n, 4 + d * elem), np.uint8)
+    rec[:, :4] = np.frombuffer(np.int32(d).tobytes(), np.uint8)
+    rec[:, 4:] = body.view(np.uint8).reshape(n, -1)
+    cases = {"ok": rec.tobytes(), "trunc": rec.tobytes()[:-3], "short": b"\x01\x00",
+             "nonpos": np.int32(-2).tobytes() + rec.tobytes()[4:], "empty": b""}
+    bad = rec.copy()
+    bad[777, :4] = np.frombuffer(np.int32(d + 1).tobytes(), np.uint8)
+    bad[901, :4] = 0
+    cases["inconsistent"] = bad.tobytes()
+    for name, raw in cases.items():
+        p = tmp_path / f"{name}.{ext}"
+        p.write_bytes(raw)
+        want = O.read_vecs(raw, ext == "bvecs")
+        if isinstance(want, str):
+            with pytest.raises(FormatError, match=want):
+                read_fvecs(p, chunk_bytes=40 * (4 + d * elem))
+        else:
+            out = read_fvecs(p, chunk_bytes=40 * (4 + d * elem))
+            assert out.n == want.shape[0]
+            if want.size:
+                assert np.array_equal(out.host_f64(), want)

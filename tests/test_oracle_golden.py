@@ -190,3 +190,20 @@ def test_refine_pipeline_golden():
         assert np.array_equal(out["labels"], arr[f"small_p2_g{g}_labels"])
         assert np.array_equal(out["radii"], arr[f"small_p2_g{g}_radii"])
         assert out["objective"] == rm[f"small_p2_g{g}"]["objective"]
+
+
+@pytest.mark.parametrize("ext", ["fvecs", "bvecs"])
+def test_vector_files_golden(ext, tmp_path):
+    """Oracle reader against the reference's read_fvecs output; the package's
+    (host-side) writer is byte-identical to the reference's write_fvecs."""
+    import os
+    from tests.golden_io import GOLDEN
+    arr = npz("io")
+    path = os.path.join(GOLDEN, f"io_small.{ext}")
+    raw = open(path, "rb").read()
+    assert np.array_equal(O.read_vecs(raw, ext == "bvecs"), arr[ext])
+    from paper_2106_10515_b200.io import write_fvecs
+    from paper_2106_10515_b200.data import DenseData
+    out = tmp_path / f"w.{ext}"
+    write_fvecs(out, DenseData(arr["src"]))
+    assert out.read_bytes() == raw
