@@ -289,9 +289,11 @@ int geek_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, uint64
 /* Exact digit column sums keyed by label: digits[(labels[i]*d + c)*nd + q]
  * += row i's column c in base-2^32 digits relative to 2^emin (the
  * geek_exact_sums representation; ADDED to, so shards reduce by addition).
- * Rows stream once, coalesced; labels outside [0, k) are skipped.  ASYNC.   */
-int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64_t* labels, uint64_t k,
-                    int emin, int nd, int64_t* digits, void* stream);
+ * Rows stream once in storage order (order NULL) or in the order of the row
+ * permutation `order` (e.g. sorted by label, so equal labels form register
+ * runs); labels outside [0, k) are skipped.  ASYNC.                         */
+int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64_t* labels,
+                    const int64_t* order, uint64_t k, int emin, int nd, int64_t* digits, void* stream);
 
 /* counts[(labels[i]*d + c)*cs + codes[i*d + c]] += 1 (categorical modes of
  * the current clusters, assignment.py:122-126).  ASYNC.                      */

@@ -81,7 +81,7 @@ _SIGS = {
     "geek_doph_reduce": (i32, [vp, vp, vp, vp, u64, u64, u64, vp, vp, vp, vp]),
     "geek_mode_counts": (i32, [vp, u64, i32, u64, u64, vp, vp, u64, vp, vp]),
     "geek_sparse_counts": (i32, [vp, vp, u64, u64, u64, vp, vp, u64, vp, vp]),
-    "geek_label_sums": (i32, [vp, i32, u64, i32, vp, u64, i32, i32, vp, vp]),
+    "geek_label_sums": (i32, [vp, i32, u64, i32, vp, vp, u64, i32, i32, vp, vp]),
     "geek_label_mode_counts": (i32, [vp, u64, i32, vp, u64, u64, vp, vp]),
     "geek_label_sparse_counts": (i32, [vp, vp, u64, vp, u64, u64, vp, vp]),
     "geek_unpack_vecs": (i32, [vp, u64, i32, i32, vp, vp, vp]),

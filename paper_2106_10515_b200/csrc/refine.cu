@@ -7,7 +7,9 @@
 //   * label_sums: exact base-2^32 digit column sums (the K7 representation,
 //     centers.cu), accumulated in registers while consecutive rows share a
 //     label and flushed with integer atomics when it changes -- exact and
-//     order-free, so any shard split / launch shape gives the same digits;
+//     order-free, so any shard split / launch shape gives the same digits.
+//     Rows are visited in storage order, or through a label-sorted row
+//     permutation when the labels change too often for register runs;
 //   * label_mode_counts: per (cluster, attribute, code) counts (categorical
 //     modes, seeding.py:180-185);
 //   * label_sparse_counts: per (cluster, element) membership counts (sparse
@@ -40,9 +42,25 @@ __device__ __forceinline__ bool split_bits(double v, long long& M, int& L) {
 }
 
 constexpr int kRunRows = 256;  // rows per block-chunk
+constexpr int kPrefetch = 8;   // row values loaded ahead per thread
+
+// Lanes acc[q] hold sums of (M << rb) placed at digit q (weight 2^(32q)); a
+// float32 term is < 2^56 in magnitude, so a lane absorbs 64 terms before it
+// is carried down into 32-bit digits (normalise) -- 1 select-add per lane
+// per term instead of splitting every term into three digits.
+template <int ND>
+__device__ __forceinline__ void normalise(long long (&acc)[ND]) {
+#pragma unroll
+  for (int q = 0; q + 1 < ND; ++q) {
+    const long long c = acc[q] >> 32;  // floor
+    acc[q] -= c * 4294967296ll;        // now in [0, 2^32)
+    acc[q + 1] += c;
+  }
+}
 
 template <int ND>
 __device__ __forceinline__ void flush_digits(long long (&acc)[ND], long long* dst) {
+  normalise<ND>(acc);
 #pragma unroll
   for (int q = 0; q < ND; ++q) {
     if (acc[q]) atomicAdd(reinterpret_cast<unsigned long long*>(dst + q), (unsigned long long)acc[q]);
@@ -51,41 +69,72 @@ __device__ __forceinline__ void flush_digits(long long (&acc)[ND], long long* ds
 }
 
 template <class T, int ND>
+__device__ __forceinline__ void add_term(long long (&acc)[ND], T v, int emin) {
+  long long M;
+  int L;
+  if (!split_bits(v, M, L)) return;
+  const int sh = L - emin;  // >= 0
+  const int q0 = sh >> 5, rb = sh & 31;
+  if (sizeof(T) == 4) {  // |M << rb| < 2^56: one lane
+    const long long w = M * (1ll << rb);
+#pragma unroll
+    for (int q = 0; q < ND; ++q) acc[q] += (q == q0) ? w : 0ll;
+  } else {  // |M| < 2^53: low 32 bits of M << rb at q0, the rest (< 2^53 in magnitude) at q0 + 1
+    const long long lo = (long long)(((unsigned long long)M << rb) & 0xFFFFFFFFull);
+    const long long hi = (long long)(((__int128)M << rb) >> 32);
+#pragma unroll
+    for (int q = 0; q < ND; ++q) acc[q] += (q == q0) ? lo : ((q == q0 + 1) ? hi : 0ll);
+  }
+}
+
+// rows r0..r0+rows of the (optionally permuted) row order; labels are read
+// through the same order so a sorted permutation gives long label runs
+template <class T, int ND>
 __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X, uint64_t nrows, int d,
-                                                         const int64_t* __restrict__ labels, uint64_t k,
+                                                         const int64_t* __restrict__ labels,
+                                                         const int64_t* __restrict__ order, uint64_t k,
                                                          int emin, long long* __restrict__ digits) {
   __shared__ int64_t lab[kRunRows];
+  __shared__ int64_t row[kRunRows];
   const uint64_t nchunks = (nrows + kRunRows - 1) / kRunRows;
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const uint64_t r0 = ch * kRunRows;
     const int rows = (int)min((uint64_t)kRunRows, nrows - r0);
     __syncthreads();
-    for (int r = threadIdx.x; r < rows; r += blockDim.x) lab[r] = labels[r0 + r];
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const int64_t i = order ? order[r0 + r] : (int64_t)(r0 + r);
+      const int64_t l = labels[i];
+      row[r] = i;
+      lab[r] = (l >= 0 && (uint64_t)l < k) ? l : -1;
+    }
     __syncthreads();
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       long long acc[ND];
 #pragma unroll
       for (int q = 0; q < ND; ++q) acc[q] = 0;
       int64_t cur = -1;
-      const T* col = X + r0 * (uint64_t)d + c;
-      for (int r = 0; r < rows; ++r) {
-        const int64_t l = lab[r];
-        if (l != cur) {
-          if (cur >= 0) flush_digits<ND>(acc, digits + ((uint64_t)cur * d + c) * ND);
-          cur = (l >= 0 && (uint64_t)l < k) ? l : -1;
-        }
-        long long M;
-        int L;
-        const T v = col[(uint64_t)r * d];
-        if (cur < 0 || !split_bits(v, M, L)) continue;
-        const int sh = L - emin;  // >= 0
-        const int q0 = sh >> 5, rb = sh & 31;
-        const __int128 w = (__int128)M << rb;
-        const long long d0 = (long long)(uint32_t)(w & 0xFFFFFFFF);
-        const long long d1 = (long long)(uint32_t)((w >> 32) & 0xFFFFFFFF);
-        const long long d2 = (long long)(w >> 64);
+      int since = 0;  // terms since the last normalisation
+      for (int rb = 0; rb < rows; rb += kPrefetch) {
+        T v[kPrefetch];
 #pragma unroll
-        for (int q = 0; q < ND; ++q) acc[q] += (q == q0) * d0 + (q == q0 + 1) * d1 + (q == q0 + 2) * d2;
+        for (int u = 0; u < kPrefetch; ++u)
+          v[u] = (rb + u < rows) ? X[(uint64_t)row[rb + u] * d + c] : T(0);
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+          if (rb + u >= rows) break;
+          const int64_t l = lab[rb + u];
+          if (l != cur) {
+            if (cur >= 0) flush_digits<ND>(acc, digits + ((uint64_t)cur * d + c) * ND);
+            cur = l;
+            since = 0;
+          }
+          if (cur < 0) continue;
+          add_term<T, ND>(acc, v[u], emin);
+          if (++since == 64) {
+            normalise<ND>(acc);
+            since = 0;
+          }
+        }
       }
       if (cur >= 0) flush_digits<ND>(acc, digits + ((uint64_t)cur * d + c) * ND);
     }
@@ -126,12 +175,12 @@ __global__ void label_sparse_counts_kernel(const uint32_t* __restrict__ set_flat
 }
 
 template <class T, int ND>
-static void launch_label_sums(const void* X, uint64_t nrows, int d, const int64_t* labels, uint64_t k, int emin,
-                              long long* digits, cudaStream_t s) {
+static void launch_label_sums(const void* X, uint64_t nrows, int d, const int64_t* labels, const int64_t* order,
+                              uint64_t k, int emin, long long* digits, cudaStream_t s) {
   const int threads = d >= 128 ? 128 : 32 * ((d + 31) / 32);
   const uint64_t nchunks = (nrows + kRunRows - 1) / kRunRows;
-  label_sums_kernel<T, ND><<<grid_for(nchunks, 1, 148 * 16), threads, 0, s>>>((const T*)X, nrows, d, labels, k,
-                                                                              emin, digits);
+  label_sums_kernel<T, ND><<<grid_for(nchunks, 1, 148 * 16), threads, 0, s>>>((const T*)X, nrows, d, labels,
+                                                                              order, k, emin, digits);
 }
 
 }  // namespace geek
@@ -140,8 +189,8 @@ using namespace geek;
 
 extern "C" {
 
-int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64_t* labels, uint64_t k, int emin,
-                    int nd, int64_t* digits, void* stream) {
+int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64_t* labels, const int64_t* order,
+                    uint64_t k, int emin, int nd, int64_t* digits, void* stream) {
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 or 1");
   GEEK_REQUIRE(d > 0, "d must be positive");
@@ -151,9 +200,9 @@ int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64
 #define GEEK_LSUMS_CASE(NDV)                                                          \
   case NDV:                                                                           \
     if (dtype == 0)                                                                   \
-      launch_label_sums<float, NDV>(X, nrows, d, labels, k, emin, dg, s);             \
+      launch_label_sums<float, NDV>(X, nrows, d, labels, order, k, emin, dg, s);             \
     else                                                                              \
-      launch_label_sums<double, NDV>(X, nrows, d, labels, k, emin, dg, s);            \
+      launch_label_sums<double, NDV>(X, nrows, d, labels, order, k, emin, dg, s);            \
     break;
   switch (nd) {
     GEEK_LSUMS_CASE(3)

@@ -95,14 +95,24 @@ def sparse_centers(data: SparseData, groups: GroupSet) -> torch.Tensor:
 
 # ---- refinement: statistics keyed by the current labels (assignment.py:110-137) ----
 
-def label_sums(X: torch.Tensor, labels: torch.Tensor, k: int, emin: int, nd: int) -> torch.Tensor:
+_SORT_RUNS = 8  # mean label-run length below which rows are visited in label order
+
+
+def label_sums(X: torch.Tensor, labels: torch.Tensor, k: int, emin: int, nd: int, order=None) -> torch.Tensor:
     """int64 [k, d, nd] exact digit sums of the rows with each label (one
-    coalesced pass over X; shards add their partials exactly)."""
-    d = X.shape[1]
+    pass over X; shards add their partials exactly).  Rows stream in storage
+    order while labels come in runs (cluster-ordered data); otherwise through
+    a stable label sort, so every run flushes once instead of once per row."""
+    n, d = X.shape
+    labels = labels.contiguous()
     digits = _lib.zeros(max(1, k * d * nd), torch.int64)
-    if k and X.shape[0]:
-        _lib.call("geek_label_sums", _lib.ptr(X), _lib.dtype_code(X), X.shape[0], d, _lib.ptr(labels.contiguous()),
-                  k, emin, nd, _lib.ptr(digits), _lib.stream())
+    if k and n:
+        if order is None and n > 1:
+            changes = int((labels[1:] != labels[:-1]).sum().item())
+            if changes * _SORT_RUNS > n:
+                order = torch.sort(labels, stable=True).indices
+        _lib.call("geek_label_sums", _lib.ptr(X), _lib.dtype_code(X), n, d, _lib.ptr(labels),
+                  _lib.ptr(order), k, emin, nd, _lib.ptr(digits), _lib.stream())
     return digits[: k * d * nd].view(k, d, nd)
 
 

@@ -535,7 +535,8 @@ def test_refine_c08_golden():
     _check_refined(G.refine(cat, c0, "jaccard", 2), arr, rm, "c08cat_p2")
 
 
-def test_refine_label_sums_ragged():
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_refine_label_sums_ragged(dtype):
     """Label-keyed exact sums equal the member-list sums (geek_exact_sums) on
     shuffled labels, a float32 input, coordinates over many binades, d not a
     multiple of 32 and an empty cluster."""
@@ -543,18 +544,21 @@ def test_refine_label_sums_ragged():
     from paper_2106_10515_b200.tables import GroupSet
     rng = np.random.default_rng(5)
     n, d, k = 4099, 45, 37
-    X = (rng.standard_normal((n, d)) * np.exp2(rng.integers(-30, 30, (n, d)))).astype(np.float32)
+    X = (rng.standard_normal((n, d)) * np.exp2(rng.integers(-30, 30, (n, d)))).astype(dtype)
     X[rng.random((n, d)) < 0.05] = 0.0
     lab = rng.integers(0, k, n)
     lab[lab == 7] = 8  # cluster 7 empty
     Xd = _lib.to_dev(X)
     emin, emax = numeric.exponent_range(Xd)
     nd = numeric.digit_count(emin, emax)
-    got = numeric.label_sums(Xd, _lib.to_dev(lab.astype(np.int64)), k, emin, nd)
+    labd = _lib.to_dev(lab.astype(np.int64))
+    got = numeric.label_sums(Xd, labd, k, emin, nd)  # short runs: label-sorted row order
     want = numeric.partial_sums(Xd, GroupSet.from_host([np.flatnonzero(lab == j) for j in range(k)]), emin, nd)
+    storage = numeric.label_sums(Xd, labd, k, emin, nd, order=torch.arange(n, device=labd.device))
+    C0 = numeric.round_means(storage, torch.bincount(labd, minlength=k), emin, nd).cpu().numpy()
     C1 = numeric.round_means(got, torch.bincount(_lib.to_dev(lab), minlength=k), emin, nd).cpu().numpy()
     C2 = numeric.round_means(want, torch.bincount(_lib.to_dev(lab), minlength=k), emin, nd).cpu().numpy()
-    assert np.array_equal(C1, C2)
+    assert np.array_equal(C1, C2) and np.array_equal(C0, C2)
     for j in (0, 13, 36):
         assert np.array_equal(C1[j], O.exact_mean(X[lab == j].astype(np.float64)))
 
