@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
                                                          const int64_t* __restrict__ labels,
                                                          const int64_t* __restrict__ order, uint64_t k,
                                                          int emin, long long* __restrict__ digits) {
-  __shared__ int64_t lab[kRunRows];
-  __shared__ int64_t row[kRunRows];
+  __shared__ int32_t lab[kRunRows];
+  __shared__ uint64_t row[kRunRows];  // element offset of the row in X
   const uint64_t nchunks = (nrows + kRunRows - 1) / kRunRows;
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const uint64_t r0 = ch * kRunRows;
@@ -104,25 +104,25 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
     for (int r = threadIdx.x; r < rows; r += blockDim.x) {
       const int64_t i = order ? order[r0 + r] : (int64_t)(r0 + r);
       const int64_t l = labels[i];
-      row[r] = i;
-      lab[r] = (l >= 0 && (uint64_t)l < k) ? l : -1;
+      row[r] = (uint64_t)i * d;
+      lab[r] = (l >= 0 && (uint64_t)l < k) ? (int32_t)l : -1;
     }
     __syncthreads();
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       long long acc[ND];
 #pragma unroll
       for (int q = 0; q < ND; ++q) acc[q] = 0;
-      int64_t cur = -1;
+      int32_t cur = -1;
       int since = 0;  // terms since the last normalisation
       for (int rb = 0; rb < rows; rb += kPrefetch) {
         T v[kPrefetch];
 #pragma unroll
         for (int u = 0; u < kPrefetch; ++u)
-          v[u] = (rb + u < rows) ? X[(uint64_t)row[rb + u] * d + c] : T(0);
+          v[u] = (rb + u < rows) ? X[row[rb + u] + c] : T(0);
 #pragma unroll
         for (int u = 0; u < kPrefetch; ++u) {
           if (rb + u >= rows) break;
-          const int64_t l = lab[rb + u];
+          const int32_t l = lab[rb + u];
           if (l != cur) {
             if (cur >= 0) flush_digits<ND>(acc, digits + ((uint64_t)cur * d + c) * ND);
             cur = l;
@@ -194,6 +194,7 @@ int geek_label_sums(const void* X, int dtype, uint64_t nrows, int d, const int64
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 or 1");
   GEEK_REQUIRE(d > 0, "d must be positive");
+  GEEK_REQUIRE(k < (1ull << 31), "k = %llu clusters exceeds the 31-bit label range", (unsigned long long)k);
   GEEK_REQUIRE(nd >= 3 && nd <= 40, "digit count %d outside [3, 40]", nd);
   if (nrows == 0 || k == 0) return GEEK_OK;
   long long* dg = reinterpret_cast<long long*>(digits);
