@@ -506,6 +506,48 @@ def sparse_modes_from_labels(sets, universe: int, labels: np.ndarray, k: int) ->
 
 
 # --------------------------------------------------------------------------
+# comparison methods (baselines.py:34-136), dense Euclidean
+
+def seed_random_idx(n: int, k: int, seed: int) -> np.ndarray:
+    return np.random.default_rng(seed).choice(n, size=k, replace=False)
+
+
+def kmeanspp_idx(X: np.ndarray, k: int, seed: int) -> list:
+    """baselines.py:52-80 with the Euclidean weights best**2."""
+    rng = np.random.default_rng(seed)
+    n = X.shape[0]
+    chosen = [int(rng.integers(n))]
+    best = None
+    while len(chosen) < k:
+        d_new = l2_distances(X, X[chosen[-1]][None, :])[:, 0]
+        best = d_new if best is None else np.minimum(best, d_new)
+        w = best ** 2
+        w[chosen] = 0.0
+        total = w.sum()
+        if total <= 0.0:
+            chosen.append(int(rng.choice(np.setdiff1d(np.arange(n), np.array(chosen)))))
+        else:
+            chosen.append(int(rng.choice(n, p=w / total)))
+    return chosen
+
+
+def lloyd_dense(X: np.ndarray, k: int, seed: int, max_iters: int = 100, tol: float = 1e-6):
+    """baselines.py:83-114 -> dict(centers, labels, radii, objective)."""
+    X = np.asarray(X, dtype=np.float64)
+    C = X[seed_random_idx(X.shape[0], k, seed)]
+    lab, best, radii, obj = assign_l2(X, C)
+    for _ in range(max_iters):
+        newC, _ = centers_from_labels(X, lab, C.shape[0])
+        alive = np.bincount(lab, minlength=C.shape[0]) > 0
+        moved = max((float(np.linalg.norm(a - b)) for a, b in zip(C[alive], newC)), default=0.0)
+        C = newC
+        lab, best, radii, obj = assign_l2(X, C)
+        if moved < tol:
+            break
+    return dict(centers=C, labels=lab, radii=radii, objective=obj)
+
+
+# --------------------------------------------------------------------------
 # vector files (io.py:21-48)
 
 def read_vecs(raw: bytes, bvecs: bool):

@@ -28,3 +28,8 @@ def csr(flat, off):
 def refine_meta():
     with open(os.path.join(GOLDEN, "refine.json")) as f:
         return json.load(f)
+
+
+def baselines_meta():
+    with open(os.path.join(GOLDEN, "baselines.json")) as f:
+        return json.load(f)

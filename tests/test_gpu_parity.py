@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle import geek_oracle as O
-from tests.golden_io import csr, groups as golden_groups, meta, npz, refine_meta
+from tests.golden_io import baselines_meta, csr, groups as golden_groups, meta, npz, refine_meta
 
 pytestmark = pytest.mark.gpu
 
@@ -640,3 +640,33 @@ def test_read_vecs_golden_and_errors(ext, tmp_path):
             assert out.n == want.shape[0]
             if want.size:
                 assert np.array_equal(out.host_f64(), want)
+
+
+# ---- comparison methods (baselines.py:34-136) -------------------------------
+
+def test_baselines_golden():
+    from paper_2106_10515_b200 import baselines as B
+    arr, bm = npz("baselines"), baselines_meta()
+    X, _ = O.gaussian_mixture(2000, 16, 10, 6.0, 5)
+    dense = G.DenseData(X)
+    rng = np.random.default_rng(12)
+    cat = G.CategoricalData(rng.integers(0, 5, (1500, 7)).astype(np.int32), code_space=5)
+    sp = G.SparseData(csr(arr["sp_flat"], arr["sp_off"]), bm["sp_universe"])
+
+    def vals(cs):
+        return np.stack([c.values for c in cs])
+
+    assert np.array_equal(vals(B.seed_random(dense, 12, 3)), arr["rand_dense"])
+    assert np.array_equal(vals(B.seed_kmeanspp(dense, 12, 4)), arr["pp_dense"])
+    assert np.array_equal(vals(B.seed_kmeanspp(cat, 9, 5, metric="jaccard")), arr["pp_cat"])
+    assert np.array_equal(vals(B.seed_kmeanspp(sp, 7, 6, metric="jaccard")), arr["pp_sparse"])
+    for name, cl in (("lloyd", B.lloyd(dense, 12, 7)), ("lloyd_2it", B.lloyd(dense, 12, 7, max_iters=2)),
+                     ("kmodes_cat", B.kmodes(cat, 9, 8)), ("kmodes_sparse", B.kmodes(sp, 7, 9))):
+        assert np.array_equal(vals(cl.centers), arr[f"{name}_centers"]), name
+        assert np.array_equal(cl.assignment, arr[f"{name}_labels"]), name
+        assert np.array_equal(cl.radii, arr[f"{name}_radii"]), name
+        assert cl.objective == bm[name]["objective"], name
+    with pytest.raises(G.InvalidInput):
+        B.seed_random(dense, 2001, 0)
+    with pytest.raises(G.InvalidInput):
+        B.kmodes(dense, 3, 0)

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import geek_oracle as O
-from tests.golden_io import csr, groups, meta, npz, refine_meta
+from tests.golden_io import baselines_meta, csr, groups, meta, npz, refine_meta
 
 WORKED = [  # pkg/tests/conftest.py:23-41
     (0, 0, [0, 1, 3]), (0, 1, [2, 4, 5]), (1, 0, [0, 1, 3, 4]), (1, 1, [5]),
@@ -207,3 +207,17 @@ def test_vector_files_golden(ext, tmp_path):
     out = tmp_path / f"w.{ext}"
     write_fvecs(out, DenseData(arr["src"]))
     assert out.read_bytes() == raw
+
+
+def test_baselines_dense_golden():
+    """k-means++ picks and Lloyd (baselines.py:52-114) against the reference's outputs."""
+    arr, bm = npz("baselines"), baselines_meta()
+    X, _ = O.gaussian_mixture(2000, 16, 10, 6.0, 5)
+    assert np.array_equal(X[O.seed_random_idx(2000, 12, 3)], arr["rand_dense"])
+    assert np.array_equal(X[O.kmeanspp_idx(X, 12, 4)], arr["pp_dense"])
+    for name, it in (("lloyd", 100), ("lloyd_2it", 2)):
+        out = O.lloyd_dense(X, 12, 7, max_iters=it)
+        assert np.array_equal(out["centers"], arr[f"{name}_centers"])
+        assert np.array_equal(out["labels"], arr[f"{name}_labels"])
+        assert np.array_equal(out["radii"], arr[f"{name}_radii"])
+        assert out["objective"] == bm[name]["objective"]

@@ -16,7 +16,7 @@ import torch.distributed as dist  # noqa: E402
 
 import paper_2106_10515_b200 as G  # noqa: E402
 from oracle import geek_oracle as O  # noqa: E402
-from tests.golden_io import groups as golden_groups, meta, npz  # noqa: E402
+from tests.golden_io import groups as golden_groups, meta, npz, refine_meta  # noqa: E402
 
 
 def main():
@@ -75,6 +75,35 @@ def main():
                 print(f"[G={world}] {name} f32 g={g}: {'OK' if good else 'MISMATCH'} groups={len(got)} "
                       f"bytes={out.transport_bytes} warnings={out.warnings if hasattr(out, 'warnings') else ''}",
                       flush=True)
+    # refinement passes across ranks (engine.py:519-537): label-keyed digit
+    # sums all-reduced, against the reference's run_pipeline(passes=2)
+    rarr, rmeta = npz("refine"), refine_meta()
+    m = meta()["pipelines"]["small"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    for g in (1, 2):
+        if g % world:
+            continue
+        for x in (X, X.astype(np.float32)):
+            cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(g),
+                                   homo=G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]),
+                                   seeding=G.SeedingParams(m["K"], m["L"], min_group_size=m["delta"],
+                                                           seed=m["sseed"]), passes=2)
+            cl = G.run_pipeline(G.DenseData(x), cfg).clustering
+            if x.dtype == np.float32:
+                ref = O.pipeline_dense(x.astype(np.float64), m["m"], m["t"], m["tseed"], m["K"], m["L"],
+                                       m["delta"], m["sseed"], g=g, passes=2)
+                good = (np.array_equal(cl.assignment, ref["labels"]) and cl.objective == ref["objective"]
+                        and np.array_equal(np.stack([c.values for c in cl.centers]), ref["centers"]))
+            else:
+                nm = f"small_p2_g{g}"
+                good = (np.array_equal(cl.assignment, rarr[f"{nm}_labels"])
+                        and np.array_equal(cl.radii, rarr[f"{nm}_radii"])
+                        and np.array_equal(np.stack([c.values for c in cl.centers]), rarr[f"{nm}_centers"])
+                        and cl.objective == rmeta[nm]["objective"])
+            ok &= good
+            if rank == 0:
+                print(f"[G={world}] small passes=2 {x.dtype} g={g}: {'OK' if good else 'MISMATCH'}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     if not ok:
