@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
                                                          const int64_t* __restrict__ order, uint64_t k,
                                                          int emin, long long* __restrict__ digits) {
   __shared__ int32_t lab[kRunRows];
-  __shared__ uint64_t row[kRunRows];  // element offset of the row in X
+  __shared__ uint64_t row[kRunRows];            // element offset of the row in X
+  __shared__ int32_t run8[kRunRows / kPrefetch];  // label of a full 8-row group with one label, else -1
   const uint64_t nchunks = (nrows + kRunRows - 1) / kRunRows;
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const uint64_t r0 = ch * kRunRows;
@@ -106,6 +107,16 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
       const int64_t l = labels[i];
       row[r] = (uint64_t)i * d;
       lab[r] = (l >= 0 && (uint64_t)l < k) ? (int32_t)l : -1;
+    }
+    __syncthreads();
+    for (int gi = threadIdx.x; gi < kRunRows / kPrefetch; gi += blockDim.x) {
+      int32_t l = -1;
+      if ((gi + 1) * kPrefetch <= rows) {
+        l = lab[gi * kPrefetch];
+        for (int u = 1; u < kPrefetch; ++u)
+          if (lab[gi * kPrefetch + u] != l) l = -1;
+      }
+      run8[gi] = l;
     }
     __syncthreads();
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
@@ -119,7 +130,17 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
 #pragma unroll
         for (int u = 0; u < kPrefetch; ++u)
           v[u] = (rb + u < rows) ? X[row[rb + u] + c] : T(0);
+        const int32_t g8 = run8[rb / kPrefetch];
+        if (g8 >= 0 && g8 == cur) {  // inside a run: no per-row label checks
 #pragma unroll
+          for (int u = 0; u < kPrefetch; ++u) add_term<T, ND>(acc, v[u], emin);
+          since += kPrefetch;
+          if (since >= 64) {  // lanes hold < 72 terms of < 2^56 each
+            normalise<ND>(acc);
+            since = 0;
+          }
+          continue;
+        }
         for (int u = 0; u < kPrefetch; ++u) {
           if (rb + u >= rows) break;
           const int32_t l = lab[rb + u];
@@ -130,7 +151,7 @@ __global__ void __launch_bounds__(128) label_sums_kernel(const T* __restrict__ X
           }
           if (cur < 0) continue;
           add_term<T, ND>(acc, v[u], emin);
-          if (++since == 64) {
+          if (++since >= 64) {
             normalise<ND>(acc);
             since = 0;
           }
