@@ -282,6 +282,51 @@ __global__ void combine_kernel(const uint32_t* node, const uint32_t* left, const
     val[node[q]] = __dadd_rn(val[left[q]], val[right[q]]);
 }
 
+// device copy of a SumTree's index arrays (leaves; per level node/left/right)
+struct DevSumTree {
+  uint64_t* leaf_off = nullptr;
+  uint32_t* leaf_len = nullptr;
+  uint32_t* leaf_node = nullptr;
+  uint32_t* lv = nullptr;
+  std::vector<uint64_t> lv_count;
+  uint64_t nleaf = 0;
+  uint32_t nnodes = 0;
+  void* mem = nullptr;
+  DevSumTree() = default;
+  DevSumTree(const DevSumTree&) = delete;
+  DevSumTree& operator=(const DevSumTree&) = delete;
+  ~DevSumTree() {
+    if (mem) cudaFree(mem);
+  }
+  int build(const SumTree& t) {
+    nleaf = t.leaf_off.size();
+    nnodes = t.nnodes;
+    uint64_t ninternal = 0;
+    for (auto& l : t.lv_node) {
+      lv_count.push_back(l.size());
+      ninternal += l.size();
+    }
+    const uint64_t bytes = nleaf * 16 + ninternal * 12 + 16;
+    GEEK_CHECK_CUDA(cudaMalloc(&mem, bytes));
+    leaf_off = static_cast<uint64_t*>(mem);
+    leaf_len = reinterpret_cast<uint32_t*>(leaf_off + nleaf);
+    leaf_node = leaf_len + nleaf;
+    lv = leaf_node + nleaf;
+    GEEK_CHECK_CUDA(cudaMemcpy(leaf_off, t.leaf_off.data(), nleaf * 8, cudaMemcpyHostToDevice));
+    GEEK_CHECK_CUDA(cudaMemcpy(leaf_len, t.leaf_len.data(), nleaf * 4, cudaMemcpyHostToDevice));
+    GEEK_CHECK_CUDA(cudaMemcpy(leaf_node, t.leaf_node.data(), nleaf * 4, cudaMemcpyHostToDevice));
+    uint32_t* p = lv;
+    for (size_t L = 0; L < t.lv_node.size(); ++L) {
+      const uint64_t c = t.lv_node[L].size();
+      GEEK_CHECK_CUDA(cudaMemcpy(p, t.lv_node[L].data(), c * 4, cudaMemcpyHostToDevice));
+      GEEK_CHECK_CUDA(cudaMemcpy(p + c, t.lv_left[L].data(), c * 4, cudaMemcpyHostToDevice));
+      GEEK_CHECK_CUDA(cudaMemcpy(p + 2 * c, t.lv_right[L].data(), c * 4, cudaMemcpyHostToDevice));
+      p += 3 * c;
+    }
+    return GEEK_OK;
+  }
+};
+
 // ---- screened assignment (float32 data) -----------------------------------
 //
 // screen: s(x, c) = |c|^2 - 2 x.c in float32 (SIMT register-blocked GEMM,
@@ -989,47 +1034,38 @@ int geek_pairwise_sum(const double* v, uint64_t n, double* out, void* stream) {
     GEEK_CHECK_CUDA(cudaMemsetAsync(out, 0, 8, s));
     return GEEK_OK;
   }
+  // the tree's index arrays live on the device, built and uploaded once per
+  // (device, n): the per-call work is one leaf pass and one launch per level
   static std::mutex mu;
-  static std::map<uint64_t, std::shared_ptr<SumTree>> cache;
-  std::shared_ptr<SumTree> t;
+  static std::map<std::pair<int, uint64_t>, std::shared_ptr<DevSumTree>> cache;
+  int dev = 0;
+  GEEK_CHECK_CUDA(cudaGetDevice(&dev));
+  std::shared_ptr<DevSumTree> t;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(n);
+    auto it = cache.find({dev, n});
     if (it == cache.end()) {
-      t = make_tree(n);
+      GEEK_CHECK_CUDA(cudaStreamSynchronize(s));  // a cleared entry's arrays may still be in use
       if (cache.size() > 8) cache.clear();
-      cache[n] = t;
+      t = std::make_shared<DevSumTree>();
+      GEEK_TRY(t->build(*make_tree(n)));
+      cache[{dev, n}] = t;
     } else {
       t = it->second;
     }
   }
-  const uint64_t nleaf = t->leaf_off.size();
-  uint64_t ninternal = 0;
-  for (auto& l : t->lv_node) ninternal += l.size();
-  Scratch val, lf, lv;
+  Scratch val;
   GEEK_TRY(val.alloc((uint64_t)t->nnodes * 8, s));
-  GEEK_TRY(lf.alloc(nleaf * 16, s));
-  GEEK_TRY(lv.alloc(ninternal * 12 + 16, s));
-  uint64_t* loff = lf.as<uint64_t>();
-  uint32_t* llen = reinterpret_cast<uint32_t*>(loff + nleaf);
-  uint32_t* lnode = llen + nleaf;
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(loff, t->leaf_off.data(), nleaf * 8, cudaMemcpyHostToDevice, s));
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(llen, t->leaf_len.data(), nleaf * 4, cudaMemcpyHostToDevice, s));
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(lnode, t->leaf_node.data(), nleaf * 4, cudaMemcpyHostToDevice, s));
-  leaf_sum_kernel<<<grid_for(nleaf, 128), 128, 0, s>>>(v, loff, llen, lnode, nleaf, val.as<double>());
+  leaf_sum_kernel<<<grid_for(t->nleaf, 128), 128, 0, s>>>(v, t->leaf_off, t->leaf_len, t->leaf_node, t->nleaf,
+                                                          val.as<double>());
   GEEK_CHECK_LAUNCH();
-  uint32_t* base = lv.as<uint32_t>();
-  for (size_t L = 0; L < t->lv_node.size(); ++L) {
-    const uint64_t c = t->lv_node[L].size();
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(base, t->lv_node[L].data(), c * 4, cudaMemcpyHostToDevice, s));
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(base + c, t->lv_left[L].data(), c * 4, cudaMemcpyHostToDevice, s));
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(base + 2 * c, t->lv_right[L].data(), c * 4, cudaMemcpyHostToDevice, s));
+  const uint32_t* base = t->lv;
+  for (uint64_t c : t->lv_count) {
     combine_kernel<<<grid_for(c, 128), 128, 0, s>>>(base, base + c, base + 2 * c, c, val.as<double>());
     GEEK_CHECK_LAUNCH();
     base += 3 * c;
   }
   GEEK_CHECK_CUDA(cudaMemcpyAsync(out, val.as<double>(), 8, cudaMemcpyDeviceToDevice, s));
-  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));  // host plan vectors are cached; scratch freed in order
   return GEEK_OK;
 }
 
