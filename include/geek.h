@@ -315,6 +315,16 @@ int geek_label_sparse_counts(const uint32_t* set_flat, const uint64_t* set_off, 
 int geek_unpack_vecs(const void* raw, uint64_t nrec, int d, int elem_bytes, float* out, uint64_t* bad_rec,
                      void* stream);
 
+/* ---- artifacts (serialize.py:129-162) ------------------------------------ */
+
+/* Byte image of lshclust.serialize.dump_buckets' bucket records at out + base:
+ * bucket b (table t with table_off[t] <= b < table_off[t+1], slot b -
+ * table_off[t]) takes 34 + 8*size bytes starting at base + 34*b + 8*offsets[b]
+ * (<q table><q slot><q length><B 1><B 1><q size> + int64 ids, little-endian).
+ * table_off is a device array of ntables+1 entries.  ASYNC.                  */
+int geek_pack_buckets(const uint32_t* flat, const uint64_t* offsets, const uint64_t* table_off, int ntables,
+                      uint64_t nbuckets, uint64_t base, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

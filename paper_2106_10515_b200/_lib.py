@@ -85,6 +85,7 @@ _SIGS = {
     "geek_label_mode_counts": (i32, [vp, u64, i32, vp, u64, u64, vp, vp]),
     "geek_label_sparse_counts": (i32, [vp, vp, u64, vp, u64, u64, vp, vp]),
     "geek_unpack_vecs": (i32, [vp, u64, i32, i32, vp, vp, vp]),
+    "geek_pack_buckets": (i32, [vp, vp, vp, i32, u64, u64, vp, vp]),
 }
 
 _lock = threading.Lock()

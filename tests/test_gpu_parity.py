@@ -670,3 +670,29 @@ def test_baselines_golden():
         B.seed_random(dense, 2001, 0)
     with pytest.raises(G.InvalidInput):
         B.kmodes(dense, 3, 0)
+
+
+# ---- LSHC v1 artifacts (serialize.py:129-198) --------------------------------
+
+def test_artifacts_byte_identical():
+    """dump_buckets of a device BucketTable (geek_pack_buckets), seed groups
+    and clustering of the 'small' case equal the reference's files byte for
+    byte (sha256 in tests/golden/artifacts.json)."""
+    import hashlib
+    import json
+    import os
+    from tests.golden_io import GOLDEN
+    from paper_2106_10515_b200 import serialize as S
+    want = json.load(open(os.path.join(GOLDEN, "artifacts.json")))
+    m = meta()["pipelines"]["small"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    bt = G.transform_homo(G.DenseData(X), G.HomoTransformParams(8, 30, seed=1))
+    raw = S.dump_buckets(bt)
+    assert hashlib.sha256(raw).hexdigest() == want["small_buckets"]["sha256"]
+    assert raw == S.dump_buckets(list(bt))  # device packing == host packing
+    back = S.load_buckets(raw)
+    assert [(b.table, b.slot) for b in back] == [(b.table, b.slot) for b in bt]
+    out = G.run_pipeline(G.DenseData(X), dense_config(m, 2))
+    assert hashlib.sha256(S.dump_seed_groups(out.seed_groups)).hexdigest() == want["small_groups"]["sha256"]
+    assert hashlib.sha256(S.dump_clustering(out.clustering)).hexdigest() == want["small_clustering"]["sha256"]

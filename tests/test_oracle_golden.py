@@ -221,3 +221,24 @@ def test_baselines_dense_golden():
         assert np.array_equal(out["labels"], arr[f"{name}_labels"])
         assert np.array_equal(out["radii"], arr[f"{name}_radii"])
         assert out["objective"] == bm[name]["objective"]
+
+
+def test_artifacts_reference_files_roundtrip():
+    """LSHC v1 files written by the reference load with the package's readers
+    and re-dump byte-identically (host-side packing; serialize.py:129-198)."""
+    import os
+    from tests.golden_io import GOLDEN
+    from paper_2106_10515_b200 import serialize as S
+    raw = {n: open(os.path.join(GOLDEN, f"art_{n}.lshc"), "rb").read() for n in ("buckets", "groups", "clustering")}
+    bk = S.load_buckets(raw["buckets"])
+    assert [(b.table, b.slot, b.members.tolist()) for b in bk] == [(t, s_, m) for t, s_, m in WORKED]
+    assert S.dump_buckets(bk) == raw["buckets"]
+    assert S.dump_seed_groups(S.load_seed_groups(raw["groups"])) == raw["groups"]
+    cl = S.load_clustering(raw["clustering"])
+    assert S.dump_clustering(cl) == raw["clustering"]
+    with pytest.raises(S.FormatError, match="bad magic"):
+        S.load_buckets(b"XXXX" + raw["buckets"][4:])
+    with pytest.raises(S.FormatError, match="expected 1"):
+        S.load_buckets(raw["groups"])
+    with pytest.raises(S.FormatError, match="truncated"):
+        S.load_buckets(raw["buckets"][:-5])
