@@ -129,6 +129,160 @@ __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restr
   }
 }
 
+// Exact assignment for wide rows (d > 128, where neither screen applies):
+// one thread per center, kCtP points of the block in SMEM (as float64), the
+// centers transposed (ct[j*kpad + c]) so a warp's center loads coalesce and
+// each center value is loaded once for the kCtP points.  Every distance is
+// the same float64 pairwise-ordered sum as assign_l2_kernel (same plan,
+// same rounding steps); the argmin over centers is a lexicographic
+// (distance, index) minimum -- numpy's first-index rule.
+constexpr int kCtThreads = 128;
+constexpr int kCtP = 4;
+
+template <int P>
+__device__ __forceinline__ void ct_leaf(const double* xs, int d, const double* __restrict__ ct, uint64_t kpad,
+                                        uint64_t c, int off, int n, double (&res)[P]) {
+  auto sq = [&](int p, int j, double cj) {
+    const double df = __dsub_rn(xs[p * d + j], cj);
+    return __dmul_rn(df, df);
+  };
+  if (n < 8) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) res[p] = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double cj = ct[(uint64_t)(off + i) * kpad + c];
+#pragma unroll
+      for (int p = 0; p < P; ++p) res[p] = __dadd_rn(res[p], sq(p, off + i, cj));
+    }
+    return;
+  }
+  double r[P][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double cj = ct[(uint64_t)(off + u) * kpad + c];
+#pragma unroll
+    for (int p = 0; p < P; ++p) r[p][u] = sq(p, off + u, cj);
+  }
+  int i = 8;
+  const int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+    double cj[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cj[u] = ct[(uint64_t)(off + i + u) * kpad + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int p = 0; p < P; ++p) r[p][u] = __dadd_rn(r[p][u], sq(p, off + i + u, cj[u]));
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    res[p] = __dadd_rn(__dadd_rn(__dadd_rn(r[p][0], r[p][1]), __dadd_rn(r[p][2], r[p][3])),
+                       __dadd_rn(__dadd_rn(r[p][4], r[p][5]), __dadd_rn(r[p][6], r[p][7])));
+  for (; i < n; ++i) {
+    const double cj = ct[(uint64_t)(off + i) * kpad + c];
+#pragma unroll
+    for (int p = 0; p < P; ++p) res[p] = __dadd_rn(res[p], sq(p, off + i, cj));
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kCtThreads) assign_l2_ct_kernel(const T* __restrict__ X, uint64_t n, int d,
+                                                                  const double* __restrict__ ct, uint64_t k,
+                                                                  uint64_t kpad, const PwPlan plan,
+                                                                  int64_t* labels, double* best) {
+  extern __shared__ double xs[];  // [kCtP][d]
+  __shared__ double wd[kCtP][kCtThreads / 32];
+  __shared__ long long wl[kCtP][kCtThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t p0 = (uint64_t)blockIdx.x * kCtP; p0 < n; p0 += (uint64_t)gridDim.x * kCtP) {
+    const int np = (int)min((uint64_t)kCtP, n - p0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kCtP * d; e += kCtThreads) {
+      const int p = e / d;
+      xs[e] = p < np ? (double)X[(p0 + p) * d + (e - p * d)] : 0.0;
+    }
+    __syncthreads();
+    double bd[kCtP];
+    long long bl[kCtP];
+#pragma unroll
+    for (int p = 0; p < kCtP; ++p) {
+      bd[p] = 0.0;
+      bl[p] = -1;
+    }
+    for (uint64_t c = threadIdx.x; c < kpad; c += kCtThreads) {
+      const bool cv = c < k;
+      const uint64_t cc = cv ? c : 0;
+      double st[6][kCtP];
+      int sp = 0;
+      for (int o = 0; o < plan.nops; ++o) {
+        if (plan.op[o] == 0) {
+          double r[kCtP];
+          ct_leaf<kCtP>(xs, d, ct, kpad, cc, plan.off[o], plan.len[o], r);
+#pragma unroll
+          for (int p = 0; p < kCtP; ++p) st[sp][p] = r[p];
+          ++sp;
+        } else {
+#pragma unroll
+          for (int p = 0; p < kCtP; ++p) st[sp - 2][p] = __dadd_rn(st[sp - 2][p], st[sp - 1][p]);
+          --sp;
+        }
+      }
+      if (!cv) continue;
+#pragma unroll
+      for (int p = 0; p < kCtP; ++p) {
+        const double dist = __dsqrt_rn(st[0][p]);
+        if (bl[p] < 0 || dist < bd[p]) {  // c ascends per thread: first index kept on ties
+          bd[p] = dist;
+          bl[p] = (long long)c;
+        }
+      }
+    }
+    // lexicographic (distance, index) minimum over the block
+#pragma unroll
+    for (int p = 0; p < kCtP; ++p) {
+      double d0 = bd[p];
+      long long l0 = bl[p];
+      for (int o = 16; o; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, d0, o);
+        const long long ol = __shfl_xor_sync(0xffffffffu, l0, o);
+        if (ol >= 0 && (l0 < 0 || od < d0 || (od == d0 && ol < l0))) {
+          d0 = od;
+          l0 = ol;
+        }
+      }
+      if (lane == 0) {
+        wd[p][warp] = d0;
+        wl[p][warp] = l0;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < np) {
+      const int p = threadIdx.x;
+      double d0 = wd[p][0];
+      long long l0 = wl[p][0];
+      for (int w = 1; w < kCtThreads / 32; ++w) {
+        const double od = wd[p][w];
+        const long long ol = wl[p][w];
+        if (ol >= 0 && (l0 < 0 || od < d0 || (od == d0 && ol < l0))) {
+          d0 = od;
+          l0 = ol;
+        }
+      }
+      labels[p0 + p] = l0;
+      best[p0 + p] = d0;
+    }
+  }
+}
+
+__global__ void transpose_centers_kernel(const double* C, uint64_t k, int d, uint64_t kpad, double* ct) {
+  const uint64_t total = (uint64_t)d * kpad;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = e / kpad, c = e - j * kpad;
+    ct[e] = c < k ? C[c * d + j] : 0.0;
+  }
+}
+
 // Exact argmin for the few points whose screen window overflowed: one block
 // per point, threads over centers (first index wins ties, as np.argmin).
 constexpr int kFsThreads = 256;
@@ -972,6 +1126,28 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
   }
   const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
   const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;
+  if (!screened && d > 128 && !getenv("GEEK_NO_CT")) {
+    const uint64_t kpad = (k + 31) / 32 * 32;
+    Scratch ctb;
+    GEEK_TRY(ctb.alloc(kpad * d * 8, s));
+    transpose_centers_kernel<<<grid_for(kpad * d, 256), 256, 0, s>>>(C, k, d, kpad, ctb.as<double>());
+    const size_t xsm = sizeof(double) * kCtP * d;
+    if (xsm + 1024 > 48 * 1024) {  // + the static reduction arrays
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_ct_kernel<float>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm));
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_ct_kernel<double>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm));
+    }
+    const unsigned grid = grid_for((n + kCtP - 1) / kCtP, 1, 148 * 16);
+    if (dtype == 0)
+      assign_l2_ct_kernel<float><<<grid, kCtThreads, xsm, s>>>((const float*)X, n, d, ctb.as<double>(), k, kpad,
+                                                               plan, labels, best);
+    else
+      assign_l2_ct_kernel<double><<<grid, kCtThreads, xsm, s>>>((const double*)X, n, d, ctb.as<double>(), k,
+                                                                kpad, plan, labels, best);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
   if (!screened) {
     unsigned grid = (unsigned)((n + kAsgThreads - 1) / kAsgThreads);
     if (dtype == 0)

@@ -239,6 +239,23 @@ def test_assign_pairwise_order_vs_oracle(d):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("d,k,n", [(960, 150, 1001), (257, 129, 7), (1536, 3, 5)])
+def test_assign_wide_rows_vs_oracle(d, k, n):
+    """d > 128 without a screen: the transposed-center kernel (one thread per
+    center, points in SMEM), float32 rows, duplicate centers, ragged n and k
+    beyond one 128-center pass."""
+    rng = np.random.default_rng(d + k)
+    C = rng.standard_normal((k, d)) * 2
+    X = (C[rng.integers(0, k, n)] + rng.standard_normal((n, d))).astype(np.float32)
+    C[k - 1] = C[0]
+    X[0] = C[0].astype(np.float32)
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
 @pytest.mark.parametrize("d,k,offset", [(128, 37, 0.0), (128, 300, 300.0), (16, 5, 0.0), (200, 64, 50.0)])
 def test_assign_screened_f32_vs_oracle(d, k, offset):
     """float32 data takes the float32 screen + exact recheck path."""
