@@ -1,4 +1,5 @@
-"""GIST-like configuration (BASELINE configs[2]): synthetic 10M x 960 float32,
+"""GIST-like configuration (BASELINE configs[2]): synthetic 10M x 960 float32 (argv[1] = n,
+argv[2] = points per bucket, default 1000),
 1000 planted clusters, m = 40, t = n/1000, L = 20, K = 2, delta = 10, g = 8;
 one warm and one timed run of the pipeline with per-stage times and the
 libgeek call times, and an exact float64 spot check of 20K sampled labels /
@@ -21,7 +22,7 @@ X = gaussian_mixture_device(n, d, 1000, 10.0, 0)
 torch.cuda.synchronize()
 gen_s = time.time() - t0
 cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(8),
-                       homo=G.HomoTransformParams(40, max(1, n // 1000), seed=1),
+                       homo=G.HomoTransformParams(40, max(1, n // int(sys.argv[2]) if len(sys.argv) > 2 else n // 1000), seed=1),
                        seeding=G.SeedingParams(2, 20, min_group_size=10, seed=2))
 out = G.run_pipeline_shard(X, n, cfg)
 tm = _lib.CallTimer()
