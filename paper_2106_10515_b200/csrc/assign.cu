@@ -139,11 +139,12 @@ __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restr
 constexpr int kCtThreads = 128;
 constexpr int kCtP = 4;
 
-template <int P>
-__device__ __forceinline__ void ct_leaf(const double* xs, int d, const double* __restrict__ ct, uint64_t kpad,
+// x(p, j): coordinate j of the p-th point as float64 (SMEM tile or global row)
+template <int P, class XA>
+__device__ __forceinline__ void ct_leaf(const XA& x, const double* __restrict__ ct, uint64_t kpad,
                                         uint64_t c, int off, int n, double (&res)[P]) {
   auto sq = [&](int p, int j, double cj) {
-    const double df = __dsub_rn(xs[p * d + j], cj);
+    const double df = __dsub_rn(x(p, j), cj);
     return __dmul_rn(df, df);
   };
   if (n < 8) {
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kCtThreads) assign_l2_ct_kernel(const T* __res
       for (int o = 0; o < plan.nops; ++o) {
         if (plan.op[o] == 0) {
           double r[kCtP];
-          ct_leaf<kCtP>(xs, d, ct, kpad, cc, plan.off[o], plan.len[o], r);
+          ct_leaf<kCtP>([&](int p, int j) { return xs[p * d + j]; }, ct, kpad, cc, plan.off[o], plan.len[o], r);
 #pragma unroll
           for (int p = 0; p < kCtP; ++p) st[sp][p] = r[p];
           ++sp;
@@ -270,6 +271,62 @@ __global__ void __launch_bounds__(kCtThreads) assign_l2_ct_kernel(const T* __res
       }
       labels[p0 + p] = l0;
       best[p0 + p] = d0;
+    }
+  }
+}
+
+// Small k (<= 32): a warp holds 32/S segments of S = pow2 >= k lanes, lane
+// l of a segment evaluates center l for the segment's kCtP points, read
+// straight from their global rows (one address per segment per load).
+template <class T>
+__global__ void __launch_bounds__(kCtThreads) assign_l2_ctk_kernel(const T* __restrict__ X, uint64_t n, int d,
+                                                                   const double* __restrict__ ct, uint64_t k,
+                                                                   uint64_t kpad, int S, const PwPlan plan,
+                                                                   int64_t* labels, double* best) {
+  const int l = threadIdx.x & (S - 1);
+  const uint64_t gt = blockIdx.x * (uint64_t)kCtThreads + threadIdx.x;
+  const uint64_t wseg0 = (gt >> 5) * (32 / S);  // first segment of this warp
+  const uint64_t nseg = (uint64_t)gridDim.x * kCtThreads / S;
+  const bool cv = (uint64_t)l < k;
+  const uint64_t cc = cv ? l : 0;
+  // the loop bound is warp-uniform (the shuffles below need every lane);
+  // segments past the end compute on clamped rows and write nothing
+  for (uint64_t base = wseg0 * kCtP; base < n; base += nseg * kCtP) {
+    const uint64_t p0 = base + (uint64_t)((threadIdx.x & 31) / S) * kCtP;
+    const T* xr[kCtP];
+#pragma unroll
+    for (int p = 0; p < kCtP; ++p) xr[p] = X + min(p0 + p, n - 1) * d;
+    double st[6][kCtP];
+    int sp = 0;
+    for (int o = 0; o < plan.nops; ++o) {
+      if (plan.op[o] == 0) {
+        double r[kCtP];
+        ct_leaf<kCtP>([&](int p, int j) { return (double)xr[p][j]; }, ct, kpad, cc, plan.off[o], plan.len[o], r);
+#pragma unroll
+        for (int p = 0; p < kCtP; ++p) st[sp][p] = r[p];
+        ++sp;
+      } else {
+#pragma unroll
+        for (int p = 0; p < kCtP; ++p) st[sp - 2][p] = __dadd_rn(st[sp - 2][p], st[sp - 1][p]);
+        --sp;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < kCtP; ++p) {
+      double d0 = __dsqrt_rn(st[0][p]);
+      long long l0 = cv ? (long long)l : -1;
+      for (int o = 1; o < S; o <<= 1) {  // lexicographic (distance, index) minimum in the segment
+        const double od = __shfl_xor_sync(0xffffffffu, d0, o);
+        const long long ol = __shfl_xor_sync(0xffffffffu, l0, o);
+        if (ol >= 0 && (l0 < 0 || od < d0 || (od == d0 && ol < l0))) {
+          d0 = od;
+          l0 = ol;
+        }
+      }
+      if (l == 0 && p0 + p < n) {
+        labels[p0 + p] = l0;
+        best[p0 + p] = d0;
+      }
     }
   }
 }
@@ -1137,6 +1194,19 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm));
       GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_ct_kernel<double>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm));
+    }
+    if (k <= 16) {
+      int S = 1;
+      while ((uint64_t)S < k) S <<= 1;
+      const unsigned gk = grid_for((n + kCtP - 1) / kCtP, kCtThreads / S, 148 * 16);
+      if (dtype == 0)
+        assign_l2_ctk_kernel<float><<<gk, kCtThreads, 0, s>>>((const float*)X, n, d, ctb.as<double>(), k, kpad, S,
+                                                              plan, labels, best);
+      else
+        assign_l2_ctk_kernel<double><<<gk, kCtThreads, 0, s>>>((const double*)X, n, d, ctb.as<double>(), k, kpad,
+                                                               S, plan, labels, best);
+      GEEK_CHECK_LAUNCH();
+      return GEEK_OK;
     }
     const unsigned grid = grid_for((n + kCtP - 1) / kCtP, 1, 148 * 16);
     if (dtype == 0)

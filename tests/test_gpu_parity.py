@@ -239,7 +239,8 @@ def test_assign_pairwise_order_vs_oracle(d):
     assert got.objective == obj
 
 
-@pytest.mark.parametrize("d,k,n", [(960, 150, 1001), (257, 129, 7), (1536, 3, 5)])
+@pytest.mark.parametrize("d,k,n", [(960, 150, 1001), (257, 129, 7), (1536, 3, 5), (960, 8, 3333), (300, 16, 999),
+                                   (129, 1, 77), (640, 5, 100_003)])
 def test_assign_wide_rows_vs_oracle(d, k, n):
     """d > 128 without a screen: the transposed-center kernel (one thread per
     center, points in SMEM), float32 rows, duplicate centers, ragged n and k
