@@ -621,10 +621,7 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
             if mp.target_dims <= data.universe:
                 red = DophReducer(derive_seed(mp.seed, 0xD0), data.universe, mp.target_dims)
                 flat, off = red.reduce_device(*data.csr(), data.n)
-                o = off.cpu().numpy()
-                v = flat.cpu().numpy().view(np.uint32).astype(np.int64)
-                data = SparseData([v[o[i]:o[i + 1]] for i in range(data.n)], mp.target_dims)
-                object.__setattr__(data, "_cache", {"csr": (flat, off)})
+                data = SparseData.from_csr(flat.to(torch.int64) & 0xFFFFFFFF, off, mp.target_dims)
             flat, off = data.csr()
             universe = data.universe
     n = data.n

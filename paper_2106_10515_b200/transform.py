@@ -263,10 +263,8 @@ def transform_sparse(data: SparseData, params: MinhashTransformParams):
     else:
         red = DophReducer(derive_seed(params.seed, 0xD0), data.universe, params.target_dims)
         flat, off = red.reduce_device(*data.csr(), data.n)
-        o = off.cpu().numpy()
-        v = flat.cpu().numpy().view(np.uint32).astype(np.int64)
-        reduced = SparseData([v[o[i]:o[i + 1]] for i in range(data.n)], params.target_dims)
-        object.__setattr__(reduced, "_cache", {"csr": (flat, off)})
+        reduced = SparseData.from_csr(flat.to(torch.int64) & 0xFFFFFFFF, off, params.target_dims)
+        flat, off = reduced.csr()
     scheme = params.scheme(universe=reduced.universe)
     codes, tsizes = signature_bucket_codes(scheme, flat, off, reduced.n)
     return BucketTable(codes, reduced.n, tsizes, "sig", even=False), reduced
