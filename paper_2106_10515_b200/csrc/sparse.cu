@@ -4,6 +4,9 @@
 // categorical / sparse centers (seeding.py:180-194, engine.py:312-322).
 #include "common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace geek {
 
 // one warp per set: bin-minimum flags and tokens (bin + rel) mod r
@@ -67,6 +70,66 @@ __global__ void doph_emit_kernel(const uint32_t* tok, const uint8_t* ismin, cons
   }
 }
 
+// One warp per set, r <= kDophSmemR: bin minima of the permuted ids by
+// shared-memory atomicMin over r slots, then the tokens of the occupied bins
+// set bits of an r-bit map, and the set's distinct tokens leave in ascending
+// order by popcount prefix -- O(|set| + r/32) per set instead of the pairwise
+// scans of doph_tokens / doph_emit.
+constexpr uint32_t kDophSmemR = 4096;
+
+__global__ void doph_smem_kernel(const uint32_t* __restrict__ p, const uint64_t* __restrict__ off,
+                                 uint64_t nsets, uint64_t width, uint32_t r, uint32_t* counts,
+                                 const uint64_t* out_off, uint32_t* out_flat) {
+  extern __shared__ uint32_t sm[];
+  const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t words = (r + 31) / 32;
+  uint32_t* bmin = sm + (size_t)w * (r + words);
+  uint32_t* bits = bmin + r;
+  for (uint64_t s = blockIdx.x * (uint64_t)wpb + w; s < nsets; s += (uint64_t)gridDim.x * wpb) {
+    const uint64_t b = off[s], e = off[s + 1];
+    for (uint32_t j = lane; j < r; j += 32) bmin[j] = 0xFFFFFFFFu;
+    for (uint32_t j = lane; j < words; j += 32) bits[j] = 0u;
+    __syncwarp();
+    for (uint64_t i = b + lane; i < e; i += 32) {
+      const uint32_t pi = p[i];
+      atomicMin(&bmin[pi / width], pi);
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < r; j += 32) {
+      const uint32_t pm = bmin[j];
+      if (pm != 0xFFFFFFFFu) {
+        const uint32_t t = (uint32_t)(((uint64_t)j + (pm - (uint64_t)j * width)) % r);
+        atomicOr(&bits[t >> 5], 1u << (t & 31));
+      }
+    }
+    __syncwarp();
+    uint32_t base = 0;
+    for (uint32_t w0 = 0; w0 < words; w0 += 32) {
+      const uint32_t wi = w0 + lane;
+      const uint32_t v = wi < words ? bits[wi] : 0u;
+      const uint32_t c = __popc(v);
+      uint32_t incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      if (out_flat && v) {
+        uint32_t pos = base + incl - c;
+        uint32_t m = v;
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          out_flat[out_off[s] + pos++] = wi * 32 + bit;
+          m &= m - 1;
+        }
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0 && counts) counts[s] = base;
+    __syncwarp();
+  }
+}
+
 __global__ void assign_cat_kernel(const int32_t* __restrict__ codes, uint64_t n, int d,
                                   const int32_t* __restrict__ modes, uint64_t k, int64_t* labels, double* best) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -122,6 +185,95 @@ __global__ void assign_sparse_kernel(const uint32_t* flat, const uint64_t* off, 
     }
     labels[i] = bl;
     best[i] = bd;
+  }
+}
+
+// Bitset Jaccard assignment for universes <= 32*WM ids: modes as bitsets
+// staged in SMEM tiles, each thread's set as WM register words; per pair
+// inter = sum popc(x & c), union = |x| + |c| - inter.  With |x|, |c| <= 2048
+// distinct similarities inter/union differ by more than 2^-22, so comparing
+// them exactly as fractions (inter * u' vs inter' * u) orders them as the
+// reference's float64 1 - inter/union does, ties included (first index kept);
+// the winner's distance is then evaluated with the reference's float64 ops.
+constexpr int kBitTile = 256;
+
+__global__ void mode_bits_kernel(const int32_t* modes, uint64_t k, uint64_t u, int W, uint32_t* bits,
+                                 uint32_t* sizes) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k; c += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t tot = 0;
+    for (int w = 0; w < W; ++w) {
+      uint32_t v = 0;
+      for (int b = 0; b < 32; ++b) {
+        const uint64_t e = (uint64_t)w * 32 + b;
+        if (e < u && modes[c * u + e] != 0) v |= 1u << b;
+      }
+      bits[c * W + w] = v;
+      tot += __popc(v);
+    }
+    sizes[c] = tot;
+  }
+}
+
+template <int WM>
+__global__ void __launch_bounds__(128) assign_sparse_bits_kernel(const uint32_t* __restrict__ flat,
+                                                                 const uint64_t* __restrict__ off, uint64_t n,
+                                                                 const uint32_t* __restrict__ mbits,
+                                                                 const uint32_t* __restrict__ msize, uint64_t k,
+                                                                 int W, int64_t* labels, double* best) {
+  __shared__ uint32_t sb[kBitTile * WM];
+  __shared__ uint32_t ss[kBitTile];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t first = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  // block-uniform trip count (the tiles are loaded cooperatively)
+  const uint64_t iters = (n + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t i = first + it * stride;
+    const bool valid = i < n;
+    uint32_t x[WM];
+#pragma unroll
+    for (int w = 0; w < WM; ++w) x[w] = 0;
+    uint32_t xs = 0;
+    if (valid) {
+      const uint64_t b = off[i], e = off[i + 1];
+      xs = (uint32_t)(e - b);
+      for (uint64_t q = b; q < e; ++q) {
+        const uint32_t v = flat[q];
+        const uint32_t wv = v >> 5, bit = 1u << (v & 31);
+#pragma unroll
+        for (int w = 0; w < WM; ++w) x[w] |= (wv == (uint32_t)w) ? bit : 0u;
+      }
+    }
+    uint32_t bi = 0, bu = 1;
+    long long bl = -1;
+    for (uint64_t c0 = 0; c0 < k; c0 += kBitTile) {
+      const int nc = (int)min((uint64_t)kBitTile, k - c0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nc * W; e += blockDim.x) {
+        const int c = e / W, w = e - c * W;
+        sb[c * WM + w] = mbits[(c0 + c) * W + w];
+      }
+      for (int c = threadIdx.x; c < nc; c += blockDim.x) ss[c] = msize[c0 + c];
+      __syncthreads();
+      if (!valid) continue;
+      for (int c = 0; c < nc; ++c) {
+        uint32_t in = 0;
+#pragma unroll
+        for (int w = 0; w < WM; ++w) in += __popc(x[w] & sb[c * WM + w]);
+        const uint32_t un = xs + ss[c] - in;
+        // similarity in/un strictly larger (un >= 1: sets are non-empty)
+        if (bl < 0 || (unsigned long long)in * bu > (unsigned long long)bi * un) {
+          bi = in;
+          bu = un;
+          bl = (long long)(c0 + c);
+        }
+      }
+    }
+    if (valid) {
+      const double uni = __dsub_rn(__dadd_rn((double)xs, (double)(bu + bi - xs)), (double)bi);
+      const double sim = uni > 0.0 ? __ddiv_rn((double)bi, uni) : 1.0;
+      labels[i] = bl;
+      best[i] = __dsub_rn(1.0, sim);
+    }
   }
 }
 
@@ -181,10 +333,22 @@ int geek_doph_reduce(const geek_perm_t* perm_host, const uint32_t* tables, const
   GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
   Scratch p, tok, mn;
   GEEK_TRY(p.alloc(total * 4, s));
-  GEEK_TRY(tok.alloc(total * 4, s));
-  GEEK_TRY(mn.alloc(total, s));
   GEEK_TRY(geek_perm_forward(perm_host, 1, tables, flat, total, p.as<uint32_t>(), stream));
   const uint64_t width = (D + r - 1) / r;
+  if (r <= kDophSmemR && !getenv("GEEK_DOPH_PAIRWISE")) {
+    const size_t per_warp = 4 * ((size_t)r + (r + 31) / 32);
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp));
+    const size_t smem = per_warp * wpb;
+    if (smem > 48 * 1024)
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(doph_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    doph_smem_kernel<<<grid_for(nsets, wpb, 148 * 16), 32 * wpb, smem, s>>>(p.as<uint32_t>(), offsets, nsets, width,
+                                                                            (uint32_t)r, counts, out_off, out_flat);
+    GEEK_CHECK_LAUNCH();
+    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
+    return GEEK_OK;
+  }
+  GEEK_TRY(tok.alloc(total * 4, s));
+  GEEK_TRY(mn.alloc(total, s));
   doph_tokens_kernel<<<grid_for(nsets * 32, 256), 256, 0, s>>>(p.as<uint32_t>(), offsets, nsets, width, r,
                                                                tok.as<uint32_t>(), mn.as<uint8_t>());
   GEEK_CHECK_LAUNCH();
@@ -210,6 +374,25 @@ int geek_assign_sparse(const uint32_t* flat, const uint64_t* offsets, uint64_t n
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(k >= 1, "cannot assign without centers");
   if (n == 0) return GEEK_OK;
+  if (universe <= 1024 && !getenv("GEEK_SPARSE_DENSE")) {
+    const int W = (int)((universe + 31) / 32);
+    Scratch mb, ms;
+    GEEK_TRY(mb.alloc(k * W * 4, s));
+    GEEK_TRY(ms.alloc(k * 4, s));
+    mode_bits_kernel<<<grid_for(k, 128), 128, 0, s>>>(modes, k, universe, W, mb.as<uint32_t>(), ms.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    const unsigned grid = grid_for(n, 128, 148 * 8);
+#define GEEK_BITS(WMV)                                                                                     \
+  assign_sparse_bits_kernel<WMV><<<grid, 128, 0, s>>>(flat, offsets, n, mb.as<uint32_t>(), ms.as<uint32_t>(), k, \
+                                                      W, labels, best)
+    if (W <= 4) GEEK_BITS(4);
+    else if (W <= 8) GEEK_BITS(8);
+    else if (W <= 16) GEEK_BITS(16);
+    else GEEK_BITS(32);
+#undef GEEK_BITS
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
   Scratch msz;
   GEEK_TRY(msz.alloc(k * 8, s));
   mode_sizes_kernel<<<grid_for(k, 128), 128, 0, s>>>(modes, k, universe, msz.as<double>());

@@ -714,3 +714,21 @@ def test_artifacts_byte_identical():
     out = G.run_pipeline(G.DenseData(X), dense_config(m, 2))
     assert hashlib.sha256(S.dump_seed_groups(out.seed_groups)).hexdigest() == want["small_groups"]["sha256"]
     assert hashlib.sha256(S.dump_clustering(out.clustering)).hexdigest() == want["small_clustering"]["sha256"]
+
+
+@pytest.mark.parametrize("u,k", [(20, 7), (400, 300), (1000, 33), (2000, 9)])
+def test_assign_sparse_bitsets_vs_oracle(u, k):
+    """Jaccard assignment of sparse sets: bitset kernel (u <= 1024) and the
+    dense-mode kernel above it, against the oracle's float64 formula; empty
+    and duplicate modes, exact-tie similarities."""
+    rng = np.random.default_rng(u + k)
+    sets = [np.unique(rng.integers(0, u, rng.integers(1, min(u, 60)))) for _ in range(3001)]
+    M = (rng.random((k, u)) < 0.08).astype(np.int32)
+    M[0] = 0
+    M[k - 1] = M[1]
+    data = G.SparseData(sets, u)
+    got = G.assign(data, [G.CentralVector("mode", m) for m in M], "jaccard")
+    lab, best, radii, obj = O.assign_generic(lambda a, b: O.sparse_distances(sets[a:b], u, M), len(sets), k)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
