@@ -30,8 +30,8 @@ from .assignment import assign_cat_device, assign_l2_device, assign_sparse_devic
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
-from .numeric import (digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, mode_counts,
-                      partial_sums, round_means, sparse_counts)
+from .numeric import (digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, mode_centers,
+                      mode_counts, partial_sums, round_means, sparse_counts)
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
 from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
@@ -638,7 +638,7 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
             groups = _fallback_groups(n, g, config.fallback_seed, warnings)
     with tm.stage("centers"):
         if isinstance(data, CategoricalData):
-            M = torch.argmax(mode_counts(data.device_codes(), data.code_space, groups), dim=2).to(torch.int32)
+            M = mode_centers(data.device_codes(), data.code_space, groups)
         else:
             cnt = sparse_counts(data, groups)
             M = (2 * cnt > groups.sizes()[:, None]).to(torch.int32)

@@ -75,8 +75,36 @@ def mode_counts(codes: torch.Tensor, code_space: int, groups: GroupSet, row_lo: 
 
 
 def mode_centers(codes: torch.Tensor, code_space: int, groups: GroupSet) -> torch.Tensor:
-    # argmax returns the first maximum: ties go to the smallest code (seeding.py:184)
-    return torch.argmax(mode_counts(codes, code_space, groups), dim=2).to(torch.int32)
+    """int32 [k, d] per-attribute modes, ties to the smallest code (seeding.py:180-185)."""
+    k, d = groups.count, codes.shape[1]
+    if k * d * code_space <= (1 << 31):
+        # argmax returns the first maximum: ties go to the smallest code
+        return torch.argmax(mode_counts(codes, code_space, groups), dim=2).to(torch.int32)
+    return sparse_mode_centers(codes, code_space, groups.flat, groups.off)
+
+
+def sparse_mode_centers(codes: torch.Tensor, code_space: int, flat: torch.Tensor, off: torch.Tensor) -> torch.Tensor:
+    """Modes without a dense [k, d, code_space] table (large code spaces, e.g.
+    Criteo-like cardinalities): per attribute, the (group, code) pairs of all
+    members are counted by a device sort + run-length pass; each group keeps
+    its most frequent code, the smallest among equal counts."""
+    k = off.numel() - 1
+    d = codes.shape[1]
+    sizes = off[1:] - off[:-1]
+    total = int(off[-1].item())
+    ids = flat[:total].to(torch.int64) & 0xFFFFFFFF
+    grp = torch.repeat_interleave(torch.arange(k, device=codes.device), sizes)
+    out = torch.zeros((k, d), dtype=torch.int32, device=codes.device)
+    for c in range(d):
+        key = grp * code_space + codes[ids, c].to(torch.int64)
+        uk, cnt = torch.unique(key, sorted=True, return_counts=True)
+        g = uk // code_space
+        top = torch.zeros(k, dtype=cnt.dtype, device=cnt.device).scatter_reduce(0, g, cnt, "amax", include_self=False)
+        win = cnt == top[g]
+        code = torch.full((k,), code_space, dtype=torch.int64, device=cnt.device)
+        code = code.scatter_reduce(0, g[win], (uk - g * code_space)[win], "amin", include_self=True)
+        out[:, c] = code.to(torch.int32)
+    return out
 
 
 def sparse_counts(data: SparseData, groups: GroupSet, row_lo: int = 0, csr=None) -> torch.Tensor:

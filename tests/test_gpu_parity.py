@@ -732,3 +732,17 @@ def test_assign_sparse_bitsets_vs_oracle(u, k):
     assert np.array_equal(got.assignment, lab)
     assert np.array_equal(got.radii, radii)
     assert got.objective == obj
+
+
+def test_sparse_mode_centers_match_dense_counts():
+    """Large-code-space modes (sort + run-length, no [k, d, code_space] table)
+    equal the dense-count argmax, ties to the smallest code."""
+    from paper_2106_10515_b200 import _lib, numeric
+    from paper_2106_10515_b200.tables import GroupSet
+    rng = np.random.default_rng(9)
+    codes = rng.integers(0, 6, (5000, 7)).astype(np.int32)
+    groups = GroupSet.from_host([np.sort(rng.choice(5000, rng.integers(1, 40), replace=False)) for _ in range(300)])
+    cd = _lib.to_dev(codes, torch.int32)
+    dense = torch.argmax(numeric.mode_counts(cd, 6, groups), dim=2).to(torch.int32)
+    sparse = numeric.sparse_mode_centers(cd, 6, groups.flat, groups.off)
+    assert torch.equal(dense, sparse)
