@@ -295,13 +295,58 @@ def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=N
                 info["vote_winners"] = nw
                 info["raw_groups"] = groups.count
             return groups, bins, won
-    pbin, pid = membership_pairs(bins, buckets, csr, sizes)
-    groups, won = vote(pbin, pid, bins, params.min_group_size)
+    groups, won, npairs = _batched_votes(bins, buckets, csr, sizes, params.min_group_size)
     if info is not None:
         info["bins"] = bins.count
-        info["vote_pairs"] = int(pbin.numel())
+        info["vote_pairs"] = npairs
         info["raw_groups"] = groups.count
     return groups, bins, won
+
+
+_PAIR_BATCH = 1 << 28  # (bin, id) pairs materialised at once
+
+
+def _batched_votes(bins: Bins, buckets, csr, sizes, delta):
+    """membership_pairs + vote over contiguous bin-id ranges holding at most
+    _PAIR_BATCH pairs each (bins are independent; the concatenation keeps the
+    bin-id order of the single pass), so giant buckets -- e.g. low-cardinality
+    categorical attributes -- do not need all pairs in memory at once."""
+    B = bins.count
+    pb_sizes = sizes[bins.pair_bucket] if bins.pair_bucket.numel() else sizes[:0]
+    total = int(pb_sizes.sum().item()) if pb_sizes.numel() else 0
+    if total <= _PAIR_BATCH or B <= 1:
+        pbin, pid = membership_pairs(bins, buckets, csr, sizes)
+        g, w = vote(pbin, pid, bins, delta)
+        return g, w, int(pbin.numel())
+    per_bin = torch.zeros(B, dtype=torch.int64, device=pb_sizes.device).index_add_(0, bins.pair_bin, pb_sizes)
+    cum = torch.cumsum(per_bin, 0).cpu().numpy()
+    cuts, b0 = [0], 0
+    while b0 < B:
+        before = cum[b0 - 1] if b0 else 0
+        b1 = int(np.searchsorted(cum, before + _PAIR_BATCH, side="right"))
+        b1 = min(B, max(b1, b0 + 1))
+        cuts.append(b1)
+        b0 = b1
+    parts, wons, npairs = [], [], 0
+    for b0, b1 in zip(cuts[:-1], cuts[1:]):
+        m = (bins.pair_bin >= b0) & (bins.pair_bin < b1)
+        sub = Bins(bins.pair_bucket[m], bins.pair_bin[m] - b0, bins.bin_size[b0:b1], bins.bin_table[b0:b1],
+                   bins.bin_sig[b0:b1])
+        pbin, pid = membership_pairs(sub, buckets, csr, sizes)
+        npairs += int(pbin.numel())
+        g, w = vote(pbin, pid, sub, delta)
+        del pbin, pid
+        if g.count:
+            parts.append(g)
+            wons.append(w + b0)
+    if not parts:
+        return GroupSet.empty(), torch.zeros(0, dtype=torch.int64, device=pb_sizes.device), npairs
+    flat = torch.cat([g.flat[: int(g.off[-1].item())] for g in parts])
+    offs, base = [torch.zeros(1, dtype=torch.int64, device=flat.device)], 0
+    for g in parts:
+        offs.append(g.off[1:] + base)
+        base += int(g.off[-1].item())
+    return GroupSet(flat.contiguous(), torch.cat(offs)), torch.cat(wons), npairs
 
 
 # ---------------------------------------------------------------------------

@@ -746,3 +746,25 @@ def test_sparse_mode_centers_match_dense_counts():
     dense = torch.argmax(numeric.mode_counts(cd, 6, groups), dim=2).to(torch.int32)
     sparse = numeric.sparse_mode_centers(cd, 6, groups.flat, groups.off)
     assert torch.equal(dense, sparse)
+
+
+def test_batched_votes_match_single_pass(monkeypatch):
+    """Votes over bin-id batches (bounded pair memory) give the same seed
+    groups and results as one pass (sparse and mixed golden pipelines)."""
+    from paper_2106_10515_b200 import seeding
+    monkeypatch.setattr(seeding, "_PAIR_BATCH", 64)
+    arr = npz("pipelines")
+    data = G.SparseData(csr(arr["sp_flat"], arr["sp_off"]), 20_000)
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="sparse", workers=G.WorkerConfig(2),
+                           minhash=G.MinhashTransformParams(3, 6, seed=4, target_dims=400),
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=5))
+    out = G.run_pipeline(data, cfg)
+    assert keys(out.seed_groups) == keys(golden_groups(arr, "sp_g2"))
+    assert np.array_equal(out.clustering.assignment, arr["sp_g2_labels"])
+    data = G.MixedData(arr["mx_num"], arr["mx_cat"])
+    cfg = G.PipelineConfig(metric="jaccard", transform_kind="mixed", workers=G.WorkerConfig(1),
+                           minhash=G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16),
+                           seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9))
+    out = G.run_pipeline(data, cfg)
+    assert keys(out.seed_groups) == keys(golden_groups(arr, "mx_g1"))
+    assert np.array_equal(out.clustering.assignment, arr["mx_g1_labels"])
