@@ -3,6 +3,8 @@
 // bucket member lists (hashing.py:126-140, :265-282; engine.py:256-266).
 #include "common.cuh"
 
+#include <cstdlib>
+
 #include <cmath>
 
 namespace geek {
@@ -55,6 +57,47 @@ __global__ void set_minhash_kernel(const geek_perm_t* perms, int nperm, const ui
       uint32_t v = valid ? perm_forward(sp[p], tables, x) : 0xFFFFFFFFu;
       uint32_t mn = __reduce_min_sync(peers, v);
       if (leader) atomicMin(&sig[s * nperm + p], mn);
+    }
+  }
+}
+
+// Rank-table regime (every function is a table over a universe u <= 4096,
+// hashing.py:80-95): all nperm tables sit in shared memory, one warp per set
+// keeps up to 4 of the set's ids per lane in registers, and each function's
+// minimum is a shared-memory lookup per id plus one warp min-reduction --
+// no segment search and no atomics.
+constexpr int kTabSetRegs = 4;
+
+__global__ void __launch_bounds__(256) set_minhash_tables_kernel(const geek_perm_t* perms, int nperm,
+                                                                 const uint32_t* tables, uint32_t u,
+                                                                 const uint32_t* __restrict__ flat,
+                                                                 const uint64_t* __restrict__ off,
+                                                                 uint64_t nsets, uint32_t* sig) {
+  extern __shared__ uint32_t st[];  // [nperm][u]
+  for (int p = 0; p < nperm; ++p)
+    for (uint32_t i = threadIdx.x; i < u; i += blockDim.x) st[(size_t)p * u + i] = tables[perms[p].table + i];
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t wpb = blockDim.x >> 5;
+  for (uint64_t s = blockIdx.x * wpb + (threadIdx.x >> 5); s < nsets; s += (uint64_t)gridDim.x * wpb) {
+    const uint64_t b = off[s], e = off[s + 1];
+    uint32_t x[kTabSetRegs];
+#pragma unroll
+    for (int r = 0; r < kTabSetRegs; ++r) {
+      const uint64_t q = b + lane + 32ull * r;
+      x[r] = q < e ? flat[q] : 0xFFFFFFFFu;
+    }
+    const bool more = e - b > 32ull * kTabSetRegs;
+    for (int p = 0; p < nperm; ++p) {
+      const uint32_t* tp = st + (size_t)p * u;
+      uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+      for (int r = 0; r < kTabSetRegs; ++r)
+        if (x[r] != 0xFFFFFFFFu) mn = min(mn, tp[x[r]]);
+      if (more)
+        for (uint64_t q = b + lane + 32ull * kTabSetRegs; q < e; q += 32) mn = min(mn, tp[flat[q]]);
+      mn = __reduce_min_sync(0xffffffffu, mn);
+      if (lane == 0) sig[s * nperm + p] = mn;
     }
   }
 }
@@ -120,6 +163,19 @@ int geek_set_minhash(const geek_perm_t* perms_host, int nperm, const uint32_t* t
   GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(sig, 0xFF, nsets * nperm * 4ull, s));
   if (total == 0) return GEEK_OK;
+  bool all_tables = nperm > 0;
+  uint32_t u = nperm > 0 ? perms_host[0].u : 0;
+  for (int p = 0; p < nperm; ++p) all_tables = all_tables && perms_host[p].table != GEEK_NONE && perms_host[p].u == u;
+  const size_t tsm = (size_t)nperm * u * 4;
+  if (all_tables && u <= 4096 && tsm <= 200 * 1024 && !getenv("GEEK_MINHASH_GENERIC")) {
+    if (tsm > 48 * 1024)
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(set_minhash_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)tsm));
+    set_minhash_tables_kernel<<<grid_for(nsets, 8, 148 * (tsm > 100 * 1024 ? 1 : 2) * 4), 256, tsm, s>>>(
+        pb.as<geek_perm_t>(), nperm, tables, u, flat, offsets, nsets, sig);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
   size_t smem = sizeof(geek_perm_t) * nperm;
   set_minhash_kernel<<<grid_for(total, 256, 148 * 16), 256, smem, s>>>(pb.as<geek_perm_t>(), nperm,
                                                                       tables, flat, offsets, nsets,
