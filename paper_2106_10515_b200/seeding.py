@@ -328,9 +328,16 @@ def _batched_votes(bins: Bins, buckets, csr, sizes, delta):
         cuts.append(b1)
         b0 = b1
     parts, wons, npairs = [], [], 0
-    for b0, b1 in zip(cuts[:-1], cuts[1:]):
-        m = (bins.pair_bin >= b0) & (bins.pair_bin < b1)
-        sub = Bins(bins.pair_bucket[m], bins.pair_bin[m] - b0, bins.bin_size[b0:b1], bins.bin_table[b0:b1],
+    pbn = bins.pair_bin
+    ordered = bool((pbn[1:] >= pbn[:-1]).all().item())  # find_bins emits pairs in bin order
+    if ordered:
+        bounds = torch.searchsorted(pbn, torch.tensor(cuts, dtype=pbn.dtype, device=pbn.device)).cpu().numpy()
+    for q, (b0, b1) in enumerate(zip(cuts[:-1], cuts[1:])):
+        if ordered:
+            m = slice(int(bounds[q]), int(bounds[q + 1]))
+        else:
+            m = (pbn >= b0) & (pbn < b1)
+        sub = Bins(bins.pair_bucket[m], pbn[m] - b0, bins.bin_size[b0:b1], bins.bin_table[b0:b1],
                    bins.bin_sig[b0:b1])
         pbin, pid = membership_pairs(sub, buckets, csr, sizes)
         npairs += int(pbin.numel())
