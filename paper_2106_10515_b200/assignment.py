@@ -128,7 +128,7 @@ def _centers_from_assignment(data, assignment, k) -> list:
     j, so the statistics come from one pass over the rows keyed by label
     (geek_label_sums / geek_label_mode_counts / geek_label_sparse_counts)
     instead of materialised member lists."""
-    from .numeric import digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, \
+    from .numeric import digit_count, exponent_range, label_mode_centers, label_sparse_counts, label_sums, \
         round_means
 
     labels = _lib.to_dev(np.ascontiguousarray(assignment, dtype=np.int64))
@@ -144,8 +144,7 @@ def _centers_from_assignment(data, assignment, k) -> list:
         C = round_means(label_sums(X, labels, k, emin, nd)[keep].contiguous(), counts, emin, nd).cpu().numpy()
         return [CentralVector("centroid", C[i], int(w[i])) for i in range(len(w))]
     if isinstance(data, CategoricalData):
-        cnt = label_mode_counts(data.device_codes(), data.code_space, labels, k)[keep]
-        M = torch.argmax(cnt, dim=2).to(torch.int32).cpu().numpy()  # ties: smallest code
+        M = label_mode_centers(data.device_codes(), data.code_space, labels, k, keep).cpu().numpy()
     else:
         flat, off = data.csr()
         cnt = label_sparse_counts(flat, off, data.n, data.universe, labels, k)[keep]

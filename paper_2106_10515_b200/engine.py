@@ -30,8 +30,8 @@ from .assignment import assign_cat_device, assign_l2_device, assign_sparse_devic
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
-from .numeric import (digit_count, exponent_range, label_mode_counts, label_sparse_counts, label_sums, mode_centers,
-                      mode_counts, partial_sums, round_means, sparse_counts)
+from .numeric import (digit_count, exponent_range, label_mode_centers, label_sparse_counts, label_sums,
+                      mode_centers, mode_counts, partial_sums, round_means, sparse_counts)
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
 from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
@@ -655,8 +655,7 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
             keep = torch.nonzero(sizes > 0).flatten()
             weights = sizes[keep].contiguous()
             if isinstance(data, CategoricalData):
-                cnt = label_mode_counts(data.device_codes(), data.code_space, labels, M.shape[0])[keep]
-                M = torch.argmax(cnt, dim=2).to(torch.int32)
+                M = label_mode_centers(data.device_codes(), data.code_space, labels, M.shape[0], keep)
             else:
                 cnt = label_sparse_counts(flat, off, n, data.universe, labels, M.shape[0])[keep]
                 M = (2 * cnt > weights[:, None]).to(torch.int32)

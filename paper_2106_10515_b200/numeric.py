@@ -159,6 +159,24 @@ def label_mode_counts(codes: torch.Tensor, code_space: int, labels: torch.Tensor
     return cnt[: k * d * code_space].view(k, d, code_space)
 
 
+_DENSE_MODE_LIMIT = 1 << 31
+
+
+def label_mode_centers(codes: torch.Tensor, code_space: int, labels: torch.Tensor, k: int,
+                       keep: torch.Tensor) -> torch.Tensor:
+    """int32 [len(keep), d] modes of the clusters `keep` (non-empty, ascending)
+    from the labels: dense label-keyed counts when [k, d, code_space] fits,
+    else the members grouped by a stable label sort and the sort-based mode."""
+    d = codes.shape[1]
+    if k * d * code_space <= _DENSE_MODE_LIMIT:
+        return torch.argmax(label_mode_counts(codes, code_space, labels, k)[keep], dim=2).to(torch.int32)
+    order = torch.sort(labels, stable=True).indices
+    sizes = torch.bincount(labels, minlength=k)[keep]
+    off = torch.zeros(keep.numel() + 1, dtype=torch.int64, device=labels.device)
+    torch.cumsum(sizes, 0, out=off[1:])
+    return sparse_mode_centers(codes, code_space, order.to(torch.int32).contiguous(), off)
+
+
 def label_sparse_counts(flat, off, n: int, universe: int, labels: torch.Tensor, k: int) -> torch.Tensor:
     cnt = _lib.zeros(max(1, k * universe), torch.int64)
     _lib.call("geek_label_sparse_counts", _lib.ptr(flat), _lib.ptr(off), n, _lib.ptr(labels.contiguous()), k,

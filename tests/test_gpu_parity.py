@@ -768,3 +768,17 @@ def test_batched_votes_match_single_pass(monkeypatch):
     out = G.run_pipeline(data, cfg)
     assert keys(out.seed_groups) == keys(golden_groups(arr, "mx_g1"))
     assert np.array_equal(out.clustering.assignment, arr["mx_g1_labels"])
+
+
+def test_label_mode_centers_sort_path(monkeypatch):
+    """Refinement modes for code spaces too large for dense counts (sort
+    path) equal the dense label-keyed counts."""
+    from paper_2106_10515_b200 import _lib, numeric
+    rng = np.random.default_rng(4)
+    codes = _lib.to_dev(rng.integers(0, 5, (4000, 6)).astype(np.int32), torch.int32)
+    labels = _lib.to_dev(rng.integers(0, 40, 4000).astype(np.int64))
+    labels[labels == 7] = 8
+    keep = torch.nonzero(torch.bincount(labels, minlength=40) > 0).flatten()
+    dense = numeric.label_mode_centers(codes, 5, labels, 40, keep)
+    monkeypatch.setattr(numeric, "_DENSE_MODE_LIMIT", 0)
+    assert torch.equal(numeric.label_mode_centers(codes, 5, labels, 40, keep), dense)
