@@ -128,6 +128,22 @@ int geek_rank_split_counted(const uint64_t* keys, uint64_t n, int m, uint64_t t,
 int geek_rank_split(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
                     uint64_t* stats_host, void* stream);
 
+/* Rank-split boundary exceptions (north_star tie tolerance; transform.py:103-109
+ * ranks OpenBLAS dgemv projections, engine.py:178-181).  For every table j and
+ * bucket boundary s, midpoint = (max key of bucket s + min key of bucket s+1)/2;
+ * counts[0] = ids whose key lies within tol_abs[j] (device double [m]) of a
+ * neighbouring midpoint -- the only ids whose code may differ from the
+ * reference's; counts[1] / counts[2] = ids within rel_a / rel_b * |midpoint|;
+ * counts[3] = entries offered to list.  list (device uint32 [cap][2]) receives
+ * (table, id) of the tol_abs ids.  keys [m][n] as geek_project_keys writes
+ * them, codes[i*code_stride + j] as geek_rank_split writes them.  Scratch:
+ * workspace of geek_split_boundary_workspace(m, t) bytes.  Stream-ordered.  */
+uint64_t geek_split_boundary_workspace(uint64_t m, uint64_t t);
+int geek_split_boundary_stats(const uint64_t* keys, uint64_t n, int m, uint64_t t, const uint32_t* codes,
+                              uint64_t code_stride, const double* tol_abs, double rel_a, double rel_b,
+                              unsigned long long* counts, uint32_t* list, uint64_t cap, void* workspace,
+                              uint64_t workspace_bytes, void* stream);
+
 /* Same split for a single column of keys written with a row stride:
  * codes[i*stride + col] (used for numeric discretisation, transform.py:131-155). */
 int geek_rank_split_strided(const uint64_t* keys, uint64_t n, uint64_t t, uint32_t* codes,
@@ -206,10 +222,21 @@ int geek_exponent_range(const void* X, int dtype, uint64_t n, int d, int* out_ho
 /* Exact per-group column sums in base-2^32 digits relative to 2^emin
  * (numeric.py:19-40): digits[(g*d + c)*nd + k] (int64, ADDED to).  Members
  * are global ids; rows outside [row_lo, row_lo + nrows) are skipped (a shard
- * contributes only its own rows; engine.py:299-311).                        */
+ * contributes only its own rows; engine.py:299-311).  *nonfinite (device,
+ * may be NULL) is OR-ed with 1 when a member coordinate is NaN / inf -- the
+ * reference raises ValueError("non-finite value in exact sum") there
+ * (numeric.py:24-25).  Stream-ordered (chunk table built on the device).    */
 int geek_exact_sums(const void* X, int dtype, uint64_t nrows, int d, uint64_t row_lo,
                     const uint32_t* flat, const uint64_t* offsets, uint64_t ngroups,
-                    int emin, int nd, int64_t* digits, void* stream);
+                    int emin, int nd, int64_t* digits, unsigned* nonfinite, void* stream);
+
+/* Transport accounting of the reference's LocalCenters message
+ * (serialize.py pack_center_stats -> numeric.py pack_bigints): *out (device)
+ * += sum over (group, column) of 8 + (bitlen|T| + 8) / 8 + 1 bytes, where
+ * T = S * 2^(emin + 1074) is the reference's scaled-integer sum of the digit
+ * sums S.  Stream-ordered.                                                  */
+int geek_sum_pack_bytes(const int64_t* digits, uint64_t ngroups, int d, int nd, int emin,
+                        unsigned long long* out, void* stream);
 
 /* Correctly rounded means from the digit sums (numeric.py:43-46).           */
 int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngroups, int d,

@@ -162,6 +162,28 @@ def slot_codes(values: np.ndarray, parts: int) -> np.ndarray:
     return codes
 
 
+def boundary_counts(values: np.ndarray, parts: int, rels=(1e-12, 1e-6)) -> list:
+    """Ids whose projection lies within rel * |boundary| of a rank-split
+    boundary midpoint (the north_star tie window around transform.py:103-109's
+    split): per boundary s the midpoint of the last key of bucket s and the
+    first key of bucket s+1 in the lexsort order; each id is measured against
+    the two boundaries around its key (tests/golden/make_benchlaw_golden.py
+    dumps the reference's own counts the same way)."""
+    n = values.shape[0]
+    order = np.lexsort((np.arange(n), values))
+    vs = values[order]
+    bounds = np.cumsum(split_sizes(n, parts))[:-1]
+    if bounds.size == 0:
+        return [0 for _ in rels]
+    mid = vs[bounds - 1] + 0.5 * (vs[bounds] - vs[bounds - 1])
+    pos = np.searchsorted(mid, values)
+    lo_mid = mid[np.clip(pos - 1, 0, parts - 2)]
+    hi_mid = mid[np.clip(pos, 0, parts - 2)]
+    dist = np.minimum(np.abs(values - lo_mid), np.abs(values - hi_mid))
+    scale = np.maximum(np.abs(lo_mid), np.abs(hi_mid))
+    return [int((dist <= r * scale).sum()) for r in rels]
+
+
 def homo_buckets(X: np.ndarray, m: int, t: int, seed: int = 0, dirs=None):
     """transform_homo (transform.py:112-128) -> list of (table, slot, members)."""
     X = np.asarray(X, dtype=np.float64)

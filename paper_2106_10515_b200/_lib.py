@@ -56,6 +56,9 @@ _SIGS = {
     "geek_fine_layout": (i32, [vp, i32, u64, vp, vp, vp, vp]),
     "geek_rank_split_counted": (i32, [vp, u64, i32, u64, vp, vp, vp, vp, vp]),
     "geek_rank_split": (i32, [vp, u64, i32, u64, vp, vp, vp]),
+    "geek_split_boundary_workspace": (u64, [u64, u64]),
+    "geek_split_boundary_stats": (i32, [vp, u64, i32, u64, vp, u64, vp, C.c_double, C.c_double, vp, vp, u64, vp,
+                                        u64, vp]),
     "geek_rank_split_strided": (i32, [vp, u64, u64, vp, u64, u64, vp]),
     "geek_column_keys": (i32, [vp, i32, u64, u64, u64, vp, vp]),
     "geek_group_rows": (i32, [vp, u64, i32, vp, vp, vp, vp, vp]),
@@ -66,7 +69,8 @@ _SIGS = {
     "geek_pick_representatives": (i32, [vp, vp, vp, vp, u64, vp, vp]),
     "geek_sort_groups": (i32, [vp, vp, u64, vp, vp]),
     "geek_exponent_range": (i32, [vp, i32, u64, i32, vp, vp]),
-    "geek_exact_sums": (i32, [vp, i32, u64, i32, u64, vp, vp, u64, i32, i32, vp, vp]),
+    "geek_exact_sums": (i32, [vp, i32, u64, i32, u64, vp, vp, u64, i32, i32, vp, vp, vp]),
+    "geek_sum_pack_bytes": (i32, [vp, u64, i32, i32, i32, vp, vp]),
     "geek_round_means": (i32, [vp, vp, u64, i32, i32, i32, vp, vp]),
     "geek_assign_l2": (i32, [vp, i32, u64, i32, vp, u64, vp, vp, vp]),
     "geek_assign_last_rechecked": (u64, []),

@@ -61,26 +61,45 @@ __global__ void exponent_range_kernel(const T* X, uint64_t total, int* out) {
 
 constexpr int kSumChunk = 256;  // members per block
 
+// chunk c of the member list covers members [off[g] + 256 (c - coff[g]), ...)
+// of group g, coff = exclusive scan of ceil(size_g / 256): built on the device
+__global__ void chunk_count_kernel(const uint64_t* off, uint64_t ngroups, uint64_t* cnt) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g <= ngroups;
+       g += (uint64_t)gridDim.x * blockDim.x)
+    cnt[g] = g < ngroups ? (off[g + 1] - off[g] + kSumChunk - 1) / kSumChunk : 0;
+}
+
 template <class T, int ND>
 __global__ void exact_sums_kernel(const T* __restrict__ X, uint64_t nrows, int d, uint64_t row_lo,
                                   const uint32_t* __restrict__ flat, const uint64_t* __restrict__ off,
-                                  const uint64_t* __restrict__ chunk_group,
-                                  const uint64_t* __restrict__ chunk_begin, uint64_t nchunks, int emin,
-                                  long long* digits) {
+                                  const uint64_t* __restrict__ coff, uint64_t ngroups, int emin,
+                                  long long* digits, unsigned* nonfinite) {
+  const uint64_t nchunks = coff[ngroups];
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const uint64_t g = chunk_group[ch];
-    const uint64_t b = chunk_begin[ch];
+    uint64_t lo = 0, hi = ngroups;  // last g with coff[g] <= ch
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (coff[mid] <= ch) lo = mid;
+      else hi = mid;
+    }
+    const uint64_t g = lo;
+    const uint64_t b = off[g] + (ch - coff[g]) * kSumChunk;
     const uint64_t e = min(b + (uint64_t)kSumChunk, off[g + 1]);
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       long long acc[ND];
 #pragma unroll
       for (int q = 0; q < ND; ++q) acc[q] = 0;
+      bool bad = false;
       for (uint64_t k = b; k < e; ++k) {
         const uint64_t id = flat[k];
         if (id < row_lo || id >= row_lo + nrows) continue;
         long long M;
         int L;
-        if (!decompose<T>(X[(id - row_lo) * d + c], M, L)) continue;
+        const T xv = X[(id - row_lo) * d + c];
+        if (!decompose<T>(xv, M, L)) {
+          bad |= !isfinite((double)xv);
+          continue;
+        }
         const int sh = L - emin;  // >= 0
         const int q0 = sh >> 5, r = sh & 31;
         const __int128 v = (__int128)M << r;  // < 2^(P+32)
@@ -90,6 +109,7 @@ __global__ void exact_sums_kernel(const T* __restrict__ X, uint64_t nrows, int d
 #pragma unroll
         for (int q = 0; q < ND; ++q) acc[q] += (q == q0) * d0 + (q == q0 + 1) * d1 + (q == q0 + 2) * d2;
       }
+      if (bad && nonfinite) atomicOr(nonfinite, 1u);
       long long* dst = digits + ((uint64_t)g * d + c) * ND;
 #pragma unroll
       for (int q = 0; q < ND; ++q)
@@ -184,11 +204,44 @@ __global__ void round_means_kernel(const long long* digits, const uint64_t* coun
 
 template <class T, int ND>
 static void launch_sums(const void* X, uint64_t nrows, int d, uint64_t row_lo, const uint32_t* flat,
-                        const uint64_t* off, const uint64_t* cg, const uint64_t* cb, uint64_t nch, int emin,
-                        long long* digits, cudaStream_t s) {
+                        const uint64_t* off, const uint64_t* coff, uint64_t ngroups, int emin, long long* digits,
+                        unsigned* nonfinite, cudaStream_t s) {
   int threads = d >= 128 ? 128 : 32 * ((d + 31) / 32);
-  exact_sums_kernel<T, ND><<<grid_for(nch, 1, 148 * 16), threads, 0, s>>>(
-      (const T*)X, nrows, d, row_lo, flat, off, cg, cb, nch, emin, digits);
+  exact_sums_kernel<T, ND><<<148 * 16, threads, 0, s>>>((const T*)X, nrows, d, row_lo, flat, off, coff, ngroups,
+                                                        emin, digits, nonfinite);
+}
+
+// sum over (group, column) of the bytes numeric.pack_bigints spends on the
+// exact sum T = S * 2^(emin + 1074): 8 (length) + (bitlen|T| + 8) / 8 + 1
+__global__ void pack_bytes_kernel(const long long* digits, uint64_t total, int nd, int emin,
+                                  unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (uint64_t gc = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gc < total;
+       gc += (uint64_t)gridDim.x * blockDim.x) {
+    const long long* dg = digits + gc * nd;
+    uint32_t w[kMaxWords];
+    const int nw = nd + 2;
+    __int128 carry = 0;
+    for (int q = 0; q < nw; ++q) {
+      __int128 v = carry + (q < nd ? (__int128)dg[q] : (__int128)0);
+      w[q] = (uint32_t)(v & 0xFFFFFFFF);
+      carry = v >> 32;
+    }
+    if (carry < 0 || (w[nw - 1] & 0x80000000u)) {
+      uint64_t c = 1;
+      for (int q = 0; q < nw; ++q) {
+        uint64_t v = (uint64_t)(~w[q]) + c;
+        w[q] = (uint32_t)v;
+        c = v >> 32;
+      }
+    }
+    int top = nw - 1;
+    while (top >= 0 && w[top] == 0) --top;
+    const long long bl = top < 0 ? 0 : (long long)top * 32 + (32 - __clz(w[top])) + emin + 1074;
+    acc += 8 + (unsigned long long)((bl + 8) / 8 + 1);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 }  // namespace geek
@@ -230,36 +283,26 @@ int geek_exponent_range(const void* X, int dtype, uint64_t n, int d, int* out_ho
 
 int geek_exact_sums(const void* X, int dtype, uint64_t nrows, int d, uint64_t row_lo, const uint32_t* flat,
                     const uint64_t* offsets, uint64_t ngroups, int emin, int nd, int64_t* digits,
-                    void* stream) {
+                    unsigned* nonfinite, void* stream) {
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 or 1");
   GEEK_REQUIRE(nd >= 3 && nd <= 40, "digit count %d outside [3, 40]", nd);
   if (ngroups == 0) return GEEK_OK;
-  // chunk table: (group, begin) for every kSumChunk members
-  std::vector<uint64_t> off(ngroups + 1);
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(off.data(), offsets, (ngroups + 1) * 8, cudaMemcpyDeviceToHost, s));
-  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint64_t> cg, cb;
-  for (uint64_t g = 0; g < ngroups; ++g)
-    for (uint64_t b = off[g]; b < off[g + 1]; b += kSumChunk) {
-      cg.push_back(g);
-      cb.push_back(b);
-    }
-  const uint64_t nch = cg.size();
-  if (nch == 0) return GEEK_OK;
-  Scratch tab;
-  GEEK_TRY(tab.alloc(nch * 16, s));
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(tab.ptr, cg.data(), nch * 8, cudaMemcpyHostToDevice, s));
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(tab.as<uint64_t>() + nch, cb.data(), nch * 8, cudaMemcpyHostToDevice, s));
-  const uint64_t* dcg = tab.as<uint64_t>();
-  const uint64_t* dcb = dcg + nch;
+  // chunk offsets on the device: no host round trip, stream-ordered
+  Scratch cnt, coff;
+  GEEK_TRY(cnt.alloc((ngroups + 1) * 8, s));
+  GEEK_TRY(coff.alloc((ngroups + 1) * 8, s));
+  chunk_count_kernel<<<grid_for(ngroups + 1, 256), 256, 0, s>>>(offsets, ngroups, cnt.as<uint64_t>());
+  GEEK_CHECK_LAUNCH();
+  GEEK_TRY(exclusive_scan_u64(cnt.as<uint64_t>(), coff.as<uint64_t>(), ngroups + 1, s));
+  const uint64_t* dco = coff.as<uint64_t>();
   long long* dg = reinterpret_cast<long long*>(digits);
-#define GEEK_SUMS_CASE(NDV)                                                                     \
-  case NDV:                                                                                     \
-    if (dtype == 0)                                                                             \
-      launch_sums<float, NDV>(X, nrows, d, row_lo, flat, offsets, dcg, dcb, nch, emin, dg, s);  \
-    else                                                                                        \
-      launch_sums<double, NDV>(X, nrows, d, row_lo, flat, offsets, dcg, dcb, nch, emin, dg, s); \
+#define GEEK_SUMS_CASE(NDV)                                                                           \
+  case NDV:                                                                                           \
+    if (dtype == 0)                                                                                   \
+      launch_sums<float, NDV>(X, nrows, d, row_lo, flat, offsets, dco, ngroups, emin, dg, nonfinite, s);  \
+    else                                                                                              \
+      launch_sums<double, NDV>(X, nrows, d, row_lo, flat, offsets, dco, ngroups, emin, dg, nonfinite, s); \
     break;
   switch (nd) {
     GEEK_SUMS_CASE(3)
@@ -276,7 +319,18 @@ int geek_exact_sums(const void* X, int dtype, uint64_t nrows, int d, uint64_t ro
   }
 #undef GEEK_SUMS_CASE
   GEEK_CHECK_LAUNCH();
-  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));  // chunk table is freed with `tab`
+  return GEEK_OK;
+}
+
+int geek_sum_pack_bytes(const int64_t* digits, uint64_t ngroups, int d, int nd, int emin,
+                        unsigned long long* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  GEEK_REQUIRE(nd >= 1 && nd + 2 <= kMaxWords, "digit count %d too large", nd);
+  const uint64_t total = ngroups * (uint64_t)d;
+  if (total == 0) return GEEK_OK;
+  pack_bytes_kernel<<<grid_for(total, 128), 128, 0, s>>>(reinterpret_cast<const long long*>(digits), total, nd,
+                                                         emin, out);
+  GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 

@@ -30,13 +30,13 @@ from .assignment import assign_cat_device, assign_l2_device, assign_sparse_devic
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
-from .numeric import (digit_count, exponent_range, label_mode_centers, label_sparse_counts, label_sums,
-                      mode_centers, mode_counts, partial_sums, round_means, sparse_counts)
+from .numeric import (center_stats_bytes, digit_count, exponent_range, label_mode_centers, label_sparse_counts,
+                      label_sums, mode_centers, mode_counts, partial_sums, round_means, sparse_counts)
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
 from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
-                        discretize_numeric, even_partition_sizes, project_keys, rank_split_codes,
-                        signature_bucket_codes)
+                        discretize_numeric, even_partition_sizes, project_keys, projection_tolerance,
+                        rank_split_codes, signature_bucket_codes, split_boundary_stats)
 
 __all__ = ["EngineError", "WorkerConfig", "PipelineConfig", "PipelineResult", "split_data", "run_pipeline"]
 
@@ -490,7 +490,84 @@ def _fallback_groups(n, g, seed, warnings):
     return GroupSet.from_host([np.array([p]) for p in picks])
 
 
-def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: PipelineConfig, comm: _Comm):
+class _Logical:
+    """Transport accounting of the reference's g in-process workers
+    (engine.py:79-104 Transport, serialize.py message bodies) when the g
+    logical workers share one process: the bytes each message kind would
+    carry, so `transport_bytes` reads as the reference's at G = 1."""
+
+    def __init__(self, n: int, g: int, m: int):
+        self.n, self.g, self.m = n, g, m
+        self.spans = split_data(n, g)
+        self.bytes = {}
+        self._dev = None
+
+    def add(self, kind, nbytes):
+        if self.g > 1:
+            self.bytes[kind] = self.bytes.get(kind, 0) + int(nbytes)
+
+    def fragments(self, per_row: int, head: int):
+        """BucketShard (engine.py:198-207): worker w sends table j to owner
+        j % g != w; pack_fragment = 17 bytes + pack_array(body)."""
+        for w, (lo, hi) in enumerate(self.spans):
+            own = len(range(w, self.m, self.g))
+            self.add("BucketShard", (self.m - own) * (17 + head + per_row * (hi - lo)))
+
+    def seed_groups(self, groups: GroupSet):
+        """SeedGroups (engine.py:285-287): every worker broadcasts its local
+        groups (8 + per group pack_array(int64 members) = 18 + 8 len)."""
+        total = int(groups.off[-1].item()) if groups.count else 0
+        self.add("SeedGroups", (self.g - 1) * (8 * self.g + 18 * groups.count + 8 * total))
+
+    def center_stats(self, k: int, per_group_fixed: int, value_bytes: int = 0):
+        """LocalCenters (engine.py:486-490): every worker broadcasts 8 + per
+        group (qB + body) bytes; value_bytes = the exact sums' pack_bigints
+        bytes summed over workers (dense) or 0 (fixed-size count arrays)."""
+        self.add("LocalCenters", (self.g - 1) * (self.g * (8 + per_group_fixed * k) + value_bytes))
+
+    def device_counter(self):
+        if self._dev is None:
+            self._dev = _lib.zeros(1, torch.int64)
+        return self._dev
+
+    def flush_device(self, kind):
+        if self._dev is not None and self.g > 1:
+            self.add(kind, (self.g - 1) * int(self._dev.item()))
+            self._dev.zero_()
+
+
+def _check_budget(config: PipelineConfig, n: int):
+    """engine.py:359-366 (_chunk_tables): a table's member lists take 8 n
+    bytes; a budget below one table is an error of worker 0's seeding stage
+    (worker 0 always owns table 0).  Larger budgets only change the
+    reference's load chunking, never the result (engine.py:244-248)."""
+    budget = config.workers.memory_budget
+    if 8 * n > budget:
+        raise EngineError(f"stage seeding, worker 0: memory budget {budget} below single table of {8 * n} bytes")
+
+
+def _worker_digits(X_local, groups, emin, nd, logical, nonfinite, labels=None, k=None, keep=None):
+    """Exact digit sums as the reference's workers form them (one partial per
+    logical worker, engine.py:299-311 / 481-516), summed; each worker's
+    pack_bigints bytes are accumulated for the LocalCenters accounting."""
+    if logical is None or logical.g == 1:
+        if labels is None:
+            return partial_sums(X_local, groups, emin, nd, 0, nonfinite=nonfinite)
+        return label_sums(X_local, labels, k, emin, nd)
+    ctr = logical.device_counter()
+    total = None
+    for lo, hi in logical.spans:
+        if labels is None:
+            part = partial_sums(X_local[lo:hi], groups, emin, nd, lo, nonfinite=nonfinite)
+        else:
+            part = label_sums(X_local[lo:hi], labels[lo:hi], k, emin, nd)
+        center_stats_bytes(part if keep is None else part[keep].contiguous(), emin, ctr)
+        total = part if total is None else total.add_(part)
+    return total
+
+
+def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: PipelineConfig, comm: _Comm,
+                    diagnostics: bool = False):
     g = config.workers.num_workers
     p: HomoTransformParams = config.homo
     sp: SeedingParams = config.seeding
@@ -504,6 +581,9 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
     tm = _Timer()
     A = p.direction_matrix(d)
     own = [j for j in range(m) if j % G == rank]
+    logical = None if comm.on else _Logical(n, g, m)
+    if logical:
+        logical.fragments(8, 18)  # float64 projection fragments (pack_array 1-D f8)
     keys_own, counted = None, None
     with tm.stage("transform"):
         exprange = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32,
@@ -534,8 +614,17 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
             codes = rank_split_counted(keys_own, t, counted[0], counted[1], stats)
         else:
             codes = rank_split_codes(keys_own.contiguous(), t, stats)
-        del keys_own, counted
         info["rank_split"] = stats
+    if diagnostics:  # boundary exceptions of the split (north_star tie tolerance)
+        with tm.stage("diagnostics"):
+            xe = exprange[1:2].to(torch.int64)
+            if comm.on:  # not a reference message kind: kept out of transport_bytes
+                dist.all_reduce(xe, op=dist.ReduceOp.MAX)
+            if own:
+                tol = projection_tolerance(A[own], int(xe.item()))
+                info["split_boundary"] = split_boundary_stats(keys_own, codes, t, tol, tables=own)
+    del keys_own, counted
+    _check_budget(config, n)
     with tm.stage("seeding"):
         if own:
             bt = BucketTable(codes, n, [t] * len(own), "rank", even=True)
@@ -544,15 +633,23 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         else:
             local = GroupSet.empty()
         merged = _merge_groups(comm, local)
+        if logical:
+            logical.seed_groups(merged)
         groups = dedup_device(merged, sp, n)
         if groups.count == 0:
             groups = _fallback_groups(n, g, config.fallback_seed, warnings)
+    nonfinite = _lib.zeros(1, torch.int32)
     with tm.stage("centers"):
         r = torch.stack([-exprange[0], exprange[1]]).to(torch.int64)
         comm.all_reduce(r, dist.ReduceOp.MAX, "LocalCenters")
         emin, emax = -int(r[0].item()), int(r[1].item())
         nd = digit_count(emin, emax)
-        digits = partial_sums(X_local, groups, emin, nd, row_lo)
+        if logical:
+            digits = _worker_digits(X_local, groups, emin, nd, logical, nonfinite)
+            logical.center_stats(groups.count, 25)
+            logical.flush_device("LocalCenters")
+        else:
+            digits = partial_sums(X_local, groups, emin, nd, row_lo, nonfinite=nonfinite)
         comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
         C = round_means(digits, groups.sizes(), emin, nd)
     with tm.stage("assign"):
@@ -578,15 +675,25 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         radii, sizes, obj = reduce_assignment(labels, best, groups.count)
     for _ in range(config.passes):  # _refine_distributed (engine.py:519-537)
         with tm.stage("centers"):
-            digits = label_sums(X_local, labels, C.shape[0], emin, nd)
-            comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
             keep = torch.nonzero(sizes > 0).flatten()  # empty clusters are dropped
+            if logical:
+                digits = _worker_digits(X_local, None, emin, nd, logical, None, labels=labels, k=C.shape[0],
+                                        keep=keep)
+                logical.center_stats(keep.numel(), 25)
+                logical.flush_device("LocalCenters")
+            else:
+                digits = label_sums(X_local, labels, C.shape[0], emin, nd)
+            comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
             weights = sizes[keep].contiguous()
             C = round_means(digits[keep].contiguous(), weights, emin, nd)
         with tm.stage("assign"):
             labels, best = assign_l2_device(X_local, C)
             radii, sizes, obj = reduce_assignment(labels, best, C.shape[0])
     timings = tm.finish()
+    if comm.on:
+        dist.all_reduce(nonfinite, op=dist.ReduceOp.MAX)
+    if int(nonfinite.item()):  # numeric.py:24-25 (exact_column_sums)
+        raise InvalidInput("non-finite value in exact sum")
     sizes_h = weights.cpu().numpy()
 
     def centers():
@@ -595,7 +702,7 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
 
     gather = (lambda: comm.all_gather_var(labels, "Assignments")) if comm.on else None
     return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings,
-                          dict(comm.bytes), warnings, info, gather)
+                          dict(comm.bytes) if comm.on else dict(logical.bytes), warnings, info, gather)
 
 
 def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
@@ -627,16 +734,25 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
     n = data.n
     if g > n:
         raise EngineError(f"stage setup: cannot split {n} objects across {g} workers")
+    logical = _Logical(n, g, mp.num_tables)
+    logical.fragments(8 * mp.num_hashes, 26)  # signature fragments (pack_array 2-D u8)
     with tm.stage("transform"):
         codes, tsizes = signature_bucket_codes(mp.scheme(universe), flat, off, n)
         bt = BucketTable(codes, n, tsizes, "sig", even=False)
+    _check_budget(config, n)
     with tm.stage("seeding"):
         owner = _lib.to_dev(np.concatenate([np.full(ts, j % g, dtype=np.int32) for j, ts in enumerate(tsizes)]))
         local, _, _ = silk_votes(bt, sp, n, owner, info)
+        logical.seed_groups(local)
         groups = dedup_device(local, sp, n)
         if groups.count == 0:
             groups = _fallback_groups(n, g, config.fallback_seed, warnings)
+    # LocalCenters bodies: per group qB + pack_array of the count table
+    # (categorical [dim, code_space] int64, sparse [universe] int64)
+    stat_fixed = (9 + 26 + 8 * data.dim * data.code_space if isinstance(data, CategoricalData)
+                  else 9 + 18 + 8 * data.universe)
     with tm.stage("centers"):
+        logical.center_stats(groups.count, stat_fixed)
         if isinstance(data, CategoricalData):
             M = mode_centers(data.device_codes(), data.code_space, groups)
         else:
@@ -653,6 +769,7 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
     for _ in range(config.passes):  # _refine_distributed (engine.py:519-537) on one device
         with tm.stage("centers"):
             keep = torch.nonzero(sizes > 0).flatten()
+            logical.center_stats(keep.numel(), stat_fixed)
             weights = sizes[keep].contiguous()
             if isinstance(data, CategoricalData):
                 M = label_mode_centers(data.device_codes(), data.code_space, labels, M.shape[0], keep)
@@ -673,11 +790,11 @@ def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
         Mh = M.cpu().numpy()
         return [CentralVector("mode", Mh[i], int(sizes_h[i])) for i in range(Mh.shape[0])]
 
-    return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings, {}, warnings,
-                          info)
+    return PipelineResult(centers, groups, labels, best, radii, sizes, float(obj.item()), timings,
+                          dict(logical.bytes), warnings, info)
 
 
-def run_pipeline(data, config: PipelineConfig) -> PipelineResult:
+def run_pipeline(data, config: PipelineConfig, *, diagnostics: bool = False) -> PipelineResult:
     """transform -> bucket sync -> seeding -> centers -> assignment (engine.py:395-472).
 
     Under an initialised torch.distributed group of G ranks every rank calls
@@ -693,13 +810,14 @@ def run_pipeline(data, config: PipelineConfig) -> PipelineResult:
             raise EngineError(f"stage setup: cannot split {n} objects across {config.workers.num_workers} workers")
         lo, hi = split_data(n, comm.G)[comm.rank] if comm.on else (0, n)
         X = data.device_vectors()[lo:hi].contiguous() if comm.on else data.device_vectors()
-        return _dense_pipeline(X, n, lo, config, comm)
+        return _dense_pipeline(X, n, lo, config, comm, diagnostics)
     if config.transform_kind in ("mixed", "sparse"):
         return _signature_pipeline(data, config, comm)
     raise EngineError(f"stage setup: unknown transform kind {config.transform_kind!r}")
 
 
-def run_pipeline_shard(X_local: torch.Tensor, n: int, config: PipelineConfig) -> PipelineResult:
+def run_pipeline_shard(X_local: torch.Tensor, n: int, config: PipelineConfig, *,
+                       diagnostics: bool = False) -> PipelineResult:
     """Dense pipeline where each rank holds its contiguous shard (rows
     split_data(n, G)[rank]), on its GPU or in (pinned) host memory -- host
     rows are streamed to the GPU in chunks that are projected as they land."""
@@ -707,4 +825,4 @@ def run_pipeline_shard(X_local: torch.Tensor, n: int, config: PipelineConfig) ->
     lo, hi = split_data(n, comm.G)[comm.rank]
     if X_local.shape[0] != hi - lo:
         raise EngineError(f"stage setup: rank {comm.rank} holds {X_local.shape[0]} rows, expected {hi - lo}")
-    return _dense_pipeline(X_local, n, lo, config, comm)
+    return _dense_pipeline(X_local, n, lo, config, comm, diagnostics)

@@ -37,15 +37,27 @@ def digit_count(emin: int, emax: int) -> int:
     raise InvalidInput("exponent range too wide for exact sums")
 
 
-def partial_sums(X: torch.Tensor, groups: GroupSet, emin: int, nd: int, row_lo: int = 0) -> torch.Tensor:
+def partial_sums(X: torch.Tensor, groups: GroupSet, emin: int, nd: int, row_lo: int = 0, digits=None,
+                 nonfinite=None) -> torch.Tensor:
     """int64 [k, d, nd] exact digit sums over the members that are rows
-    [row_lo, row_lo + X.shape[0]) of the global id space."""
+    [row_lo, row_lo + X.shape[0]) of the global id space (added into
+    `digits` when given).  `nonfinite` (int32 [1] on the device) is set to 1
+    if a member coordinate is NaN / inf (numeric.py:24-25 raises there)."""
     k, d = groups.count, X.shape[1]
-    digits = _lib.zeros(max(1, k * d * nd), torch.int64)
+    if digits is None:
+        digits = _lib.zeros(max(1, k * d * nd), torch.int64)[: k * d * nd].view(k, d, nd)
     if k:
         _lib.call("geek_exact_sums", _lib.ptr(X), _lib.dtype_code(X), X.shape[0], d, row_lo, _lib.ptr(groups.flat),
-                  _lib.ptr(groups.off), k, emin, nd, _lib.ptr(digits), _lib.stream())
-    return digits[: k * d * nd].view(k, d, nd)
+                  _lib.ptr(groups.off), k, emin, nd, _lib.ptr(digits), _lib.ptr(nonfinite), _lib.stream())
+    return digits
+
+
+def center_stats_bytes(digits: torch.Tensor, emin: int, out: torch.Tensor):
+    """out (int64 [1], device) += the bytes the reference's pack_bigints
+    spends on these exact sums (engine.py:488-490 LocalCenters accounting)."""
+    k, d, nd = digits.shape
+    if k:
+        _lib.call("geek_sum_pack_bytes", _lib.ptr(digits.contiguous()), k, d, nd, emin, _lib.ptr(out), _lib.stream())
 
 
 def round_means(digits: torch.Tensor, counts: torch.Tensor, emin: int, nd: int) -> torch.Tensor:
@@ -60,7 +72,11 @@ def round_means(digits: torch.Tensor, counts: torch.Tensor, emin: int, nd: int) 
 def dense_centers(X: torch.Tensor, groups: GroupSet) -> torch.Tensor:
     emin, emax = exponent_range(X)
     nd = digit_count(emin, emax)
-    return round_means(partial_sums(X, groups, emin, nd), groups.sizes(), emin, nd)
+    bad = _lib.zeros(1, torch.int32)
+    digits = partial_sums(X, groups, emin, nd, nonfinite=bad)
+    if int(bad.item()):
+        raise InvalidInput("non-finite value in exact sum")
+    return round_means(digits, groups.sizes(), emin, nd)
 
 
 def mode_counts(codes: torch.Tensor, code_space: int, groups: GroupSet, row_lo: int = 0) -> torch.Tensor:

@@ -143,6 +143,46 @@ def rank_split_codes(keys: torch.Tensor, t: int, stats=None) -> torch.Tensor:
     return codes[: n * m].view(n, m)
 
 
+def projection_tolerance(A: np.ndarray, xmax_exp: int) -> np.ndarray:
+    """Per-table bound on |K1 key - reference key| (transform.py:125 / engine.py:180
+    form X @ a with OpenBLAS dgemv; K1 with DMMA FMA chains).  Any float64
+    summation order of d products is within gamma_d * sum_k |x_k a_k| of the
+    exact dot product (gamma_d = d u / (1 - d u), u = 2^-53), and
+    sum_k |x_k a_k| <= 2^xmax_exp * |a|_1 when every |x_k| < 2^xmax_exp, so
+    the two keys differ by at most twice that."""
+    A = np.asarray(A, dtype=np.float64)
+    d = A.shape[1]
+    u = 2.0 ** -53
+    gamma = d * u / (1.0 - d * u)
+    return 2.0 * gamma * np.ldexp(1.0, int(xmax_exp)) * np.abs(A).sum(axis=1) * (1.0 + 4 * u)
+
+
+def split_boundary_stats(keys: torch.Tensor, codes: torch.Tensor, t: int, tol: np.ndarray,
+                         rel=(1e-12, 1e-6), cap: int = 4096, tables=None) -> dict:
+    """Count the ids whose key lies near a rank-split boundary (north_star's
+    tie tolerance): `ambiguous` within the float64 order bound `tol` (their
+    code may differ from the reference's; listed as (table, id) in
+    `ambiguous_ids`), `within_rel` within rel * |boundary| for each rel."""
+    m, n = keys.shape
+    L = _lib.lib()
+    wsb = int(L.geek_split_boundary_workspace(m, t))
+    ws = _lib.empty(max(1, (wsb + 7) // 8), torch.int64)
+    tol_d = _lib.to_dev(np.ascontiguousarray(tol, dtype=np.float64))
+    counts = _lib.zeros(4, torch.int64)
+    lst = _lib.empty(max(2, 2 * cap), torch.int32)
+    _lib.call("geek_split_boundary_stats", _lib.ptr(keys), n, m, t, _lib.ptr(codes), codes.shape[1],
+              _lib.ptr(tol_d), float(rel[0]), float(rel[1]), _lib.ptr(counts), _lib.ptr(lst), cap, _lib.ptr(ws),
+              wsb, _lib.stream())
+    c = counts.cpu().numpy()
+    k = int(min(c[3], cap))
+    ids = lst[: 2 * k].view(k, 2).cpu().numpy().astype(np.int64)
+    if tables is not None and k:
+        ids[:, 0] = np.asarray(tables)[ids[:, 0]]
+    return dict(ambiguous=int(c[0]), within_rel={f"{rel[0]:g}": int(c[1]), f"{rel[1]:g}": int(c[2])},
+                ambiguous_ids=ids, tol_max=float(np.max(tol)) if len(tol) else 0.0,
+                listed_complete=bool(c[3] <= cap))
+
+
 def homo_codes(X: torch.Tensor, params: HomoTransformParams, stats=None) -> torch.Tensor:
     n, d = X.shape
     t = params.buckets_per_table

@@ -114,13 +114,27 @@ def test_rank_split_random_vs_oracle(n, t, dup):
     if dup:  # giant tie classes exercise the sorted fallback
         X[: n // 2] = X[0]
         X[n // 2:, 0] = 0.0
-    p = G.HomoTransformParams(3, t, seed=11)
-    bt = G.transform_homo(G.DenseData(X), p)
+    from paper_2106_10515_b200 import transform as T
+
     A = O.directions(11, 3, 5)
+    assert np.array_equal(A, G.HomoTransformParams(3, t, seed=11).direction_matrix(5))
+    Xd = torch.from_numpy(X).cuda()
+    keys = T.project_keys(Xd, A)
+    codes = T.rank_split_codes(keys, t)
+    tol = T.projection_tolerance(A, int(np.frexp(np.abs(X).max())[1]))
+    st = T.split_boundary_stats(keys, codes, t, tol)
     want = np.stack([O.slot_codes(X.astype(np.float64) @ A[j], t) for j in range(3)])
-    got = bt.codes_host()
-    # float64 projection order may differ from BLAS only on exact near-ties
-    assert (got != want).sum() <= 2, (got != want).sum()
+    got = codes.cpu().numpy().T
+    # the float64 projection order differs from BLAS, so a code may differ only
+    # for an id the boundary pass reports as ambiguous (within the order bound)
+    bad = set(zip(*np.nonzero(got != want)))
+    amb = set(map(tuple, st["ambiguous_ids"].tolist()))
+    assert st["listed_complete"] and bad <= amb, (len(bad), st["ambiguous"])
+    assert st["ambiguous"] == len(amb)
+    if not dup:  # window counts against the oracle's (searchsorted on the exact lexsort)
+        V = X.astype(np.float64) @ A.T
+        want_rel = np.sum([O.boundary_counts(V[:, j], t) for j in range(3)], axis=0)
+        assert [st["within_rel"]["1e-12"], st["within_rel"]["1e-06"]] == want_rel.tolist()
 
 
 @pytest.mark.parametrize("name", ["c06", "small"])
