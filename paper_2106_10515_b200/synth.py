@@ -1,8 +1,9 @@
-"""Synthetic inputs with the reference generator's law (synth.py:39-104).
+"""Synthetic inputs with the reference generator's law (synth.py:1-139).
 
-`gaussian_mixture_host` reproduces gen_synthetic("gaussian-mixture") exactly
-(same numpy stream) for parity-sized inputs; `gaussian_mixture_device`
-draws the same law at benchmark scale directly into HBM: cluster means from
+`gen_synthetic` reproduces the reference's generator for all three kinds
+(same numpy stream, so `gen` output files are byte-identical) -- host work
+sized for parity fixtures and the CLI; `gaussian_mixture_device` draws the
+gaussian-mixture law at benchmark scale directly into HBM: cluster means from
 the host spiral (`spread_means`), labels uniform then sorted (so ids are
 cluster-contiguous, as in the reference), x = mean + N(0, 1) from torch's
 Philox generator, float32.
@@ -10,8 +11,83 @@ Philox generator, float32.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
+
+from .data import CategoricalData, DenseData, SparseData
+from .errors import InvalidInput
+
+KINDS = ("gaussian-mixture", "categorical-patterns", "sparse-overlap")
+
+
+@dataclass(frozen=True)
+class SyntheticSpec:
+    """synth.py:17-30"""
+
+    kind: str
+    n: int
+    dim: int
+    clusters: int
+    separation: float = 10.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise InvalidInput(f"unknown synthetic kind {self.kind!r}")
+        if self.n < self.clusters or self.clusters < 1:
+            raise InvalidInput("need n >= clusters >= 1")
+
+
+@dataclass(frozen=True)
+class SyntheticResult:
+    data: object
+    labels: np.ndarray
+    true_radii: np.ndarray
+
+
+def gen_synthetic(spec: SyntheticSpec) -> SyntheticResult:
+    """synth.py:39-83: labels uniform then sorted (every cluster populated),
+    then the kind's law, drawn from one default_rng(seed) stream."""
+    rng = np.random.default_rng(spec.seed)
+    labels = np.sort(rng.integers(0, spec.clusters, spec.n))
+    labels[: spec.clusters] = np.arange(spec.clusters)
+    labels = np.sort(labels)
+    k = spec.clusters
+    if spec.kind == "gaussian-mixture":
+        means = spread_means(k, spec.dim, spec.separation, rng)
+        points = means[labels] + rng.standard_normal((spec.n, spec.dim))
+        radii = np.zeros(k)
+        for j in range(k):
+            radii[j] = np.sqrt(((points[labels == j] - means[j]) ** 2).sum(-1)).max()
+        return SyntheticResult(DenseData(points), labels, radii)
+    if spec.kind == "categorical-patterns":
+        code_space = max(k * 2, 8)
+        patterns = rng.integers(0, code_space, (k, spec.dim))
+        codes = patterns[labels].copy()
+        flips = rng.random((spec.n, spec.dim)) < (1.0 / max(spec.separation, 1.1))
+        codes[flips] = rng.integers(0, code_space, int(flips.sum()))
+        radii = np.zeros(k)
+        for j in range(k):
+            match = (codes[labels == j] == patterns[j]).sum(-1)
+            radii[j] = (1.0 - match / (2 * spec.dim - match)).max()
+        return SyntheticResult(CategoricalData(codes.astype(np.int32), code_space), labels, radii)
+    universe = max(spec.dim, 16)
+    base_size = max(universe // (k * 4), 8)
+    bases = [np.sort(rng.choice(universe, base_size, replace=False)) for _ in range(k)]
+    sets = []
+    for lab in labels:
+        base = bases[lab]
+        mask = rng.random(base.size) < 0.95
+        kept = base[mask] if mask.any() else base[:1]
+        extras = rng.choice(universe, max(1, int(base_size * 0.05)), replace=False)
+        sets.append(np.union1d(kept, extras))
+    radii = np.zeros(k)
+    for i, lab in enumerate(labels):
+        inter = np.intersect1d(sets[i], bases[lab], assume_unique=True).size
+        radii[lab] = max(radii[lab], 1.0 - inter / (sets[i].size + bases[lab].size - inter))
+    return SyntheticResult(SparseData(sets, universe), labels, radii)
 
 
 def spread_means(k: int, dim: int, separation: float, rng) -> np.ndarray:
