@@ -133,7 +133,8 @@ int geek_rank_split(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_
  * bucket boundary s, midpoint = (max key of bucket s + min key of bucket s+1)/2;
  * counts[0] = ids whose key lies within tol_abs[j] (device double [m]) of a
  * neighbouring midpoint -- the only ids whose code may differ from the
- * reference's; counts[1] / counts[2] = ids within rel_a / rel_b * |midpoint|;
+ * reference's (a boundary whose two keys are equal is decided by id, so ids
+ * holding exactly that key are not counted there); counts[1] / counts[2] = ids within rel_a / rel_b * |midpoint|;
  * counts[3] = entries offered to list.  list (device uint32 [cap][2]) receives
  * (table, id) of the tol_abs ids.  keys [m][n] as geek_project_keys writes
  * them, codes[i*code_stride + j] as geek_rank_split writes them.  Scratch:

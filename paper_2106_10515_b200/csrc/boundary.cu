@@ -76,6 +76,8 @@ __global__ void __launch_bounds__(256) boundary_count_kernel(const uint64_t* __r
                                                              const uint32_t* __restrict__ codes, uint64_t n,
                                                              int m, uint64_t stride, uint64_t t,
                                                              const double* __restrict__ mid,
+                                                             const unsigned long long* __restrict__ bmin,
+                                                             const unsigned long long* __restrict__ bmax,
                                                              const double* __restrict__ tol_abs, double rel_a,
                                                              double rel_b, unsigned long long* counts,
                                                              uint32_t* list, uint64_t cap) {
@@ -89,21 +91,30 @@ __global__ void __launch_bounds__(256) boundary_count_kernel(const uint64_t* __r
     for (int j = 0; j < m; ++j) {
       bool amb = false, r1 = false, r2 = false;
       if (ok && nb > 0) {
-        const double v = key_to_f64(__ldg(keys + (uint64_t)j * n + i));
+        const uint64_t key = __ldg(keys + (uint64_t)j * n + i);
+        const double v = key_to_f64(key);
         const uint32_t c = __ldg(codes + i * stride + j);
         const double* mj = mid + (uint64_t)j * nb;
-        double dist = INFINITY, scale = 0.0;
+        const unsigned long long* lo = bmax + (uint64_t)j * t;  // lo[s] / hi[s+1]: keys either side of s
+        const unsigned long long* hi = bmin + (uint64_t)j * t;
+        double dist = INFINITY, scale = 0.0, adist = INFINITY;
         if (c > 0) {
           const double b = __ldg(mj + c - 1);
           dist = fabs(v - b);
           scale = fabs(b);
+          // a boundary whose two keys are EQUAL is decided by id in any
+          // implementation that computes equal keys for them (identical rows):
+          // ids holding that exact key are not ambiguous there
+          if (!(__ldg(lo + c - 1) == __ldg(hi + c) && key == __ldg(hi + c))) adist = dist;
         }
         if ((uint64_t)c < nb) {
           const double b = __ldg(mj + c);
-          dist = fmin(dist, fabs(v - b));
+          const double dd = fabs(v - b);
+          dist = fmin(dist, dd);
           scale = fmax(scale, fabs(b));
+          if (!(__ldg(lo + c) == __ldg(hi + c + 1) && key == __ldg(lo + c))) adist = fmin(adist, dd);
         }
-        amb = dist <= __ldg(tol_abs + j);
+        amb = adist <= __ldg(tol_abs + j);
         r1 = dist <= rel_a * scale;
         r2 = dist <= rel_b * scale;
         if (amb) {
@@ -157,8 +168,8 @@ int geek_split_boundary_stats(const uint64_t* keys, uint64_t n, int m, uint64_t 
   GEEK_CHECK_LAUNCH();
   boundary_mid_kernel<<<grid_for((uint64_t)m * (t - 1), 256), 256, 0, s>>>(bmin, bmax, m, t, mid);
   GEEK_CHECK_LAUNCH();
-  boundary_count_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(keys, codes, n, m, code_stride, t, mid, tol_abs,
-                                                                   rel_a, rel_b, counts, list, cap);
+  boundary_count_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(keys, codes, n, m, code_stride, t, mid, bmin,
+                                                                   bmax, tol_abs, rel_a, rel_b, counts, list, cap);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
