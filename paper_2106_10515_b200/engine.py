@@ -18,6 +18,7 @@ sums are all-reduced; radii (max) and sizes (sum) are all-reduced.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -192,8 +193,41 @@ class _Timer:
 
 
 _SYMM = {}
-_ROUTED_OFF = [bool(__import__('os').environ.get('GEEK_NO_ROUTED'))]
-_FUSED_COUNTS = bool(__import__('os').environ.get('GEEK_FUSED_COUNTS'))
+_SYMM_DECISION = {}
+_FUSED_COUNTS = bool(os.environ.get('GEEK_FUSED_COUNTS'))
+
+
+def _symm_ready(comm: _Comm, rows: int, cols: int, device) -> bool:
+    """Decide TOGETHER whether the peer-mapped key buffers can be used.
+
+    Every rank checks locally (symmetric-memory module, all ranks on this
+    node, GEEK_NO_ROUTED unset) and the flags are MIN-reduced; only if all
+    ranks agree does the (collective) rendezvous run, and its outcome is
+    MIN-reduced again.  So either every rank takes the routed projection or
+    every rank takes the all_to_all path -- no rank can fall back alone after
+    a barrier.  The decision is cached per shape, identically on every rank."""
+    key = (comm.G, rows, cols, device.index)
+    if key in _SYMM_DECISION:
+        return _SYMM_DECISION[key]
+    ok = not os.environ.get("GEEK_NO_ROUTED")
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+        ok = ok and int(os.environ.get("LOCAL_WORLD_SIZE", comm.G)) == comm.G
+    except Exception:
+        ok = False
+    flag = torch.tensor([int(ok)], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    ok = bool(flag.item())
+    if ok:
+        try:
+            _symm_keys(comm, rows, cols, device)
+        except Exception:
+            ok = False
+        flag.fill_(int(ok))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = bool(flag.item())
+    _SYMM_DECISION[key] = ok
+    return ok
 
 
 def _symm_keys(comm: _Comm, rows: int, cols: int, device):
@@ -331,7 +365,7 @@ def _stream_host_rows(X_host: torch.Tensor, A: np.ndarray, n: int, row_lo: int, 
         X_dev = torch.empty(X_host.shape, dtype=X_host.dtype, device=dev)
         _XBUF[key] = X_dev
     fused = (X_host.dtype == torch.float32 and d % 4 == 0 and 4 <= d <= 128 and 1 <= m <= 48 and G <= 8
-             and not _ROUTED_OFF[0] and n_local > 0)
+             and (G == 1 or _symm_ready(comm, -(-m // G), n, dev)))
     main = torch.cuda.current_stream()
     if not fused:
         X_dev.copy_(X_host, non_blocking=True)
@@ -590,17 +624,12 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
                                 device=torch.device("cuda", torch.cuda.current_device()))
         if not X_local.is_cuda:  # host rows: copied in chunks, each projected as it lands
             X_local, keys_own = _stream_host_rows(X_local, A, n, row_lo, comm, exprange, own)
-        if keys_own is None and _routable(X_local, m, G) and not _ROUTED_OFF[0] and (comm.on or _FUSED_COUNTS):
-            try:
-                if _FUSED_COUNTS:  # measured slower on B200 (the counts stall the DMMA warps); kept opt-in
-                    keys_own, counted = project_counted(X_local, A, n, row_lo, comm, exprange, own)
-                else:
-                    keys_own = project_routed(X_local, A, n, row_lo, comm, exprange)
-            except Exception as exc:  # no peer mappings here: the all-to-all path below
-                _ROUTED_OFF[0] = True
-                keys_own, counted = None, None
-                exprange.copy_(torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32))
-                warnings.append(f"fused projection unavailable ({exc}); using all_to_all")
+        if (keys_own is None and _routable(X_local, m, G) and (comm.on or _FUSED_COUNTS)
+                and (not comm.on or _symm_ready(comm, -(-m // G), n, X_local.device))):
+            if _FUSED_COUNTS:  # measured slower on B200 (the counts stall the DMMA warps); kept opt-in
+                keys_own, counted = project_counted(X_local, A, n, row_lo, comm, exprange, own)
+            else:
+                keys_own = project_routed(X_local, A, n, row_lo, comm, exprange)
         if keys_own is None:
             keys = project_keys(X_local, A, exprange)  # [m, n_local]; exponent window fused
     with tm.stage("sync_buckets"):

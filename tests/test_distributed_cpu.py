@@ -1,4 +1,4 @@
-"""Multi-process plumbing of the engine on CPU (gloo, world_size 2): table
+"""Multi-process plumbing of the engine on CPU (gloo, world_size 2 and 4): table
 routing to owners (engine.py:199-238), seed-group all-gather (engine.py:285-295),
 the float64 radii MAX reduction over bit patterns, the variable-size gather and
 the sharded numpy-order pairwise sum of the objective.
@@ -68,12 +68,13 @@ def _worker(rank, world, port, n, m, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,m", [(103, 5), (40, 8)])
-def test_engine_exchanges_gloo_world2(n, m):
+@pytest.mark.parametrize("world,n,m", [(2, 103, 5), (2, 40, 8), (4, 103, 5), (4, 1001, 9)])
+def test_engine_exchanges_gloo(world, n, m):
+    """world 2 and 4, n not divisible by the world size, m not a multiple of it"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, m, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]

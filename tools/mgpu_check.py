@@ -104,6 +104,66 @@ def main():
             ok &= good
             if rank == 0:
                 print(f"[G={world}] small passes=2 {x.dtype} g={g}: {'OK' if good else 'MISMATCH'}", flush=True)
+    # the fused projection (keys stored into the owners' symmetric buffers over
+    # NVLink) against projection + all_to_all of the same rows, and host rows
+    # streamed through the API against device rows
+    from paper_2106_10515_b200 import engine as E
+    from paper_2106_10515_b200.transform import project_keys
+    comm = E._Comm()
+    rng = np.random.default_rng(5)
+    for n, d, m in ((10_007, 128, 40), (3001, 32, 7)):
+        Xf = rng.standard_normal((n, d)).astype(np.float32)
+        A = rng.standard_normal((m, d))
+        lo, hi = E.split_data(n, world)[rank]
+        Xl = torch.from_numpy(Xf[lo:hi]).cuda()
+        er = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device="cuda")
+        assert E._symm_ready(comm, -(-m // world), n, Xl.device)
+        routed = E.project_routed(Xl, A, n, lo, comm, er).clone()
+        a2a = E.route_tables(project_keys(Xl, A), n, comm)
+        good = bool(torch.equal(routed, a2a))
+        ok &= good
+        if rank == 0:
+            print(f"[G={world}] routed projection == all_to_all (n={n}, d={d}, m={m}): {'OK' if good else 'MISMATCH'}",
+                  flush=True)
+    m = meta()["pipelines"]["cfg1"]
+    _, n, d, C, sep, seed = m["spec"]
+    X, _ = O.gaussian_mixture(n, d, C, sep, seed)
+    X = X.astype(np.float32)
+    lo, hi = E.split_data(n, world)[rank]
+    cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(8),
+                           homo=G.HomoTransformParams(m["m"], m["t"], seed=m["tseed"]),
+                           seeding=G.SeedingParams(m["K"], m["L"], min_group_size=m["delta"], seed=m["sseed"]))
+    dev = G.run_pipeline_shard(torch.from_numpy(X[lo:hi]).cuda(), n, cfg)
+    host = G.run_pipeline_shard(torch.from_numpy(X[lo:hi]).pin_memory(), n, cfg)
+    good = (torch.equal(dev.labels_device, host.labels_device) and torch.equal(dev.radii_device, host.radii_device)
+            and dev.objective == host.objective)
+    ok &= good
+    if rank == 0:
+        print(f"[G={world}] host rows streamed == device rows (cfg1 f32): {'OK' if good else 'MISMATCH'}", flush=True)
+    # the benchmark's law at 1M against the reference (tests/golden/benchlaw.*)
+    import json as _json
+    bpath = os.path.join(ROOT, "tests", "golden", "benchlaw.json")
+    if os.path.exists(bpath):
+        bm = _json.load(open(bpath))
+        barr = np.load(os.path.join(ROOT, "tests", "golden", "benchlaw.npz"))
+        Xb, _ = O.gaussian_mixture(bm["n"], bm["d"], bm["clusters"], bm["separation"], bm["data_seed"])
+        Xb = Xb.astype(np.float32)
+        lo, hi = E.split_data(bm["n"], world)[rank]
+        cfg = G.PipelineConfig(metric="euclidean", transform_kind="dense", workers=G.WorkerConfig(bm["g"]),
+                               homo=G.HomoTransformParams(bm["m"], bm["t"], seed=bm["tseed"]),
+                               seeding=G.SeedingParams(bm["K"], bm["L"], min_group_size=bm["delta"],
+                                                       seed=bm["sseed"]))
+        out = G.run_pipeline_shard(torch.from_numpy(Xb[lo:hi]).cuda(), bm["n"], cfg)
+        grp = out.seed_groups
+        cl = out.clustering
+        good = (np.array_equal(np.concatenate([x.members for x in grp]).astype(np.int32), barr["gflat"])
+                and np.array_equal(np.stack([c.values for c in cl.centers]), barr["centers"])
+                and np.array_equal(cl.assignment, barr["labels"]) and np.array_equal(cl.radii, barr["radii"])
+                and cl.objective == bm["objective"])
+        ok &= good
+        if rank == 0:
+            print(f"[G={world}] bench law 1M vs reference: {'OK' if good else 'MISMATCH'} groups={len(grp)} "
+                  f"bytes={out.transport_bytes}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     if not ok:
