@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/t_all.log 2>&1
-echo "all rc=$?" >> gpurun_out/t_all.log
+nvidia-smi -L > gpurun_out/smi2.txt
+timeout 1500 python -m pytest tests/test_gpu_multi.py -q -s > gpurun_out/t_multi.log 2>&1
+echo "multi rc=$?" >> gpurun_out/t_multi.log
