@@ -735,6 +735,12 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
 //            error of f16 subnormals, at most 2^-25 per scaled coordinate:
 //            2^-25 sqrt(d) (|x'| + |c'|) / s, and the three f16 parts of
 //            s^2 |c'|^2 / 2 (3 * 2^-25 / s^2 + 2^-33 |c'|^2 / 2).
+//   nprod 17 (tile-local FP16, xn = |x''| = |x' - c'_j0|): one f16 product
+//            of s x'' and s c' (2^-11 relative each, as nprod 1), fp32
+//            accumulation of d products, f16 subnormals as nprod 16, and the
+//            float64 table E[j0][j] (|E| <= 3|c'|^2) rounded to float32 and
+//            added in float32; the float32 rounding of x' = fl(x - mu),
+//            |x'| <= |x''| + |c'|, and of x'' itself.
 // cmax_bits[0] = |c'|max, cmax_bits[3] = 1/s (FP16 only, else 0).
 // Every product is bounded through sum |x'_i||c'_i| <= |x'||c'| (Cauchy-Schwarz).
 // E64 bounds numpy's float64 evaluation of the squared distance, and the last
@@ -751,6 +757,12 @@ __device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int 
     const double is = __longlong_as_double((long long)cmax_bits[3]);
     const double t25 = 2.9802322387695312e-08;  // 2^-25
     E += 1.05 * (t25 * sqrt((double)d) * (xn + cn) * is + 3.0 * t25 * is * is + 1.1641532182693481e-10 * 0.5 * cn * cn);
+  }
+  if (nprod == 17) {
+    const double is = __longlong_as_double((long long)cmax_bits[3]);
+    const double t25 = 2.9802322387695312e-08;  // 2^-25
+    E = 1.05 * ((1.953125e-03 + 2.0 * acc + 10.0 * u) * xn * cn + 12.0 * u * cn * cn + 4.0 * u * (xn + cn) * cn +
+                t25 * sqrt((double)d) * (xn + cn) * is);
   }
   const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
   return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
@@ -805,7 +817,7 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
     xnorm[i] = xn;
     const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
-    if (k == 1 || (double)v.s1 - s0 > T) {
+    if (v.i0 >= 0 && (k == 1 || (double)v.s1 - s0 > T)) {
       const int lab = v.i0;
       const float* xr = X + i * d;
       const double* cr = C + (uint64_t)lab * d;
@@ -814,7 +826,7 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
         const double df = __dsub_rn((double)xr[j], cr[j]);
         return __dmul_rn(df, df);
       });
-    } else if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) {
+    } else if (v.i0 < 0 || (double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) {
       full[atomicAdd(nfull, 1ull)] = (uint32_t)i;  // candidate window overflows the kept lists
     } else {
       amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
@@ -849,7 +861,7 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
     if (a == 0) xnorm[i] = xn;
     const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
-    const bool certain = k == 1 || (double)v.s1 - s0 > T;
+    const bool certain = v.i0 >= 0 && (k == 1 || (double)v.s1 - s0 > T);
     if (certain) {
       const int lab = v.i0;
       const float* xr = X + i * d;
@@ -879,7 +891,7 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
         best[i] = __dsqrt_rn(res);
       }
     } else if (a == 0) {
-      if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
+      if (v.i0 < 0 || (double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
       else amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
     }
   }
@@ -921,7 +933,7 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
     if (h == 0) xnorm[i] = xn;
     const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
-    if (k == 1 || (double)v.s1 - s0 > T) {
+    if (v.i0 >= 0 && (k == 1 || (double)v.s1 - s0 > T)) {
       const int lab = v.i0;
       const double2* cr = reinterpret_cast<const double2*>(C + (uint64_t)lab * d);
       double r0, r1, r2, r3;
@@ -956,7 +968,7 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
         best[i] = __dsqrt_rn(res);
       }
     } else if (h == 0) {
-      if ((double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
+      if (v.i0 < 0 || (double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) full[atomicAdd(nfull, 1ull)] = (uint32_t)i;
       else amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
     }
   }
@@ -1084,9 +1096,17 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     // and GEEK_SCREEN=1 the single TF32 product, whose bound ~2e-3|x'||c'|
     // only separates data whose cluster gaps are large against |x'||c'|)
     // -> classification -> candidate / full recheck
+    // default FP16x3; GEEK_SCREEN=17 selects the tile-local FP16 screen (one
+    // product per K slice against each point tile's origin center: a third of
+    // the MMAs, but on the benchmark data the kernel is bound by its epilogue,
+    // not the tensor pipe -- 83.5 vs 86.4 ms -- and its wider window sends
+    // 21M instead of 12M points to the recheck, so it loses overall:
+    // profiles/r2_screen.md), 3 / 1 TF32x3 / one TF32 product
     const char* sel = getenv("GEEK_SCREEN");
-    int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : 16;
-    Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt;
+    const bool local_ok = k <= 3840 && d % 8 == 0;  // 4 x 48 KB B stages + two origin-table rows in SMEM
+    int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : (atoi(sel) == 17 && local_ok) ? 17 : 16;
+    Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt, lcf, les, lj0;
+    TcLocal loc{nullptr, nullptr, nullptr};
     GEEK_TRY(cnt.alloc(48, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
     unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16)
@@ -1096,9 +1116,13 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     int nct = 0;
     float xscale = 1.f;
     GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
-    if (nprod == 16) {
+    if (nprod >= 16) {
       const double is = 1.0 / (double)xscale;
       GEEK_CHECK_CUDA(cudaMemcpyAsync(cmax + 3, &is, 8, cudaMemcpyHostToDevice, s));
+    }
+    if (nprod == 17) {
+      GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s));
+      loc.cmax = cmax;
     }
     GEEK_TRY(ts.alloc(n * 32, s));
     GEEK_TRY(ti.alloc(n * 32, s));
@@ -1114,8 +1138,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     const bool use_xp = nprod != 1 && d % 8 == 0 && d <= 128;
     if (use_xp) GEEK_TRY(xp.alloc(n * 16, s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
-                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s));
-    if (nprod == 16) {  // a point coordinate beyond the f16 range: redo the screen in TF32x3
+                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s, &loc));
+    if (nprod >= 16) {  // a point coordinate beyond the f16 range: redo the screen in TF32x3
       unsigned hov = 0;
       GEEK_CHECK_CUDA(cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, s));
       GEEK_CHECK_CUDA(cudaStreamSynchronize(s));

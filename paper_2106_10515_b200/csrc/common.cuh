@@ -187,9 +187,20 @@ int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStre
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s);
+// nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu
+struct TcLocal {
+  const float* cf;  // [k][d] float32 c'
+  const int* j0;    // [ntiles] origin center per 128-point tile
+  const float* Es;  // [k][nct * 192] origin table
+  const unsigned long long* cmax;  // [0] |c'|max bits (from tc_screen_prepare)
+};
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s);
+                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s, const TcLocal* loc = nullptr,
+                     int xstride = 1, const unsigned* run_if = nullptr);
+int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
+                     const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
+                     cudaStream_t s);
 
 __global__ void iota_u32(uint32_t* p, uint64_t n);
 __global__ void fill_u32(uint32_t* p, uint32_t v, uint64_t n);

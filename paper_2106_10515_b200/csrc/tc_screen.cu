@@ -57,32 +57,57 @@ constexpr int kTcAPart = (kTcKmax / 8) * kTcSliceBytes;           // 64 KB: one 
 // NPROD = 16 is the FP16x3 screen: the same three products on kind::f16
 // MMAs (twice the TF32 rate, half the operand bytes) over power-of-two scaled
 // operands; a K slice is 32 bytes per row in both formats (8 tf32 / 16 f16).
+//
+// NPROD = 17 is the tile-local FP16 screen: ONE kind::f16 product per K
+// slice.  Every 128-point tile gets an origin, the center c_j0 nearest to its
+// first point (a TF32 pre-pass over the tiles' first rows), and
+//   s_j = |c'_j|^2 - 2 x'.c'_j = E[j0][j] - 2 x''.c'_j,
+//   x'' = x' - c'_j0,   E[j0][j] = |c'_j|^2 - 2 c'_j0.c'_j  (float64 -> f32 table)
+// so the large part of every dot product is exact in the table and the
+// tensor cores only see x'', the point's offset from a nearby center: the
+// f16 error scales with |x''||c'| instead of |x'||c'|, which on
+// cluster-ordered data (the reference generator's id order) makes one f16
+// product as selective as FP16x3 at a third of the MMAs.  The classifier's
+// bound uses |x''| (left in xpart by this kernel), so the labels stay exact
+// for ANY data -- points far from their tile's origin only reach the exact
+// recheck more often.
 template <int NPROD>
 struct TcCfg {
-  static constexpr bool kF16 = NPROD == 16;
+  static constexpr bool kF16 = NPROD == 16 || NPROD == 17;
+  static constexpr bool kLocal = NPROD == 17;
   static constexpr int kSliceDims = kF16 ? 16 : 8;               // dims per K slice
-  static constexpr int kChunkDims = 2 * kSliceDims;              // dims per B stage (two slices)
-  static constexpr int kParts = NPROD == 1 ? 1 : 2;              // hi (+ lo)
-  // NPROD = 3 / 16 keep the hi part of the point tile in TMEM (columns 384..)
-  // and only the lo part in SMEM: the SMEM this frees deepens the B ring
+  // K slices per B stage: two, or for NPROD = 17 the whole padded dimension
+  // (one 48 KB stage per center tile: one barrier wait and one commit per
+  // 8 MMAs instead of per 2 -- the per-stage handshake, not the tensor pipe,
+  // bounded the single-product issue loop)
+  static constexpr int kSlices = kLocal ? kTcKmax / kSliceDims : 2;
+  static constexpr int kChunkDims = kSlices * kSliceDims;         // dims per B stage
+  static constexpr int kParts = (NPROD == 1 || NPROD == 17) ? 1 : 2;  // hi (+ lo)
+  // NPROD = 3 / 16 / 17 keep the hi part of the point tile in TMEM (columns
+  // 384..) and only the lo part (none for 17) in SMEM: the SMEM this frees
+  // deepens the B ring
   static constexpr bool kATmem = NPROD != 1;
-  static constexpr int kABytes = (kTcKmax / kSliceDims) * kTcSliceBytes;
+  static constexpr int kABytes = kLocal ? 0 : (kTcKmax / kSliceDims) * kTcSliceBytes;
   // NPROD = 1: point tiles double-buffered; NPROD = 3: single-buffered, the
   // SMEM goes to the resident |c'|^2 slices instead (chunked hand-off keeps
   // the tile switch short)
-  static constexpr int kABuf = NPROD == 1 ? 2 : 1;
-  static constexpr int kStageBytes = kParts * kTcHalfStage;
+  // NPROD = 17: double-buffered in TMEM (64 columns of packed f16 per
+  // buffer), so the next tile's A lands while the MMAs still read this one's
+  static constexpr int kABuf = (NPROD == 1 || NPROD == 17) ? 2 : 1;
+  static constexpr int kHalfStage = kSlices * kTcBSliceBytes;     // one part of a B stage
+  static constexpr int kStageBytes = kParts * kHalfStage;
   static constexpr int kStages = 4;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kTmemA = 2 * kTcN;                   // TMEM A operand after the two accumulators
+  static constexpr uint32_t kTmemAStride = kF16 ? 64 : 128;      // TMEM columns of one A buffer
   static constexpr size_t kSmemFixed = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
 };
 
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
 // chunk (B slice with |c'|^2/2, then the all-ones A slice)
 constexpr int kTcC2Bytes = kTcBSliceBytes + kTcSliceBytes;  // |c'|^2 B slice, then the all-ones A slice
-__host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts, int chunk_dims = kTcChunk) {
-  return (uint64_t)((d + chunk_dims - 1) / chunk_dims) * parts * kTcHalfStage + kTcC2Bytes;
+__host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts, int chunk_dims = kTcChunk, int slices = 2) {
+  return (uint64_t)((d + chunk_dims - 1) / chunk_dims) * parts * slices * kTcBSliceBytes + kTcC2Bytes;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -289,10 +314,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 struct Top4 {
   float s[4];
   int i[4];
-  __device__ void init() {
+  __device__ void init(float bound = INFINITY) {
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      s[a] = INFINITY;
+      s[a] = bound;
       i[a] = -1;
     }
   }
@@ -360,6 +385,14 @@ struct TcParams {
   float xscale;       // NPROD = 16: x' is multiplied by this power of two before the f16 split
   float oscale;       // top_s = oscale * (accumulator): 2 (TF32) or 2 / xscale^2 (FP16)
   unsigned* ovf;      // NPROD = 16: set when a scaled operand leaves the f16 range (caller reruns in TF32x3)
+  // NPROD = 17 (tile-local origin)
+  const float* cf;    // [k][d] float32 c' = fl32(c - mu), the origins
+  const int* j0;      // [ntiles] origin center of every point tile
+  const float* Es;    // [k][kpadE] E[j0][j] * xscale^2 / 2 (+inf for padding centers)
+  int kpadE;          // nct * kTcN
+  int xstride;        // rows between consecutive screened points (1; kTcM for the tiles' first rows)
+  const unsigned* run_if;  // may be null: the kernel does nothing unless *run_if != 0 (device-side fallback)
+  const unsigned long long* cmax;  // NPROD = 17: [0] |c'|max bits, [3] 1/xscale bits (the lists' starting bound)
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
@@ -387,6 +420,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   static_assert(Cfg::kStages <= 8 && Cfg::kABuf <= 2, "barrier map");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (P.run_if && *P.run_if == 0) return;  // a fallback launch that is not needed
+  float* Ebuf = reinterpret_cast<float*>(bars + 40);  // NPROD = 17: E rows of the current / next point tile
+  float2* Upart = reinterpret_cast<float2*>(Ebuf + 2 * P.kpadE);  // [2][128 rows][2 halves] (|x''|^2, |x'|^2)
   if (tid == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -414,8 +450,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   const uint32_t tmem = *tmem_slot;
   const int nck = (P.d + kTcAChunk - 1) / kTcAChunk;  // 32-dim point-tile chunks
   const int nbk = (P.d + Cfg::kChunkDims - 1) / Cfg::kChunkDims;  // B chunks per center tile
-  const uint32_t qct = (uint32_t)nbk + (P.c2res ? 0u : 1u);  // + the |c'|^2 slice when it is not resident
-  const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts, Cfg::kChunkDims);
+  // + the |c'|^2 slice when it is not resident (NPROD = 17: none, E carries |c'|^2)
+  const uint32_t qct = (uint32_t)nbk + ((P.c2res || Cfg::kLocal) ? 0u : 1u);
+  const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts, Cfg::kChunkDims, Cfg::kSlices);
   const uint32_t total_q = (uint32_t)P.nct * qct;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -438,7 +475,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
       for (uint64_t q = 0; q < total_chunks; ++q) {
         const uint32_t s = (uint32_t)(q % Cfg::kStages);
-        if (q >= (uint64_t)Cfg::kStages) mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+        if (q >= (uint64_t)Cfg::kStages) {
+          if (P.sleepwait > 1) mbar_wait_sleep(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+          else mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+        }
         const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
         const uint32_t ct = (cq + blockIdx.x) % (uint32_t)P.nct;  // CTAs start on different center tiles
         const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
@@ -465,6 +505,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           const long long c0 = clock64();
           mbar_wait(bar, par);
           acc += clock64() - c0;
+        } else if (P.sleepwait > 1) {
+          mbar_wait_sleep(bar, par);
         } else {
           mbar_wait(bar, par);
         }
@@ -495,26 +537,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           // the last center tile runs with N = its valid centers rounded up to 16
           const uint32_t idesc = (int)((ct + blockIdx.x) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
           for (int kc = 0; kc < nbk; ++kc) {
-            const int ac = kc * Cfg::kChunkDims / kTcAChunk;  // point-tile chunk holding these dims
-            if (ct == 0 && (kc * Cfg::kChunkDims) % kTcAChunk == 0) {  // first use of this chunk of the point tile
-              timed_wait(&afull[ab * 4 + ac], apar, w_afull);
-              fence_after();
+            // point-tile chunks (32 dims) holding this B chunk's dims
+            const int ac0 = kc * Cfg::kChunkDims / kTcAChunk;
+            const int ac1 = min(nck - 1, ((kc + 1) * Cfg::kChunkDims - 1) / kTcAChunk);
+            if (ct == 0) {  // first use of a point-tile chunk: wait for its writers
+              bool waited = false;
+              for (int ac = ac0; ac <= ac1; ++ac)
+                if (ac * kTcAChunk >= kc * Cfg::kChunkDims) {
+                  timed_wait(&afull[ab * 4 + ac], apar, w_afull);
+                  waited = true;
+                }
+              if (waited) fence_after();
             }
             const uint32_t s = next_stage();
             // descriptors differ from the stage / tile bases by constant
             // address offsets (the 14-bit address field never carries)
             const uint32_t blo32 = b_lo32 + ((s * Cfg::kStageBytes) >> 4);
-            // two K slices per chunk; a slice is 8 TMEM columns of A (8 tf32 or 16 f16)
-            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * 2 * kTcSliceBytes) >> 4);
-            const uint32_t at = tmem + Cfg::kTmemA + ab * 128 + kc * 16;
+            // kSlices K slices per chunk; a slice is 8 TMEM columns of A (8 tf32 or 16 f16)
+            const uint32_t alo32 = a_lo32 + ((ab * Cfg::kABytes + kc * Cfg::kSlices * kTcSliceBytes) >> 4);
+            const uint32_t at = tmem + Cfg::kTmemA + ab * Cfg::kTmemAStride + kc * Cfg::kSlices * 8;
+            // slices past d hold zero B rows and unwritten A columns: never issued
+            const int nsl = min(Cfg::kSlices, (P.d - kc * Cfg::kChunkDims + Cfg::kSliceDims - 1) / Cfg::kSliceDims);
             const long long c_is = P.dbg ? clock64() : 0;
             if (leader && P.prof != 2) {
 #pragma unroll
-              for (int j = 0; j < 2; ++j) {
+              for (int j = 0; j < Cfg::kSlices; ++j) {
+                if (j >= nsl) break;
                 const uint64_t bhi = desc_of(blo32 + ((j * kTcBSliceBytes) >> 4), d_hi32);
                 const uint32_t acc = (kc | j) ? 1u : 0u;
-                if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
-                  const uint64_t blo = desc_of(blo32 + ((kTcHalfStage + j * kTcBSliceBytes) >> 4), d_hi32);
+                if (Cfg::kLocal) {  // one f16 product: A (x'') from TMEM
+                  tc_mma_ta<true>(dt, at + j * 8, bhi, idesc, acc);
+                } else if (Cfg::kATmem) {  // hi in TMEM, lo in SMEM
+                  const uint64_t blo = desc_of(blo32 + ((Cfg::kHalfStage + j * kTcBSliceBytes) >> 4), d_hi32);
                   const uint64_t alo = desc_of(alo32 + ((j * kTcSliceBytes) >> 4), d_hi32);
                   tc_mma_ta<Cfg::kF16>(dt, at + j * 8, bhi, idesc, acc);
                   tc_mma_ta<Cfg::kF16>(dt, at + j * 8, blo, idesc, 1u);
@@ -525,12 +579,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               }
             }
             if (P.dbg) w_issue += clock64() - c_is;
-            if (ct == P.nct - 1 && leader && (((kc + 1) * Cfg::kChunkDims) % kTcAChunk == 0 || kc == nbk - 1))
-              tc_commit(&aempty[ab * 4 + ac]);  // last read of this point-tile chunk
+            if (ct == P.nct - 1 && leader)  // last read of these point-tile chunks
+              for (int ac = ac0; ac <= ac1; ++ac)
+                if ((ac + 1) * kTcAChunk <= (kc + 1) * Cfg::kChunkDims || kc == nbk - 1) tc_commit(&aempty[ab * 4 + ac]);
             stage_done(s);
           }
           const long long c_c2 = P.dbg ? clock64() : 0;
-          if (P.c2res) {  // |c'|^2 / 2, added last, from the resident slices
+          if (Cfg::kLocal) {
+            // no |c'|^2 slice: the epilogue adds E[j0][j]
+          } else if (P.c2res) {  // |c'|^2 / 2, added last, from the resident slices
             if (t == 0 && ct == 0) {
               mbar_wait(c2full, 0);
               fence_after();
@@ -585,6 +642,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           tc_ld32_async(trow + c0, v);
           tc_wait_ld();
           tc_regs_ready(v);
+          if (Cfg::kLocal) {  // s / oscale = acc + E[j0][j] * xscale^2 / 2 (the tile's E row, staged in SMEM)
+            const float4* er =
+                reinterpret_cast<const float4*>(Ebuf + (t & 1) * P.kpadE + cta * kTcN + ch * (kTcN / 2) + c0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float4 e = er[u];
+              v[4 * u] += e.x;
+              v[4 * u + 1] += e.y;
+              v[4 * u + 2] += e.z;
+              v[4 * u + 3] += e.w;
+            }
+          }
           if (last) {
 #pragma unroll
             for (int u = 0; u < 32; ++u)
@@ -661,10 +730,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           const uint64_t i = p0 + row;
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
           if (kc < nck && i < P.n) {
+            const uint64_t ri = i * (uint64_t)P.xstride;
             if (P.d == kTcKmax) {
-              v = __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax + e0));
+              v = __ldg(reinterpret_cast<const float4*>(P.X + ri * kTcKmax + e0));
             } else {
-              const float* xr = P.X + i * P.d;
+              const float* xr = P.X + ri * P.d;
               if (e0 < P.d) v.x = xr[e0];
               if (e0 + 1 < P.d) v.y = xr[e0 + 1];
               if (e0 + 2 < P.d) v.z = xr[e0 + 2];
@@ -677,7 +747,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       {  // pull the tile after it towards L2 while this one is in flight
         const uint64_t row = tile_p0(t + 1) + (warp * 32 + lane) / 2;
         if (row < P.n) {
-          const char* base = reinterpret_cast<const char*>(P.X + row * P.d) + (lane & 1) * 256;
+          const char* base = reinterpret_cast<const char*>(P.X + row * (uint64_t)P.xstride * P.d) + (lane & 1) * 256;
           for (int b = 0; b < 256 && (lane & 1) * 256 + b < P.d * 4; b += 128)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
         }
@@ -689,6 +759,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       uint8_t* Ab = A + ab * Cfg::kABytes;
       const uint64_t p0 = tile_p0(t);
       float xs[4] = {0.f, 0.f, 0.f, 0.f};  // |x'|^2 over this thread's half of the row's dims (kATmem layout)
+      float xa[4] = {0.f, 0.f, 0.f, 0.f};  // NPROD = 17: |x'|^2 (xs then holds |x''|^2)
+      const float* org = Cfg::kLocal ? P.cf + (uint64_t)P.j0[blockIdx.x + (uint64_t)t * gridDim.x] * P.d : nullptr;
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         if (kc < nck) {
@@ -713,8 +785,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               if (e0 + 3 < P.d) m4.w = __ldg(P.mu + e0 + 3);
             }
             const float4 x = q[kc * 4 + p];
-            const float x0 = valid ? x.x - m4.x : 0.f, x1 = valid ? x.y - m4.y : 0.f;
-            const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
+            float x0 = valid ? x.x - m4.x : 0.f, x1 = valid ? x.y - m4.y : 0.f;
+            float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
+            if (Cfg::kLocal) {
+              xa[p] = fmaf(x0, x0, xa[p]);
+              xa[p] = fmaf(x1, x1, xa[p]);
+              xa[p] = fmaf(x2, x2, xa[p]);
+              xa[p] = fmaf(x3, x3, xa[p]);
+            }
+            if (Cfg::kLocal && valid) {  // x'' = x' - c'_j0 (the tile's origin)
+              float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (P.d == kTcKmax) {
+                o4 = __ldg(reinterpret_cast<const float4*>(org + e0));
+              } else {
+                if (e0 < P.d) o4.x = __ldg(org + e0);
+                if (e0 + 1 < P.d) o4.y = __ldg(org + e0 + 1);
+                if (e0 + 2 < P.d) o4.z = __ldg(org + e0 + 2);
+                if (e0 + 3 < P.d) o4.w = __ldg(org + e0 + 3);
+              }
+              x0 -= o4.x;
+              x1 -= o4.y;
+              x2 -= o4.z;
+              x3 -= o4.w;
+            }
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
             if (Cfg::kATmem) {
@@ -736,9 +829,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               const __half2 l23 = __floats2half2_rn(y2 - b23.x, y3 - b23.y);
               hp[2 * p] = *reinterpret_cast<const uint32_t*>(&g01);
               hp[2 * p + 1] = *reinterpret_cast<const uint32_t*>(&g23);
-              const uint32_t offh = (e0 >> 4) * kTcSliceBytes + core_off_b(row, (e0 & 15) * 2, P.lbo, P.sbo);
-              *reinterpret_cast<uint2*>(Ab + offh) =
-                  make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+              if (!Cfg::kLocal) {
+                const uint32_t offh = (e0 >> 4) * kTcSliceBytes + core_off_b(row, (e0 & 15) * 2, P.lbo, P.sbo);
+                *reinterpret_cast<uint2*>(Ab + offh) =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+              }
             } else if (Cfg::kATmem) {
               hi[4 * p] = h0;
               hi[4 * p + 1] = h1;
@@ -753,13 +848,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           if (Cfg::kF16) {
             if (big) atomicOr(P.ovf, 1u);
             if (P.prof != 3 && (P.prof < 5 || P.prof > 7))
-              tc_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 16 + (warp >> 2) * 8,
+              tc_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * Cfg::kTmemAStride + kc * 16 + (warp >> 2) * 8,
                      hp);
             tc_wait_st();
             fence_before();
           } else if (Cfg::kATmem) {
             if (P.prof != 3 && (P.prof < 5 || P.prof > 7))
-              tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * 128 + kc * 32 + (warp >> 2) * 16,
+              tc_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + Cfg::kTmemA + ab * Cfg::kTmemAStride + kc * 32 + (warp >> 2) * 16,
                       hi);
             tc_wait_st();
             fence_before();
@@ -773,6 +868,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         const uint64_t i = p0 + (warp & 3) * 32 + lane;
         if (i < P.n) P.xpart[i * 2 + (warp >> 2)] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
       }
+      if (Cfg::kLocal)  // this half's |x''|^2, |x'|^2 for the lists' starting bound of the tile
+        Upart[(ab * 128 + (warp & 3) * 32 + lane) * 2 + (warp >> 2)] =
+            make_float2((xs[0] + xs[1]) + (xs[2] + xs[3]), (xa[0] + xa[1]) + (xa[2] + xa[3]));
+    };
+    // NPROD = 17: every list starts at a bound U instead of +inf, so a column
+    // is a candidate only if it beats U.  s(x, c_j0) = |x''|^2 - |x'|^2 >= the
+    // best s, and U adds four times the classifier's window to it, so the
+    // window around the best is below U and only a few columns per point are
+    // ever inserted.  Any U is exact: a list that ends with an entry (value U,
+    // center -1) inside the window reads as an overflow (full scan), and the
+    // classifier never takes a -1 winner.
+    auto start_bound = [&](uint32_t t) -> float {
+      const int ab = t % Cfg::kABuf;
+      const int r = (warp & 3) * 32 + lane;
+      const float2 h0 = Upart[(ab * 128 + r) * 2], h1 = Upart[(ab * 128 + r) * 2 + 1];
+      const float xpp = h0.x + h1.x, xp = h0.y + h1.y;
+      const float cn = (float)__longlong_as_double((long long)P.cmax[0]);
+      const float win = 2.2f * (1.953125e-3f * sqrtf(xpp) * cn + 1e-5f * cn * cn) + 1e-4f * xp;
+      const float us = xpp - xp + 4.f * win + 1.f;  // s units
+      return us / P.oscale;                          // accumulator units (v = s / oscale)
     };
     if (my_tiles > 0) {
       load_regs(0);
@@ -781,10 +896,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     for (uint32_t t = 0; t < my_tiles; ++t) {
       const bool more = t + 1 < my_tiles;
       if (more) load_regs(t + 1);  // in flight during the epilogues below
+      if (Cfg::kLocal) {  // the tile's E row -> SMEM buffer t & 1 (read by every epilogue warp)
+        const float4* src =
+            reinterpret_cast<const float4*>(P.Es + (uint64_t)P.j0[blockIdx.x + (uint64_t)t * gridDim.x] * P.kpadE);
+        float4* dst = reinterpret_cast<float4*>(Ebuf + (t & 1) * P.kpadE);
+        for (int e = tid; e < P.kpadE / 4; e += kTcEpiThreads) dst[e] = __ldg(src + e);
+        asm volatile("bar.sync 1, %0;" ::"r"(kTcEpiThreads) : "memory");
+        cur.init(start_bound(t));
+      }
       for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
       if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
       finish(t, cur);
-      cur.init();
+      if (!Cfg::kLocal) cur.init();
     }
   }
   fence_before();
@@ -811,11 +934,12 @@ __global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu
 // s^2 |c'|^2 / 2 as three f16 parts, and the ones slice is f16 1.0.
 __global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, int parts,
                                     uint32_t lbo, uint32_t sbo, float* Bimg, float* c2,
-                                    unsigned long long* cmax_bits, int f16, float xscale) {
-  const int chunk = f16 ? 32 : kTcChunk, sdims = f16 ? 16 : 8, eb = f16 ? 2 : 4;
+                                    unsigned long long* cmax_bits, int f16, float xscale, int slices) {
+  const int sdims = f16 ? 16 : 8, eb = f16 ? 2 : 4, chunk = slices * sdims;
   const int nchunks_k = (d + chunk - 1) / chunk;
-  const uint64_t stage = (uint64_t)parts * kTcHalfStage;
-  const uint64_t ct_bytes = tc_ct_bytes(d, parts, chunk);
+  const uint64_t half = (uint64_t)slices * kTcBSliceBytes;
+  const uint64_t stage = (uint64_t)parts * half;
+  const uint64_t ct_bytes = tc_ct_bytes(d, parts, chunk, slices);
   const uint64_t total = (uint64_t)nct * kTcN;
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < total;
        c += (uint64_t)gridDim.x * blockDim.x) {
@@ -837,11 +961,11 @@ __global__ void center_image_kernel(const double* C, uint64_t k, int d, const fl
           const float y = -cv * xscale;
           const __half hi = __float2half_rn(y);
           *reinterpret_cast<__half*>(img + off) = hi;
-          if (parts == 2) *reinterpret_cast<__half*>(img + kTcHalfStage + off) = __float2half_rn(y - __half2float(hi));
+          if (parts == 2) *reinterpret_cast<__half*>(img + half + off) = __float2half_rn(y - __half2float(hi));
         } else {
           const float hi = tf32_round(-cv);
           *reinterpret_cast<float*>(img + off) = hi;
-          if (parts == 2) *reinterpret_cast<float*>(img + kTcHalfStage + off) = tf32_round(-cv - hi);
+          if (parts == 2) *reinterpret_cast<float*>(img + half + off) = tf32_round(-cv - hi);
         }
       }
     }
@@ -891,14 +1015,63 @@ __global__ void center_absmax_kernel(const double* C, uint64_t k, int d, const f
   atomicMax(out, m);
 }
 
+// ---- tile-local origins (NPROD = 17) ------------------------------------------
+
+__global__ void centered_f32_kernel(const double* C, uint64_t k, int d, const float* mu, float* cf) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < k * (uint64_t)d;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    cf[e] = (float)(C[e] - (double)mu[e % d]);  // exactly the screen's c' (center_image_kernel)
+}
+
+// Es[j0][j] = (|c'_j|^2 - 2 c'_j0 . c'_j) * xscale^2 / 2 in float64 over the
+// float32 c', rounded once to float32; +inf for the padding centers j >= k
+__global__ void origin_table_kernel(const float* cf, uint64_t k, int d, int kpadE, double half_s2, float* Es) {
+  const uint64_t total = k * (uint64_t)kpadE;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = q / kpadE, j = q % kpadE;
+    if (j >= k) {
+      Es[q] = INFINITY;
+      continue;
+    }
+    const float* ca = cf + a * d;
+    const float* cj = cf + j * d;
+    double e = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const double y = (double)cj[t];
+      e = fma(y, y - 2.0 * (double)ca[t], e);
+    }
+    Es[q] = (float)(e * half_s2);
+  }
+}
+
+// origin of every point tile: the screened nearest center of its first row
+__global__ void pick_origin_kernel(const float* top_s, const int* top_i, uint64_t ntiles, int* j0) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    float b = INFINITY;
+    int bi = 0;
+    for (int a = 0; a < 8; ++a) {
+      const float v = top_s[t * 8 + a];
+      if (v < b && top_i[t * 8 + a] >= 0) {
+        b = v;
+        bi = top_i[t * 8 + a];
+      }
+    }
+    j0[t] = bi;
+  }
+}
+
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s) {
-  GEEK_REQUIRE(nprod == 1 || nprod == 3 || nprod == 16, "screen precision must be 1 or 3 TF32 products or 16 (FP16x3)");
+  GEEK_REQUIRE(nprod == 1 || nprod == 3 || nprod == 16 || nprod == 17,
+               "screen precision must be 1 or 3 TF32 products, 16 (FP16x3) or 17 (tile-local FP16)");
   nct = (int)((k + kTcN - 1) / kTcN);
-  const int parts = nprod == 1 ? 1 : 2;
-  const bool f16 = nprod == 16;
-  GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts, f16 ? 32 : kTcChunk), s));
+  const int parts = (nprod == 1 || nprod == 17) ? 1 : 2;
+  const bool f16 = nprod == 16 || nprod == 17;
+  const int slices = nprod == 17 ? kTcKmax / 16 : 2;
+  GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts, slices * (f16 ? 16 : 8), slices), s));
   GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
   GEEK_TRY(mu.alloc((size_t)d * 4 + 16, s));
   center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
@@ -920,15 +1093,18 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
     xscale = ldexpf(1.f, 4 - e);
   }
   center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(
-      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev, f16 ? 1 : 0, xscale);
+      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev, f16 ? 1 : 0, xscale,
+      slices);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
 
 template <int NPROD>
 static int launch_screen(const TcParams& P, cudaStream_t s) {
-  static_assert(TcCfg<NPROD>::kTmemA + 128 <= TcCfg<NPROD>::kTmemCols, "TMEM map");
-  const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0);
+  static_assert(TcCfg<NPROD>::kTmemA + (TcCfg<NPROD>::kATmem ? TcCfg<NPROD>::kABuf : 1) * TcCfg<NPROD>::kTmemAStride <=
+                    TcCfg<NPROD>::kTmemCols, "TMEM map");
+  const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0) +
+                      (TcCfg<NPROD>::kLocal ? (size_t)2 * P.kpadE * sizeof(float) + 2 * 128 * 2 * sizeof(float2) : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -943,10 +1119,19 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
 
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
-                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s) {
-  GEEK_REQUIRE(nprod != 16 || ovf, "FP16 screen needs the overflow flag");
+                     double* xpart, float xscale, unsigned* ovf, cudaStream_t s, const TcLocal* loc, int xstride,
+                     const unsigned* run_if) {
+  GEEK_REQUIRE(nprod < 16 || ovf, "FP16 screen needs the overflow flag");
+  GEEK_REQUIRE(nprod != 17 || loc, "tile-local screen needs its origins");
   GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
   TcParams P;
+  P.cf = loc ? loc->cf : nullptr;
+  P.j0 = loc ? loc->j0 : nullptr;
+  P.Es = loc ? loc->Es : nullptr;
+  P.kpadE = nct * kTcN;
+  P.xstride = xstride;
+  P.run_if = run_if;
+  P.cmax = loc ? loc->cmax : nullptr;
   P.X = X;
   P.n = n;
   P.d = d;
@@ -965,15 +1150,16 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.top_i = top_i;
   P.xpart = nprod != 1 ? xpart : nullptr;
   P.xscale = xscale;
-  P.oscale = nprod == 16 ? 2.f / (xscale * xscale) : 2.f;
+  P.oscale = nprod >= 16 ? 2.f / (xscale * xscale) : 2.f;
   P.ovf = ovf;
   P.pushcut = getenv("GEEK_SCREEN_PUSHCUT") ? atoi(getenv("GEEK_SCREEN_PUSHCUT")) : 12;
   P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
   P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
+  if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
   if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
-  P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? 1 : 0;
+  P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? atoi(getenv("GEEK_SCREEN_SLEEP")) : 0;
   P.dbg = nullptr;
   Scratch dbg;
   if (getenv("GEEK_SCREEN_DBG")) {
@@ -981,7 +1167,10 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
     GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 4 * 8 * 2, s));
     P.dbg = dbg.as<unsigned long long>();
   }
-  const int st = nprod == 16 ? launch_screen<16>(P, s) : nprod == 3 ? launch_screen<3>(P, s) : launch_screen<1>(P, s);
+  const int st = nprod == 17   ? launch_screen<17>(P, s)
+                 : nprod == 16 ? launch_screen<16>(P, s)
+                 : nprod == 3  ? launch_screen<3>(P, s)
+                               : launch_screen<1>(P, s);
   if (st == GEEK_OK && P.dbg) {  // diagnostics: where the MMA warp waits
     unsigned long long h[148 * 8];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -1002,6 +1191,41 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
             tot / 148, 100 * f / tot, 100 * a / tot, 100 * af / tot, 100 * is / tot, 100 * c2 / tot, 100 * cf / tot);
   }
   return st;
+}
+
+// Origins of the tile-local screen: c' in float32, the E table, and for every
+// 128-point tile the center nearest to its first row (a TF32x3 screen over
+// the tiles' first rows -- any choice is exact, a near one keeps
+// |x''| and with it the recheck rate small).
+int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
+                     const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
+                     cudaStream_t s) {
+  const int kpadE = nct17 * kTcN;
+  const uint64_t ntiles = (n + kTcM - 1) / kTcM;
+  GEEK_TRY(cf.alloc(k * (uint64_t)d * 4, s));
+  GEEK_TRY(Es.alloc(k * (uint64_t)kpadE * 4, s));
+  GEEK_TRY(j0.alloc(ntiles * 4, s));
+  centered_f32_kernel<<<grid_for(k * (uint64_t)d, 256), 256, 0, s>>>(C, k, d, mu17.as<float>(), cf.as<float>());
+  GEEK_CHECK_LAUNCH();
+  origin_table_kernel<<<grid_for(k * (uint64_t)kpadE, 128, 148 * 16), 128, 0, s>>>(
+      cf.as<float>(), k, d, kpadE, 0.5 * (double)xscale * (double)xscale, Es.as<float>());
+  GEEK_CHECK_LAUNCH();
+  Scratch img1, c21, mu1, ts, ti, misc;
+  GEEK_TRY(misc.alloc(32, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
+  int nct1 = 0;
+  float xs1 = 1.f;
+  GEEK_TRY(tc_screen_prepare(C, k, d, 3, lbo, sbo, img1, c21, mu1, misc.as<unsigned long long>(), nct1, xs1, s));
+  GEEK_TRY(ts.alloc(ntiles * 32, s));
+  GEEK_TRY(ti.alloc(ntiles * 32, s));
+  GEEK_TRY(tc_screen_launch(X, ntiles, d, 3, img1, c21, mu1, k, nct1, lbo, sbo, ts.as<float>(), ti.as<int>(), nullptr,
+                            1.f, nullptr, s, nullptr, kTcM, nullptr));
+  pick_origin_kernel<<<grid_for(ntiles, 256), 256, 0, s>>>(ts.as<float>(), ti.as<int>(), ntiles, j0.as<int>());
+  GEEK_CHECK_LAUNCH();
+  loc.cf = cf.as<float>();
+  loc.j0 = j0.as<int>();
+  loc.Es = Es.as<float>();
+  return GEEK_OK;
 }
 
 // ---- self-test of the operand layout and the measured screen error -------------
@@ -1080,8 +1304,14 @@ extern "C" int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* o
   float xscale = 1.f;
   GEEK_TRY(tc_screen_prepare(C.as<double>(), k, d, nprod, lbo, sbo, img, c2, mu, cmax, nct, xscale, s));
   unsigned* ovf = reinterpret_cast<unsigned*>(misc.as<unsigned long long>() + 3);
+  Scratch lcf, les, lj0;
+  TcLocal loc{nullptr, nullptr, nullptr};
+  if (nprod == 17) {
+    GEEK_TRY(tc_local_prepare(C.as<double>(), k, d, X.as<float>(), n, lbo, sbo, mu, xscale, nct, lcf, les, lj0, loc, s));
+    loc.cmax = cmax;
+  }
   GEEK_TRY(tc_screen_launch(X.as<float>(), n, d, nprod, img, c2, mu, k, nct, lbo, sbo, ts.as<float>(), ti.as<int>(), nullptr,
-                            xscale, ovf, s));
+                            xscale, ovf, s, nprod == 17 ? &loc : nullptr));
   double* worst = reinterpret_cast<double*>(misc.as<unsigned long long>() + 1);
   unsigned long long* bad = misc.as<unsigned long long>() + 2;
   selftest_check<<<8, 128, 0, s>>>(X.as<float>(), n, d, C.as<double>(), k, mu.as<float>(), ts.as<float>(),

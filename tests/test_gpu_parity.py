@@ -302,9 +302,11 @@ def test_tcgen05_screen_selftest():
     assert L.geek_tc_selftest(128, 256, 16, out) == 0
     assert out[0] < 1e-5  # FP16x3 (scaled operands): same significand as TF32x3
     assert out[1] == 0
+    assert L.geek_tc_selftest(128, 256, 17, out) == 0
+    assert out[0] < 5e-4  # tile-local FP16: one f16 product, error ~2^-10 |x''||c'| <= 2^-10 (|x'| + |c'|)|c'|
 
 
-@pytest.mark.parametrize("mode", ["1", "3", "16"])
+@pytest.mark.parametrize("mode", ["1", "3", "16", "17"])
 def test_assign_screen_modes_vs_oracle(mode, monkeypatch):
     monkeypatch.setenv("GEEK_SCREEN", mode)
     rng = np.random.default_rng(11)
@@ -318,12 +320,12 @@ def test_assign_screen_modes_vs_oracle(mode, monkeypatch):
     assert got.objective == obj
 
 
-@pytest.mark.parametrize("d", [100, 24, 9])
-def test_fp16_screen_ragged_dims_and_tiny_coordinates(d, monkeypatch):
-    """FP16x3 at dims that are not a multiple of the 16-dim K slice, with
-    coordinates spanning ~9 orders of magnitude (scaled lo parts underflow to
-    f16 subnormals: the bound's absolute term covers them)."""
-    monkeypatch.setenv("GEEK_SCREEN", "16")
+@pytest.mark.parametrize("d,mode", [(100, "16"), (24, "16"), (9, "16"), (104, "17"), (24, "17")])
+def test_fp16_screen_ragged_dims_and_tiny_coordinates(d, mode, monkeypatch):
+    """FP16x3 / tile-local FP16 at dims that are not a multiple of the 16-dim
+    K slice, with coordinates spanning ~9 orders of magnitude (scaled parts
+    underflow to f16 subnormals: the bound's absolute term covers them)."""
+    monkeypatch.setenv("GEEK_SCREEN", mode)
     rng = np.random.default_rng(100 + d)
     C = rng.standard_normal((90, d)) * 500.0
     C[:, : d // 3] *= 1e-6
@@ -337,10 +339,11 @@ def test_fp16_screen_ragged_dims_and_tiny_coordinates(d, monkeypatch):
     assert got.objective == obj
 
 
-def test_fp16_screen_range_fallback(monkeypatch):
+@pytest.mark.parametrize("mode", ["16", "17"])
+def test_fp16_screen_range_fallback(mode, monkeypatch):
     """A point far outside the centers' range overflows the scaled f16 operand:
     the screen is redone in TF32x3 and the labels stay exact."""
-    monkeypatch.setenv("GEEK_SCREEN", "16")
+    monkeypatch.setenv("GEEK_SCREEN", mode)
     rng = np.random.default_rng(12)
     C = rng.standard_normal((40, 64)) * 3
     X = (C[rng.integers(0, 40, 5_000)] + rng.standard_normal((5_000, 64)) * 0.5).astype(np.float32)
@@ -351,6 +354,32 @@ def test_fp16_screen_range_fallback(monkeypatch):
     assert np.array_equal(got.assignment, lab)
     assert np.array_equal(got.radii, radii)
     assert got.objective == obj
+
+
+@pytest.mark.parametrize("order", ["clustered", "shuffled"])
+def test_tile_local_screen_orders(order, monkeypatch):
+    """The tile-local screen (GEEK_SCREEN=17): exact labels whatever the id order; on
+    cluster-ordered ids (the reference generator's order) each tile's origin
+    sits next to its points, so almost nothing beyond the near-duplicate
+    centers reaches the recheck."""
+    monkeypatch.setenv("GEEK_SCREEN", "17")
+    rng = np.random.default_rng(21)
+    k, d, n = 400, 128, 60_000
+    C = np.cumsum(rng.standard_normal((k, d)) * 2.0, axis=0) + 100.0  # a long chain: large |x'|
+    C[9] = C[8] + 1e-6  # near-duplicate centers: always rechecked
+    lab0 = np.sort(rng.integers(0, k, n))
+    X = (C[lab0] + rng.standard_normal((n, d))).astype(np.float32)
+    if order == "shuffled":
+        X = X[rng.permutation(n)]
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    L = G._lib.load_library()
+    assert L.geek_assign_last_screen_mode() == 17
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+    if order == "clustered":
+        assert L.geek_assign_last_rechecked() < 0.02 * n + 2 * (lab0 == 8).sum() + 2 * (lab0 == 9).sum()
 
 
 def test_tie_to_lowest_index():

@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-nvidia-smi -L > gpurun_out/smi2.txt
-timeout 1500 python -m pytest tests/test_gpu_multi.py -q -s > gpurun_out/t_multi.log 2>&1
-echo "multi rc=$?" >> gpurun_out/t_multi.log
+export PROBE_SORTED=1 PROBE_SCREENS=16,17 PROBE_MODES=0
+for sl in 0 1 2; do GEEK_SCREEN_SLEEP=$sl timeout 600 python tools/screen_probe.py 20000000 963 128 >> gpurun_out/probe2.log 2>&1; done

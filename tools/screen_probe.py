@@ -18,6 +18,8 @@ if os.environ.get("_PROBE_CHILD"):
     for i in range(0, n, 10_000_000):
         j = min(n, i + 10_000_000)
         lab = torch.randint(0, k, (j - i,), device="cuda", generator=g)
+        if os.environ.get("PROBE_SORTED"):  # cluster-ordered ids, as the reference generator's
+            lab = torch.sort(lab).values
         X[i:j] = (C[lab] + torch.randn(j - i, d, device="cuda", dtype=torch.float64, generator=g)).float()
     labels = torch.empty(n, dtype=torch.int64, device="cuda")
     best = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -27,8 +29,10 @@ if os.environ.get("_PROBE_CHILD"):
         torch.cuda.synchronize()
         ms.append(L.load_library().geek_assign_last_screen_ms())
     print(f"mode={os.environ.get('GEEK_SCREEN_PROF','0')} screen={os.environ.get('GEEK_SCREEN','16')} "
+          f"sleep={os.environ.get('GEEK_SCREEN_SLEEP','0')} "
           f"screen_ms={min(ms[1:]):.2f} all={['%.2f' % v for v in ms]}", flush=True)
 else:
-    for mode in os.environ.get("PROBE_MODES", "0,1,2,3").split(","):
-        env = dict(os.environ, _PROBE_CHILD="1", GEEK_SCREEN_PROF=mode, GEEK_SCREEN_ONLY="1")
-        subprocess.run([sys.executable, __file__] + sys.argv[1:], env=env, check=False)
+    for scr in os.environ.get("PROBE_SCREENS", os.environ.get("GEEK_SCREEN", "16")).split(","):
+        for mode in os.environ.get("PROBE_MODES", "0,1,2,3").split(","):
+            env = dict(os.environ, _PROBE_CHILD="1", GEEK_SCREEN_PROF=mode, GEEK_SCREEN_ONLY="1", GEEK_SCREEN=scr)
+            subprocess.run([sys.executable, __file__] + sys.argv[1:], env=env, check=False)
