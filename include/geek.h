@@ -245,31 +245,43 @@ int geek_round_means(const int64_t* digits, const uint64_t* counts, uint64_t ngr
 
 /* ---- assignment -------------------------------------------------------- */
 
+/* Statistics of one geek_assign_l2 call, written on the device (stream-ordered;
+ * replaces round 1's process-global geek_assign_last_* counters).           */
+typedef struct {
+  unsigned long long rechecked;   /* points re-evaluated exactly (screen candidates + full scans) */
+  unsigned long long full_scans;  /* of those, points whose candidate window overflowed: all centers */
+  unsigned long long screen_mode; /* 16 FP16x3, 3 TF32x3 (also after an f16 overflow), 17 tile-local
+                                     FP16, 1 TF32, 0 no tensor-core screen */
+  unsigned long long reserved;
+} geek_assign_stats_t;
+
 /* Nearest center by float64 direct-difference distance with numpy's pairwise
  * summation order and first-index ties (assignment.py:54-62, :95-99):
  * labels[i], best[i] = distance.  C is [k][d] float64.  float32 X with
  * d <= 128 and k >= 4 goes through the tcgen05 screen (FP16x3; env
- * GEEK_SCREEN=3 / 1 selects TF32x3 / TF32) and an exact float64 recheck.     */
+ * GEEK_SCREEN=17 / 3 / 1 selects tile-local FP16 / TF32x3 / TF32) and an
+ * exact float64 recheck.  Fully stream-ordered (no host synchronisation):
+ *   stats (device, may be NULL)       receives geek_assign_stats_t;
+ *   ev_screen_begin / ev_screen_end   (cudaEvent_t, may be NULL) are recorded
+ *                                     around the screen launches, so the
+ *                                     caller can time the dominant kernel;
+ *   workspace / workspace_bytes       caller scratch of at least
+ *                                     geek_assign_l2_workspace_size(n, d, k)
+ *                                     bytes; NULL = the stream-ordered pool;
+ *                                     too small -> GEEK_ERANGE.            */
+uint64_t geek_assign_l2_workspace_size(uint64_t n, int d, uint64_t k);
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
-                   int64_t* labels, double* best, void* stream);
+                   int64_t* labels, double* best, geek_assign_stats_t* stats, void* ev_screen_begin,
+                   void* ev_screen_end, void* workspace, uint64_t workspace_bytes, void* stream);
 
 /* Self-test of the tcgen05 screen on a synthetic problem (1000 x 128
  * points, 300 centers): out_host[0] = max |s_tc - S_f64| / (|x'||c'|max)
  * over every kept entry, out_host[1] = points whose screened top-1 is not
  * the f64 argmin.  lbo/sbo are the canonical-layout core-matrix strides in
- * bytes; nprod = 1 (TF32), 3 (TF32x3) or 16 (FP16x3 over power-of-two
- * scaled operands, the default screen of geek_assign_l2).                  */
+ * bytes; nprod = 1 (TF32), 3 (TF32x3), 16 (FP16x3 over power-of-two
+ * scaled operands, the default screen of geek_assign_l2) or 17 (tile-local
+ * FP16).  SYNC (test entry point).                                          */
 int geek_tc_selftest(uint32_t lbo, uint32_t sbo, int nprod, double* out_host);
-
-/* number of points the last geek_assign_l2 call re-checked exactly because
- * the float32 screen could not separate their two nearest centers        */
-uint64_t geek_assign_last_rechecked(void);
-/* CUDA-event duration (ms) of the last tensor-core screen kernel launch     */
-double geek_assign_last_screen_ms(void);
-/* of those, points whose candidate window overflowed (exact scan over all)   */
-uint64_t geek_assign_last_full_scans(void);
-/* precision of that screen: 16 = FP16x3 (scaled operands), 3 = TF32x3, 1 = TF32 */
-int geek_assign_last_screen_mode(void);
 
 /* radii[c] = max best over members (0 if none), sizes[c] = member count
  * (assignment.py:100-101, data.py:243-245).  Accumulates (call on zeroed

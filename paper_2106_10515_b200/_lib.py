@@ -72,11 +72,8 @@ _SIGS = {
     "geek_exact_sums": (i32, [vp, i32, u64, i32, u64, vp, vp, u64, i32, i32, vp, vp, vp]),
     "geek_sum_pack_bytes": (i32, [vp, u64, i32, i32, i32, vp, vp]),
     "geek_round_means": (i32, [vp, vp, u64, i32, i32, i32, vp, vp]),
-    "geek_assign_l2": (i32, [vp, i32, u64, i32, vp, u64, vp, vp, vp]),
-    "geek_assign_last_rechecked": (u64, []),
-    "geek_assign_last_screen_ms": (C.c_double, []),
-    "geek_assign_last_screen_mode": (i32, []),
-    "geek_assign_last_full_scans": (u64, []),
+    "geek_assign_l2_workspace_size": (u64, [u64, i32, u64]),
+    "geek_assign_l2": (i32, [vp, i32, u64, i32, vp, u64, vp, vp, vp, vp, vp, vp, u64, vp]),
     "geek_tc_selftest": (i32, [C.c_uint32, C.c_uint32, i32, vp]),
     "geek_radii_sizes": (i32, [vp, vp, u64, u64, vp, vp, vp]),
     "geek_pairwise_sum": (i32, [vp, u64, vp, vp]),

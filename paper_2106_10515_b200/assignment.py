@@ -33,14 +33,45 @@ def _check_compat(data, centers, metric):
         raise InvalidInput("jaccard assignment needs categorical or sparse data and modes")
 
 
-def assign_l2_device(X: torch.Tensor, C: torch.Tensor):
+class AssignStats:
+    """Device-side statistics of one geek_assign_l2 call (geek_assign_stats_t)
+    plus CUDA events around its screen; read them after the stream reaches
+    them (`read()` synchronises on the end event)."""
+
+    def __init__(self):
+        self.dev = _lib.zeros(4, torch.int64)
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+        self.ev0.record()  # materialise the events (torch creates them lazily)
+        self.ev1.record()
+
+    def read(self) -> dict:
+        v = self.dev.cpu().tolist()
+        self.ev1.synchronize()
+        ms = self.ev0.elapsed_time(self.ev1)
+        return dict(assign_rechecked=int(v[0]), assign_full_scans=int(v[1]), screen_mode=int(v[2]),
+                    screen_ms=float(ms) if v[2] else 0.0)
+
+
+_LAST = [None]
+
+
+def last_assign_stats() -> dict:
+    """Statistics of this process's last assign_l2_device call (tests, tools)."""
+    return _LAST[0].read() if _LAST[0] is not None else {}
+
+
+def assign_l2_device(X: torch.Tensor, C: torch.Tensor, stats: AssignStats = None):
     """(labels int64, best float64) on the device."""
     n, d = X.shape
     k = C.shape[0]
     labels = _lib.empty(max(1, n), torch.int64)
     best = _lib.empty(max(1, n), torch.float64)
+    st = stats if stats is not None else AssignStats()
     _lib.call("geek_assign_l2", _lib.ptr(X), _lib.dtype_code(X), n, d, _lib.ptr(C.contiguous()), k,
-              _lib.ptr(labels), _lib.ptr(best), _lib.stream())
+              _lib.ptr(labels), _lib.ptr(best), _lib.ptr(st.dev), _lib.C.c_void_p(st.ev0.cuda_event),
+              _lib.C.c_void_p(st.ev1.cuda_event), None, 0, _lib.stream())
+    _LAST[0] = st
     return labels[:n], best[:n]
 
 

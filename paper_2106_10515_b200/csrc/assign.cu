@@ -92,13 +92,18 @@ __device__ __forceinline__ double pw_sum(const PwPlan& p, const G& get) {
 constexpr int kAsgThreads = 128;
 constexpr int kAsgCenters = 16;  // centers staged per shared-memory tile
 
+// n_dev (may be null): the point count lives on the device (the queue of a
+// screen); the grid then strides over it
 template <class T>
 __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restrict__ X, uint64_t n, int d,
                                                                 const double* __restrict__ C, uint64_t k,
                                                                 const PwPlan plan, int64_t* labels,
-                                                                double* best, const uint32_t* idx) {
+                                                                double* best, const uint32_t* idx,
+                                                                const unsigned long long* n_dev = nullptr) {
   extern __shared__ double sC[];  // [kAsgCenters][d]
-  const uint64_t q = blockIdx.x * (uint64_t)kAsgThreads + threadIdx.x;
+  if (n_dev) n = *n_dev;
+  for (uint64_t base = blockIdx.x * (uint64_t)kAsgThreads; base < n; base += (uint64_t)gridDim.x * kAsgThreads) {
+  const uint64_t q = base + threadIdx.x;
   const bool valid = q < n;
   const uint64_t i = (idx && valid) ? idx[q] : q;
   const T* xr = X + (valid ? i : 0) * d;
@@ -126,6 +131,7 @@ __global__ void __launch_bounds__(kAsgThreads) assign_l2_kernel(const T* __restr
   if (valid) {
     labels[i] = bl;
     best[i] = bd;
+  }
   }
 }
 
@@ -346,11 +352,15 @@ constexpr int kFsThreads = 256;
 __global__ void __launch_bounds__(kFsThreads) full_scan_kernel(const float* __restrict__ X, int d,
                                                                const double* __restrict__ C, uint64_t k,
                                                                const PwPlan plan, const uint32_t* idx,
-                                                               int64_t* labels, double* best) {
+                                                               const unsigned long long* nidx, int64_t* labels,
+                                                               double* best) {
   extern __shared__ double sx[];  // [d]
   __shared__ double rd[kFsThreads / 32];
   __shared__ long long rl[kFsThreads / 32];
-  const uint64_t i = idx[blockIdx.x];
+  const uint64_t nq = *nidx;
+  for (uint64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+  const uint64_t i = idx[q];
+  __syncthreads();  // the previous point's reads of sx / rd / rl are done
   for (int j = threadIdx.x; j < d; j += kFsThreads) sx[j] = (double)X[i * d + j];
   __syncthreads();
   double bd = INFINITY;
@@ -389,6 +399,7 @@ __global__ void __launch_bounds__(kFsThreads) full_scan_kernel(const float* __re
       }
     labels[i] = bl;
     best[i] = bd;
+  }
   }
 }
 
@@ -549,25 +560,9 @@ struct DevSumTree {
 // label is final and only best = dist(x, c_label) is evaluated exactly;
 // otherwise the point is re-scanned exactly over all centers.
 
-static uint64_t& last_ambiguous() {
-  static uint64_t v = 0;
-  return v;
-}
-
-static double& last_screen_ms() {
-  static double v = 0.0;
-  return v;
-}
-
-static int& last_screen_mode() {  // 1 / 3 TF32 products, 16 = FP16x3
-  static int v = 0;
-  return v;
-}
-
-static uint64_t& last_full() {
-  static uint64_t v = 0;
-  return v;
-}
+// effective screen mode of a call: an FP16 screen whose scaled operand left the
+// f16 range was redone in TF32x3 (the fallback launch ran when *ovf != 0)
+__device__ __forceinline__ int eff_mode(int nprod, const unsigned* ovf) { return (ovf && *ovf) ? 3 : nprod; }
 
 constexpr int kScrP = 128, kScrC = 128, kScrK = 16, kScrThreads = 256;
 
@@ -803,9 +798,10 @@ __device__ __forceinline__ ScreenView screen_view(const float* s8, const int* i8
 __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                    uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
                                    float* xnorm, const float* mu, const unsigned long long* cmax_bits, int nprod,
-                                   int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb,
-                                   uint32_t* full, unsigned long long* nfull) {
+                                   const unsigned* ovf, int64_t* labels, double* best, uint32_t* amb,
+                                   unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
+  nprod = eff_mode(nprod, ovf);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const ScreenView v = screen_view(top_s + i * 8, top_i + i * 8);
     double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
@@ -840,9 +836,10 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
 __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C,
                                     uint64_t k, const float* top_s, const int* top_i, float* xnorm,
                                     const float* mu, const unsigned long long* cmax_bits, int nprod,
-                                    int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb,
-                                    uint32_t* full, unsigned long long* nfull) {
+                                    const unsigned* ovf, int64_t* labels, double* best, uint32_t* amb,
+                                    unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
+  nprod = eff_mode(nprod, ovf);
   const unsigned lane = threadIdx.x & 31, a = lane & 7;
   const unsigned gmask = 0xFFu << (lane & 24);
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
@@ -904,9 +901,10 @@ __global__ void tc_classify8_kernel(const float* __restrict__ X, uint64_t n, int
 __global__ void __launch_bounds__(256) tc_classify2_kernel(
     const float* __restrict__ X, uint64_t n, int d, const double* __restrict__ C, uint64_t k,
     const float* __restrict__ top_s, const int* __restrict__ top_i, float* xnorm, const float* __restrict__ mu,
-    const double* __restrict__ xpart, const unsigned long long* cmax_bits, int nprod, int64_t* labels, double* best,
-    uint32_t* amb, unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
+    const double* __restrict__ xpart, const unsigned long long* cmax_bits, int nprod, const unsigned* ovf,
+    int64_t* labels, double* best, uint32_t* amb, unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
+  nprod = eff_mode(nprod, ovf);
   const unsigned lane = threadIdx.x & 31, h = lane & 1;
   const unsigned pmask = 3u << (lane & 30);
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 1;
@@ -978,9 +976,11 @@ __global__ void __launch_bounds__(256) tc_classify2_kernel(
 // window); ties -> lower index
 __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const double* __restrict__ C, uint64_t k,
                                   const PwPlan plan, const float* top_s, const int* top_i, const float* xnorm,
-                                  const unsigned long long* cmax_bits, int nprod, const uint32_t* amb, uint64_t na,
-                                  int64_t* labels, double* best) {
+                                  const unsigned long long* cmax_bits, int nprod, const unsigned* ovf,
+                                  const uint32_t* amb, const unsigned long long* na_dev, int64_t* labels, double* best) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
+  nprod = eff_mode(nprod, ovf);
+  const uint64_t na = *na_dev;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < na; q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = amb[q];
     const float* s8 = top_s + i * 8;
@@ -1014,8 +1014,11 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, int d, const doub
 __global__ void tc_recheck8_kernel(const float* __restrict__ X, int d, const double* __restrict__ C,
                                    const float* __restrict__ top_s, const int* __restrict__ top_i,
                                    const float* __restrict__ xnorm, const unsigned long long* cmax_bits, int nprod,
-                                   const uint32_t* __restrict__ amb, uint64_t na, int64_t* labels, double* best) {
+                                   const unsigned* ovf, const uint32_t* __restrict__ amb,
+                                   const unsigned long long* na_dev, int64_t* labels, double* best) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
+  nprod = eff_mode(nprod, ovf);
+  const uint64_t na = *na_dev;
   const unsigned lane = threadIdx.x & 31, a = lane & 7;
   const unsigned gmask = 0xFFu << (lane & 24);
   const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 3;
@@ -1067,18 +1070,39 @@ __global__ void tc_recheck8_kernel(const float* __restrict__ X, int d, const dou
   }
 }
 
+__global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
+                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st) {
+  st->rechecked = (namb ? *namb : 0ull) + (nfull ? *nfull : 0ull);
+  st->full_scans = nfull ? *nfull : 0ull;
+  st->screen_mode = (unsigned long long)eff_mode(nprod, ovf);
+  st->reserved = 0;
+}
+
 }  // namespace geek
 
 using namespace geek;
 
 extern "C" {
 
+uint64_t geek_assign_l2_workspace_size(uint64_t n, int d, uint64_t k) {
+  // an upper bound over every path: per-point screen lists and queues
+  // (top-4 values / centers of both column halves, |x'|, queues, |x'|^2
+  // halves), the center operand images of the FP16 screen and its TF32x3
+  // fallback (<= 320 KB per 192-center tile at d <= 128), the tile-local
+  // origin table, the wide-row transposed centers, and alignment slack
+  const uint64_t nct = (k + 191) / 192, ntiles = (n + 127) / 128;
+  return n * 100 + nct * (330ull << 10) + k * (uint64_t)d * 24 + k * nct * 192 * 4 + ntiles * 80 + (4ull << 20);
+}
+
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k, int64_t* labels,
-                   double* best, void* stream) {
+                   double* best, geek_assign_stats_t* stats, void* ev_screen_begin, void* ev_screen_end,
+                   void* workspace, uint64_t workspace_bytes, void* stream) {
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 or 1");
   GEEK_REQUIRE(k >= 1, "cannot assign without centers");
   GEEK_REQUIRE(d >= 1 && d <= 1536, "dimension %d outside [1, 1536]", d);
+  WorkspaceScope scope(workspace, workspace_bytes);
+  if (stats) GEEK_CHECK_CUDA(cudaMemsetAsync(stats, 0, sizeof(geek_assign_stats_t), s));
   if (n == 0) return GEEK_OK;
   PwPlan plan;
   pw_build(plan, 0, d);
@@ -1090,23 +1114,21 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_CUDA(cudaFuncSetAttribute(assign_l2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
   }
-  if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull && !getenv("GEEK_NO_TC")) {
-    // tensor-core screen (FP16x3 over power-of-two scaled operands by default;
-    // GEEK_SCREEN=3 selects TF32x3 -- the same accuracy at half the MMA rate --
-    // and GEEK_SCREEN=1 the single TF32 product, whose bound ~2e-3|x'||c'|
-    // only separates data whose cluster gaps are large against |x'||c'|)
-    // -> classification -> candidate / full recheck
-    // default FP16x3; GEEK_SCREEN=17 selects the tile-local FP16 screen (one
+  if (dtype == 0 && k >= 4 && d <= 128 && n < 0xFFFFFFFFull) {
+    // tensor-core screen -> classification -> candidate / full recheck, all
+    // stream-ordered: the FP16 scale is chosen on the device, the TF32x3 redo
+    // after an f16 overflow is a launch that exits unless the overflow flag is
+    // set, and the rechecks stride over their device-side queue lengths.
+    // Default FP16x3; GEEK_SCREEN=17 selects the tile-local FP16 screen (one
     // product per K slice against each point tile's origin center: a third of
     // the MMAs, but on the benchmark data the kernel is bound by its epilogue,
-    // not the tensor pipe -- 83.5 vs 86.4 ms -- and its wider window sends
-    // 21M instead of 12M points to the recheck, so it loses overall:
-    // profiles/r2_screen.md), 3 / 1 TF32x3 / one TF32 product
+    // not the tensor pipe, and its wider window sends 21M instead of 12M
+    // points to the recheck: profiles/r2_screen.md), 3 / 1 TF32x3 / one TF32
     const char* sel = getenv("GEEK_SCREEN");
     const bool local_ok = k <= 3840 && d % 8 == 0;  // 4 x 48 KB B stages + two origin-table rows in SMEM
-    int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : (atoi(sel) == 17 && local_ok) ? 17 : 16;
-    Scratch img, c2s, mus, ts, ti, xn, amb, full, cnt, lcf, les, lj0;
-    TcLocal loc{nullptr, nullptr, nullptr};
+    const int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : (atoi(sel) == 17 && local_ok) ? 17 : 16;
+    Scratch img, c2s, mus, img3, c2s3, mus3, ts, ti, xn, amb, full, cnt, lcf, les, lj0, xp;
+    TcLocal loc{nullptr, nullptr, nullptr, nullptr};
     GEEK_TRY(cnt.alloc(48, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
     unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16)
@@ -1116,10 +1138,6 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     int nct = 0;
     float xscale = 1.f;
     GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
-    if (nprod >= 16) {
-      const double is = 1.0 / (double)xscale;
-      GEEK_CHECK_CUDA(cudaMemcpyAsync(cmax + 3, &is, 8, cudaMemcpyHostToDevice, s));
-    }
     if (nprod == 17) {
       GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s));
       loc.cmax = cmax;
@@ -1129,85 +1147,58 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_TRY(xn.alloc(n * 4, s));
     GEEK_TRY(amb.alloc(n * 4, s));
     GEEK_TRY(full.alloc(n * 4, s));
-    cudaEvent_t ev0, ev1;
-    GEEK_CHECK_CUDA(cudaEventCreate(&ev0));
-    GEEK_CHECK_CUDA(cudaEventCreate(&ev1));
-    GEEK_CHECK_CUDA(cudaEventRecord(ev0, s));
-    // TF32x3 screen also leaves |x'|^2 per row half for the 2-lane classifier
-    Scratch xp;
+    // the screens also leave |x'|^2 per row half for the 2-lane classifier
     const bool use_xp = nprod != 1 && d % 8 == 0 && d <= 128;
     if (use_xp) GEEK_TRY(xp.alloc(n * 16, s));
+    if (ev_screen_begin) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_screen_begin), s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
-                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s, &loc));
-    if (nprod >= 16) {  // a point coordinate beyond the f16 range: redo the screen in TF32x3
-      unsigned hov = 0;
-      GEEK_CHECK_CUDA(cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, s));
-      GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-      if (hov) {
-        nprod = 3;
-        xscale = 1.f;
-        GEEK_CHECK_CUDA(cudaMemsetAsync(cmax, 0, 48, s));
-        GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
-        GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO,
-                                  ts.as<float>(), ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s));
-      }
+                              ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s,
+                              nprod == 17 ? &loc : nullptr));
+    if (nprod >= 16) {  // a point coordinate beyond the f16 range: the TF32x3 redo runs (device-predicated)
+      int nct3 = 0;
+      float xs3 = 1.f;
+      GEEK_TRY(tc_screen_prepare(C, k, d, 3, kTcLBO, kTcSBO, img3, c2s3, mus3, cmax, nct3, xs3, s));
+      GEEK_TRY(tc_screen_launch((const float*)X, n, d, 3, img3, c2s3, mus3, k, nct3, kTcLBO, kTcSBO, ts.as<float>(),
+                                ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xs3, ovf, s, nullptr, 1, ovf));
     }
-    GEEK_CHECK_CUDA(cudaEventRecord(ev1, s));
-    last_screen_mode() = nprod;
-    if (getenv("GEEK_SCREEN_ONLY")) {  // profiling hook: time the screen alone (labels are not written)
-      GEEK_CHECK_CUDA(cudaEventSynchronize(ev1));
-      float ms = 0.f;
-      GEEK_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-      last_screen_ms() = ms;
-      cudaEventDestroy(ev0);
-      cudaEventDestroy(ev1);
-      return GEEK_OK;
-    }
+    if (ev_screen_end) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_screen_end), s));
+    // (after a redo the mean / images of the TF32x3 prepare are the ones that match;
+    // both prepares compute the same mean, and |c'|max is an atomic maximum of the same values)
+    const float* mu_cls = mus.as<float>();
     if (d % 8 == 0 && d <= 128)
       tc_classify2_kernel<<<grid_for(n * 2, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(),
-          use_xp ? xp.as<double>() : nullptr, cmax, nprod, labels, best, amb.as<uint32_t>(), namb,
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu_cls,
+          use_xp ? xp.as<double>() : nullptr, cmax, nprod, ovf, labels, best, amb.as<uint32_t>(), namb,
           full.as<uint32_t>(), nfull);
     else if (d >= 8)
       tc_classify8_kernel<<<grid_for(n * 8, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax, nprod,
+          (const float*)X, n, d, C, k, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu_cls, cmax, nprod, ovf,
           labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     else
       tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
-          (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mus.as<float>(), cmax,
-          nprod, labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+          (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu_cls, cmax, nprod, ovf,
+          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
     GEEK_CHECK_LAUNCH();
-    unsigned long long cnts[2];
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(cnts, namb, 16, cudaMemcpyDeviceToHost, s));
-    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-    last_ambiguous() = cnts[0] + cnts[1];
-    last_full() = cnts[1];
-    float ms = 0.f;
-    GEEK_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    last_screen_ms() = ms;
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    if (cnts[0] && d >= 8) {
-      tc_recheck8_kernel<<<grid_for(cnts[0] * 8, 256, 148 * 16), 256, 0, s>>>(
-          (const float*)X, d, C, ts.as<float>(), ti.as<int>(), xn.as<float>(), cmax, nprod, amb.as<uint32_t>(),
-          cnts[0], labels, best);
-      GEEK_CHECK_LAUNCH();
-    } else if (cnts[0]) {
-      tc_recheck_kernel<<<grid_for(cnts[0], 128), 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(),
-                                                               ti.as<int>(), xn.as<float>(), cmax, nprod,
-                                                               amb.as<uint32_t>(), cnts[0], labels, best);
-      GEEK_CHECK_LAUNCH();
-    }
-    if (cnts[1]) {
-      full_scan_kernel<<<(unsigned)cnts[1], kFsThreads, sizeof(double) * d, s>>>(
-          (const float*)X, d, C, k, plan, full.as<uint32_t>(), labels, best);
+    if (d >= 8)
+      tc_recheck8_kernel<<<148 * 16, 256, 0, s>>>((const float*)X, d, C, ts.as<float>(), ti.as<int>(), xn.as<float>(),
+                                                  cmax, nprod, ovf, amb.as<uint32_t>(), namb, labels, best);
+    else
+      tc_recheck_kernel<<<148 * 8, 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(), ti.as<int>(),
+                                                xn.as<float>(), cmax, nprod, ovf, amb.as<uint32_t>(), namb, labels,
+                                                best);
+    GEEK_CHECK_LAUNCH();
+    full_scan_kernel<<<148 * 4, kFsThreads, sizeof(double) * d, s>>>((const float*)X, d, C, k, plan,
+                                                                     full.as<uint32_t>(), nfull, labels, best);
+    GEEK_CHECK_LAUNCH();
+    if (stats) {
+      assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, ovf, nprod, stats);
       GEEK_CHECK_LAUNCH();
     }
     return GEEK_OK;
   }
   const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
   const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;
-  if (!screened && d > 128 && !getenv("GEEK_NO_CT")) {
+  if (!screened && d > 128) {
     const uint64_t kpad = (k + 31) / 32 * 32;
     Scratch ctb;
     GEEK_TRY(ctb.alloc(kpad * d * 8, s));
@@ -1253,6 +1244,8 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     GEEK_CHECK_LAUNCH();
     return GEEK_OK;
   }
+  // float32 SIMT screen (129 <= d with its SMEM tile in 200 KB): certain points
+  // are labelled in the screen, the queued ones exactly over all centers
   Scratch cf, c2, amb, cnt;
   GEEK_TRY(cf.alloc(k * d * 4, s));
   GEEK_TRY(c2.alloc(k * 4, s));
@@ -1265,28 +1258,20 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
   GEEK_CHECK_LAUNCH();
   GEEK_CHECK_CUDA(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scr_smem));
   const unsigned grid = (unsigned)((n + kScrP - 1) / kScrP);
+  if (ev_screen_begin) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_screen_begin), s));
   screen_kernel<<<grid, kScrThreads, scr_smem, s>>>((const float*)X, n, d, cf.as<float>(), c2.as<float>(), C, k,
                                                     cmax, plan, labels, best, amb.as<uint32_t>(), namb);
   GEEK_CHECK_LAUNCH();
-  unsigned long long na = 0;
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(&na, namb, 8, cudaMemcpyDeviceToHost, s));
-  GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-  last_ambiguous() = na;
-  if (na) {
-    assign_l2_kernel<float><<<(unsigned)((na + kAsgThreads - 1) / kAsgThreads), kAsgThreads, smem, s>>>(
-        (const float*)X, na, d, C, k, plan, labels, best, amb.as<uint32_t>());
+  if (ev_screen_end) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_screen_end), s));
+  assign_l2_kernel<float><<<148 * 8, kAsgThreads, smem, s>>>((const float*)X, n, d, C, k, plan, labels, best,
+                                                             amb.as<uint32_t>(), namb);
+  GEEK_CHECK_LAUNCH();
+  if (stats) {
+    assign_stats_kernel<<<1, 1, 0, s>>>(namb, nullptr, nullptr, 0, stats);
     GEEK_CHECK_LAUNCH();
   }
   return GEEK_OK;
 }
-
-uint64_t geek_assign_last_rechecked(void) { return last_ambiguous(); }
-
-double geek_assign_last_screen_ms(void) { return last_screen_ms(); }
-
-int geek_assign_last_screen_mode(void) { return last_screen_mode(); }
-
-uint64_t geek_assign_last_full_scans(void) { return last_full(); }
 
 int geek_radii_sizes(const int64_t* labels, const double* best, uint64_t n, uint64_t k, double* radii,
                      int64_t* sizes, void* stream) {

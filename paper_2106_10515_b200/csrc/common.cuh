@@ -50,21 +50,57 @@ struct Status {
 // (the default release threshold of 0 unmaps it at every sync)
 void ensure_pool();
 
-// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
+// Caller-provided workspace: while a WorkspaceScope is alive on this host
+// thread, every Scratch carves its buffer out of the caller's device memory
+// (256-byte aligned bump allocation, nothing freed until the scope ends)
+// instead of the stream-ordered pool.
+struct Workspace {
+  char* base = nullptr;
+  size_t size = 0, used = 0;
+};
+Workspace*& tls_workspace();
+struct WorkspaceScope {
+  Workspace ws;
+  Workspace* prev;
+  WorkspaceScope(void* base, size_t bytes) : prev(tls_workspace()) {
+    ws.base = static_cast<char*>(base);
+    ws.size = bytes;
+    tls_workspace() = base ? &ws : nullptr;
+  }
+  ~WorkspaceScope() { tls_workspace() = prev; }
+  WorkspaceScope(const WorkspaceScope&) = delete;
+  WorkspaceScope& operator=(const WorkspaceScope&) = delete;
+};
+
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync), or a slice
+// of the caller's workspace inside a WorkspaceScope.
 struct Scratch {
   void* ptr = nullptr;
   cudaStream_t stream = nullptr;
+  bool pooled = false;
   Scratch() = default;
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
   ~Scratch() {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (ptr && pooled) cudaFreeAsync(ptr, stream);
   }
   int alloc(size_t bytes, cudaStream_t s) {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (ptr && pooled) cudaFreeAsync(ptr, stream);
     ptr = nullptr;
     stream = s;
     if (bytes == 0) bytes = 16;
+    if (Workspace* w = tls_workspace()) {
+      const size_t off = (w->used + 255) & ~(size_t)255;
+      if (off + bytes > w->size) {
+        set_error("workspace of %zu bytes too small (needs more than %zu)", w->size, off + bytes);
+        return GEEK_ERANGE;
+      }
+      ptr = w->base + off;
+      w->used = off + bytes;
+      pooled = false;
+      return GEEK_OK;
+    }
+    pooled = true;
     ensure_pool();
     cudaError_t e = cudaMallocAsync(&ptr, bytes, s);
     if (e != cudaSuccess) {
@@ -187,6 +223,8 @@ int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStre
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s);
+// {xscale, oscale} of a prepared screen (device memory inside its mu scratch)
+const float* tc_scal(const Scratch& mu, int d);
 // nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu
 struct TcLocal {
   const float* cf;  // [k][d] float32 c'

@@ -21,6 +21,11 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_last_error.c_str(); }
 
+Workspace*& tls_workspace() {
+  static thread_local Workspace* w = nullptr;
+  return w;
+}
+
 void ensure_pool() {
   static std::mutex mu;
   static bool done[64] = {};

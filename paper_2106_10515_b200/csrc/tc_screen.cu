@@ -382,8 +382,8 @@ struct TcParams {
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes, 8 = no top-4 inserts,
                       // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
-  float xscale;       // NPROD = 16: x' is multiplied by this power of two before the f16 split
-  float oscale;       // top_s = oscale * (accumulator): 2 (TF32) or 2 / xscale^2 (FP16)
+  const float* scal;  // device {xscale, oscale}: x' (FP16: times xscale, a power of two, before the f16
+                      // split); top_s = oscale * (accumulator): 2 (TF32) or 2 / xscale^2 (FP16)
   unsigned* ovf;      // NPROD = 16: set when a scaled operand leaves the f16 range (caller reruns in TF32x3)
   // NPROD = 17 (tile-local origin)
   const float* cf;    // [k][d] float32 c' = fl32(c - mu), the origins
@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (P.run_if && *P.run_if == 0) return;  // a fallback launch that is not needed
+  const float xscale = __ldg(P.scal), oscale = __ldg(P.scal + 1);
   float* Ebuf = reinterpret_cast<float*>(bars + 40);  // NPROD = 17: E rows of the current / next point tile
   float2* Upart = reinterpret_cast<float2*>(Ebuf + 2 * P.kpadE);  // [2][128 rows][2 halves] (|x''|^2, |x'|^2)
   if (tid == 0) {
@@ -693,7 +694,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       if (i < P.n) {  // two column halves -> [n][8] of s = 2 * (s / 2) (exact); the classifier merges them
         const int h = (warp >> 2) * 4;
         *reinterpret_cast<float4*>(P.top_s + i * 8 + h) =
-            make_float4(P.oscale * top.s[0], P.oscale * top.s[1], P.oscale * top.s[2], P.oscale * top.s[3]);
+            make_float4(oscale * top.s[0], oscale * top.s[1], oscale * top.s[2], oscale * top.s[3]);
         *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
       }
     };
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             }
             if (P.prof == 3 || (P.prof >= 5 && P.prof <= 7)) continue;
             if (Cfg::kF16) {
-              const float y0 = x0 * P.xscale, y1 = x1 * P.xscale, y2 = x2 * P.xscale, y3 = x3 * P.xscale;
+              const float y0 = x0 * xscale, y1 = x1 * xscale, y2 = x2 * xscale, y3 = x3 * xscale;
               big |= fmaxf(fmaxf(fabsf(y0), fabsf(y1)), fmaxf(fabsf(y2), fabsf(y3))) > 32768.f;
               // packed conversions: element 2j in the low half (the K-major f16 order)
               const __half2 g01 = __floats2half2_rn(y0, y1), g23 = __floats2half2_rn(y2, y3);
@@ -887,7 +888,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const float cn = (float)__longlong_as_double((long long)P.cmax[0]);
       const float win = 2.2f * (1.953125e-3f * sqrtf(xpp) * cn + 1e-5f * cn * cn) + 1e-4f * xp;
       const float us = xpp - xp + 4.f * win + 1.f;  // s units
-      return us / P.oscale;                          // accumulator units (v = s / oscale)
+      return us / oscale;                            // accumulator units (v = s / oscale)
     };
     if (my_tiles > 0) {
       load_regs(0);
@@ -934,7 +935,8 @@ __global__ void center_mean_kernel(const double* C, uint64_t k, int d, float* mu
 // s^2 |c'|^2 / 2 as three f16 parts, and the ones slice is f16 1.0.
 __global__ void center_image_kernel(const double* C, uint64_t k, int d, const float* mu, int nct, int parts,
                                     uint32_t lbo, uint32_t sbo, float* Bimg, float* c2,
-                                    unsigned long long* cmax_bits, int f16, float xscale, int slices) {
+                                    unsigned long long* cmax_bits, int f16, const float* scal, int slices) {
+  const float xscale = __ldg(scal);
   const int sdims = f16 ? 16 : 8, eb = f16 ? 2 : 4, chunk = slices * sdims;
   const int nchunks_k = (d + chunk - 1) / chunk;
   const uint64_t half = (uint64_t)slices * kTcBSliceBytes;
@@ -1025,8 +1027,9 @@ __global__ void centered_f32_kernel(const double* C, uint64_t k, int d, const fl
 
 // Es[j0][j] = (|c'_j|^2 - 2 c'_j0 . c'_j) * xscale^2 / 2 in float64 over the
 // float32 c', rounded once to float32; +inf for the padding centers j >= k
-__global__ void origin_table_kernel(const float* cf, uint64_t k, int d, int kpadE, double half_s2, float* Es) {
+__global__ void origin_table_kernel(const float* cf, uint64_t k, int d, int kpadE, const float* scal, float* Es) {
   const uint64_t total = k * (uint64_t)kpadE;
+  const double half_s2 = 0.5 * (double)__ldg(scal) * (double)__ldg(scal);
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t a = q / kpadE, j = q % kpadE;
@@ -1062,6 +1065,27 @@ __global__ void pick_origin_kernel(const float* top_s, const int* top_i, uint64_
   }
 }
 
+// the screen's scales, on the device (no host round trip): FP16 modes take
+// s = 2^e with max |s c'_j| < 16 (so s^2 |c'|^2 / 2 < 2^14 stays inside f16
+// in three parts), oscale = 2 / s^2, and cmax_bits[3] = 1/s for the
+// classifier's bound; TF32 modes s = 1, oscale = 2
+__global__ void screen_scale_kernel(const unsigned* amax, int f16, float* scal, unsigned long long* cmax_bits) {
+  float xs = 1.f;
+  if (f16) {
+    const float m = __uint_as_float(*amax);
+    int e = 0;
+    if (m > 0.f && isfinite(m)) frexpf(m, &e);  // m < 2^e
+    xs = ldexpf(1.f, 4 - e);
+    cmax_bits[3] = (unsigned long long)__double_as_longlong(1.0 / (double)xs);
+  }
+  scal[0] = xs;
+  scal[1] = 2.f / (xs * xs);
+}
+
+const float* tc_scal(const Scratch& mu, int d) {  // {xscale, oscale} inside the mu scratch
+  return reinterpret_cast<const float*>(reinterpret_cast<const char*>(mu.ptr) + ((size_t)d * 4 + 15) / 16 * 16 + 16);
+}
+
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s) {
@@ -1073,27 +1097,22 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
   const int slices = nprod == 17 ? kTcKmax / 16 : 2;
   GEEK_TRY(img.alloc((size_t)nct * tc_ct_bytes(d, parts, slices * (f16 ? 16 : 8), slices), s));
   GEEK_TRY(c2.alloc((size_t)nct * kTcN * 4, s));
-  GEEK_TRY(mu.alloc((size_t)d * 4 + 16, s));
+  // mu: [d] float, then the |s c'| maximum (u32 bits), then {xscale, oscale}
+  GEEK_TRY(mu.alloc(((size_t)d * 4 + 15) / 16 * 16 + 32, s));
+  unsigned* amax = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(mu.ptr) + ((size_t)d * 4 + 15) / 16 * 16);
+  float* scal = const_cast<float*>(tc_scal(mu, d));
   center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
   GEEK_CHECK_LAUNCH();
-  xscale = 1.f;
-  if (f16) {  // s = 2^e with max |s c'_j| < 16: s^2 |c'|^2 / 2 < 2^14 stays inside f16 in three parts
-    unsigned* amax = reinterpret_cast<unsigned*>(mu.as<float>() + d);
-    GEEK_CHECK_CUDA(cudaMemsetAsync(amax, 0, 4, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(amax, 0, 4, s));
+  if (f16) {
     center_absmax_kernel<<<grid_for(k * (uint64_t)d, 256, 148 * 4), 256, 0, s>>>(C, k, d, mu.as<float>(), amax);
     GEEK_CHECK_LAUNCH();
-    unsigned h = 0;
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(&h, amax, 4, cudaMemcpyDeviceToHost, s));
-    GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-    float m;
-    memcpy(&m, &h, 4);
-    GEEK_REQUIRE(std::isfinite(m), "FP16 screen: non-finite center coordinate");
-    int e = 0;
-    if (m > 0.f) frexpf(m, &e);  // m < 2^e
-    xscale = ldexpf(1.f, 4 - e);
   }
+  screen_scale_kernel<<<1, 1, 0, s>>>(amax, f16 ? 1 : 0, scal, cmax_dev);
+  GEEK_CHECK_LAUNCH();
+  xscale = 0.f;  // lives on the device (tc_scal)
   center_image_kernel<<<grid_for((uint64_t)nct * kTcN, 128), 128, 0, s>>>(
-      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev, f16 ? 1 : 0, xscale,
+      C, k, d, mu.as<float>(), nct, parts, lbo, sbo, img.as<float>(), c2.as<float>(), cmax_dev, f16 ? 1 : 0, scal,
       slices);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
@@ -1142,36 +1161,41 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   {
     const uint64_t last = k - (uint64_t)(nct - 1) * kTcN;  // 1..kTcN valid centers
     P.nlast = (int)((last + 15) / 16 * 16);
-    if (getenv("GEEK_SCREEN_FULLN")) P.nlast = kTcN;
   }
   P.lbo = lbo;
   P.sbo = sbo;
   P.top_s = top_s;
   P.top_i = top_i;
   P.xpart = nprod != 1 ? xpart : nullptr;
-  P.xscale = xscale;
-  P.oscale = nprod >= 16 ? 2.f / (xscale * xscale) : 2.f;
+  P.scal = tc_scal(mu, d);
+  (void)xscale;
   P.ovf = ovf;
-  P.pushcut = getenv("GEEK_SCREEN_PUSHCUT") ? atoi(getenv("GEEK_SCREEN_PUSHCUT")) : 12;
-  P.prof = getenv("GEEK_SCREEN_PROF") ? atoi(getenv("GEEK_SCREEN_PROF")) : 0;
-  // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
-                ? 1 : 0;
-  if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
-  if (getenv("GEEK_SCREEN_C2RING")) P.c2res = 0;
-  P.sleepwait = getenv("GEEK_SCREEN_SLEEP") ? atoi(getenv("GEEK_SCREEN_SLEEP")) : 0;
+  // profiling knobs that change or skip work exist only in a -DGEEK_DEBUG_KNOBS
+  // build (tools/screen_probe.py); the product library always runs the full screen
+  P.pushcut = 12;
+  P.prof = 0;
+  P.sleepwait = 0;
   P.dbg = nullptr;
   Scratch dbg;
+#ifdef GEEK_DEBUG_KNOBS
+  if (getenv("GEEK_SCREEN_PUSHCUT")) P.pushcut = atoi(getenv("GEEK_SCREEN_PUSHCUT"));
+  if (getenv("GEEK_SCREEN_PROF")) P.prof = atoi(getenv("GEEK_SCREEN_PROF"));
+  if (getenv("GEEK_SCREEN_SLEEP")) P.sleepwait = atoi(getenv("GEEK_SCREEN_SLEEP"));
   if (getenv("GEEK_SCREEN_DBG")) {
     GEEK_TRY(dbg.alloc(148 * 4 * 8 * 2, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 4 * 8 * 2, s));
     P.dbg = dbg.as<unsigned long long>();
   }
+#endif
+  // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
+  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
+                ? 1 : 0;
+  if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
   const int st = nprod == 17   ? launch_screen<17>(P, s)
                  : nprod == 16 ? launch_screen<16>(P, s)
                  : nprod == 3  ? launch_screen<3>(P, s)
                                : launch_screen<1>(P, s);
-  if (st == GEEK_OK && P.dbg) {  // diagnostics: where the MMA warp waits
+  if (st == GEEK_OK && P.dbg) {  // diagnostics (GEEK_DEBUG_KNOBS builds): where the MMA warp waits
     unsigned long long h[148 * 8];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -1208,7 +1232,7 @@ int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_
   centered_f32_kernel<<<grid_for(k * (uint64_t)d, 256), 256, 0, s>>>(C, k, d, mu17.as<float>(), cf.as<float>());
   GEEK_CHECK_LAUNCH();
   origin_table_kernel<<<grid_for(k * (uint64_t)kpadE, 128, 148 * 16), 128, 0, s>>>(
-      cf.as<float>(), k, d, kpadE, 0.5 * (double)xscale * (double)xscale, Es.as<float>());
+      cf.as<float>(), k, d, kpadE, tc_scal(mu17, d), Es.as<float>());
   GEEK_CHECK_LAUNCH();
   Scratch img1, c21, mu1, ts, ti, misc;
   GEEK_TRY(misc.alloc(32, s));

@@ -27,7 +27,8 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .assignment import assign_cat_device, assign_l2_device, assign_sparse_device, pairwise_sum, radii_sizes
+from .assignment import (AssignStats, assign_cat_device, assign_l2_device, assign_sparse_device, pairwise_sum,
+                         radii_sizes)
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
@@ -682,11 +683,8 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
         comm.all_reduce(digits, dist.ReduceOp.SUM, "LocalCenters")
         C = round_means(digits, groups.sizes(), emin, nd)
     with tm.stage("assign"):
-        labels, best = assign_l2_device(X_local, C)
-        info["assign_rechecked"] = int(_lib.load_library().geek_assign_last_rechecked())
-        info["screen_ms"] = float(_lib.load_library().geek_assign_last_screen_ms())
-        info["screen_mode"] = int(_lib.load_library().geek_assign_last_screen_mode())
-        info["assign_full_scans"] = int(_lib.load_library().geek_assign_last_full_scans())
+        astats = AssignStats()
+        labels, best = assign_l2_device(X_local, C, astats)
         info["centers"] = int(groups.count)
     weights = groups.sizes()
 
@@ -719,6 +717,7 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
             labels, best = assign_l2_device(X_local, C)
             radii, sizes, obj = reduce_assignment(labels, best, C.shape[0])
     timings = tm.finish()
+    info.update(astats.read())  # device counters + screen events of the first assignment
     if comm.on:
         dist.all_reduce(nonfinite, op=dist.ReduceOp.MAX)
     if int(nonfinite.item()):  # numeric.py:24-25 (exact_column_sums)

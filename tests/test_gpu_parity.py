@@ -285,7 +285,7 @@ def test_assign_screened_f32_vs_oracle(d, k, offset):
     assert np.array_equal(got.assignment, lab)
     assert np.array_equal(got.radii, radii)
     assert got.objective == obj
-    assert G._lib.load_library().geek_assign_last_rechecked() >= 50
+    assert G.assignment.last_assign_stats()["assign_rechecked"] >= 50
 
 
 def test_tcgen05_screen_selftest():
@@ -373,13 +373,45 @@ def test_tile_local_screen_orders(order, monkeypatch):
         X = X[rng.permutation(n)]
     got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
     lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
-    L = G._lib.load_library()
-    assert L.geek_assign_last_screen_mode() == 17
+    st = G.assignment.last_assign_stats()
+    assert st["screen_mode"] == 17
     assert np.array_equal(got.assignment, lab)
     assert np.array_equal(got.radii, radii)
     assert got.objective == obj
     if order == "clustered":
-        assert L.geek_assign_last_rechecked() < 0.02 * n + 2 * (lab0 == 8).sum() + 2 * (lab0 == 9).sum()
+        assert st["assign_rechecked"] < 0.02 * n + 2 * (lab0 == 8).sum() + 2 * (lab0 == 9).sum()
+
+
+def test_assign_abi_workspace_stats_events():
+    """The C-ABI contract of geek_assign_l2: caller workspace (size query;
+    too small -> GEEK_ERANGE), device-side statistics, caller events around
+    the screen, no host synchronisation needed to launch it."""
+    from paper_2106_10515_b200 import _lib
+    from paper_2106_10515_b200.assignment import AssignStats
+
+    rng = np.random.default_rng(3)
+    k, d, n = 300, 128, 50_000
+    C = rng.standard_normal((k, d)) * 3
+    X = (C[np.sort(rng.integers(0, k, n))] + rng.standard_normal((n, d))).astype(np.float32)
+    Xd, Cd = torch.from_numpy(X).cuda(), torch.from_numpy(C).cuda()
+    L = _lib.load_library()
+    wsb = int(L.geek_assign_l2_workspace_size(n, d, k))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    lab = torch.empty(n, dtype=torch.int64, device="cuda")
+    best = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = AssignStats()
+    _lib.call("geek_assign_l2", _lib.ptr(Xd), 0, n, d, _lib.ptr(Cd), k, _lib.ptr(lab), _lib.ptr(best),
+              _lib.ptr(st.dev), _lib.C.c_void_p(st.ev0.cuda_event), _lib.C.c_void_p(st.ev1.cuda_event),
+              _lib.ptr(ws), wsb, _lib.stream())
+    info = st.read()
+    want_lab, want_best, _, _ = O.assign_l2(X.astype(np.float64), C)
+    assert np.array_equal(lab.cpu().numpy(), want_lab)
+    assert np.array_equal(best.cpu().numpy(), want_best)
+    assert info["screen_mode"] == 16 and info["screen_ms"] > 0 and info["assign_rechecked"] >= info["assign_full_scans"]
+    small = torch.empty(1 << 16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(G.EngineError, match="workspace"):
+        _lib.call("geek_assign_l2", _lib.ptr(Xd), 0, n, d, _lib.ptr(Cd), k, _lib.ptr(lab), _lib.ptr(best), None, None,
+                  None, _lib.ptr(small), small.numel(), _lib.stream())
 
 
 def test_tie_to_lowest_index():

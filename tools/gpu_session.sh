@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-export PROBE_SORTED=1 PROBE_SCREENS=16,17 PROBE_MODES=0
-for sl in 0 1 2; do GEEK_SCREEN_SLEEP=$sl timeout 600 python tools/screen_probe.py 20000000 963 128 >> gpurun_out/probe2.log 2>&1; done
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t_all.log 2>&1
+echo "all rc=$?" >> gpurun_out/t_all.log
+timeout 900 python bench.py --steps 3 --warmup 3 --no-checks --no-e2e > gpurun_out/bench3.json 2> gpurun_out/bench3.err
