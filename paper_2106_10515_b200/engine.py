@@ -32,13 +32,15 @@ from .assignment import (AssignStats, assign_cat_device, assign_l2_device, assig
 from .data import CategoricalData, CentralVector, Clustering, DenseData, MixedData, SeedGroup, SparseData
 from .errors import EngineError, InvalidInput
 from .hashing import DophReducer, derive_seed
-from .numeric import (center_stats_bytes, digit_count, exponent_range, label_mode_centers, label_sparse_counts,
-                      label_sums, mode_centers, mode_counts, partial_sums, round_means, sparse_counts)
+from .numeric import (center_stats_bytes, digit_count, exponent_range, label_mode_centers, label_mode_counts,
+                      label_sparse_counts, label_sums, mode_centers, mode_counts, partial_sums, round_means,
+                      sparse_counts)
 from .seeding import SeedingParams, dedup_device, silk_votes
 from .tables import BucketTable, GroupSet
 from .transform import (HomoTransformParams, MinhashTransformParams, categorical_token_csr, directions_device,
-                        discretize_numeric, even_partition_sizes, project_keys, projection_tolerance,
-                        rank_split_codes, signature_bucket_codes, split_boundary_stats)
+                        discretize_numeric, even_partition_sizes, group_signature_tables, project_keys,
+                        projection_tolerance, rank_split_codes, signature_bucket_codes, signature_rows,
+                        split_boundary_stats)
 
 __all__ = ["EngineError", "WorkerConfig", "PipelineConfig", "PipelineResult", "split_data", "run_pipeline"]
 
@@ -733,10 +735,215 @@ def _dense_pipeline(X_local: torch.Tensor, n: int, row_lo: int, config: Pipeline
                           dict(comm.bytes) if comm.on else dict(logical.bytes), warnings, info, gather)
 
 
+def route_signature_rows(sig: torch.Tensor, n: int, K: int, comm: _Comm) -> torch.Tensor:
+    """Bucket synchronisation for signature tables (engine.py:186-207, 227-238):
+    rank r holds the [n_local, m*K] signatures of its contiguous rows; table j
+    goes to rank j % G, which receives [m_own, n, K] with the shards in id order."""
+    n_local, mK = sig.shape
+    m, G, rank = mK // K, comm.G, comm.rank
+    spans = split_data(n, G)
+    mine = [[j for j in range(m) if j % G == q] for q in range(G)]
+    own = mine[rank]
+    r3 = sig.view(n_local, m, K)
+    send = torch.cat([r3[:, mine[q], :].permute(1, 0, 2).reshape(-1) for q in range(G)])
+    send_sizes = [len(mine[q]) * n_local * K for q in range(G)]
+    recv_sizes = [len(own) * (hi - lo) * K for lo, hi in spans]
+    recv = torch.empty(sum(recv_sizes), dtype=sig.dtype, device=sig.device)
+    dist.all_to_all_single(recv, send, recv_sizes, send_sizes)
+    comm.count("BucketShard", (send.numel() - len(own) * n_local * K) * sig.element_size())
+    parts = torch.split(recv, recv_sizes)
+    return torch.cat([pt.view(len(own), hi - lo, K) for pt, (lo, hi) in zip(parts, spans)], dim=1).contiguous()
+
+
+def _dist_modes(keys: list, k: int, cs: int, comm: _Comm) -> torch.Tensor:
+    """Per-attribute modes over a code space too large for dense counts, with the
+    rows spread over ranks: keys[c] holds group * cs + code of this rank's rows;
+    (key, count) runs are routed to the rank owning the group (group % G), summed
+    there, each owned group keeps its most frequent code (the smallest among
+    equal counts, seeding.py:180-185), and a MIN all-reduce assembles [k, d]."""
+    G = comm.G
+    dev = keys[0].device if keys else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((k, len(keys)), dtype=torch.int32, device=dev)
+    for c, key in enumerate(keys):
+        uk, cnt = torch.unique(key, sorted=True, return_counts=True)
+        owner = (uk // cs) % G
+        order = torch.sort(owner, stable=True).indices
+        uk, cnt = uk[order].contiguous(), cnt[order].contiguous()
+        send_n = torch.bincount(owner, minlength=G)
+        recv_n = torch.empty_like(send_n)
+        dist.all_to_all_single(recv_n, send_n)
+        ss, rs = send_n.tolist(), recv_n.tolist()
+        rk = torch.empty(sum(rs), dtype=uk.dtype, device=dev)
+        rc = torch.empty(sum(rs), dtype=cnt.dtype, device=dev)
+        dist.all_to_all_single(rk, uk, rs, ss)
+        dist.all_to_all_single(rc, cnt, rs, ss)
+        comm.count("LocalCenters", (uk.numel() + cnt.numel()) * 8)
+        best = torch.full((k,), cs, dtype=torch.int64, device=dev)
+        if rk.numel():
+            u2, inv = torch.unique(rk, sorted=True, return_inverse=True)
+            c2 = torch.zeros(u2.numel(), dtype=rc.dtype, device=dev).scatter_add_(0, inv, rc)
+            g = u2 // cs
+            top = torch.zeros(k, dtype=c2.dtype, device=dev).scatter_reduce(0, g, c2, "amax", include_self=False)
+            win = c2 == top[g]
+            best = best.scatter_reduce(0, g[win], (u2 - g * cs)[win], "amin", include_self=True)
+        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+        out[:, c] = best.to(torch.int32)
+    return out
+
+
+def _signature_pipeline_sharded(data, config: PipelineConfig, comm: _Comm):
+    """mixed / sparse data over G ranks (engine.py:173-238 signature fragments,
+    :379-392 dataset-wide preprocessing).  Every rank holds the full input (the
+    reference's run_pipeline contract); the dataset-wide step (numeric
+    discretisation) runs identically on every rank, then each rank hashes its
+    contiguous rows (DOPH is per set), the signature rows of table j go to rank
+    j % G, which groups them into buckets and votes; seed groups are
+    all-gathered and deduplicated identically; mode / membership counts are
+    summed over ranks (exact); assignment is local; radii MAX, sizes SUM, the
+    objective is numpy's pairwise sum over all ranks' rows."""
+    g = config.workers.num_workers
+    mp: MinhashTransformParams = config.minhash
+    sp: SeedingParams = config.seeding
+    G, rank = comm.G, comm.rank
+    if g % G:
+        raise EngineError(f"stage setup: {G} GPUs must divide the {g} logical workers")
+    info, warnings = {}, []
+    tm = _Timer()
+    with tm.stage("prepare"):
+        if config.transform_kind == "mixed":
+            if isinstance(data, (MixedData, DenseData)):
+                data = discretize_numeric(data, mp.bins_per_attribute)
+            if not isinstance(data, CategoricalData):
+                raise EngineError("stage setup: mixed transform expects mixed or categorical data")
+            n = data.n
+            if g > n:
+                raise EngineError(f"stage setup: cannot split {n} objects across {g} workers")
+            lo, hi = split_data(n, G)[rank]
+            cat = CategoricalData(data.codes[lo:hi], code_space=data.code_space)
+            flat, off = categorical_token_csr(cat)
+            universe = data.dim * data.code_space
+        else:
+            if not isinstance(data, SparseData):
+                raise EngineError("stage setup: sparse transform expects sparse data")
+            n = data.n
+            if g > n:
+                raise EngineError(f"stage setup: cannot split {n} objects across {g} workers")
+            lo, hi = split_data(n, G)[rank]
+            full_flat, full_off = data.csr()
+            off_l = (full_off[lo:hi + 1] - full_off[lo]).contiguous()
+            flat_l = full_flat[int(full_off[lo].item()):int(full_off[hi].item())].contiguous()
+            universe = data.universe
+            if mp.target_dims <= data.universe:
+                red = DophReducer(derive_seed(mp.seed, 0xD0), data.universe, mp.target_dims)
+                flat_l, off_l = red.reduce_device(flat_l, off_l, hi - lo)
+                universe = mp.target_dims
+            cat = SparseData.from_csr(flat_l.to(torch.int64) & 0xFFFFFFFF, off_l, universe)
+            flat, off = cat.csr()
+    n_local = hi - lo
+    own = [j for j in range(mp.num_tables) if j % G == rank]
+    _check_budget(config, n)
+    with tm.stage("transform"):
+        sig = signature_rows(mp.scheme(universe), flat, off, n_local)
+    with tm.stage("sync_buckets"):
+        sig_own = route_signature_rows(sig, n, mp.num_hashes, comm)  # [m_own, n, K]
+        del sig
+        if own:
+            sig_own = sig_own.permute(1, 0, 2).reshape(n, len(own) * mp.num_hashes).contiguous()
+            codes, tsizes = group_signature_tables(sig_own, mp.num_hashes, universe)
+        del sig_own
+    with tm.stage("seeding"):
+        if own:
+            bt = BucketTable(codes, n, tsizes, "sig", even=False)
+            owner = _lib.to_dev(np.concatenate([np.full(ts, j % g, dtype=np.int32) for j, ts in zip(own, tsizes)]))
+            local, _, _ = silk_votes(bt, sp, n, owner, info)
+        else:
+            local = GroupSet.empty()
+        merged = _merge_groups(comm, local)
+        groups = dedup_device(merged, sp, n)
+        if groups.count == 0:
+            groups = _fallback_groups(n, g, config.fallback_seed, warnings)
+    categorical = isinstance(cat, CategoricalData)
+    cs = cat.code_space if categorical else 0
+
+    def modes_of(keys_fn, k, counts_fn):
+        if k * cat.dim * cs <= (1 << 31):
+            cnt = counts_fn()
+            comm.all_reduce(cnt, dist.ReduceOp.SUM, "LocalCenters")
+            return torch.argmax(cnt, dim=2).to(torch.int32)
+        return _dist_modes(keys_fn(), k, cs, comm)
+
+    with tm.stage("centers"):
+        if categorical:
+            codes_l = cat.device_codes()
+
+            def group_keys():
+                sizes = groups.sizes()
+                gidx = torch.repeat_interleave(torch.arange(groups.count, device=sizes.device), sizes)
+                ids = groups.flat[: int(groups.off[-1].item())].to(torch.int64) & 0xFFFFFFFF
+                sel = (ids >= lo) & (ids < hi)
+                gi, li = gidx[sel], ids[sel] - lo
+                return [gi * cs + codes_l[li, c].to(torch.int64) for c in range(cat.dim)]
+
+            M = modes_of(group_keys, groups.count, lambda: mode_counts(codes_l, cs, groups, lo))
+        else:
+            cnt = sparse_counts(cat, groups, lo, (flat, off))
+            comm.all_reduce(cnt, dist.ReduceOp.SUM, "LocalCenters")
+            M = (2 * cnt > groups.sizes()[:, None]).to(torch.int32)
+
+    def assign_reduce(M):
+        if categorical:
+            labels, best = assign_cat_device(codes_l, M)
+        else:
+            labels, best = assign_sparse_device(flat, off, n_local, universe, M)
+        radii, sizes = radii_sizes(labels, best, M.shape[0])
+        comm.all_reduce(radii.view(torch.int64), dist.ReduceOp.MAX, "Assignments")
+        comm.all_reduce(sizes, dist.ReduceOp.SUM, "Assignments")
+        obj = sharded_pairwise_sum(best, n, lo, comm)
+        return labels, best, radii, sizes, obj
+
+    with tm.stage("assign"):
+        labels, best, radii, sizes, obj = assign_reduce(M)
+    weights = groups.sizes()
+    for _ in range(config.passes):  # _refine_distributed (engine.py:519-537)
+        with tm.stage("centers"):
+            keep = torch.nonzero(sizes > 0).flatten()
+            weights = sizes[keep].contiguous()
+            k = M.shape[0]
+            if categorical:
+                def label_keys():
+                    pos = torch.full((k,), -1, dtype=torch.int64, device=keep.device)
+                    pos[keep] = torch.arange(keep.numel(), device=keep.device)
+                    lp = pos[labels]
+                    return [lp * cs + codes_l[:, c].to(torch.int64) for c in range(cat.dim)]
+
+                if k * cat.dim * cs <= (1 << 31):
+                    cnt = label_mode_counts(codes_l, cs, labels, k)
+                    comm.all_reduce(cnt, dist.ReduceOp.SUM, "LocalCenters")
+                    M = torch.argmax(cnt[keep], dim=2).to(torch.int32)
+                else:
+                    M = _dist_modes(label_keys(), keep.numel(), cs, comm)
+            else:
+                cnt = label_sparse_counts(flat, off, n_local, universe, labels, k)
+                comm.all_reduce(cnt, dist.ReduceOp.SUM, "LocalCenters")
+                M = (2 * cnt[keep] > weights[:, None]).to(torch.int32)
+        with tm.stage("assign"):
+            labels, best, radii, sizes, obj = assign_reduce(M)
+    timings = tm.finish()
+    sizes_h = weights.cpu().numpy()
+
+    def centers():
+        Mh = M.cpu().numpy()
+        return [CentralVector("mode", Mh[i], int(sizes_h[i])) for i in range(Mh.shape[0])]
+
+    gather = lambda: comm.all_gather_var(labels, "Assignments")  # noqa: E731
+    return PipelineResult(centers, groups, labels, best, radii, sizes, obj, timings, dict(comm.bytes), warnings,
+                          info, gather)
+
+
 def _signature_pipeline(data, config: PipelineConfig, comm: _Comm):
     """mixed / sparse data on one device (logical g emulated)."""
     if comm.on:
-        raise EngineError("stage setup: multi-GPU runs support dense data only")
+        return _signature_pipeline_sharded(data, config, comm)
     g = config.workers.num_workers
     mp: MinhashTransformParams = config.minhash
     sp: SeedingParams = config.seeding

@@ -255,19 +255,25 @@ def categorical_token_csr(cat: CategoricalData):
     return flat.to(torch.int32).contiguous(), off
 
 
-def signature_bucket_codes(scheme: SignatureScheme, flat: torch.Tensor, off: torch.Tensor, n: int):
-    """Per table, objects grouped by K-signature with slots numbered in sorted
-    signature order (transform.py:158-169) -> (codes [n, L] int32, tsizes)."""
-    L, K = scheme.num_tables, scheme.num_hashes
+def signature_rows(scheme: SignatureScheme, flat: torch.Tensor, off: torch.Tensor, n: int) -> torch.Tensor:
+    """[n, L*K] MinHash signatures of every set for every table (hashing.py:250-282)."""
     funcs = scheme.all_functions()
-    sig = set_signatures_device(funcs, flat, off, n, PermBatch(funcs))  # [n, L*K]
-    codes = _lib.empty(max(1, n * L), _lib.U32).view(-1)
-    codes = codes[: n * L].view(n, L) if n else codes[:0].view(0, L)
+    return set_signatures_device(funcs, flat, off, n, PermBatch(funcs))
+
+
+def group_signature_tables(sig: torch.Tensor, K: int, universe: int):
+    """Per table (K consecutive columns of sig [n, T*K]): objects grouped by
+    K-signature, slots numbered in sorted signature order (transform.py:158-169,
+    np.unique(axis=0)) -> (codes [n, T] int32, tsizes)."""
+    n = sig.shape[0]
+    T = sig.shape[1] // K
+    codes = _lib.empty(max(1, n * T), _lib.U32).view(-1)
+    codes = codes[: n * T].view(n, T) if n else codes[:0].view(0, T)
     tsizes = []
-    bits = np.full(K, max(1, int(scheme.universe - 1).bit_length()), dtype=np.int32)
+    bits = np.full(K, max(1, int(universe - 1).bit_length()), dtype=np.int32)
     perm = _lib.empty(max(1, n), _lib.U32)
     gid = _lib.empty(max(1, n), _lib.U32)
-    for tb in range(L):
+    for tb in range(T):
         rows = sig[:, tb * K:(tb + 1) * K].contiguous()
         ng = np.zeros(1, dtype=np.uint64)
         _lib.call("geek_group_rows", _lib.ptr(rows), n, K, _lib.hptr(bits), _lib.ptr(perm), _lib.ptr(gid),
@@ -277,6 +283,13 @@ def signature_bucket_codes(scheme: SignatureScheme, flat: torch.Tensor, off: tor
         codes[:, tb] = col
         tsizes.append(int(ng[0]))
     return codes.contiguous(), tsizes
+
+
+def signature_bucket_codes(scheme: SignatureScheme, flat: torch.Tensor, off: torch.Tensor, n: int):
+    """Per table, objects grouped by K-signature with slots numbered in sorted
+    signature order (transform.py:158-169) -> (codes [n, L] int32, tsizes)."""
+    sig = signature_rows(scheme, flat, off, n)  # [n, L*K]
+    return group_signature_tables(sig, scheme.num_hashes, scheme.universe)
 
 
 def transform_hetero(data, params: MinhashTransformParams):

@@ -1,5 +1,6 @@
 """Multi-process plumbing of the engine on CPU (gloo, world_size 2 and 4): table
-routing to owners (engine.py:199-238), seed-group all-gather (engine.py:285-295),
+routing to owners (engine.py:199-238) for projection keys and signature rows,
+the sharded per-attribute mode reduction, seed-group all-gather (engine.py:285-295),
 the float64 radii MAX reduction over bit patterns, the variable-size gather and
 the sharded numpy-order pairwise sum of the objective.
 The kernels themselves need a GPU; these tests cover the host-side exchange
@@ -63,6 +64,25 @@ def _worker(rank, world, port, n, m, q):
             plo, phi = split_data(npts, world)[rank]
             got_pw = E.sharded_pairwise_sum(torch.from_numpy(vals[plo:phi].copy()), npts, plo, comm)
             ok_pw &= got_pw == float(np.add.reduce(vals))
+        # signature rows routed to table owners, and the sharded mode reduction
+        from paper_2106_10515_b200.engine import _dist_modes, route_signature_rows
+        K = 3
+        sig_full = (torch.arange(n * m * K, dtype=torch.int32).view(n, m * K) * 13) % 1009
+        got_sig = route_signature_rows(sig_full[lo:hi].contiguous(), n, K, comm)
+        own_t = [j for j in range(m) if j % world == rank]
+        want_sig = sig_full.view(n, m, K)[:, own_t, :].permute(1, 0, 2)
+        ok_route &= bool(torch.equal(got_sig, want_sig))
+        rng = np.random.default_rng(7)
+        kk, cs, dd = 6, 50, 2
+        grp = rng.integers(0, kk, n)
+        cod = rng.integers(0, cs, (n, dd))
+        keys = [torch.from_numpy(grp[lo:hi] * cs + cod[lo:hi, c]).to(torch.int64) for c in range(dd)]
+        modes = _dist_modes(keys, kk, cs, comm).numpy()
+        for gi in range(kk):
+            for c in range(dd):
+                vals = cod[grp == gi, c]
+                want = np.argmax(np.bincount(vals, minlength=cs)) if vals.size else cs
+                ok_merge &= int(modes[gi, c]) == int(want)
         q.put((rank, ok_route, ok_merge, ok_radii, ok_gather and ok_pw, dict(comm.bytes)))
     finally:
         dist.destroy_process_group()

@@ -104,6 +104,39 @@ def main():
             ok &= good
             if rank == 0:
                 print(f"[G={world}] small passes=2 {x.dtype} g={g}: {'OK' if good else 'MISMATCH'}", flush=True)
+    # sparse and mixed pipelines over the ranks (signature rows routed to the
+    # table owners, counts summed): the reference's g = 2 goldens
+    from tests.golden_io import csr as _csr
+    if 2 % world == 0:
+        sm = meta()["sparse"]
+        data = G.SparseData(_csr(arr["sp_flat"], arr["sp_off"]), 20_000)
+        cfg = G.PipelineConfig(metric="jaccard", transform_kind="sparse", workers=G.WorkerConfig(2),
+                               minhash=G.MinhashTransformParams(3, 6, seed=4, target_dims=400),
+                               seeding=G.SeedingParams(3, 6, min_group_size=3, seed=5))
+        out = G.run_pipeline(data, cfg)
+        cl = out.clustering
+        good = ([tuple(x.members.tolist()) for x in out.seed_groups] ==
+                [tuple(x.tolist()) for x in golden_groups(arr, "sp_g2")]
+                and np.array_equal(np.stack([c.values for c in cl.centers]), arr["sp_g2_centers"])
+                and np.array_equal(cl.assignment, arr["sp_g2_labels"]) and np.array_equal(cl.radii, arr["sp_g2_radii"])
+                and cl.objective == sm["runs"]["2"]["objective"])
+        ok &= good
+        if rank == 0:
+            print(f"[G={world}] sparse g=2: {'OK' if good else 'MISMATCH'} bytes={out.transport_bytes}", flush=True)
+        mm = meta()["mixed"]
+        cfg = G.PipelineConfig(metric="jaccard", transform_kind="mixed", workers=G.WorkerConfig(2),
+                               minhash=G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16),
+                               seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9))
+        out = G.run_pipeline(G.MixedData(arr["mx_num"], arr["mx_cat"]), cfg)
+        cl = out.clustering
+        good = ([tuple(x.members.tolist()) for x in out.seed_groups] ==
+                [tuple(x.tolist()) for x in golden_groups(arr, "mx_g2")]
+                and np.array_equal(np.stack([c.values for c in cl.centers]), arr["mx_g2_centers"])
+                and np.array_equal(cl.assignment, arr["mx_g2_labels"]) and np.array_equal(cl.radii, arr["mx_g2_radii"])
+                and cl.objective == mm["runs"]["2"]["objective"])
+        ok &= good
+        if rank == 0:
+            print(f"[G={world}] mixed g=2: {'OK' if good else 'MISMATCH'} bytes={out.transport_bytes}", flush=True)
     # the fused projection (keys stored into the owners' symmetric buffers over
     # NVLink) against projection + all_to_all of the same rows, and host rows
     # streamed through the API against device rows
