@@ -730,6 +730,9 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
 //            error of f16 subnormals, at most 2^-25 per scaled coordinate:
 //            2^-25 sqrt(d) (|x'| + |c'|) / s, and the three f16 parts of
 //            s^2 |c'|^2 / 2 (3 * 2^-25 / s^2 + 2^-33 |c'|^2 / 2).
+//   nprod 64 (wide rows, float64 cuBLAS GEMM over uncentered x, c; xn = |x|,
+//            cn = max |c|): gamma_{d+2} for the dot products and |c|^2, plus
+//            the float32 rounding of the stored s = |c|^2 - 2 x.c.
 //   nprod 17 (tile-local FP16, xn = |x''| = |x' - c'_j0|): one f16 product
 //            of s x'' and s c' (2^-11 relative each, as nprod 1), fp32
 //            accumulation of d products, f16 subnormals as nprod 16, and the
@@ -752,6 +755,10 @@ __device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int 
     const double is = __longlong_as_double((long long)cmax_bits[3]);
     const double t25 = 2.9802322387695312e-08;  // 2^-25
     E += 1.05 * (t25 * sqrt((double)d) * (xn + cn) * is + 3.0 * t25 * is * is + 1.1641532182693481e-10 * 0.5 * cn * cn);
+  }
+  if (nprod == 64) {  // float64 GEMM screen of wide rows (x, c uncentered: mu = 0), s stored as float32
+    const double g = (d + 2.0) * 1.1102230246251565e-16;
+    E = 1.05 * (2.0 * g * xn * cn + g * cn * cn + u * (cn * cn + 2.0 * xn * cn));
   }
   if (nprod == 17) {
     const double is = __longlong_as_double((long long)cmax_bits[3]);
@@ -1070,6 +1077,158 @@ __global__ void tc_recheck8_kernel(const float* __restrict__ X, int d, const dou
   }
 }
 
+// ---- wide rows (d > 128): float64 GEMM screen ----------------------------------
+
+__global__ void to_f64_kernel(const float* X, uint64_t count, double* Y) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count; e += (uint64_t)gridDim.x * blockDim.x)
+    Y[e] = (double)X[e];
+}
+
+// c2[j] = |c_j|^2 (float64), cmax_bits[0] = max_j |c_j| (1 + 1e-6)
+__global__ void center_norms_kernel(const double* C, uint64_t k, int d, double* c2, unsigned long long* cmax_bits) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += (uint64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int e = 0; e < d; ++e) s = fma(C[j * d + e], C[j * d + e], s);
+    c2[j] = s;
+    atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(s) * (1.0 + 1e-6)));
+  }
+}
+
+// one warp per row: s_j = |c_j|^2 - 2 x.c_j over the GEMM row, the 8 smallest
+// kept as (e0 e1 e2 e7 | e3 e4 e5 e6) -- the classifier reads entries 3 and 7
+// as the two lists' 4th values, so a window reaching the 7th smallest counts
+// as an overflow (full scan) and every entry of the 8 is a candidate
+__global__ void __launch_bounds__(256) top8_rows_kernel(const double* __restrict__ G, uint64_t rows, uint64_t k,
+                                                        const double* __restrict__ c2, float* top_s, int* top_i,
+                                                        uint64_t row0) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += wstride) {
+    double v[8];
+    int id[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      v[a] = INFINITY;
+      id[a] = -1;
+    }
+    const double* g = G + r * k;
+    for (uint64_t j = lane; j < k; j += 32) {
+      const double sv = c2[j] - 2.0 * g[j];
+      if (sv < v[7]) {  // insertion, column order kept among equal values
+        int p = 7;
+        while (p > 0 && v[p - 1] > sv) {
+          v[p] = v[p - 1];
+          id[p] = id[p - 1];
+          --p;
+        }
+        v[p] = sv;
+        id[p] = (int)j;
+      }
+    }
+    double e[8];
+    int ei[8];
+    int head = 0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {  // 8 rounds of a warp (value, index) minimum over the lanes' heads
+      double hv = INFINITY;
+      int hi = -1;
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (b == head) {
+          hv = v[b];
+          hi = id[b];
+        }
+      double bv = hv;
+      int bi = hi, bl = lane;
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const bool take = ov < bv || (ov == bv && ((unsigned)oi < (unsigned)bi));
+        if (take) {
+          bv = ov;
+          bi = oi;
+          bl = ol;
+        }
+      }
+      e[a] = bv;
+      ei[a] = bi;
+      if (lane == bl && head < 8) ++head;
+    }
+    if (lane == 0) {
+      const uint64_t i = row0 + r;
+      const int pos[8] = {0, 1, 2, 4, 5, 6, 7, 3};  // e_a -> slot
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        top_s[i * 8 + pos[a]] = (float)e[a];
+        top_i[i * 8 + pos[a]] = ei[a];
+      }
+    }
+  }
+}
+
+__global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
+                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st);
+
+// float64 GEMM screen for wide float32 rows: cuBLAS DGEMM in point chunks, the
+// top-8 per point, then the exact classification / recheck of the tensor-core path
+static int assign_wide_screen(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
+                              const PwPlan& plan, int64_t* labels, double* best, geek_assign_stats_t* stats,
+                              void* ev0, void* ev1, cudaStream_t s) {
+  Scratch cnt, c2, ts, ti, xn, amb, full, mu0, x64, G;
+  GEEK_TRY(cnt.alloc(48, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
+  unsigned long long* cmax = cnt.as<unsigned long long>();
+  unsigned long long* namb = cmax + 1;
+  unsigned long long* nfull = cmax + 2;
+  GEEK_TRY(c2.alloc(k * 8, s));
+  GEEK_TRY(mu0.alloc((size_t)d * 4, s));
+  GEEK_CHECK_CUDA(cudaMemsetAsync(mu0.ptr, 0, (size_t)d * 4, s));
+  center_norms_kernel<<<grid_for(k, 128), 128, 0, s>>>(C, k, d, c2.as<double>(), cmax);
+  GEEK_CHECK_LAUNCH();
+  GEEK_TRY(ts.alloc(n * 32, s));
+  GEEK_TRY(ti.alloc(n * 32, s));
+  GEEK_TRY(xn.alloc(n * 4, s));
+  GEEK_TRY(amb.alloc(n * 4, s));
+  GEEK_TRY(full.alloc(n * 4, s));
+  const uint64_t P = std::max<uint64_t>(1, std::min<uint64_t>(n, (3ull << 30) / (8ull * (d + k))));
+  if (dtype == 0) GEEK_TRY(x64.alloc(P * d * 8, s));
+  GEEK_TRY(G.alloc(P * k * 8, s));
+  if (ev0) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev0), s));
+  for (uint64_t r0 = 0; r0 < n; r0 += P) {
+    const uint64_t rows = std::min(P, n - r0);
+    const double* A;
+    if (dtype == 0) {
+      to_f64_kernel<<<grid_for(rows * d, 256), 256, 0, s>>>((const float*)X + r0 * d, rows * d, x64.as<double>());
+      GEEK_CHECK_LAUNCH();
+      A = x64.as<double>();
+    } else {
+      A = (const double*)X + r0 * d;
+    }
+    GEEK_TRY(dgemm_nt(A, C, G.as<double>(), (int)rows, (int)k, d, s));
+    top8_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, s>>>(G.as<double>(), rows, k, c2.as<double>(),
+                                                              ts.as<float>(), ti.as<int>(), r0);
+    GEEK_CHECK_LAUNCH();
+  }
+  if (ev1) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev1), s));
+  // one lane per point: d > 128 needs numpy's full pairwise recursion (the PwPlan), not one 8-accumulator leaf
+  tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
+      (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu0.as<float>(), cmax, 64,
+      nullptr, labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+  GEEK_CHECK_LAUNCH();
+  tc_recheck_kernel<<<148 * 8, 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(), ti.as<int>(),
+                                            xn.as<float>(), cmax, 64, nullptr, amb.as<uint32_t>(), namb, labels, best);
+  GEEK_CHECK_LAUNCH();
+  full_scan_kernel<<<148 * 4, kFsThreads, sizeof(double) * d, s>>>((const float*)X, d, C, k, plan,
+                                                                   full.as<uint32_t>(), nfull, labels, best);
+  GEEK_CHECK_LAUNCH();
+  if (stats) {
+    assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, nullptr, 64, stats);
+    GEEK_CHECK_LAUNCH();
+  }
+  return GEEK_OK;
+}
+
 __global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
                                     const unsigned* ovf, int nprod, geek_assign_stats_t* st) {
   st->rechecked = (namb ? *namb : 0ull) + (nfull ? *nfull : 0ull);
@@ -1198,6 +1357,14 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
   }
   const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
   const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;
+  if (dtype == 0 && d > 128 && k >= 4 && n < 0xFFFFFFFFull) {
+    // float64 GEMM screen (cuBLAS DGEMM: 2 flops per element with FMA, where the
+    // exact numpy-order evaluation below needs 3 unfused ops per element)
+    const int st = assign_wide_screen(X, dtype, n, d, C, k, plan, labels, best, stats, ev_screen_begin,
+                                      ev_screen_end, s);
+    if (st == GEEK_OK) return GEEK_OK;
+    if (st != GEEK_ECUDA) return st;  // cuBLAS not loadable: the exact SIMT kernels below
+  }
   if (!screened && d > 128) {
     const uint64_t kpad = (k + 31) / 32 * 32;
     Scratch ctb;

@@ -223,6 +223,8 @@ int exponent_range_f32_device(const float* X, uint64_t total, int* out, cudaStre
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s);
+// C[n][m] = A[n][kk] . B[m][kk]^T in float64 through cuBLAS (blas.cu, loaded at run time)
+int dgemm_nt(const double* A, const double* B, double* Cout, int n, int m, int kk, cudaStream_t s);
 // {xscale, oscale} of a prepared screen (device memory inside its mu scratch)
 const float* tc_scal(const Scratch& mu, int d);
 // nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu

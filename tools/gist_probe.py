@@ -5,8 +5,11 @@ one warm and one timed run of the pipeline with per-stage times and the
 libgeek call times, and an exact float64 spot check of 20K sampled labels /
 best distances against a numpy evaluation of the reference's distance."""
 import json
+import os
 import sys
 import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch

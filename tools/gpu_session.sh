@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t_all.log 2>&1
-echo "all rc=$?" >> gpurun_out/t_all.log
-timeout 900 python bench.py --steps 3 --warmup 3 --no-checks --no-e2e > gpurun_out/bench3.json 2> gpurun_out/bench3.err
+timeout 900 python tools/gist_probe.py 10000000 10000 > gpurun_out/gist.log 2>&1
+echo "rc=$?" >> gpurun_out/gist.log
+GEEK_NO_WIDE_GEMM=1 timeout 900 python tools/gist_probe.py 10000000 10000 > gpurun_out/gist_old.log 2>&1
