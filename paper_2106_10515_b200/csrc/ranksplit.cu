@@ -399,12 +399,23 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   return GEEK_OK;
 }
 
+int rank_split_v2(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes, uint64_t code_stride,
+                  uint64_t col, uint64_t* stats_host, cudaStream_t s);  // ranksplit2.cu
+
 static int rank_split_impl(const uint64_t* keys, uint64_t n, int m, uint64_t t, uint32_t* codes,
                            uint64_t code_stride, uint64_t col, uint64_t* stats_host, cudaStream_t s,
                            const uint32_t* hist_in = nullptr, const uint32_t* fcnt_in = nullptr) {
   GEEK_REQUIRE(t >= 1 && t <= n, "cannot split %llu objects into %llu buckets",
                (unsigned long long)n, (unsigned long long)t);
   GEEK_REQUIRE(n < 0xFFFFFFFFull, "n must be < 2^32");
+  if (!hist_in && !fcnt_in && getenv("GEEK_SPLIT_V2")) {
+    // experimental shared-memory split (ranksplit2.cu): exact, but on the
+    // benchmark data its coarser bins stage 3-8 % of the ids and its histogram
+    // and codes passes run latency-bound at one or two blocks per SM -- 125-145
+    // ms against this split's 56 ms (profiles/r2_split_v2.md), so it is opt-in
+    const int st = rank_split_v2(keys, n, m, t, codes, code_stride, col, stats_host, s);
+    if (st != 1) return st;
+  }
   SplitGeom g;
   g.n = n;
   g.t = t;
