@@ -201,20 +201,25 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
       atomicAdd(overflow, 1ull);
       nb = kRowBins;
     }
-    // winners: first occurrence of each bin whose multiplicity is a strict majority
-    auto is_winner = [&](int a) -> bool {
-      if (2u * (uint32_t)nb <= rs[a]) return false;  // count <= nb cannot be a strict majority
-      int c = 0;
-      bool first = true;
-      for (int q = 0; q < nb; ++q) {
-        const bool eq = rb[q] == rb[a];
-        c += eq;
-        first &= !(q < a && eq);
-      }
-      return first && 2u * (uint32_t)c > rs[a];
-    };
-    uint32_t cnt = 0;
-    for (int a = 0; a < nb; ++a) cnt += is_winner(a);
+    // winners: first occurrence of each bin whose multiplicity is a strict
+    // majority -- one pass: each entry's later duplicates are counted once and
+    // marked seen (kRowBins <= 64 entries: 64-bit masks), the winner mask is
+    // kept for the emission
+    static_assert(kRowBins <= 64, "winner masks are 64-bit");
+    uint64_t win = 0, seen = 0;
+    for (int a = 0; a < nb; ++a) {
+      if ((seen >> a) & 1ull) continue;
+      const uint32_t ba = rb[a], sz = rs[a];
+      if (2u * (uint32_t)nb <= sz) continue;  // count <= nb cannot be a strict majority
+      uint32_t c = 1;
+      for (int q = a + 1; q < nb; ++q)
+        if (rb[q] == ba) {
+          ++c;
+          seen |= 1ull << q;
+        }
+      if (2u * c > sz) win |= 1ull << a;
+    }
+    const uint32_t cnt = (uint32_t)__popcll(win);
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -227,14 +232,13 @@ __global__ void __launch_bounds__(kEwThreads) emit_winners_kernel(
     if (lane == 31) wbase = atomicAdd(cursor, (unsigned long long)total);
     wbase = __shfl_sync(0xffffffffu, wbase, 31);
     unsigned long long pos = wbase + incl - cnt;
-    for (int a = 0; a < nb && cnt; ++a) {
-      if (is_winner(a)) {
-        if (pos < cap) {
-          out_bin[pos] = rb[a];
-          out_id[pos] = static_cast<uint32_t>(i);
-        }
-        ++pos;
+    for (uint64_t w = win; w; w &= w - 1) {
+      const int a = __ffsll((long long)w) - 1;
+      if (pos < cap) {
+        out_bin[pos] = rb[a];
+        out_id[pos] = static_cast<uint32_t>(i);
       }
+      ++pos;
     }
   }
 }
