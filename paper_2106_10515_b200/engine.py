@@ -819,7 +819,7 @@ def _signature_pipeline_sharded(data, config: PipelineConfig, comm: _Comm):
             if g > n:
                 raise EngineError(f"stage setup: cannot split {n} objects across {g} workers")
             lo, hi = split_data(n, G)[rank]
-            cat = CategoricalData(data.codes[lo:hi], code_space=data.code_space)
+            cat = CategoricalData.from_device(data.device_codes()[lo:hi], code_space=data.code_space)
             flat, off = categorical_token_csr(cat)
             universe = data.dim * data.code_space
         else:

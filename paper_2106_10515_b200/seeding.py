@@ -109,7 +109,7 @@ class Bins:
         self.pair_bucket = pair_bucket  # int64 [P] bucket position
         self.pair_bin = pair_bin        # int64 [P] global bin id
         self.bin_size = bin_size        # int32 [B] buckets per bin
-        self.bin_table = bin_table      # numpy [B] SILK table of each bin
+        self.bin_table = bin_table      # int64 [B] SILK table of each bin (device)
         self.bin_sig = bin_sig          # int32 [B, K] signature of each bin
 
     @property
@@ -118,7 +118,7 @@ class Bins:
 
 
 def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Tensor = None,
-              tables=None) -> Bins:
+              tables=None, prune=None) -> Bins:
     """Per SILK table, group buckets by (owner, signature); keep groups of
     >= 2 buckets (seeding.py:83-104, engine.py:270-277).  Bin ids are
     table-major, then in sorted (owner, signature) order."""
@@ -128,7 +128,7 @@ def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Ten
     nt = len(tables)
     if nb == 0 or nt == 0:
         z = torch.zeros(0, dtype=torch.int64, device=dev)
-        return Bins(z, z, torch.zeros(0, dtype=torch.int32, device=dev), np.zeros(0, np.int64),
+        return Bins(z, z, torch.zeros(0, dtype=torch.int32, device=dev), z,
                     torch.zeros((0, K), dtype=torch.int32, device=dev))
     # all SILK tables in one group-by: rows (table, owner, signature), the
     # table column most significant, so groups come out table-major
@@ -162,8 +162,30 @@ def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Ten
     first[1:] = g[1:] != g[:-1]
     heads = p64[sel & first]
     bt = torch.tensor(tables, dtype=torch.int64, device=dev)[rows[heads, 0].to(torch.int64)]
-    return Bins(psel % nb, newid[g][sel], counts[binned].to(torch.int32), bt.cpu().numpy(),
-                rows[heads][:, -K:])
+    bins = Bins(psel % nb, newid[g][sel], counts[binned].to(torch.int32), bt, rows[heads][:, -K:])
+    return _prune_bins(bins, *prune) if prune is not None else bins
+
+
+def _prune_bins(bins: Bins, bucket_sizes: torch.Tensor, delta: int) -> Bins:
+    """Drop the bins that cannot yield a group of >= delta winners (exact:
+    a winner lies in >= need = |bin| // 2 + 1 of the bin's buckets, so
+    #winners <= sum of the bin's bucket sizes // need).  Pipeline use only --
+    the reference-facing bin_buckets / collect_votes keep every bin.  On
+    signature buckets this removes the bins of one id's identical singleton
+    buckets across its owner's tables (one winner each)."""
+    B = bins.count
+    if B == 0:
+        return bins
+    tot = torch.zeros(B, dtype=torch.int64, device=bins.pair_bin.device).index_add_(
+        0, bins.pair_bin, bucket_sizes[bins.pair_bucket].to(torch.int64))
+    need = bins.bin_size.to(torch.int64) // 2 + 1
+    keep = tot // need >= max(1, int(delta))
+    if bool(keep.all().item()):
+        return bins
+    newid = torch.cumsum(keep.to(torch.int64), 0) - 1
+    pk = keep[bins.pair_bin]
+    return Bins(bins.pair_bucket[pk], newid[bins.pair_bin[pk]], bins.bin_size[keep], bins.bin_table[keep],
+                bins.bin_sig[keep])
 
 
 # ---------------------------------------------------------------------------
@@ -276,12 +298,55 @@ def fused_votes_codes(bins: Bins, bt: BucketTable, bucket_sizes: torch.Tensor, d
     return GroupSet(oi[:k].contiguous(), off), ub, nw
 
 
+def _concat_bins(parts) -> Bins:
+    """Bins of consecutive SILK tables -> one Bins (bin ids offset, table-major kept)."""
+    if len(parts) == 1:
+        return parts[0]
+    offs, base = [], 0
+    for b in parts:
+        offs.append(base)
+        base += b.count
+    return Bins(torch.cat([b.pair_bucket for b in parts]),
+                torch.cat([b.pair_bin + o for b, o in zip(parts, offs)]),
+                torch.cat([b.bin_size for b in parts]), torch.cat([b.bin_table for b in parts]),
+                torch.cat([b.bin_sig for b in parts]))
+
+
+def _bins_per_table(buckets: BucketTable, scheme: SignatureScheme, K: int, L: int, universe: int, owner, delta):
+    """Signature buckets (member CSR): SILK signatures and the group-by one
+    SILK table at a time, so neither the [L*K, buckets] signatures nor the
+    L * buckets group-by rows exist at once (Criteo-like inputs reach ~10^8
+    buckets per table).  Same bins, same table-major order."""
+    flat, off = buckets.member_csr()
+    nb = len(buckets)
+    sizes = off[1:] - off[:-1]
+    parts = []
+    for st in range(L):
+        sig = bucket_signatures_csr(flat, off, nb, scheme.functions(st))  # [K, nb]
+        b = find_bins(sig, K, 1, universe, owner, tables=[0], prune=(sizes, delta))
+        del sig
+        b.bin_table = torch.full_like(b.bin_table, st)
+        parts.append(b)
+    return _concat_bins(parts), (flat, off)
+
+
+_SPLIT_ROWS = 1 << 28  # group-by rows above which signature-bucket bins are formed table by table
+
+
 def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=None):
     """Every surviving vote of every SILK table (collect_votes / local_votes)
     -> (GroupSet, Bins, winning bin ids)."""
     scheme = params.scheme(universe)
-    sig, nb, csr = silk_signatures(buckets, scheme, info)
-    bins = find_bins(sig, params.num_hashes, params.num_tables, universe, owner)
+    if (isinstance(buckets, BucketTable) and not (buckets.even and buckets.n == scheme.universe)
+            and len(buckets) * params.num_tables > _SPLIT_ROWS):
+        bins, csr = _bins_per_table(buckets, scheme, params.num_hashes, params.num_tables, universe, owner,
+                                    params.min_group_size)
+    else:
+        sig, nb, csr = silk_signatures(buckets, scheme, info)
+        bins = find_bins(sig, params.num_hashes, params.num_tables, universe, owner)
+        del sig
+        if isinstance(buckets, BucketTable) and not buckets.even:
+            bins = _prune_bins(bins, buckets.bucket_sizes(), params.min_group_size)
     if isinstance(buckets, BucketTable):
         sizes = buckets.bucket_sizes()
     else:
@@ -431,9 +496,10 @@ def collect_votes(buckets, params: SeedingParams, universe: int, trace=None) -> 
     if trace is not None and out:
         pbk = bins.pair_bucket.cpu().numpy()
         pbn = bins.pair_bin.cpu().numpy()
+        btab = bins.bin_table.cpu().numpy()
         for g, b in zip(out, won.cpu().numpy().tolist()):
             idx = np.sort(pbk[pbn == b])
-            trace.append((int(bins.bin_table[b]), tuple(buckets[int(i)].bucket_id for i in idx), g))
+            trace.append((int(btab[b]), tuple(buckets[int(i)].bucket_id for i in idx), g))
     return out
 
 

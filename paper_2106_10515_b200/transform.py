@@ -240,7 +240,7 @@ def discretize_numeric(data, bins_per_attribute: int) -> CategoricalData:
     codes = discretize_codes(numeric, bins_per_attribute, dn + dc)
     if dc:
         codes[:, dn:] = _lib.to_dev(categorical, torch.int32)
-    return CategoricalData(codes.cpu().numpy())
+    return CategoricalData.from_device(codes)  # stays on the device (no host round trip)
 
 
 def categorical_token_csr(cat: CategoricalData):

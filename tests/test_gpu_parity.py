@@ -526,6 +526,32 @@ def test_mixed_pipeline_golden(g):
     assert out.clustering.objective == m["runs"][str(g)]["objective"]
 
 
+@pytest.mark.parametrize("kind", ["sparse", "mixed"])
+def test_signature_bins_table_by_table(kind, monkeypatch):
+    """Large signature-bucket sets form their SILK bins one table at a time
+    (memory); forced here on the golden sparse / mixed pipelines: same output."""
+    monkeypatch.setattr(G.seeding, "_SPLIT_ROWS", 0)
+    arr = npz("pipelines")
+    if kind == "sparse":
+        m = meta()["sparse"]
+        data = G.SparseData(csr(arr["sp_flat"], arr["sp_off"]), 20_000)
+        cfg = G.PipelineConfig(metric="jaccard", transform_kind="sparse", workers=G.WorkerConfig(2),
+                               minhash=G.MinhashTransformParams(3, 6, seed=4, target_dims=400),
+                               seeding=G.SeedingParams(3, 6, min_group_size=3, seed=5))
+        pre = "sp_g2"
+    else:
+        m = meta()["mixed"]
+        data = G.MixedData(arr["mx_num"], arr["mx_cat"])
+        cfg = G.PipelineConfig(metric="jaccard", transform_kind="mixed", workers=G.WorkerConfig(2),
+                               minhash=G.MinhashTransformParams(3, 6, seed=7, bins_per_attribute=16),
+                               seeding=G.SeedingParams(3, 6, min_group_size=3, seed=9))
+        pre = "mx_g2"
+    out = G.run_pipeline(data, cfg)
+    assert keys(out.seed_groups) == keys(golden_groups(arr, pre))
+    assert np.array_equal(out.clustering.assignment, arr[pre + "_labels"])
+    assert out.clustering.objective == m["runs"]["2"]["objective"]
+
+
 @pytest.mark.parametrize("owners", [2, 3, 8])
 def test_routed_projection_layout(owners):
     """geek_project_keys_routed (the fused bucket synchronisation) writes the

@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_benchlaw.py -q -x -k "seeding or vote or pipeline or benchlaw or silk or winners" > gpurun_out/t_vote.log 2>&1
-echo "rc=$?" >> gpurun_out/t_vote.log
-timeout 900 python bench.py --steps 3 --warmup 3 --no-checks --no-e2e > gpurun_out/bench5.json 2> gpurun_out/bench5.err
+timeout 900 python -m pytest tests -q -x -m gpu -k "seeding or bins or trace or mixed or sparse or worked or table_by_table" > gpurun_out/t_seed.log 2>&1
+echo "rc=$?" >> gpurun_out/t_seed.log
+timeout 900 python tools/mixed_probe.py 20000000 > gpurun_out/mixed20m.log 2>&1
+timeout 1800 python tools/mixed_probe.py 50000000 > gpurun_out/mixed50m.log 2>&1

@@ -9,8 +9,11 @@ g = 8.  One warm and one timed run; exact spot check of 2,000 sampled labels
     python tools/mixed_probe.py N
 """
 import json
+import os
 import sys
 import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch
