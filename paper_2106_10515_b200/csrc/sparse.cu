@@ -152,6 +152,84 @@ __global__ void assign_cat_kernel(const int32_t* __restrict__ codes, uint64_t n,
   }
 }
 
+// Tiled categorical assignment (d <= 64, k < 2^24): every thread keeps one
+// center's DP codes in registers, the block streams 256-point (128 for d > 40) tiles of codes
+// through shared memory (a broadcast read per 4 attributes) and keeps each
+// point's best key max(mt << 24 | (2^24 - 1 - c)) -- the largest match count
+// mt, first center on ties -- in shared memory across the center chunks.
+// The Jaccard-style distance 1 - mt / (2d - mt) decreases strictly with mt, so
+// the key's order is the reference's `dist < best` scan order
+// (assignment.py:63-67; numpy argmin's first index).
+__device__ __forceinline__ void cat_match(int& m, int x, int c) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}" : "+r"(m) : "r"(x), "r"(c));
+}
+
+template <int DP>
+constexpr int cat_pt() { return DP <= 40 ? 256 : 128; }  // points per tile: <= 41 KB static smem
+
+template <int DP>
+__global__ void __launch_bounds__(256) assign_cat_tiled_kernel(const int32_t* __restrict__ codes, uint64_t n, int d,
+                                                                 const int32_t* __restrict__ modesT, uint64_t kpad,
+                                                                 uint64_t k, int64_t* labels, double* best) {
+  constexpr int PT = cat_pt<DP>();
+  __shared__ __align__(16) int32_t sp[PT * DP];
+  __shared__ unsigned sbest[PT];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t ntiles = (n + PT - 1) / PT;
+  const uint64_t nchunks = (k + 255) / 256;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t p0 = tile * PT;
+    const int np = (int)((n - p0) < (uint64_t)PT ? (n - p0) : (uint64_t)PT);
+    const int32_t* src = codes + p0 * (uint64_t)d;
+    for (int e = tid; e < PT * DP; e += 256) {
+      const int p = e / DP, a = e - p * DP;
+      sp[e] = (p < np && a < d) ? src[(uint64_t)p * d + a] : 0;  // pad attributes read 0
+    }
+    if (tid < PT) sbest[tid] = 0;
+    __syncthreads();
+    for (uint64_t ch = 0; ch < nchunks; ++ch) {
+      const uint64_t c = ch * 256 + tid;
+      int32_t cm[DP];
+#pragma unroll
+      for (int a = 0; a < DP; ++a) cm[a] = modesT[(uint64_t)a * kpad + c];  // pad rows hold 1
+      const unsigned tag = (c < k) ? (0xFFFFFFu - (unsigned)c) : 0u;
+      const bool valid = c < k;
+      for (int p = 0; p < np; ++p) {
+        const int4* row = reinterpret_cast<const int4*>(sp + p * DP);
+        int m0 = 0, m1 = 0;  // two chains: compare + predicated increment per attribute
+#pragma unroll
+        for (int q = 0; q < DP / 4; ++q) {
+          const int4 v = row[q];
+          cat_match(m0, v.x, cm[4 * q]);
+          cat_match(m1, v.y, cm[4 * q + 1]);
+          cat_match(m0, v.z, cm[4 * q + 2]);
+          cat_match(m1, v.w, cm[4 * q + 3]);
+        }
+        const int mt = m0 + m1;
+        const unsigned key = valid ? (((unsigned)mt << 24) | tag) : 0u;
+        const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+        if (lane == 0) atomicMax(&sbest[p], wk);
+      }
+    }
+    __syncthreads();
+    if (tid < np) {
+      const unsigned key = sbest[tid];
+      const int mt = (int)(key >> 24);
+      labels[p0 + tid] = (int64_t)(0xFFFFFFu - (key & 0xFFFFFFu));
+      best[p0 + tid] = __dsub_rn(1.0, __ddiv_rn((double)mt, (double)(2 * d - mt)));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void modes_transpose_kernel(const int32_t* modes, uint64_t k, int d, int DP, uint64_t kpad, int32_t* out) {
+  const uint64_t total = (uint64_t)DP * kpad;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = e / kpad, c = e - a * kpad;
+    out[e] = ((int)a < d && c < k) ? modes[c * d + a] : 1;  // pad rows/centers never meet a point's 0 pad
+  }
+}
+
 __global__ void mode_sizes_kernel(const int32_t* modes, uint64_t k, uint64_t u, double* sz) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k;
        c += (uint64_t)gridDim.x * blockDim.x) {
@@ -364,7 +442,32 @@ int geek_assign_categorical(const int32_t* codes, uint64_t n, int d, const int32
   cudaStream_t s = as_stream(stream);
   GEEK_REQUIRE(k >= 1 && d >= 1, "cannot assign without centers");
   if (n == 0) return GEEK_OK;
-  assign_cat_kernel<<<grid_for(n, 128), 128, 0, s>>>(codes, n, d, modes, k, labels, best);
+  if (d > 64 || k >= (1ull << 24) || getenv("GEEK_CAT_NAIVE")) {
+    assign_cat_kernel<<<grid_for(n, 128), 128, 0, s>>>(codes, n, d, modes, k, labels, best);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  }
+  const int DP = (d + 7) / 8 * 8;
+  const uint64_t kpad = (k + 255) / 256 * 256;
+  Scratch mt;
+  GEEK_TRY(mt.alloc((uint64_t)DP * kpad * 4, s));
+  modes_transpose_kernel<<<grid_for((uint64_t)DP * kpad, 256), 256, 0, s>>>(modes, k, d, DP, kpad, mt.as<int32_t>());
+  GEEK_CHECK_LAUNCH();
+  const uint64_t ntiles = (n + 127) / 128;
+  const unsigned grid = (unsigned)(ntiles < 148ull * 4 ? ntiles : 148ull * 4);
+#define GEEK_CAT(DPV)                                                                                          \
+  assign_cat_tiled_kernel<DPV><<<grid, 256, 0, s>>>(codes, n, d, mt.as<int32_t>(), kpad, k, labels, best)
+  switch (DP) {
+    case 8: GEEK_CAT(8); break;
+    case 16: GEEK_CAT(16); break;
+    case 24: GEEK_CAT(24); break;
+    case 32: GEEK_CAT(32); break;
+    case 40: GEEK_CAT(40); break;
+    case 48: GEEK_CAT(48); break;
+    case 56: GEEK_CAT(56); break;
+    default: GEEK_CAT(64); break;
+  }
+#undef GEEK_CAT
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }

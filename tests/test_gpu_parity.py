@@ -835,6 +835,27 @@ def test_assign_sparse_bitsets_vs_oracle(u, k):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("d,k,n", [(1, 3, 500), (7, 1, 300), (13, 300, 1031), (39, 513, 2000),
+                                   (41, 257, 777), (64, 70, 900), (65, 40, 300)])
+def test_assign_categorical_vs_oracle(d, k, n):
+    """Categorical assignment: the register-tiled kernel (d <= 64: ragged d,
+    center chunks of 256, partial point tiles) and the per-thread kernel
+    (d > 64) against the oracle's 1 - m / (2d - m) argmin; duplicate modes and
+    many exact ties (small code space) pin the first-index rule."""
+    rng = np.random.default_rng(d * 1000 + k)
+    codes = rng.integers(0, 3, (n, d)).astype(np.int32)
+    codes[:, ::3] = rng.integers(0, 40, (n, (d + 2) // 3))
+    M = rng.integers(0, 3, (k, d)).astype(np.int32)
+    M[k - 1] = M[0]
+    M[k // 2] = codes[0]
+    data = G.CategoricalData(codes, 64)
+    got = G.assign(data, [G.CentralVector("mode", m) for m in M], "jaccard")
+    lab, best, radii, obj = O.assign_generic(lambda a, b: O.cat_distances(codes[a:b], M), n, k)
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
 def test_sparse_mode_centers_match_dense_counts():
     """Large-code-space modes (sort + run-length, no [k, d, code_space] table)
     equal the dense-count argmax, ties to the smallest code."""
