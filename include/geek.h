@@ -61,6 +61,12 @@ int geek_device_sms(void);
 int geek_perm_forward(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
                       const uint32_t* x, uint64_t count, uint32_t* out, void* stream);
 
+/* out[p*count + i] = pi_p^-1(r[i]), r[i] < universe (the bijection's inverse; the
+ * inverse-rank scan's id lookup, hashing.py:97-140).  Used by the pipeline's
+ * singleton-bucket bins: the object whose singleton bucket carries a signature. */
+int geek_perm_inverse(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
+                      const uint32_t* r, uint64_t count, uint32_t* out, void* stream);
+
 /* sig[s*nperm + p] = min_{e in set s} pi_p(e); sets are CSR (flat, offsets[nsets+1]),
  * non-empty.  (SignatureScheme.signatures_for_sets, hashing.py:265-282)        */
 int geek_set_minhash(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,

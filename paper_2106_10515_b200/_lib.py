@@ -47,6 +47,7 @@ _SIGS = {
     "geek_last_error": (C.c_char_p, []),
     "geek_device_sms": (i32, []),
     "geek_perm_forward": (i32, [vp, i32, vp, vp, u64, vp, vp]),
+    "geek_perm_inverse": (i32, [vp, i32, vp, vp, u64, vp, vp]),
     "geek_set_minhash": (i32, [vp, i32, vp, vp, vp, u64, vp, vp]),
     "geek_silk_invscan": (i32, [vp, u64, i32, u64, vp, i32, vp, vp, vp, vp, vp]),
     "geek_project_keys": (i32, [vp, i32, u64, i32, vp, i32, vp, vp, vp]),

@@ -26,6 +26,15 @@ __global__ void perm_forward_kernel(const geek_perm_t* perms, int nperm, const u
     out[(uint64_t)p * count + i] = perm_forward(pm, tables, x[i]);
 }
 
+__global__ void perm_inverse_kernel(const geek_perm_t* perms, int nperm, const uint32_t* tables,
+                                    const uint32_t* r, uint64_t count, uint32_t* out) {
+  const int p = blockIdx.y;
+  const geek_perm_t pm = perms[p];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[(uint64_t)p * count + i] = perm_inverse(pm, tables, r[i]);
+}
+
 __device__ __forceinline__ uint64_t find_segment(const uint64_t* off, uint64_t nseg, uint64_t e) {
   // largest s with off[s] <= e (segments non-empty)
   uint64_t lo = 0, hi = nseg;  // invariant off[lo] <= e < off[hi]
@@ -147,6 +156,18 @@ int geek_perm_forward(const geek_perm_t* perms_host, int nperm, const uint32_t* 
   GEEK_TRY(upload_perms(perms_host, nperm, pb, s));
   dim3 grid(grid_for(count, 256, 4096), nperm);
   perm_forward_kernel<<<grid, 256, 0, s>>>(pb.as<geek_perm_t>(), nperm, tables, x, count, out);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
+int geek_perm_inverse(const geek_perm_t* perms_host, int nperm, const uint32_t* tables,
+                      const uint32_t* r, uint64_t count, uint32_t* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (count == 0) return GEEK_OK;
+  Scratch pb;
+  GEEK_TRY(upload_perms(perms_host, nperm, pb, s));
+  dim3 grid(grid_for(count, 256, 4096), nperm);
+  perm_inverse_kernel<<<grid, 256, 0, s>>>(pb.as<geek_perm_t>(), nperm, tables, r, count, out);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }

@@ -330,7 +330,121 @@ def _bins_per_table(buckets: BucketTable, scheme: SignatureScheme, K: int, L: in
     return _concat_bins(parts), (flat, off)
 
 
+def _group_all(rows: torch.Tensor, bits: np.ndarray):
+    """Group-by of device rows [nr, w] u32 in lexicographic order ->
+    (perm int64 sorted positions, gid int64 per sorted position, count)."""
+    nr = int(rows.shape[0])
+    perm = _lib.empty(nr, _lib.U32)
+    gid = _lib.empty(nr, _lib.U32)
+    ng = np.zeros(1, dtype=np.uint64)
+    _lib.call("geek_group_rows", _lib.ptr(rows), nr, int(rows.shape[1]), _lib.hptr(bits), _lib.ptr(perm),
+              _lib.ptr(gid), _lib.hptr(ng), _lib.stream())
+    return perm.to(torch.int64), gid.to(torch.int64), int(ng[0])
+
+
+def _bins_per_table_singletons(buckets: BucketTable, scheme: SignatureScheme, K: int, L: int, universe: int,
+                               owner, delta: int):
+    """_bins_per_table for delta >= 2 without group-by rows for singleton
+    buckets (most signature buckets of a Criteo-like input hold one id).
+
+    A singleton bucket {m} has signature (pi_1(m), .., pi_K(m)); pi_1 is a
+    bijection, so it shares a bin key (owner o, sigma) with a bucket B only if
+    m = pi_1^-1(sigma_1) -- B's pi_1-minimum, a member of B -- and
+    pi_j(m) = sigma_j for every j.  A bin of singletons alone holds one id c
+    times: at most c // (c // 2 + 1) <= 1 < delta winners, pruned.  So the
+    group-by runs over the buckets of >= 2 ids only, each group's candidate
+    singletons (m, o) are counted from one sorted key list, and the bins,
+    their bucket lists (ascending bucket position, as the stable group-by
+    emits them), the pruning rule and the table-major (owner, signature)
+    order are those of _bins_per_table."""
+    flat, off = buckets.member_csr()
+    nb = len(buckets)
+    dev = flat.device
+    sizes = off[1:] - off[:-1]
+    single = sizes == 1
+    nidx = torch.nonzero(~single, as_tuple=True)[0]
+    sidx = torch.nonzero(single, as_tuple=True)[0]
+    G = 1 if owner is None else int(owner.max().item()) + 1 if owner.numel() else 1
+    own = owner.to(torch.int64) if owner is not None else torch.zeros(nb, dtype=torch.int64, device=dev)
+    skey = flat[off[:-1][sidx]].to(torch.int64) * G + own[sidx]
+    skey, sord = torch.sort(skey, stable=True)  # equal keys keep ascending bucket position
+    spos = sidx[sord]
+    fN, oN = csr_gather(flat, off, nidx)
+    szN = sizes[nidx]
+    ownN = own[nidx].to(torch.int32)
+    obits = max(1, int(G - 1).bit_length())
+    bits = np.array(([obits] if owner is not None else []) + [max(1, int(universe - 1).bit_length())] * K,
+                    dtype=np.int32)
+    parts = []
+    for st in range(L):
+        funcs = scheme.functions(st)
+        empty = Bins(torch.zeros(0, dtype=torch.int64, device=dev), torch.zeros(0, dtype=torch.int64, device=dev),
+                     torch.zeros(0, dtype=torch.int32, device=dev), torch.zeros(0, dtype=torch.int64, device=dev),
+                     torch.zeros((0, K), dtype=torch.int32, device=dev))
+        if nidx.numel() == 0:
+            parts.append(empty)
+            continue
+        sig = bucket_signatures_csr(fN, oN, int(nidx.numel()), funcs)  # [K, |N|]
+        cols = ([ownN] if owner is not None else []) + [sig[j] for j in range(K)]
+        rows = torch.stack(cols, dim=1).contiguous()
+        del sig
+        perm, gid, ng = _group_all(rows, bits)
+        first = torch.ones(perm.numel(), dtype=torch.bool, device=dev)
+        first[1:] = gid[1:] != gid[:-1]
+        heads = perm[first]                                   # one N row per group, group order
+        hsig = rows[heads][:, -K:].contiguous()               # [ng, K] int32 (u32 bits)
+        hown = ownN[heads].to(torch.int64)
+        cntN = torch.bincount(gid, minlength=ng)
+        totN = torch.zeros(ng, dtype=torch.int64, device=dev).index_add_(0, gid, szN[perm])
+        # candidate singleton id of each group and its count
+        batch = PermBatch(funcs)
+        s0 = hsig[:, 0].contiguous()
+        m = _lib.empty(ng, _lib.U32)
+        st_, n_, tab_ = PermBatch(funcs[:1]).args()
+        _lib.call("geek_perm_inverse", st_, n_, tab_, _lib.ptr(s0), ng, _lib.ptr(m), _lib.stream())
+        fw = _lib.empty(max(1, ng * K), _lib.U32)
+        st_, n_, tab_ = batch.args()
+        _lib.call("geek_perm_forward", st_, n_, tab_, _lib.ptr(m), ng, _lib.ptr(fw), _lib.stream())
+        match = (fw[: ng * K].view(K, ng) == hsig.t()).all(dim=0)
+        ckey = (m.to(torch.int64) & 0xFFFFFFFF) * G + hown
+        lo = torch.searchsorted(skey, ckey, side="left")
+        hi = torch.searchsorted(skey, ckey, side="right")
+        cS = torch.where(match, hi - lo, torch.zeros_like(lo))
+        bsize = cntN + cS
+        need = bsize // 2 + 1
+        keep = (bsize >= 2) & ((totN + cS) // need >= delta)
+        kept = int(keep.sum().item())
+        if kept == 0:
+            parts.append(empty)
+            continue
+        newid = torch.cumsum(keep.to(torch.int64), 0) - 1
+        selN = keep[gid]
+        pbN = nidx[perm[selN]]
+        pnN = newid[gid[selN]]
+        kg = torch.nonzero(keep & (cS > 0), as_tuple=True)[0]
+        if kg.numel():
+            cnt = cS[kg]
+            tot = int(cnt.sum().item())
+            start = torch.repeat_interleave(lo[kg], cnt, output_size=tot)
+            ooff = torch.zeros(kg.numel() + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(cnt, 0, out=ooff[1:])
+            local = torch.arange(tot, device=dev, dtype=torch.int64) - torch.repeat_interleave(
+                ooff[:-1], cnt, output_size=tot)
+            pbS = spos[start + local]
+            pnS = torch.repeat_interleave(newid[kg], cnt, output_size=tot)
+            pb = torch.cat([pbN, pbS])
+            pn = torch.cat([pnN, pnS])
+            order = torch.argsort(pn * nb + pb)
+            pb, pn = pb[order], pn[order]
+        else:
+            pb, pn = pbN, pnN
+        parts.append(Bins(pb, pn, bsize[keep].to(torch.int32), torch.full((kept,), st, dtype=torch.int64,
+                                                                             device=dev), hsig[keep]))
+    return _concat_bins(parts), (flat, off)
+
+
 _SPLIT_ROWS = 1 << 28  # group-by rows above which signature-bucket bins are formed table by table
+_SINGLETON_BINS = True  # ... and singleton buckets join bins by lookup instead of group-by rows
 
 
 def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=None):
@@ -339,8 +453,9 @@ def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=N
     scheme = params.scheme(universe)
     if (isinstance(buckets, BucketTable) and not (buckets.even and buckets.n == scheme.universe)
             and len(buckets) * params.num_tables > _SPLIT_ROWS):
-        bins, csr = _bins_per_table(buckets, scheme, params.num_hashes, params.num_tables, universe, owner,
-                                    params.min_group_size)
+        form = _bins_per_table_singletons if _SINGLETON_BINS and params.min_group_size >= 2 else _bins_per_table
+        bins, csr = form(buckets, scheme, params.num_hashes, params.num_tables, universe, owner,
+                         params.min_group_size)
     else:
         sig, nb, csr = silk_signatures(buckets, scheme, info)
         bins = find_bins(sig, params.num_hashes, params.num_tables, universe, owner)

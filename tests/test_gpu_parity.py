@@ -526,11 +526,14 @@ def test_mixed_pipeline_golden(g):
     assert out.clustering.objective == m["runs"][str(g)]["objective"]
 
 
+@pytest.mark.parametrize("singletons", [True, False])
 @pytest.mark.parametrize("kind", ["sparse", "mixed"])
-def test_signature_bins_table_by_table(kind, monkeypatch):
+def test_signature_bins_table_by_table(kind, singletons, monkeypatch):
     """Large signature-bucket sets form their SILK bins one table at a time
-    (memory); forced here on the golden sparse / mixed pipelines: same output."""
+    (memory), singleton buckets by lookup; forced here on the golden sparse /
+    mixed pipelines: same output."""
     monkeypatch.setattr(G.seeding, "_SPLIT_ROWS", 0)
+    monkeypatch.setattr(G.seeding, "_SINGLETON_BINS", singletons)
     arr = npz("pipelines")
     if kind == "sparse":
         m = meta()["sparse"]
@@ -550,6 +553,33 @@ def test_signature_bins_table_by_table(kind, monkeypatch):
     assert keys(out.seed_groups) == keys(golden_groups(arr, pre))
     assert np.array_equal(out.clustering.assignment, arr[pre + "_labels"])
     assert out.clustering.objective == m["runs"]["2"]["objective"]
+
+
+@pytest.mark.parametrize("K,G_,delta", [(1, 3, 2), (2, 1, 2), (1, 1, 3), (3, 8, 2)])
+def test_singleton_bins_equal_group_by(K, G_, delta):
+    """Bins with singleton buckets joined by pi_1^-1 lookup equal the full
+    group-by + exact pruning, bucket lists and order included; small
+    universes and K = 1 make singletons join larger buckets often."""
+    from paper_2106_10515_b200.tables import BucketTable
+    rng = np.random.default_rng(K * 100 + G_ * 10 + delta)
+    n, m = 3000, 12
+    tsizes = [int(x) for x in rng.integers(1200, 2600, m)]
+    codes = np.stack([rng.integers(0, t, n) for t in tsizes], axis=1)
+    for j, t in enumerate(tsizes):  # every slot non-empty
+        codes[rng.permutation(n)[:t], j] = np.arange(t)
+    bt = BucketTable(torch.from_numpy(codes.astype(np.int32)).cuda(), n, tsizes, "sig", False)
+    owner = torch.from_numpy(np.concatenate([np.full(t, j % G_) for j, t in enumerate(tsizes)]).astype(np.int32)).cuda()
+    sp = G.SeedingParams(K, 5, min_group_size=delta, seed=11)
+    scheme = sp.scheme(n)
+    a, _ = G.seeding._bins_per_table(bt, scheme, K, 5, n, owner, delta)
+    b, _ = G.seeding._bins_per_table_singletons(bt, scheme, K, 5, n, owner, delta)
+    sizes = bt.bucket_sizes()
+    assert int((sizes == 1).sum()) > 1000
+    assert a.count > 0 and a.count == b.count
+    for f in ("pair_bucket", "pair_bin", "bin_size", "bin_table", "bin_sig"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
+    # some kept bins do mix singletons with larger buckets
+    assert bool((sizes[b.pair_bucket] == 1).any())
 
 
 @pytest.mark.parametrize("owners", [2, 3, 8])
