@@ -1297,8 +1297,13 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     int nct = 0;
     float xscale = 1.f;
     GEEK_TRY(tc_screen_prepare(C, k, d, nprod, kTcLBO, kTcSBO, img, c2s, mus, cmax, nct, xscale, s));
-    if (nprod == 17) {
-      GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s));
+    // FP16x3: the top-4 lists start at a bound from each point tile's origin
+    // center (GEEK_SCREEN_BOUND=0 starts them at +inf)
+    const char* bsel = getenv("GEEK_SCREEN_BOUND");
+    const bool bound16 = nprod == 16 && !(bsel && atoi(bsel) == 0);
+    if (nprod == 17 || bound16) {
+      GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s,
+                                nprod == 17));
       loc.cmax = cmax;
     }
     GEEK_TRY(ts.alloc(n * 32, s));
@@ -1312,7 +1317,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     if (ev_screen_begin) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_screen_begin), s));
     GEEK_TRY(tc_screen_launch((const float*)X, n, d, nprod, img, c2s, mus, k, nct, kTcLBO, kTcSBO, ts.as<float>(),
                               ti.as<int>(), use_xp ? xp.as<double>() : nullptr, xscale, ovf, s,
-                              nprod == 17 ? &loc : nullptr));
+                              (nprod == 17 || bound16) ? &loc : nullptr));
     if (nprod >= 16) {  // a point coordinate beyond the f16 range: the TF32x3 redo runs (device-predicated)
       int nct3 = 0;
       float xs3 = 1.f;

@@ -227,7 +227,9 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
 int dgemm_nt(const double* A, const double* B, double* Cout, int n, int m, int kk, cudaStream_t s);
 // {xscale, oscale} of a prepared screen (device memory inside its mu scratch)
 const float* tc_scal(const Scratch& mu, int d);
-// nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu
+// nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu;
+// nprod 16 with origins (no E table, with_E = false): the top-4 lists start at a bound from
+// each tile's origin center instead of +inf
 struct TcLocal {
   const float* cf;  // [k][d] float32 c'
   const int* j0;    // [ntiles] origin center per 128-point tile
@@ -240,7 +242,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
                      int xstride = 1, const unsigned* run_if = nullptr);
 int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
                      const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
-                     cudaStream_t s);
+                     cudaStream_t s, bool with_E = true);
 
 __global__ void iota_u32(uint32_t* p, uint64_t n);
 __global__ void fill_u32(uint32_t* p, uint32_t v, uint64_t n);

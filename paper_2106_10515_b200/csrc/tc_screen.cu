@@ -88,11 +88,13 @@ struct TcCfg {
   // deepens the B ring
   static constexpr bool kATmem = NPROD != 1;
   static constexpr int kABytes = kLocal ? 0 : (kTcKmax / kSliceDims) * kTcSliceBytes;
-  // NPROD = 1: point tiles double-buffered; NPROD = 3: single-buffered, the
+  // NPROD = 1: point tiles double-buffered; NPROD = 3 / 16: single-buffered, the
   // SMEM goes to the resident |c'|^2 slices instead (chunked hand-off keeps
   // the tile switch short)
   // NPROD = 17: double-buffered in TMEM (64 columns of packed f16 per
   // buffer), so the next tile's A lands while the MMAs still read this one's
+  // (NPROD = 16 double-buffered measured 0.7-1.3 ms slower per 20M points:
+  // the A writes then contend with the running MMAs)
   static constexpr int kABuf = (NPROD == 1 || NPROD == 17) ? 2 : 1;
   static constexpr int kHalfStage = kSlices * kTcBSliceBytes;     // one part of a B stage
   static constexpr int kStageBytes = kParts * kHalfStage;
@@ -624,6 +626,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
     const bool getenv_sleep = P.sleepwait != 0;
+    // lists start at a bound from the tile's origin center (always for the
+    // tile-local screen; FP16x3 when origins are given)
+    const bool bnd = Cfg::kLocal || (Cfg::kF16 && P.j0 != nullptr);
+    auto ld_org = [&](const float* org, int e0) -> float4 {
+      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (P.d == kTcKmax) {
+        o4 = __ldg(reinterpret_cast<const float4*>(org + e0));
+      } else {
+        if (e0 < P.d) o4.x = __ldg(org + e0);
+        if (e0 + 1 < P.d) o4.y = __ldg(org + e0 + 1);
+        if (e0 + 2 < P.d) o4.z = __ldg(org + e0 + 2);
+        if (e0 + 3 < P.d) o4.w = __ldg(org + e0 + 3);
+      }
+      return o4;
+    };
     Top4 cur;
     cur.init();
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
@@ -709,6 +726,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     //     lane) and dims kc*32 + 16(w/4) .. +15 of every chunk: the hi part
     //     goes to TMEM with one tcgen05.st, the lo part to the SMEM K-major tile.
     float4 q[16];
+    // FP16x3 with a start bound: the 64 origin coordinates of this warp's dims
+    // (dims kc*32 + 16(w/4) + 0..15 of chunk kc), two per lane, loaded with
+    // the point tile and broadcast by shuffles in store_chunks
+    float og[2] = {0.f, 0.f};
+    constexpr bool kBnd16 = Cfg::kF16 && !Cfg::kLocal;
+    int j0n = (kBnd16 && bnd && (uint64_t)blockIdx.x * kTcM < P.n) ? __ldg(P.j0 + blockIdx.x) : 0;
     const int rsub = lane & 7, csub = lane >> 3;
     auto tile_p0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM; };
     auto slot_of = [&](int kc, int p, int& row, int& e0) {
@@ -744,6 +767,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           }
           q[kc * 4 + p] = v;
         }
+      }
+      if (kBnd16 && bnd) {  // (tile t's origin index was loaded one tile earlier: no dependent load here)
+        const uint64_t tile = blockIdx.x + (uint64_t)t * gridDim.x;
+        if (tile * kTcM < P.n) {
+          const float* org = P.cf + (uint64_t)j0n * P.d;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int m = 2 * lane + r, e = (m >> 4) * 32 + (warp >> 2) * 16 + (m & 15);
+            og[r] = e < P.d ? __ldg(org + e) : 0.f;
+          }
+        }
+        const uint64_t nxt = tile + gridDim.x;
+        j0n = nxt * kTcM < P.n ? __ldg(P.j0 + nxt) : 0;
       }
       {  // pull the tile after it towards L2 while this one is in flight
         const uint64_t row = tile_p0(t + 1) + (warp * 32 + lane) / 2;
@@ -795,19 +831,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               xa[p] = fmaf(x3, x3, xa[p]);
             }
             if (Cfg::kLocal && valid) {  // x'' = x' - c'_j0 (the tile's origin)
-              float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (P.d == kTcKmax) {
-                o4 = __ldg(reinterpret_cast<const float4*>(org + e0));
-              } else {
-                if (e0 < P.d) o4.x = __ldg(org + e0);
-                if (e0 + 1 < P.d) o4.y = __ldg(org + e0 + 1);
-                if (e0 + 2 < P.d) o4.z = __ldg(org + e0 + 2);
-                if (e0 + 3 < P.d) o4.w = __ldg(org + e0 + 3);
-              }
+              const float4 o4 = ld_org(org, e0);
               x0 -= o4.x;
               x1 -= o4.y;
               x2 -= o4.z;
               x3 -= o4.w;
+            } else if (kBnd16 && bnd) {  // FP16x3 with a start bound: |x''|^2 only (0 for invalid rows)
+              const int m0 = kc * 16 + 4 * p;  // this element's slot among the warp's 64 origin values
+              const float o0 = __shfl_sync(0xffffffffu, og[m0 & 1], m0 >> 1);
+              const float o1 = __shfl_sync(0xffffffffu, og[(m0 + 1) & 1], (m0 + 1) >> 1);
+              const float o2 = __shfl_sync(0xffffffffu, og[(m0 + 2) & 1], (m0 + 2) >> 1);
+              const float o3 = __shfl_sync(0xffffffffu, og[(m0 + 3) & 1], (m0 + 3) >> 1);
+              const float z0 = x0 - o0, z1 = x1 - o1, z2 = x2 - o2, z3 = x3 - o3;
+              xa[p] = fmaf(z0, z0, xa[p]);
+              xa[p] = fmaf(z1, z1, xa[p]);
+              xa[p] = fmaf(z2, z2, xa[p]);
+              xa[p] = fmaf(z3, z3, xa[p]);
             }
             const float h0 = tf32_round(x0), h1 = tf32_round(x1), h2 = tf32_round(x2), h3 = tf32_round(x3);
             const uint32_t off = (e0 >> 3) * kTcSliceBytes + core_off(row, e0 & 7, P.lbo, P.sbo);
@@ -869,9 +908,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         const uint64_t i = p0 + (warp & 3) * 32 + lane;
         if (i < P.n) P.xpart[i * 2 + (warp >> 2)] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
       }
-      if (Cfg::kLocal)  // this half's |x''|^2, |x'|^2 for the lists' starting bound of the tile
-        Upart[(ab * 128 + (warp & 3) * 32 + lane) * 2 + (warp >> 2)] =
-            make_float2((xs[0] + xs[1]) + (xs[2] + xs[3]), (xa[0] + xa[1]) + (xa[2] + xa[3]));
+      if (bnd) {  // this half's |x''|^2, |x'|^2 for the lists' starting bound of the tile
+        const float s_xs = (xs[0] + xs[1]) + (xs[2] + xs[3]), s_xa = (xa[0] + xa[1]) + (xa[2] + xa[3]);
+        Upart[((t & 1) * 128 + (warp & 3) * 32 + lane) * 2 + (warp >> 2)] =
+            Cfg::kLocal ? make_float2(s_xs, s_xa) : make_float2(s_xa, s_xs);
+      }
     };
     // NPROD = 17: every list starts at a bound U instead of +inf, so a column
     // is a candidate only if it beats U.  s(x, c_j0) = |x''|^2 - |x'|^2 >= the
@@ -881,12 +922,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     // center -1) inside the window reads as an overflow (full scan), and the
     // classifier never takes a -1 winner.
     auto start_bound = [&](uint32_t t) -> float {
-      const int ab = t % Cfg::kABuf;
       const int r = (warp & 3) * 32 + lane;
-      const float2 h0 = Upart[(ab * 128 + r) * 2], h1 = Upart[(ab * 128 + r) * 2 + 1];
+      const float2 h0 = Upart[((t & 1) * 128 + r) * 2], h1 = Upart[((t & 1) * 128 + r) * 2 + 1];
       const float xpp = h0.x + h1.x, xp = h0.y + h1.y;
       const float cn = (float)__longlong_as_double((long long)P.cmax[0]);
-      const float win = 2.2f * (1.953125e-3f * sqrtf(xpp) * cn + 1e-5f * cn * cn) + 1e-4f * xp;
+      // twice the classifier's window (FP16: one product, error ~ |x''||c'| 2^-9;
+      // FP16x3: ~ |x'||c'| (2^-19 + 6 d 2^-23)), plus the float32 error of xpp - xp
+      const float win = Cfg::kLocal ? 2.2f * (1.953125e-3f * sqrtf(xpp) * cn + 1e-5f * cn * cn) + 1e-4f * xp
+                                    : 2.2f * ((2e-6f + 7.2e-7f * P.d) * sqrtf(xp) * cn + 1e-5f * cn * cn) +
+                                          1e-4f * (xp + xpp);
       const float us = xpp - xp + 4.f * win + 1.f;  // s units
       return us / oscale;                            // accumulator units (v = s / oscale)
     };
@@ -902,13 +946,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
             reinterpret_cast<const float4*>(P.Es + (uint64_t)P.j0[blockIdx.x + (uint64_t)t * gridDim.x] * P.kpadE);
         float4* dst = reinterpret_cast<float4*>(Ebuf + (t & 1) * P.kpadE);
         for (int e = tid; e < P.kpadE / 4; e += kTcEpiThreads) dst[e] = __ldg(src + e);
+      }
+      if (Cfg::kLocal) {  // both halves' |x''|^2, |x'|^2 and the E row are in SMEM
         asm volatile("bar.sync 1, %0;" ::"r"(kTcEpiThreads) : "memory");
+        cur.init(start_bound(t));
+      } else if (bnd) {  // the other half of these rows (warp w ^ 4) has left its |x''|^2, |x'|^2
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
         cur.init(start_bound(t));
       }
       for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
       if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
       finish(t, cur);
-      if (!Cfg::kLocal) cur.init();
+      if (!bnd) cur.init();
     }
   }
   fence_before();
@@ -1123,7 +1172,8 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
   static_assert(TcCfg<NPROD>::kTmemA + (TcCfg<NPROD>::kATmem ? TcCfg<NPROD>::kABuf : 1) * TcCfg<NPROD>::kTmemAStride <=
                     TcCfg<NPROD>::kTmemCols, "TMEM map");
   const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0) +
-                      (TcCfg<NPROD>::kLocal ? (size_t)2 * P.kpadE * sizeof(float) + 2 * 128 * 2 * sizeof(float2) : 0);
+                      (TcCfg<NPROD>::kLocal ? (size_t)2 * P.kpadE * sizeof(float) : 0) +
+                      (TcCfg<NPROD>::kF16 ? (size_t)2 * 128 * 2 * sizeof(float2) : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -1141,13 +1191,14 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
                      double* xpart, float xscale, unsigned* ovf, cudaStream_t s, const TcLocal* loc, int xstride,
                      const unsigned* run_if) {
   GEEK_REQUIRE(nprod < 16 || ovf, "FP16 screen needs the overflow flag");
-  GEEK_REQUIRE(nprod != 17 || loc, "tile-local screen needs its origins");
+  GEEK_REQUIRE(nprod != 17 || (loc && loc->Es), "tile-local screen needs its origins");
+  GEEK_REQUIRE(!loc || nprod >= 16, "origins are for the FP16 screens");
   GEEK_REQUIRE(d <= kTcKmax, "tensor-core screen needs d <= %d", kTcKmax);
   TcParams P;
   P.cf = loc ? loc->cf : nullptr;
   P.j0 = loc ? loc->j0 : nullptr;
   P.Es = loc ? loc->Es : nullptr;
-  P.kpadE = nct * kTcN;
+  P.kpadE = nprod == 17 ? nct * kTcN : 0;  // the origin table's row (tile-local screen only)
   P.xstride = xstride;
   P.run_if = run_if;
   P.cmax = loc ? loc->cmax : nullptr;
@@ -1188,7 +1239,8 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   }
 #endif
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
+  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed + 2 * 128 * 2 * sizeof(float2)
+              : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
   const int st = nprod == 17   ? launch_screen<17>(P, s)
@@ -1223,17 +1275,19 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
 // |x''| and with it the recheck rate small).
 int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
                      const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool with_E) {
   const int kpadE = nct17 * kTcN;
   const uint64_t ntiles = (n + kTcM - 1) / kTcM;
   GEEK_TRY(cf.alloc(k * (uint64_t)d * 4, s));
-  GEEK_TRY(Es.alloc(k * (uint64_t)kpadE * 4, s));
   GEEK_TRY(j0.alloc(ntiles * 4, s));
   centered_f32_kernel<<<grid_for(k * (uint64_t)d, 256), 256, 0, s>>>(C, k, d, mu17.as<float>(), cf.as<float>());
   GEEK_CHECK_LAUNCH();
-  origin_table_kernel<<<grid_for(k * (uint64_t)kpadE, 128, 148 * 16), 128, 0, s>>>(
-      cf.as<float>(), k, d, kpadE, tc_scal(mu17, d), Es.as<float>());
-  GEEK_CHECK_LAUNCH();
+  if (with_E) {
+    GEEK_TRY(Es.alloc(k * (uint64_t)kpadE * 4, s));
+    origin_table_kernel<<<grid_for(k * (uint64_t)kpadE, 128, 148 * 16), 128, 0, s>>>(
+        cf.as<float>(), k, d, kpadE, tc_scal(mu17, d), Es.as<float>());
+    GEEK_CHECK_LAUNCH();
+  }
   Scratch img1, c21, mu1, ts, ti, misc;
   GEEK_TRY(misc.alloc(32, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(misc.ptr, 0, 32, s));
@@ -1248,7 +1302,7 @@ int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_
   GEEK_CHECK_LAUNCH();
   loc.cf = cf.as<float>();
   loc.j0 = j0.as<int>();
-  loc.Es = Es.as<float>();
+  loc.Es = with_E ? Es.as<float>() : nullptr;
   return GEEK_OK;
 }
 

@@ -356,6 +356,34 @@ def test_fp16_screen_range_fallback(mode, monkeypatch):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("bound", ["1", "0"])
+@pytest.mark.parametrize("order", ["clustered", "shuffled", "far"])
+def test_fp16x3_start_bound_orders(order, bound, monkeypatch):
+    """The default FP16x3 screen with its lists starting at a bound from each
+    point tile's origin center (and without, GEEK_SCREEN_BOUND=0): exact labels
+    for cluster-ordered ids, shuffled ids (poor origins: more insertions) and
+    points far from every center (the bound sits far above the best)."""
+    monkeypatch.setenv("GEEK_SCREEN_BOUND", bound)
+    rng = np.random.default_rng(23)
+    k, d, n = 700, 96, 50_000
+    C = np.cumsum(rng.standard_normal((k, d)) * 2.0, axis=0) + 100.0
+    C[9] = C[8] + 1e-6
+    C[400] = C[401]  # exact duplicate centers: ties to the lower index
+    lab0 = np.sort(rng.integers(0, k, n))
+    X = (C[lab0] + rng.standard_normal((n, d))).astype(np.float32)
+    if order == "shuffled":
+        X = X[rng.permutation(n)]
+    if order == "far":
+        X[::7] += 300.0
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    st = G.assignment.last_assign_stats()
+    assert st["screen_mode"] == 16
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+
+
 @pytest.mark.parametrize("order", ["clustered", "shuffled"])
 def test_tile_local_screen_orders(order, monkeypatch):
     """The tile-local screen (GEEK_SCREEN=17): exact labels whatever the id order; on

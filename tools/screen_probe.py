@@ -11,6 +11,8 @@ if os.environ.get("_PROBE_CHILD"):
     import torch
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2106_10515_b200 import _lib as L
+    if os.environ.get("PROBE_DEBUG"):  # the -DGEEK_DEBUG_KNOBS build (tools/build_debug.py)
+        L.load_library(os.path.join(os.path.dirname(L.LIB_PATH), "libgeek_dbg.so"))
     from paper_2106_10515_b200.assignment import AssignStats
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 963
