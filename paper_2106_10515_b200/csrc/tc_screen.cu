@@ -382,7 +382,8 @@ struct TcParams {
   int c2res;          // 1: the |c'|^2/2 slices of all center tiles (+ the ones slice) stay in SMEM
   int pushcut;        // candidates per lane above which a round walks every column (GEEK_SCREEN_PUSHCUT)
   int prof;           // profiling knob (GEEK_SCREEN_PROF): 1 = no epilogue math, 2 = no MMAs, 3 = no A writes, 8 = no top-4 inserts,
-                      // 5 = neither epilogue math nor A writes, 6 = 5 without B refills
+                      // 5 = neither epilogue math nor A writes, 6 = 5 without B refills,
+                      // 9 = no start-bound barrier (lists from +inf), 10 = no |x''|^2 shuffles
   unsigned long long* dbg;  // GEEK_SCREEN_DBG: per-CTA MMA-warp wait cycles [full, acce, afull, total]
   const float* scal;  // device {xscale, oscale}: x' (FP16: times xscale, a power of two, before the f16
                       // split); top_s = oscale * (accumulator): 2 (TF32) or 2 / xscale^2 (FP16)
@@ -458,6 +459,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   const uint64_t ct_bytes = tc_ct_bytes(P.d, Cfg::kParts, Cfg::kChunkDims, Cfg::kSlices);
   const uint32_t total_q = (uint32_t)P.nct * qct;
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
+  // center-tile walk: CTAs start on different tiles (spreads the B reads), but
+  // a narrow last tile is always walked first -- ending a point tile on it
+  // would leave its short MMAs to hide the previous full tile's epilogue and
+  // the next point tile's A conversion
+  const uint32_t rot = P.nlast < kTcN ? (uint32_t)(P.nct - 1) : blockIdx.x;
   const uint32_t my_tiles = ntiles > blockIdx.x ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
   // The producer and MMA warps run their loops warp-wide (so addresses and
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           else mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
         }
         const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
-        const uint32_t ct = (cq + blockIdx.x) % (uint32_t)P.nct;  // CTAs start on different center tiles
+        const uint32_t ct = (cq + rot) % (uint32_t)P.nct;  // CTAs start on different center tiles
         const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
         if (leader && P.prof == 6 && q >= (uint64_t)Cfg::kStages) {
           mbar_arrive(&full[s]);  // profiling: keep the stale stage, no L2 traffic
@@ -538,7 +544,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
           fence_after();
           const uint32_t dt = tmem + buf * kTcN;
           // the last center tile runs with N = its valid centers rounded up to 16
-          const uint32_t idesc = (int)((ct + blockIdx.x) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
+          const uint32_t idesc = (int)((ct + rot) % P.nct) == P.nct - 1 ? idesc_last : idesc_full;
           for (int kc = 0; kc < nbk; ++kc) {
             // point-tile chunks (32 dims) holding this B chunk's dims
             const int ac0 = kc * Cfg::kChunkDims / kTcAChunk;
@@ -595,7 +601,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               mbar_wait(c2full, 0);
               fence_after();
             }
-            const uint32_t cta = (uint32_t)((ct + blockIdx.x) % P.nct);
+            const uint32_t cta = (uint32_t)((ct + rot) % P.nct);
             const uint64_t a1 = make_sdesc(smem_u32(C2), P.lbo, P.sbo);
             const uint64_t b1 = make_sdesc(smem_u32(C2) + kTcSliceBytes + cta * kTcBSliceBytes, P.lbo, P.sbo);
             if (P.prof != 2 && leader) tc_mma<Cfg::kF16>(dt, a1, b1, idesc, 1u);
@@ -651,11 +657,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       else mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
-      if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3) || P.prof == 8) {
-        const int cta = (int)((ct + blockIdx.x) % P.nct);
+      if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3) || P.prof >= 8) {
+        const int cta = (int)((ct + rot) % P.nct);
         const bool last = cta == P.nct - 1;  // columns past the last tile's MMA width hold stale sums
+        // the last center tile's 32-column chunks past its MMA width are not read at all
+        const int cend = last ? min(kTcN / 2, max(0, P.nlast - ch * (kTcN / 2))) : kTcN / 2;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kTcN / 2; c0 += 32) {
+        for (int c0 = 0; c0 < cend; c0 += 32) {
           float v[32];
           tc_ld32_async(trow + c0, v);
           tc_wait_ld();
@@ -836,7 +844,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
               x1 -= o4.y;
               x2 -= o4.z;
               x3 -= o4.w;
-            } else if (kBnd16 && bnd) {  // FP16x3 with a start bound: |x''|^2 only (0 for invalid rows)
+            } else if (kBnd16 && bnd && P.prof != 10) {  // FP16x3 with a start bound: |x''|^2 only (0 for invalid rows)
               const int m0 = kc * 16 + 4 * p;  // this element's slot among the warp's 64 origin values
               const float o0 = __shfl_sync(0xffffffffu, og[m0 & 1], m0 >> 1);
               const float o1 = __shfl_sync(0xffffffffu, og[(m0 + 1) & 1], (m0 + 1) >> 1);
@@ -950,14 +958,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       if (Cfg::kLocal) {  // both halves' |x''|^2, |x'|^2 and the E row are in SMEM
         asm volatile("bar.sync 1, %0;" ::"r"(kTcEpiThreads) : "memory");
         cur.init(start_bound(t));
-      } else if (bnd) {  // the other half of these rows (warp w ^ 4) has left its |x''|^2, |x'|^2
+      } else if (bnd && P.prof != 9) {  // the other half of these rows (warp w ^ 4) has left its |x''|^2, |x'|^2
         asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
         cur.init(start_bound(t));
       }
       for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
       if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
       finish(t, cur);
-      if (!bnd) cur.init();
+      if (!bnd || P.prof == 9) cur.init();
     }
   }
   fence_before();

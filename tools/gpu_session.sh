@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_benchlaw.py -q -x > gpurun_out/t_all.log 2>&1
-echo "rc=$?" >> gpurun_out/t_all.log
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_bnd.json 2> gpurun_out/bench_bnd.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "screen or assign or tcgen05 or bound" > gpurun_out/t_scr.log 2>&1
+echo "rc=$?" >> gpurun_out/t_scr.log
+export PROBE_DEBUG=1 PROBE_SORTED=1
+PROBE_MODES=0,1 timeout 600 python tools/screen_probe.py 20000000 963 128 >> gpurun_out/scr_dbg11.log 2>&1
+PROBE_MODES=0 timeout 600 python tools/screen_probe.py 20000000 1000 128 >> gpurun_out/scr_dbg11.log 2>&1
