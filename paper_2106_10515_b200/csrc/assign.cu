@@ -8,6 +8,8 @@
 // distances and radii are bit-identical to the reference.
 #include "common.cuh"
 
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -562,7 +564,12 @@ struct DevSumTree {
 
 // effective screen mode of a call: an FP16 screen whose scaled operand left the
 // f16 range was redone in TF32x3 (the fallback launch ran when *ovf != 0)
-__device__ __forceinline__ int eff_mode(int nprod, const unsigned* ovf) { return (ovf && *ovf) ? 3 : nprod; }
+// an f16 overflow: the FP16 tcgen05 screens were redone in TF32x3 (mode 3);
+// the wide-row FP16x3 screen (65) has no redo -- mode 0 sends every point to
+// the exact full scan
+__device__ __forceinline__ int eff_mode(int nprod, const unsigned* ovf) {
+  return (ovf && *ovf) ? (nprod >= 65 ? 0 : 3) : nprod;
+}
 
 constexpr int kScrP = 128, kScrC = 128, kScrK = 16, kScrThreads = 256;
 
@@ -730,6 +737,16 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
 //            error of f16 subnormals, at most 2^-25 per scaled coordinate:
 //            2^-25 sqrt(d) (|x'| + |c'|) / s, and the three f16 parts of
 //            s^2 |c'|^2 / 2 (3 * 2^-25 / s^2 + 2^-33 |c'|^2 / 2).
+//   nprod 65 (wide rows, FP16x3 as one cuBLAS GEMM over K = 3d: [xh xh xl] .
+//            [ch cl ch] of s x', s c', fp32 accumulation in any order): the
+//            nprod 16 terms with 3d accumulated products; |c'|^2 enters in
+//            float64 and s is rounded once to float32 (both inside 4u cn^2 +
+//            10u xn cn).
+//   nprod 66 (nprod 65 over x'' = fl32(x' - c'_j0), j0 the row tile's origin
+//            center, xn = |x''|): s = E[j0][j] - 2 x''.c'_j with the float64
+//            table E[j0][j] = |c'_j|^2 - 2 c'_j0.c'_j (equal to s(x, c_j) up to a
+//            per-point constant and the x'' rounding, 2u |x''||c'|), rounded once
+//            to float32 (|s| <= 3 cn^2 + 2 xn cn).
 //   nprod 64 (wide rows, float64 cuBLAS GEMM over uncentered x, c; xn = |x|,
 //            cn = max |c|): gamma_{d+2} for the dot products and |c|^2, plus
 //            the float32 rounding of the stored s = |c|^2 - 2 x.c.
@@ -745,13 +762,17 @@ __device__ __forceinline__ double exact_dist(const PwPlan& plan, const G& get) {
 // term keeps the correctly rounded square roots of the two best distinct.
 __device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int nprod,
                                                const unsigned long long* cmax_bits) {
+  if (nprod == 0) return INFINITY;  // no valid screen: every point is scanned exactly
   const double u = 5.9604644775390625e-08;  // 2^-24
-  const double acc = (double)d * 1.1920928955078125e-07;  // d * 2^-23
+  // fp32 accumulation of d products (the wide FP16x3 GEMM accumulates 3d)
+  const double acc = (nprod == 65 || nprod == 66 ? 3.0 : 1.0) * (double)d * 1.1920928955078125e-07;  // d * 2^-23
   // (|c'|^2/2 enters the fp32 accumulation as a last K=8 slice: one more
   // rounding of the accumulator, 2u(xn cn + cn^2) in s units, on top)
   double E = nprod != 1 ? 1.05 * ((1.9073486328125e-06 + 6.0 * acc + 10.0 * u) * xn * cn + 4.0 * u * cn * cn)
                         : 1.05 * ((1.953125e-03 + 2.0 * acc + 8.0 * u) * xn * cn + 5.0 * u * cn * cn);
-  if (nprod == 16) {
+  if (nprod == 66)  // the E table enters in float64, s = E - 2 x''.c' rounded once (|s| <= 3 cn^2 + 2 xn cn)
+    E = 1.05 * ((1.9073486328125e-06 + 6.0 * acc + 10.0 * u) * xn * cn + 12.0 * u * cn * cn);
+  if (nprod == 16 || nprod == 65 || nprod == 66) {
     const double is = __longlong_as_double((long long)cmax_bits[3]);
     const double t25 = 2.9802322387695312e-08;  // 2^-25
     E += 1.05 * (t25 * sqrt((double)d) * (xn + cn) * is + 3.0 * t25 * is * is + 1.1641532182693481e-10 * 0.5 * cn * cn);
@@ -766,8 +787,10 @@ __device__ __forceinline__ double tc_threshold(double xn, double cn, int d, int 
     E = 1.05 * ((1.953125e-03 + 2.0 * acc + 10.0 * u) * xn * cn + 12.0 * u * cn * cn + 4.0 * u * (xn + cn) * cn +
                 t25 * sqrt((double)d) * (xn + cn) * is);
   }
-  const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * (xn + cn) * (xn + cn);
-  return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * (xn + cn) * (xn + cn);
+  // |x - c| <= |x'| + |c'|, and with an origin (xn = |x''|) <= |x''| + 2 |c'|max
+  const double xc = (nprod == 17 || nprod == 66) ? xn + 2.0 * cn : xn + cn;
+  const double E64 = 1.01 * (d + 4.0) * 1.1102230246251565e-16 * xc * xc;
+  return 2.0 * E + 2.0 * E64 + 9.094947017729282e-13 * xc * xc;
 }
 
 // The screen keeps the top-4 of each accumulator column half ([8] per point).
@@ -806,21 +829,27 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
                                    uint64_t k, const PwPlan plan, const float* top_s, const int* top_i,
                                    float* xnorm, const float* mu, const unsigned long long* cmax_bits, int nprod,
                                    const unsigned* ovf, int64_t* labels, double* best, uint32_t* amb,
-                                   unsigned long long* namb, uint32_t* full, unsigned long long* nfull) {
+                                   unsigned long long* namb, uint32_t* full, unsigned long long* nfull,
+                                   const double* xn2_in) {
   const double cn = __longlong_as_double((long long)*cmax_bits);
   nprod = eff_mode(nprod, ovf);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const ScreenView v = screen_view(top_s + i * 8, top_i + i * 8);
-    double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand
-    for (int j = 0; j < d; ++j) {
-      const double xv = (double)(X[i * d + j] - mu[j]);
-      xn2 = fma(xv, xv, xn2);
+    double xn2 = 0.0;  // |x'|, x' = fl32(x - mu) exactly as the screen's operand (or the screen's |x''|^2)
+    if (xn2_in) {
+      xn2 = xn2_in[i];
+    } else {
+      for (int j = 0; j < d; ++j) {
+        const double xv = (double)(X[i * d + j] - mu[j]);
+        xn2 = fma(xv, xv, xn2);
+      }
     }
     const float xn = (float)(sqrt(xn2) * (1.0 + 1e-6));
     xnorm[i] = xn;
     const double T = tc_threshold((double)xn, cn, d, nprod, cmax_bits);
     const double s0 = v.s0;
-    if (v.i0 >= 0 && (k == 1 || (double)v.s1 - s0 > T)) {
+    const bool nos = nprod == 0;  // no valid screen (an f16 overflow of the wide FP16x3 GEMM)
+    if (!nos && v.i0 >= 0 && (k == 1 || (double)v.s1 - s0 > T)) {
       const int lab = v.i0;
       const float* xr = X + i * d;
       const double* cr = C + (uint64_t)lab * d;
@@ -829,7 +858,7 @@ __global__ void tc_classify_kernel(const float* __restrict__ X, uint64_t n, int 
         const double df = __dsub_rn((double)xr[j], cr[j]);
         return __dmul_rn(df, df);
       });
-    } else if (v.i0 < 0 || (double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) {
+    } else if (nos || v.i0 < 0 || (double)v.s3a - s0 <= T || (double)v.s3b - s0 <= T) {
       full[atomicAdd(nfull, 1ull)] = (uint32_t)i;  // candidate window overflows the kept lists
     } else {
       amb[atomicAdd(namb, 1ull)] = (uint32_t)i;
@@ -1094,14 +1123,141 @@ __global__ void center_norms_kernel(const double* C, uint64_t k, int d, double* 
   }
 }
 
+// FP16x3 operands of the wide-row screen, K = 3d: row r of A is
+// [hi(s x') | hi(s x') | lo(s x')], row j of B is [hi(s c') | lo(s c') | hi(s c')],
+// so one fp32-accumulated f16 GEMM gives s^2 (x'h.c'h + x'h.c'l + x'l.c'h)
+__global__ void wide_split_points_kernel(const float* X, uint64_t rows, int d, const float* mu, const float* scal,
+                                         __half* Aw, unsigned* ovf) {
+  const float xs = __ldg(scal);
+  bool big = false;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < rows * d; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e / d;
+    const int j = (int)(e - r * d);
+    const float y = (X[e] - __ldg(mu + j)) * xs;  // x' = fl32(x - mu), exactly the classifier's
+    big |= !(fabsf(y) <= 32768.f);
+    const __half h = __float2half_rn(y);
+    const __half l = __float2half_rn(y - __half2float(h));
+    __half* a = Aw + r * 3 * (uint64_t)d;
+    a[j] = h;
+    a[d + j] = h;
+    a[2 * d + j] = l;
+  }
+  if (big) atomicOr(ovf, 1u);
+}
+
+// mode 66 (tile origins): c' = fl32(c - mu) as float32 rows, the table
+// E[a][j] = |c'_j|^2 - 2 c'_a.c'_j (float64 over the float32 c'), and for
+// every 128-row tile the center nearest its first row (any choice is exact;
+// a near one keeps |x''| and the window small)
+__global__ void wide_cf_kernel(const double* C, uint64_t k, int d, const float* mu, float* cf) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < k * (uint64_t)d; e += (uint64_t)gridDim.x * blockDim.x)
+    cf[e] = (float)(C[e] - (double)mu[e % d]);
+}
+
+__global__ void wide_etable_kernel(const float* cf, uint64_t k, int d, double* E) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < k * k; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = q / k, j = q % k;
+    const float* ca = cf + a * d;
+    const float* cj = cf + j * d;
+    double e = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const double y = (double)cj[t];
+      e = fma(y, y - 2.0 * (double)ca[t], e);
+    }
+    E[q] = e;
+  }
+}
+
+// one warp per tile: float32 distances of the tile's first row to every center
+__global__ void wide_origin_kernel(const float* X, uint64_t n, int d, const float* mu, const float* cf, uint64_t k,
+                                   int* j0) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t ntiles = (n + 127) / 128;
+  const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles; t += wstride) {
+    const float* xr = X + t * 128 * (uint64_t)d;
+    float bv = INFINITY;
+    int bj = 0;
+    for (uint64_t j = 0; j < k; ++j) {
+      float acc = 0.f;
+      for (int e = lane; e < d; e += 32) {
+        const float z = (xr[e] - mu[e]) - cf[j * d + e];
+        acc = fmaf(z, z, acc);
+      }
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (acc < bv) {
+        bv = acc;
+        bj = (int)j;
+      }
+    }
+    if (lane == 0) j0[t] = bj;
+  }
+}
+
+// one warp per row: x'' = fl32(fl32(x - mu) - c'_j0) (j0 = the row's tile
+// origin), the FP16x3 row [hi | hi | lo] of s x'' and |x''|^2 in float64
+__global__ void wide_split_local_kernel(const float* X, uint64_t rows, uint64_t row0, int d, const float* mu,
+                                        const float* cf, const int* j0, const float* scal, __half* Aw, double* xn2,
+                                        unsigned* ovf) {
+  const int lane = threadIdx.x & 31;
+  const float xs = __ldg(scal);
+  const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  bool big = false;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += wstride) {
+    const float* xr = X + r * (uint64_t)d;
+    const float* org = cf + (uint64_t)__ldg(j0 + (row0 + r) / 128) * d;
+    __half* a = Aw + r * 3 * (uint64_t)d;
+    double q = 0.0;
+    for (int e = lane; e < d; e += 32) {
+      const float z = (xr[e] - __ldg(mu + e)) - __ldg(org + e);
+      q = fma((double)z, (double)z, q);
+      const float y = z * xs;
+      big |= !(fabsf(y) <= 32768.f);
+      const __half h = __float2half_rn(y);
+      const __half l = __float2half_rn(y - __half2float(h));
+      a[e] = h;
+      a[d + e] = h;
+      a[2 * d + e] = l;
+    }
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (lane == 0) xn2[row0 + r] = q;
+  }
+  if (big) atomicOr(ovf, 1u);
+}
+
+// centers: c' = fl32(c - mu) as the FP16 screen's image, |c'|^2 in float64 and |c'|max
+__global__ void wide_split_centers_kernel(const double* C, uint64_t k, int d, const float* mu, const float* scal,
+                                          __half* Bw, double* c2p, unsigned long long* cmax_bits) {
+  const float xs = __ldg(scal);
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k; c += (uint64_t)gridDim.x * blockDim.x) {
+    double n2 = 0.0;
+    __half* b = Bw + c * 3 * (uint64_t)d;
+    for (int j = 0; j < d; ++j) {
+      const float cv = (float)(C[c * d + j] - (double)mu[j]);
+      n2 = fma((double)cv, (double)cv, n2);
+      const float y = cv * xs;
+      const __half h = __float2half_rn(y);
+      const __half l = __float2half_rn(y - __half2float(h));
+      b[j] = h;
+      b[d + j] = l;
+      b[2 * d + j] = h;
+    }
+    c2p[c] = n2;
+    atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(sqrt(n2) * (1.0 + 1e-6)));
+  }
+}
+
 // one warp per row: s_j = |c_j|^2 - 2 x.c_j over the GEMM row, the 8 smallest
 // kept as (e0 e1 e2 e7 | e3 e4 e5 e6) -- the classifier reads entries 3 and 7
 // as the two lists' 4th values, so a window reaching the 7th smallest counts
 // as an overflow (full scan) and every entry of the 8 is a candidate
-__global__ void __launch_bounds__(256) top8_rows_kernel(const double* __restrict__ G, uint64_t rows, uint64_t k,
+// (float64 GEMM: s = c2 - 2 g; FP16x3: g = s^2 x'.c', s = c2 - (2 / s^2) g, gw = scal + 1)
+template <class T>
+__global__ void __launch_bounds__(256) top8_rows_kernel(const T* __restrict__ G, uint64_t rows, uint64_t k,
                                                         const double* __restrict__ c2, float* top_s, int* top_i,
-                                                        uint64_t row0) {
+                                                        uint64_t row0, const float* gwp, uint64_t ldg) {
   const int lane = threadIdx.x & 31;
+  const double gw = gwp ? (double)__ldg(gwp) : 2.0;
   const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += wstride) {
     double v[8];
@@ -1111,9 +1267,9 @@ __global__ void __launch_bounds__(256) top8_rows_kernel(const double* __restrict
       v[a] = INFINITY;
       id[a] = -1;
     }
-    const double* g = G + r * k;
+    const T* g = G + r * ldg;
     for (uint64_t j = lane; j < k; j += 32) {
-      const double sv = c2[j] - 2.0 * g[j];
+      const double sv = c2[j] - gw * (double)g[j];
       if (sv < v[7]) {  // insertion, column order kept among equal values
         int p = 7;
         while (p > 0 && v[p - 1] > sv) {
@@ -1167,6 +1323,90 @@ __global__ void __launch_bounds__(256) top8_rows_kernel(const double* __restrict
   }
 }
 
+// The same top-8 with the whole GEMM row in registers (k <= 32 R): R values
+// per lane, then 8 rounds of a warp (value, column) minimum -- no per-lane
+// insertion lists, every load of the row in flight at once.  Row r's
+// |c'|^2-like term is Erow = E + (E_tile ? E_tile[(row0 + r) / 128] * kE : 0):
+// the wide FP16x3 screen with tile origins (mode 66) subtracts 2 c'_j0.c'_j per tile.
+template <class T, int R>
+__global__ void __launch_bounds__(256) top8_rows_reg_kernel(const T* __restrict__ G, uint64_t rows, uint64_t k,
+                                                            uint64_t ldg, const double* __restrict__ E,
+                                                            const int* __restrict__ E_tile, uint64_t kE,
+                                                            float* top_s, int* top_i, uint64_t row0,
+                                                            const float* gwp) {
+  const int lane = threadIdx.x & 31;
+  const double gw = gwp ? (double)__ldg(gwp) : 2.0;
+  const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows; r += wstride) {
+    const T* g = G + r * ldg;
+    const double* er = E + (E_tile ? (uint64_t)__ldg(E_tile + (row0 + r) / 128) * kE : 0ull);
+    float v[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const uint64_t j = (uint64_t)a * 32 + lane;
+      v[a] = j < k ? (float)(__ldg(er + j) - gw * (double)g[j]) : INFINITY;
+    }
+    float e[8];
+    int ei[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float bv = v[0];
+      int ba = 0;
+#pragma unroll
+      for (int a = 1; a < R; ++a)
+        if (v[a] < bv) {  // strict: the lane's smallest column among equal values
+          bv = v[a];
+          ba = a;
+        }
+      int bj = bv < INFINITY ? ba * 32 + lane : 0x7FFFFFFF;
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov < bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      e[q] = bv;
+      ei[q] = bv < INFINITY ? bj : -1;
+      if (bv < INFINITY && (bj & 31) == lane) {
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+          if (a == (bj >> 5)) v[a] = INFINITY;
+      }
+    }
+    if (lane == 0) {
+      const uint64_t i = row0 + r;
+      const int pos[8] = {0, 1, 2, 4, 5, 6, 7, 3};  // e_q -> slot (as top8_rows_kernel)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        top_s[i * 8 + pos[q]] = e[q];
+        top_i[i * 8 + pos[q]] = ei[q];
+      }
+    }
+  }
+}
+
+template <class T>
+static int launch_top8(const T* G, uint64_t rows, uint64_t k, uint64_t ldg, const double* E, const int* E_tile,
+                       uint64_t kE, float* ts, int* ti, uint64_t row0, const float* gw, cudaStream_t s) {
+  const unsigned grid = grid_for(rows * 32, 256);
+#define GEEK_TOP8(RV) \
+  top8_rows_reg_kernel<T, RV><<<grid, 256, 0, s>>>(G, rows, k, ldg, E, E_tile, kE, ts, ti, row0, gw)
+  if (k <= 256) GEEK_TOP8(8);
+  else if (k <= 512) GEEK_TOP8(16);
+  else if (k <= 768) GEEK_TOP8(24);
+  else if (k <= 1024) GEEK_TOP8(32);
+  else if (!E_tile) top8_rows_kernel<T><<<grid, 256, 0, s>>>(G, rows, k, E, ts, ti, row0, gw, ldg);
+  else {
+    set_error("tile-origin top-8 needs k <= 1024");
+    return GEEK_EINVAL;
+  }
+#undef GEEK_TOP8
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
 __global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
                                     const unsigned* ovf, int nprod, geek_assign_stats_t* st);
 
@@ -1175,28 +1415,86 @@ __global__ void assign_stats_kernel(const unsigned long long* namb, const unsign
 static int assign_wide_screen(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k,
                               const PwPlan& plan, int64_t* labels, double* best, geek_assign_stats_t* stats,
                               void* ev0, void* ev1, cudaStream_t s) {
-  Scratch cnt, c2, ts, ti, xn, amb, full, mu0, x64, G;
+  // default (float32 rows, k <= 1024): the FP16x3 screen as one f16
+  // tensor-core GEMM over K = 3d of the rows centered at their tile's origin
+  // center (mode 66); GEEK_WIDE=65 the same centered at the center mean only,
+  // GEEK_WIDE=64 (and float64 rows) the float64 DGEMM screen
+  const char* wsel = getenv("GEEK_WIDE");
+  const int want = wsel ? atoi(wsel) : 66;
+  const int mode = (dtype != 0 || want == 64 || 3 * d > 65535) ? 64 : (want == 65 || k > 1024) ? 65 : 66;
+  const uint64_t kp8 = (k + 7) / 8 * 8;  // GEMM rows of B / columns of G (16-byte aligned f32 rows)
+  Scratch cnt, c2, ts, ti, xn, amb, full, mu0, x64, G, mus, Aw, Bw, cf, Et, j0, xn2;
   GEEK_TRY(cnt.alloc(48, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
-  unsigned long long* cmax = cnt.as<unsigned long long>();
+  unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16)
   unsigned long long* namb = cmax + 1;
   unsigned long long* nfull = cmax + 2;
+  unsigned* ovf = reinterpret_cast<unsigned*>(cmax + 4);
   GEEK_TRY(c2.alloc(k * 8, s));
-  GEEK_TRY(mu0.alloc((size_t)d * 4, s));
-  GEEK_CHECK_CUDA(cudaMemsetAsync(mu0.ptr, 0, (size_t)d * 4, s));
-  center_norms_kernel<<<grid_for(k, 128), 128, 0, s>>>(C, k, d, c2.as<double>(), cmax);
-  GEEK_CHECK_LAUNCH();
+  const float* mu_cls;
+  const float* gw = nullptr;
+  if (mode >= 65) {
+    GEEK_TRY(tc_wide_prepare(C, k, d, mus, cmax, s));
+    GEEK_TRY(Bw.alloc(kp8 * 3 * (uint64_t)d * 2, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(Bw.ptr, 0, kp8 * 3 * (uint64_t)d * 2, s));  // padding centers: zero rows
+    wide_split_centers_kernel<<<grid_for(k, 128), 128, 0, s>>>(C, k, d, mus.as<float>(), tc_scal(mus, d),
+                                                              Bw.as<__half>(), c2.as<double>(), cmax);
+    GEEK_CHECK_LAUNCH();
+    mu_cls = mus.as<float>();
+    gw = tc_scal(mus, d) + 1;
+    if (mode == 66) {
+      const uint64_t ntiles = (n + 127) / 128;
+      GEEK_TRY(cf.alloc(k * (uint64_t)d * 4, s));
+      GEEK_TRY(Et.alloc(k * k * 8, s));
+      GEEK_TRY(j0.alloc(ntiles * 4, s));
+      GEEK_TRY(xn2.alloc(n * 8, s));
+      wide_cf_kernel<<<grid_for(k * (uint64_t)d, 256), 256, 0, s>>>(C, k, d, mu_cls, cf.as<float>());
+      GEEK_CHECK_LAUNCH();
+      wide_etable_kernel<<<grid_for(k * k, 128), 128, 0, s>>>(cf.as<float>(), k, d, Et.as<double>());
+      GEEK_CHECK_LAUNCH();
+      wide_origin_kernel<<<grid_for(ntiles * 32, 256), 256, 0, s>>>((const float*)X, n, d, mu_cls, cf.as<float>(), k,
+                                                                    j0.as<int>());
+      GEEK_CHECK_LAUNCH();
+    }
+  } else {
+    GEEK_TRY(mu0.alloc((size_t)d * 4, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(mu0.ptr, 0, (size_t)d * 4, s));
+    center_norms_kernel<<<grid_for(k, 128), 128, 0, s>>>(C, k, d, c2.as<double>(), cmax);
+    GEEK_CHECK_LAUNCH();
+    mu_cls = mu0.as<float>();
+  }
   GEEK_TRY(ts.alloc(n * 32, s));
   GEEK_TRY(ti.alloc(n * 32, s));
   GEEK_TRY(xn.alloc(n * 4, s));
   GEEK_TRY(amb.alloc(n * 4, s));
   GEEK_TRY(full.alloc(n * 4, s));
-  const uint64_t P = std::max<uint64_t>(1, std::min<uint64_t>(n, (3ull << 30) / (8ull * (d + k))));
-  if (dtype == 0) GEEK_TRY(x64.alloc(P * d * 8, s));
-  GEEK_TRY(G.alloc(P * k * 8, s));
+  // point chunks: ~3 GB of GEMM operands and output at a time
+  const uint64_t row_bytes = mode >= 65 ? 6ull * d + 4ull * kp8 : 8ull * (d + k);
+  const uint64_t P = std::max<uint64_t>(1, std::min<uint64_t>(n, (3ull << 30) / row_bytes));
+  if (mode >= 65) {
+    GEEK_TRY(Aw.alloc(P * 3 * (uint64_t)d * 2, s));
+    GEEK_TRY(G.alloc(P * kp8 * 4, s));
+  } else {
+    if (dtype == 0) GEEK_TRY(x64.alloc(P * d * 8, s));
+    GEEK_TRY(G.alloc(P * k * 8, s));
+  }
   if (ev0) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev0), s));
   for (uint64_t r0 = 0; r0 < n; r0 += P) {
     const uint64_t rows = std::min(P, n - r0);
+    if (mode >= 65) {
+      if (mode == 66)
+        wide_split_local_kernel<<<grid_for(rows * 32, 256, 148 * 16), 256, 0, s>>>(
+            (const float*)X + r0 * d, rows, r0, d, mu_cls, cf.as<float>(), j0.as<int>(), tc_scal(mus, d),
+            Aw.as<__half>(), xn2.as<double>(), ovf);
+      else
+        wide_split_points_kernel<<<grid_for(rows * d, 256, 148 * 16), 256, 0, s>>>(
+            (const float*)X + r0 * d, rows, d, mu_cls, tc_scal(mus, d), Aw.as<__half>(), ovf);
+      GEEK_CHECK_LAUNCH();
+      GEEK_TRY(hgemm_nt_f32(Aw.ptr, Bw.ptr, G.as<float>(), (int)rows, (int)kp8, 3 * d, s));
+      GEEK_TRY(launch_top8<float>(G.as<float>(), rows, k, kp8, mode == 66 ? Et.as<double>() : c2.as<double>(),
+                                  mode == 66 ? j0.as<int>() : nullptr, k, ts.as<float>(), ti.as<int>(), r0, gw, s));
+      continue;
+    }
     const double* A;
     if (dtype == 0) {
       to_f64_kernel<<<grid_for(rows * d, 256), 256, 0, s>>>((const float*)X + r0 * d, rows * d, x64.as<double>());
@@ -1206,24 +1504,26 @@ static int assign_wide_screen(const void* X, int dtype, uint64_t n, int d, const
       A = (const double*)X + r0 * d;
     }
     GEEK_TRY(dgemm_nt(A, C, G.as<double>(), (int)rows, (int)k, d, s));
-    top8_rows_kernel<<<grid_for(rows * 32, 256), 256, 0, s>>>(G.as<double>(), rows, k, c2.as<double>(),
-                                                              ts.as<float>(), ti.as<int>(), r0);
-    GEEK_CHECK_LAUNCH();
+    GEEK_TRY(launch_top8<double>(G.as<double>(), rows, k, k, c2.as<double>(), nullptr, 0, ts.as<float>(), ti.as<int>(),
+                                 r0, nullptr, s));
   }
   if (ev1) GEEK_CHECK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev1), s));
+  const unsigned* ovf_cls = mode >= 65 ? ovf : nullptr;
   // one lane per point: d > 128 needs numpy's full pairwise recursion (the PwPlan), not one 8-accumulator leaf
   tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
-      (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu0.as<float>(), cmax, 64,
-      nullptr, labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+      (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu_cls, cmax, mode,
+      ovf_cls, labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull,
+      mode == 66 ? xn2.as<double>() : nullptr);
   GEEK_CHECK_LAUNCH();
   tc_recheck_kernel<<<148 * 8, 128, 0, s>>>((const float*)X, d, C, k, plan, ts.as<float>(), ti.as<int>(),
-                                            xn.as<float>(), cmax, 64, nullptr, amb.as<uint32_t>(), namb, labels, best);
+                                            xn.as<float>(), cmax, mode, ovf_cls, amb.as<uint32_t>(), namb, labels,
+                                            best);
   GEEK_CHECK_LAUNCH();
   full_scan_kernel<<<148 * 4, kFsThreads, sizeof(double) * d, s>>>((const float*)X, d, C, k, plan,
                                                                    full.as<uint32_t>(), nfull, labels, best);
   GEEK_CHECK_LAUNCH();
   if (stats) {
-    assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, nullptr, 64, stats);
+    assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, ovf_cls, mode, stats);
     GEEK_CHECK_LAUNCH();
   }
   return GEEK_OK;
@@ -1248,9 +1548,13 @@ uint64_t geek_assign_l2_workspace_size(uint64_t n, int d, uint64_t k) {
   // (top-4 values / centers of both column halves, |x'|, queues, |x'|^2
   // halves), the center operand images of the FP16 screen and its TF32x3
   // fallback (<= 320 KB per 192-center tile at d <= 128), the tile-local
-  // origin table, the wide-row transposed centers, and alignment slack
+  // origin table, the wide-row transposed centers, the wide-row GEMM chunk
+  // (<= 3 GB of operands and output, plus the FP16x3 center operand), and
+  // alignment slack
   const uint64_t nct = (k + 191) / 192, ntiles = (n + 127) / 128;
-  return n * 100 + nct * (330ull << 10) + k * (uint64_t)d * 24 + k * nct * 192 * 4 + ntiles * 80 + (4ull << 20);
+  const uint64_t wide = d > 128 ? std::min<uint64_t>(3ull << 30, n * (8ull * (d + k))) + k * (uint64_t)d * 10 +
+                                       k * k * 8 + n * 9 + (64ull << 10) : 0;
+  return n * 100 + nct * (330ull << 10) + k * (uint64_t)d * 24 + k * nct * 192 * 4 + ntiles * 80 + wide + (4ull << 20);
 }
 
 int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C, uint64_t k, int64_t* labels,
@@ -1341,7 +1645,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     else
       tc_classify_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(
           (const float*)X, n, d, C, k, plan, ts.as<float>(), ti.as<int>(), xn.as<float>(), mu_cls, cmax, nprod, ovf,
-          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull);
+          labels, best, amb.as<uint32_t>(), namb, full.as<uint32_t>(), nfull, nullptr);
     GEEK_CHECK_LAUNCH();
     if (d >= 8)
       tc_recheck8_kernel<<<148 * 16, 256, 0, s>>>((const float*)X, d, C, ts.as<float>(), ti.as<int>(), xn.as<float>(),
@@ -1362,13 +1666,10 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
   }
   const size_t scr_smem = sizeof(float) * ((size_t)d * (kScrP + 4) + kScrK * (kScrC + 4) + 3 * kScrP);
   const bool screened = dtype == 0 && k >= 4 && scr_smem <= 200 * 1024 && n < 0xFFFFFFFFull;
-  if (dtype == 0 && d > 128 && k >= 4 && n < 0xFFFFFFFFull) {
-    // float64 GEMM screen (cuBLAS DGEMM: 2 flops per element with FMA, where the
-    // exact numpy-order evaluation below needs 3 unfused ops per element)
-    const int st = assign_wide_screen(X, dtype, n, d, C, k, plan, labels, best, stats, ev_screen_begin,
-                                      ev_screen_end, s);
-    if (st == GEEK_OK) return GEEK_OK;
-    if (st != GEEK_ECUDA) return st;  // cuBLAS not loadable: the exact SIMT kernels below
+  if (dtype == 0 && d > 128 && k >= 4 && n < 0xFFFFFFFFull && cublas_available()) {
+    // tensor-core GEMM screen (FP16x3 over K = 3d, or the float64 DGEMM) + the
+    // exact classification; without cuBLAS the exact SIMT kernels below
+    return assign_wide_screen(X, dtype, n, d, C, k, plan, labels, best, stats, ev_screen_begin, ev_screen_end, s);
   }
   if (!screened && d > 128) {
     const uint64_t kpad = (k + 31) / 32 * 32;

@@ -225,6 +225,11 @@ int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lb
                       cudaStream_t s);
 // C[n][m] = A[n][kk] . B[m][kk]^T in float64 through cuBLAS (blas.cu, loaded at run time)
 int dgemm_nt(const double* A, const double* B, double* Cout, int n, int m, int kk, cudaStream_t s);
+bool cublas_available();
+// the same over f16 operands with fp32 accumulation and output (cublasGemmEx)
+int hgemm_nt_f32(const void* A, const void* B, float* Cout, int n, int m, int kk, cudaStream_t s);
+// mu and the FP16 scale {s, 2/s^2} of the wide-row FP16x3 screen (tc_screen.cu)
+int tc_wide_prepare(const double* C, uint64_t k, int d, Scratch& mu, unsigned long long* cmax_dev, cudaStream_t s);
 // {xscale, oscale} of a prepared screen (device memory inside its mu scratch)
 const float* tc_scal(const Scratch& mu, int d);
 // nprod 17 = tile-local FP16 (one product against each tile's origin center): see tc_screen.cu;

@@ -1143,6 +1143,22 @@ const float* tc_scal(const Scratch& mu, int d) {  // {xscale, oscale} inside the
   return reinterpret_cast<const float*>(reinterpret_cast<const char*>(mu.ptr) + ((size_t)d * 4 + 15) / 16 * 16 + 16);
 }
 
+// the FP16 scale of the wide-row screen (assign.cu, d > 128): the center
+// mean mu and {s, 2/s^2} exactly as the FP16 tcgen05 screen chooses them
+int tc_wide_prepare(const double* C, uint64_t k, int d, Scratch& mu, unsigned long long* cmax_dev, cudaStream_t s) {
+  GEEK_TRY(mu.alloc(((size_t)d * 4 + 15) / 16 * 16 + 32, s));
+  unsigned* amax = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(mu.ptr) + ((size_t)d * 4 + 15) / 16 * 16);
+  float* scal = const_cast<float*>(tc_scal(mu, d));
+  center_mean_kernel<<<grid_for(d, 128), 128, 0, s>>>(C, k, d, mu.as<float>());
+  GEEK_CHECK_LAUNCH();
+  GEEK_CHECK_CUDA(cudaMemsetAsync(amax, 0, 4, s));
+  center_absmax_kernel<<<grid_for(k * (uint64_t)d, 256, 148 * 4), 256, 0, s>>>(C, k, d, mu.as<float>(), amax);
+  GEEK_CHECK_LAUNCH();
+  screen_scale_kernel<<<1, 1, 0, s>>>(amax, 1, scal, cmax_dev);
+  GEEK_CHECK_LAUNCH();
+  return GEEK_OK;
+}
+
 int tc_screen_prepare(const double* C, uint64_t k, int d, int nprod, uint32_t lbo, uint32_t sbo, Scratch& img,
                       Scratch& c2, Scratch& mu, unsigned long long* cmax_dev, int& nct, float& xscale,
                       cudaStream_t s) {

@@ -271,6 +271,38 @@ def test_assign_wide_rows_vs_oracle(d, k, n):
     assert got.objective == obj
 
 
+@pytest.mark.parametrize("wide", ["66", "65", "64"])
+@pytest.mark.parametrize("case", ["gist", "offset", "overflow", "shuffled"])
+def test_assign_wide_screens_vs_oracle(case, wide, monkeypatch):
+    """d > 128 screens: the FP16x3 GEMM over K = 3d of rows centered at their
+    tile's origin center (default, mode 66) or at the center mean (65), and the
+    float64 DGEMM (GEEK_WIDE=64), then the exact classifier / recheck; near
+    ties (duplicate and near-duplicate centers), a large common offset,
+    shuffled rows (poor tile origins), and an f16 overflow (points far
+    outside the centers' scale: mode 0, every point scanned exactly)."""
+    monkeypatch.setenv("GEEK_WIDE", wide)
+    rng = np.random.default_rng(7)
+    d, k, n = (960, 150, 6000) if case == "gist" else (300, 64, 4000)
+    C = rng.random((k, d)) * 0.2 if case == "gist" else rng.standard_normal((k, d)) * 2 + (50.0 if case == "offset" else 0.0)
+    C[k - 1] = C[0]
+    C[5] = C[4] + 1e-7
+    lab0 = np.sort(rng.integers(0, k, n)) if case != "shuffled" else rng.integers(0, k, n)
+    X = (C[lab0] + rng.standard_normal((n, d)) * (0.02 if case == "gist" else 1.0)).astype(np.float32)
+    X[0] = C[0].astype(np.float32)
+    if case == "overflow":
+        X[::97] *= 1e4
+    got = G.assign(G.DenseData(X), [G.CentralVector("centroid", c) for c in C], "euclidean")
+    lab, best, radii, obj = O.assign_l2(X.astype(np.float64), C)
+    st = G.assignment.last_assign_stats()
+    assert np.array_equal(got.assignment, lab)
+    assert np.array_equal(got.radii, radii)
+    assert got.objective == obj
+    want_mode = 64 if wide == "64" else (0 if case == "overflow" else int(wide))
+    assert st["screen_mode"] == want_mode
+    if want_mode == 66 and case != "shuffled":
+        assert st["assign_rechecked"] < 0.2 * n
+
+
 @pytest.mark.parametrize("d,k,offset", [(128, 37, 0.0), (128, 300, 300.0), (16, 5, 0.0), (200, 64, 50.0)])
 def test_assign_screened_f32_vs_oracle(d, k, offset):
     """float32 data takes the float32 screen + exact recheck path."""
