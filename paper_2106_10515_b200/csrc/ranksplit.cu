@@ -200,6 +200,98 @@ __global__ void __launch_bounds__(256, 4) codes_kernel(const uint64_t* __restric
   }
 }
 
+// ---- group-level codes ---------------------------------------------------------
+// 64 consecutive fine bins of one table cover a contiguous rank range; when it
+// lies inside one bucket (most groups: a bucket holds ~n/t ids, a group
+// ~64 G) the group's slot is enough for all its ids.  mcode[q] = that slot as
+// 16 bits (0xFFFF: the group straddles a boundary, crosses a table, or t >
+// 65535), and codes_group_kernel reads it from an SMEM copy of the 8 tables'
+// groups: the per-id fine-bin code is fetched from L2 only in straddling groups.
+constexpr uint16_t kGroupNone = 0xFFFFu;
+
+__global__ void group_code_kernel(SplitGeom g, const uint32_t* fcnt, const uint32_t* fstart,
+                                  const uint32_t* tb_first, uint32_t nfbins, uint16_t* mcode, int kGroupShift) {
+  const uint32_t ng = (nfbins + (1u << kGroupShift) - 1) >> kGroupShift;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < ng; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f0 = (uint32_t)q << kGroupShift;
+    const uint32_t f1 = min(nfbins, f0 + (1u << kGroupShift)) - 1;  // last bin of the group
+    const int j0 = table_of_fine(tb_first, g.tb, f0), j1 = table_of_fine(tb_first, g.tb, f1);
+    uint16_t code = kGroupNone;
+    if (j0 == j1 && g.t < 0xFFFFull) {
+      const uint64_t r0 = (uint64_t)fstart[f0] - (uint64_t)j0 * g.n;
+      const uint64_t r1 = (uint64_t)fstart[f1] + fcnt[f1] - (uint64_t)j0 * g.n;  // one past the last rank
+      if (r1 == r0) code = 0;  // an empty group: never looked up
+      else if (slot_of_rank(r0, g.n, g.t) == slot_of_rank(r1 - 1, g.n, g.t)) code = (uint16_t)slot_of_rank(r0, g.n, g.t);
+    }
+    mcode[q] = code;
+  }
+}
+
+// codes_kernel with the table groups outside the id loop: per chunk of ids
+// and group of 8 tables the groups' codes [q_lo, q_lo + nq) sit in SMEM
+__global__ void __launch_bounds__(512, 2) codes_group_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                                            const uint2* __restrict__ cinfo,
+                                                            const uint32_t* __restrict__ fcode,
+                                                            const uint16_t* __restrict__ mcode,
+                                                            const uint32_t* __restrict__ tb_first, uint32_t nfbins,
+                                                            const uint32_t* __restrict__ sbase, uint32_t* sfill,
+                                                            uint32_t* codes, uint64_t* st_key, uint32_t* st_id,
+                                                            uint32_t* st_bin, uint64_t chunk, int kGroupShift) {
+  extern __shared__ uint16_t smc[];
+  const int tid = threadIdx.x;
+  const bool vec = (g.m % 4) == 0 && (g.c0 % 4) == 0;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < g.n; c0 += (uint64_t)gridDim.x * chunk) {
+    const uint64_t c1 = min(g.n, c0 + chunk);
+    for (int jb0 = 0; jb0 < g.tb; jb0 += 8) {
+      const int nt = min(8, g.tb - jb0);
+      const uint32_t flo = tb_first[jb0];
+      const uint32_t fhi = jb0 + nt < g.tb ? tb_first[jb0 + nt] : nfbins;
+      const uint32_t qlo = flo >> kGroupShift, qhi = (fhi + (1u << kGroupShift) - 1) >> kGroupShift;
+      __syncthreads();  // the previous group's readers are done
+      for (uint32_t q = qlo + tid; q < qhi; q += blockDim.x) smc[q - qlo] = mcode[q];
+      __syncthreads();
+      for (uint64_t i = c0 + tid; i < c1; i += blockDim.x) {
+        uint64_t key[8];
+        uint2 ci[8];
+        uint32_t f[8], code[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) key[u] = u < nt ? __ldg(keys + (uint64_t)(g.j0 + jb0 + u) * g.n + i) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          ci[u] = u < nt ? __ldg(cinfo + (uint64_t)(jb0 + u) * g.nc + coarse_of(key[u], g.cb)) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          f[u] = ci[u].y + static_cast<uint32_t>(((uint64_t)static_cast<uint32_t>((key[u] << g.cb) >> 32) * ci[u].x) >> 32);
+          if (ci[u].x == 0) {
+            code[u] = ci[u].y;  // (0, slot): whole cell inside one bucket
+          } else {
+            const uint16_t mc = smc[(f[u] >> kGroupShift) - qlo];
+            code[u] = mc != kGroupNone ? (uint32_t)mc : __ldg(fcode + f[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < nt && code[u] == GEEK_NONE) {
+            const uint32_t pos = sbase[f[u]] + atomicAdd(&sfill[f[u]], 1u);
+            st_key[pos] = key[u];
+            st_id[pos] = static_cast<uint32_t>(i);
+            st_bin[pos] = f[u];
+          }
+        uint32_t* crow = codes + i * (uint64_t)g.m + g.c0 + jb0;
+        if (vec && nt == 8) {
+          uint4* dst = reinterpret_cast<uint4*>(crow);
+          dst[0] = make_uint4(code[0], code[1], code[2], code[3]);
+          dst[1] = make_uint4(code[4], code[5], code[6], code[7]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u < nt) crow[u] = code[u];
+        }
+      }
+    }
+  }
+}
+
 // exact rank inside a small straddling bin by counting smaller (key, id)
 __global__ void __launch_bounds__(256) resolve_kernel(SplitGeom g, const uint64_t* __restrict__ st_key,
                                                       const uint32_t* __restrict__ st_id,
@@ -361,9 +453,42 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   GEEK_TRY(skey.alloc(nstage * 8, s));
   GEEK_TRY(sid.alloc(nstage * 4, s));
   GEEK_TRY(sbin.alloc(nstage * 4, s));
-  codes_kernel<<<grid_for(g.n, 256, 148 * 16), 256, 0, s>>>(
-      keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes,
-      skey.as<uint64_t>(), sid.as<uint32_t>(), sbin.as<uint32_t>());
+  // group-level codes when every 8-table group's group codes fit SMEM (<= 104 KB: two blocks per SM)
+  // groups of 2^gshift fine bins: the finest grouping whose SMEM copy fits (2^7 at n = 1e8:
+  // codes 31 -> 22 ms; 2^8 23 ms), GEEK_SPLIT_GROUPS=s forces 2^s, 0 the per-id fine-bin codes only
+  const char* gsel = getenv("GEEK_SPLIT_GROUPS");
+  auto group_smem = [&](int gs) {
+    size_t b = 0;
+    for (int jb0 = 0; jb0 < g.tb; jb0 += 8) {
+      const uint64_t flo = tbf[jb0], fhi = jb0 + 8 < g.tb ? tbf[jb0 + 8] : nfb;
+      b = std::max<size_t>(b, (size_t)(((fhi + (1u << gs) - 1) >> gs) - (flo >> gs) + 1) * 2);
+    }
+    return b;
+  };
+  int gshift = gsel ? atoi(gsel) : 6;
+  if (!gsel)
+    while (gshift < 10 && group_smem(gshift) > 104 * 1024) ++gshift;
+  const size_t gsmem = gshift > 0 ? group_smem(gshift) : 0;
+  if (getenv("GEEK_SPLIT_GROUPS_DBG")) fprintf(stderr, "[split] group shift %d: %zu bytes of SMEM\n", gshift, gsmem);
+  if (gshift > 0 && gsmem <= 104 * 1024) {
+    Scratch mcode;
+    const uint64_t ngrp = (nfb + (1u << gshift) - 1) >> gshift;
+    GEEK_TRY(mcode.alloc(ngrp * 2 + 16, s));
+    group_code_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
+                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, mcode.as<uint16_t>(),
+                                                           gshift);
+    GEEK_CHECK_LAUNCH();
+    GEEK_CHECK_CUDA(cudaFuncSetAttribute(codes_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+    const uint64_t chunk = 65536;
+    codes_group_kernel<<<(unsigned)std::min<uint64_t>((g.n + chunk - 1) / chunk, 148 * 2), 512, gsmem, s>>>(
+        keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), mcode.as<uint16_t>(), tbfirst.as<uint32_t>(),
+        (uint32_t)nfb, sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes, skey.as<uint64_t>(), sid.as<uint32_t>(),
+        sbin.as<uint32_t>(), chunk, gshift);
+  } else {
+    codes_kernel<<<grid_for(g.n, 256, 148 * 16), 256, 0, s>>>(
+        keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes,
+        skey.as<uint64_t>(), sid.as<uint32_t>(), sbin.as<uint32_t>());
+  }
   GEEK_CHECK_LAUNCH();
   if (nstage) {
     resolve_kernel<<<grid_for(nstage, 256, 148 * 16), 256, 0, s>>>(
