@@ -292,6 +292,100 @@ __global__ void __launch_bounds__(512, 2) codes_group_kernel(const uint64_t* __r
   }
 }
 
+// ---- group-level counting ------------------------------------------------------
+// Exact ranks are needed bin by bin only inside groups that straddle a bucket
+// boundary.  The group counts come from SMEM counters (one table per block,
+// flushed once per block), the fine-bin counts from L2 atomics only for keys
+// in straddling groups, and every other group's count is lumped into its
+// first fine bin -- the fine-bin scan then still yields every straddling
+// bin's exact rank start and every group's exact rank range.
+__global__ void __launch_bounds__(256) group_hist_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                                         const uint2* __restrict__ cinfo,
+                                                         const uint32_t* __restrict__ tb_first, uint32_t nfbins,
+                                                         int gs, uint32_t* gcnt) {
+  extern __shared__ uint32_t sg[];
+  const int jb = blockIdx.y, tid = threadIdx.x;
+  const uint32_t qlo = tb_first[jb] >> gs;
+  const uint32_t fend = jb + 1 < g.tb ? tb_first[jb + 1] : nfbins;
+  const uint32_t nq = ((fend + (1u << gs) - 1) >> gs) - qlo;
+  for (uint32_t q = tid; q < nq; q += 256) sg[q] = 0u;
+  __syncthreads();
+  const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
+  const uint2* ci = cinfo + (uint64_t)jb * g.nc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + tid; i0 < g.n; i0 += 4 * stride) {
+    uint64_t key[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) key[u] = i0 + u * stride < g.n ? __ldg(kj + i0 + u * stride) : 0ull;
+    uint2 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + coarse_of(key[u], g.cb));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * stride < g.n) {
+        const uint32_t frac = static_cast<uint32_t>((key[u] << g.cb) >> 32);
+        const uint32_t f = c[u].y + static_cast<uint32_t>(((uint64_t)frac * c[u].x) >> 32);
+        atomicAdd(&sg[(f >> gs) - qlo], 1u);
+      }
+  }
+  __syncthreads();
+  for (uint32_t q = tid; q < nq; q += 256) {
+    const uint32_t v = sg[q];
+    if (v) atomicAdd(&gcnt[qlo + q], v);
+  }
+}
+
+// gstr[q] = 1 when group q's rank range crosses a bucket boundary or a table
+__global__ void group_flag_kernel(SplitGeom g, const uint32_t* gcnt, const uint32_t* gstart,
+                                  const uint32_t* tb_first, uint32_t nfbins, int gs, uint32_t ngrp, uint8_t* gstr) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < ngrp; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f0 = (uint32_t)q << gs, f1 = min(nfbins, f0 + (1u << gs)) - 1;
+    const int j0 = table_of_fine(tb_first, g.tb, f0), j1 = table_of_fine(tb_first, g.tb, f1);
+    uint8_t st = 1;
+    if (j0 == j1) {
+      const uint32_t c = gcnt[q];
+      const uint64_t r0 = (uint64_t)gstart[q] - (uint64_t)j0 * g.n;
+      st = (c > 1 && slot_of_rank(r0, g.n, g.t) != slot_of_rank(r0 + c - 1, g.n, g.t)) ? 1 : 0;
+    }
+    gstr[q] = st;
+  }
+}
+
+// fine_hist_kernel for the keys of straddling groups only
+__global__ void __launch_bounds__(256) fine_hist_sel_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+                                                            const uint2* __restrict__ cinfo,
+                                                            const uint8_t* __restrict__ gstr, int gs,
+                                                            uint32_t* fcnt) {
+  const int jb = blockIdx.y;
+  const uint64_t* kj = keys + (uint64_t)(g.j0 + jb) * g.n;
+  const uint2* ci = cinfo + (uint64_t)jb * g.nc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < g.n; i0 += 4 * stride) {
+    uint64_t key[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) key[u] = i0 + u * stride < g.n ? __ldg(kj + i0 + u * stride) : 0ull;
+    uint2 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + coarse_of(key[u], g.cb));
+    uint32_t f[4];
+    uint8_t sel[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t frac = static_cast<uint32_t>((key[u] << g.cb) >> 32);
+      f[u] = c[u].y + static_cast<uint32_t>(((uint64_t)frac * c[u].x) >> 32);
+      sel[u] = i0 + u * stride < g.n ? __ldg(gstr + (f[u] >> gs)) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (sel[u]) atomicAdd(&fcnt[f[u]], 1u);
+  }
+}
+
+__global__ void group_lump_kernel(const uint32_t* gcnt, const uint8_t* gstr, uint32_t ngrp, int gs, uint32_t* fcnt) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < ngrp; q += (uint64_t)gridDim.x * blockDim.x)
+    if (!gstr[q]) fcnt[(uint32_t)q << gs] = gcnt[q];
+}
+
 // exact rank inside a small straddling bin by counting smaller (key, id)
 __global__ void __launch_bounds__(256) resolve_kernel(SplitGeom g, const uint64_t* __restrict__ st_key,
                                                       const uint32_t* __restrict__ st_id,
@@ -428,34 +522,9 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   GEEK_CHECK_CUDA(cudaMemcpyAsync(tbfirst.ptr, tbf.data(), g.tb * 4, cudaMemcpyHostToDevice, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(sfill.ptr, 0, nfb * 4, s));
   GEEK_CHECK_CUDA(cudaMemsetAsync(stats.ptr, 0, 32, s));
-  if (fcnt_in) {
-    GEEK_CHECK_CUDA(cudaMemcpyAsync(fcnt.ptr, fcnt_in, nfb * 4, cudaMemcpyDeviceToDevice, s));
-  } else {
-    GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
-    dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
-    fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), fcnt.as<uint32_t>());
-    GEEK_CHECK_LAUNCH();
-  }
-  GEEK_TRY(exclusive_scan_u32(fcnt.as<uint32_t>(), fstart.as<uint32_t>(), nfb, s));
-  straddle_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
-                                                      tbfirst.as<uint32_t>(), (uint32_t)nfb,
-                                                      scnt.as<uint32_t>(), fcode.as<uint32_t>(),
-                                                      stats.as<unsigned long long>());
-  GEEK_CHECK_LAUNCH();
-  uint64_t nstage = 0;
-  cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, cinfo.as<uint2>(), fcnt.as<uint32_t>(),
-                                                             fstart.as<uint32_t>(), ncell);
-  GEEK_CHECK_LAUNCH();
-  GEEK_TRY(exclusive_scan_u32(scnt.as<uint32_t>(), sbase.as<uint32_t>(), nfb, s, &nstage));
-  unsigned long long st[4] = {0, 0, 0, 0};
-  GEEK_CHECK_CUDA(cudaMemcpyAsync(st, stats.ptr, 24, cudaMemcpyDeviceToHost, s));
-  Scratch skey, sid, sbin;
-  GEEK_TRY(skey.alloc(nstage * 8, s));
-  GEEK_TRY(sid.alloc(nstage * 4, s));
-  GEEK_TRY(sbin.alloc(nstage * 4, s));
-  // group-level codes when every 8-table group's group codes fit SMEM (<= 104 KB: two blocks per SM)
-  // groups of 2^gshift fine bins: the finest grouping whose SMEM copy fits (2^7 at n = 1e8:
-  // codes 31 -> 22 ms; 2^8 23 ms), GEEK_SPLIT_GROUPS=s forces 2^s, 0 the per-id fine-bin codes only
+  // groups of 2^gshift fine bins: the finest grouping whose 8-table SMEM copy
+  // of group codes fits (2^7 at n = 1e8: codes 31 -> 22 ms; 2^8 23 ms);
+  // GEEK_SPLIT_GROUPS=s forces 2^s, 0 the per-bin paths only
   const char* gsel = getenv("GEEK_SPLIT_GROUPS");
   auto group_smem = [&](int gs) {
     size_t b = 0;
@@ -469,10 +538,72 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   if (!gsel)
     while (gshift < 10 && group_smem(gshift) > 104 * 1024) ++gshift;
   const size_t gsmem = gshift > 0 ? group_smem(gshift) : 0;
+  const bool grouped = gshift > 0 && gsmem <= 104 * 1024;
+  // group-level counting (not with counts from the projection): SMEM group
+  // counters, fine counts in straddling groups only (GEEK_SPLIT_GCOUNT=0: every key's fine count)
+  const char* gcs = getenv("GEEK_SPLIT_GCOUNT");
+  const bool gcount = grouped && !fcnt_in && !(gcs && atoi(gcs) == 0);
+  const uint64_t ngrp = grouped ? (nfb + (1u << gshift) - 1) >> gshift : 0;
+  Scratch gcnt, gstart, gstr;
+  if (fcnt_in) {
+    GEEK_CHECK_CUDA(cudaMemcpyAsync(fcnt.ptr, fcnt_in, nfb * 4, cudaMemcpyDeviceToDevice, s));
+  } else if (gcount) {
+    size_t hs = 0;  // SMEM of the largest table's groups
+    for (int jb = 0; jb < g.tb; ++jb) {
+      const uint64_t fe = jb + 1 < g.tb ? tbf[jb + 1] : nfb;
+      hs = std::max<size_t>(hs, (size_t)(((fe + (1u << gshift) - 1) >> gshift) - (tbf[jb] >> gshift)) * 4);
+    }
+    GEEK_TRY(gcnt.alloc(ngrp * 4, s));
+    GEEK_TRY(gstart.alloc(ngrp * 4, s));
+    GEEK_TRY(gstr.alloc(ngrp, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(gcnt.ptr, 0, ngrp * 4, s));
+    if (hs > 48 * 1024)
+      GEEK_CHECK_CUDA(cudaFuncSetAttribute(group_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
+    dim3 gh(grid_for(g.n, 256, 148 * 4), g.tb);
+    group_hist_kernel<<<gh, 256, hs, s>>>(keys, g, cinfo.as<uint2>(), tbfirst.as<uint32_t>(), (uint32_t)nfb, gshift,
+                                          gcnt.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    GEEK_TRY(exclusive_scan_u32(gcnt.as<uint32_t>(), gstart.as<uint32_t>(), ngrp, s));
+    group_flag_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(g, gcnt.as<uint32_t>(), gstart.as<uint32_t>(),
+                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, gshift,
+                                                           (uint32_t)ngrp, gstr.as<uint8_t>());
+    GEEK_CHECK_LAUNCH();
+    GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
+    dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
+    fine_hist_sel_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), gstr.as<uint8_t>(), gshift,
+                                            fcnt.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+    group_lump_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(gcnt.as<uint32_t>(), gstr.as<uint8_t>(), (uint32_t)ngrp,
+                                                           gshift, fcnt.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  } else {
+    GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
+    dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
+    fine_hist_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), fcnt.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  }
+  GEEK_TRY(exclusive_scan_u32(fcnt.as<uint32_t>(), fstart.as<uint32_t>(), nfb, s));
+  straddle_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
+                                                      tbfirst.as<uint32_t>(), (uint32_t)nfb,
+                                                      scnt.as<uint32_t>(), fcode.as<uint32_t>(),
+                                                      stats.as<unsigned long long>());
+  GEEK_CHECK_LAUNCH();
+  uint64_t nstage = 0;
+  if (!gcount) {  // (lumped groups hide the rank starts of bins inside them: no whole-cell shortcut then)
+    cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, cinfo.as<uint2>(), fcnt.as<uint32_t>(),
+                                                               fstart.as<uint32_t>(), ncell);
+    GEEK_CHECK_LAUNCH();
+  }
+  GEEK_TRY(exclusive_scan_u32(scnt.as<uint32_t>(), sbase.as<uint32_t>(), nfb, s, &nstage));
+  unsigned long long st[4] = {0, 0, 0, 0};
+  GEEK_CHECK_CUDA(cudaMemcpyAsync(st, stats.ptr, 24, cudaMemcpyDeviceToHost, s));
+  Scratch skey, sid, sbin;
+  GEEK_TRY(skey.alloc(nstage * 8, s));
+  GEEK_TRY(sid.alloc(nstage * 4, s));
+  GEEK_TRY(sbin.alloc(nstage * 4, s));
   if (getenv("GEEK_SPLIT_GROUPS_DBG")) fprintf(stderr, "[split] group shift %d: %zu bytes of SMEM\n", gshift, gsmem);
-  if (gshift > 0 && gsmem <= 104 * 1024) {
+  if (grouped) {  // group-level codes: the 8-table SMEM copy of the group codes (<= 104 KB: two blocks per SM)
     Scratch mcode;
-    const uint64_t ngrp = (nfb + (1u << gshift) - 1) >> gshift;
     GEEK_TRY(mcode.alloc(ngrp * 2 + 16, s));
     group_code_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
                                                            tbfirst.as<uint32_t>(), (uint32_t)nfb, mcode.as<uint16_t>(),
