@@ -229,7 +229,8 @@ __global__ void group_code_kernel(SplitGeom g, const uint32_t* fcnt, const uint3
 
 // codes_kernel with the table groups outside the id loop: per chunk of ids
 // and group of 8 tables the groups' codes [q_lo, q_lo + nq) sit in SMEM
-__global__ void __launch_bounds__(512, 2) codes_group_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) codes_group_kernel(const uint64_t* __restrict__ keys, SplitGeom g,
                                                             const uint2* __restrict__ cinfo,
                                                             const uint32_t* __restrict__ fcode,
                                                             const uint16_t* __restrict__ mcode,
@@ -378,6 +379,19 @@ __global__ void __launch_bounds__(256) fine_hist_sel_kernel(const uint64_t* __re
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (sel[u]) atomicAdd(&fcnt[f[u]], 1u);
+  }
+}
+
+// every fine bin of a lumped counting group (its ids all in one bucket) takes
+// the group's slot: the empty-looking bins behind the lump are looked up by
+// ids of a straddling code group that contains the counting group
+__global__ void group_fill_kernel(SplitGeom g, const uint32_t* gstart, const uint32_t* gcnt, const uint8_t* gstr,
+                                  const uint32_t* tb_first, uint32_t nfbins, int cs, uint32_t* fcode) {
+  for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < nfbins; f += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = (uint32_t)f >> cs;
+    if (gstr[q] || gcnt[q] == 0) continue;
+    const int jb = table_of_fine(tb_first, g.tb, (uint32_t)f);
+    fcode[f] = slot_of_rank((uint64_t)gstart[q] - (uint64_t)jb * g.n, g.n, g.t);
   }
 }
 
@@ -534,16 +548,28 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
     }
     return b;
   };
+  // SMEM budget of the code groups: 200 KB (one 1024-thread block per SM: 2^6
+  // fine bins per group at n = 1e8, codes 20.4 ms) or, GEEK_SPLIT_BIG=0, 104 KB
+  // (two 512-thread blocks: 2^7, 21.4 ms)
+  const char* bsel = getenv("GEEK_SPLIT_BIG");
+  const bool big = !(bsel && atoi(bsel) == 0);
+  const size_t gcap = big ? 200 * 1024 : 104 * 1024;
   int gshift = gsel ? atoi(gsel) : 6;
   if (!gsel)
-    while (gshift < 10 && group_smem(gshift) > 104 * 1024) ++gshift;
+    while (gshift < 10 && group_smem(gshift) > gcap) ++gshift;
   const size_t gsmem = gshift > 0 ? group_smem(gshift) : 0;
-  const bool grouped = gshift > 0 && gsmem <= 104 * 1024;
+  const bool grouped = gshift > 0 && gsmem <= gcap;
   // group-level counting (not with counts from the projection): SMEM group
   // counters, fine counts in straddling groups only (GEEK_SPLIT_GCOUNT=0: every key's fine count)
   const char* gcs = getenv("GEEK_SPLIT_GCOUNT");
   const bool gcount = grouped && !fcnt_in && !(gcs && atoi(gcs) == 0);
-  const uint64_t ngrp = grouped ? (nfb + (1u << gshift) - 1) >> gshift : 0;
+  // counting groups: 2^cshift fine bins (finer than the code groups: fewer keys in
+  // straddling groups; the code groups' rank ranges stay exact because every
+  // code-group boundary is a counting-group boundary; 2^5 at n = 1e8: group
+  // counts 7.4 ms + straddling fine counts 5.6 ms, against 21 ms of per-key atomics)
+  const char* ccs = getenv("GEEK_SPLIT_CSHIFT");
+  const int cshift = std::min(gshift, ccs ? std::max(1, atoi(ccs)) : 5);
+  const uint64_t ngrp = grouped ? (nfb + (1u << cshift) - 1) >> cshift : 0;
   Scratch gcnt, gstart, gstr;
   if (fcnt_in) {
     GEEK_CHECK_CUDA(cudaMemcpyAsync(fcnt.ptr, fcnt_in, nfb * 4, cudaMemcpyDeviceToDevice, s));
@@ -551,7 +577,7 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
     size_t hs = 0;  // SMEM of the largest table's groups
     for (int jb = 0; jb < g.tb; ++jb) {
       const uint64_t fe = jb + 1 < g.tb ? tbf[jb + 1] : nfb;
-      hs = std::max<size_t>(hs, (size_t)(((fe + (1u << gshift) - 1) >> gshift) - (tbf[jb] >> gshift)) * 4);
+      hs = std::max<size_t>(hs, (size_t)(((fe + (1u << cshift) - 1) >> cshift) - (tbf[jb] >> cshift)) * 4);
     }
     GEEK_TRY(gcnt.alloc(ngrp * 4, s));
     GEEK_TRY(gstart.alloc(ngrp * 4, s));
@@ -560,21 +586,21 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
     if (hs > 48 * 1024)
       GEEK_CHECK_CUDA(cudaFuncSetAttribute(group_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
     dim3 gh(grid_for(g.n, 256, 148 * 4), g.tb);
-    group_hist_kernel<<<gh, 256, hs, s>>>(keys, g, cinfo.as<uint2>(), tbfirst.as<uint32_t>(), (uint32_t)nfb, gshift,
+    group_hist_kernel<<<gh, 256, hs, s>>>(keys, g, cinfo.as<uint2>(), tbfirst.as<uint32_t>(), (uint32_t)nfb, cshift,
                                           gcnt.as<uint32_t>());
     GEEK_CHECK_LAUNCH();
     GEEK_TRY(exclusive_scan_u32(gcnt.as<uint32_t>(), gstart.as<uint32_t>(), ngrp, s));
     group_flag_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(g, gcnt.as<uint32_t>(), gstart.as<uint32_t>(),
-                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, gshift,
+                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, cshift,
                                                            (uint32_t)ngrp, gstr.as<uint8_t>());
     GEEK_CHECK_LAUNCH();
     GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
     dim3 gf(grid_for(g.n, 256, 148 * 8), g.tb);
-    fine_hist_sel_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), gstr.as<uint8_t>(), gshift,
+    fine_hist_sel_kernel<<<gf, 256, 0, s>>>(keys, g, cinfo.as<uint2>(), gstr.as<uint8_t>(), cshift,
                                             fcnt.as<uint32_t>());
     GEEK_CHECK_LAUNCH();
     group_lump_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(gcnt.as<uint32_t>(), gstr.as<uint8_t>(), (uint32_t)ngrp,
-                                                           gshift, fcnt.as<uint32_t>());
+                                                           cshift, fcnt.as<uint32_t>());
     GEEK_CHECK_LAUNCH();
   } else {
     GEEK_CHECK_CUDA(cudaMemsetAsync(fcnt.ptr, 0, nfb * 4, s));
@@ -589,6 +615,12 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
                                                       stats.as<unsigned long long>());
   GEEK_CHECK_LAUNCH();
   uint64_t nstage = 0;
+  if (gcount && cshift < gshift) {
+    group_fill_kernel<<<grid_for(nfb, 256), 256, 0, s>>>(g, gstart.as<uint32_t>(), gcnt.as<uint32_t>(), gstr.as<uint8_t>(),
+                                                          tbfirst.as<uint32_t>(), (uint32_t)nfb, cshift,
+                                                          fcode.as<uint32_t>());
+    GEEK_CHECK_LAUNCH();
+  }
   if (!gcount) {  // (lumped groups hide the rank starts of bins inside them: no whole-cell shortcut then)
     cell_shortcut_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, cinfo.as<uint2>(), fcnt.as<uint32_t>(),
                                                                fstart.as<uint32_t>(), ncell);
@@ -604,17 +636,27 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   if (getenv("GEEK_SPLIT_GROUPS_DBG")) fprintf(stderr, "[split] group shift %d: %zu bytes of SMEM\n", gshift, gsmem);
   if (grouped) {  // group-level codes: the 8-table SMEM copy of the group codes (<= 104 KB: two blocks per SM)
     Scratch mcode;
-    GEEK_TRY(mcode.alloc(ngrp * 2 + 16, s));
-    group_code_kernel<<<grid_for(ngrp, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
-                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, mcode.as<uint16_t>(),
-                                                           gshift);
+    const uint64_t ncg = (nfb + (1u << gshift) - 1) >> gshift;
+    GEEK_TRY(mcode.alloc(ncg * 2 + 16, s));
+    group_code_kernel<<<grid_for(ncg, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
+                                                          tbfirst.as<uint32_t>(), (uint32_t)nfb, mcode.as<uint16_t>(),
+                                                          gshift);
     GEEK_CHECK_LAUNCH();
-    GEEK_CHECK_CUDA(cudaFuncSetAttribute(codes_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
     const uint64_t chunk = 65536;
-    codes_group_kernel<<<(unsigned)std::min<uint64_t>((g.n + chunk - 1) / chunk, 148 * 2), 512, gsmem, s>>>(
-        keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), mcode.as<uint16_t>(), tbfirst.as<uint32_t>(),
-        (uint32_t)nfb, sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes, skey.as<uint64_t>(), sid.as<uint32_t>(),
-        sbin.as<uint32_t>(), chunk, gshift);
+    const unsigned nchunk = (unsigned)((g.n + chunk - 1) / chunk);
+#define GEEK_CODES_GROUP(NT, MINB)                                                                                 \
+  GEEK_CHECK_CUDA(cudaFuncSetAttribute(codes_group_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                       (int)gsmem));                                                                \
+  codes_group_kernel<NT, MINB><<<std::min(nchunk, 148u * MINB), NT, gsmem, s>>>(                                   \
+      keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), mcode.as<uint16_t>(), tbfirst.as<uint32_t>(), (uint32_t)nfb, \
+      sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes, skey.as<uint64_t>(), sid.as<uint32_t>(), sbin.as<uint32_t>(), \
+      chunk, gshift)
+    if (gsmem > 104 * 1024) {
+      GEEK_CODES_GROUP(1024, 1);
+    } else {
+      GEEK_CODES_GROUP(512, 2);
+    }
+#undef GEEK_CODES_GROUP
   } else {
     codes_kernel<<<grid_for(g.n, 256, 148 * 16), 256, 0, s>>>(
         keys, g, cinfo.as<uint2>(), fcode.as<uint32_t>(), sbase.as<uint32_t>(), sfill.as<uint32_t>(), codes,
