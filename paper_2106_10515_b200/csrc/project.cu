@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
     }
     const float* st = sX + (q % kPsStages) * kPsStageFloats + (warp * 32 + rr) * kPsLdp + kr;
     const double* sa = sA + (kc * 32 + kr) * LDA + rr;
-#pragma unroll 2
+#pragma unroll
     for (int ks = 0; ks < 32; ks += 4) {
       double a[4], b[NT];
 #pragma unroll
