@@ -249,7 +249,12 @@ __global__ void __launch_bounds__(NT, MINB) codes_group_kernel(const uint64_t* _
       const uint32_t fhi = jb0 + nt < g.tb ? tb_first[jb0 + nt] : nfbins;
       const uint32_t qlo = flo >> kGroupShift, qhi = (fhi + (1u << kGroupShift) - 1) >> kGroupShift;
       __syncthreads();  // the previous group's readers are done
-      for (uint32_t q = qlo + tid; q < qhi; q += blockDim.x) smc[q - qlo] = mcode[q];
+      {  // 16-byte copies from the 8-aligned group below qlo (mcode is padded to whole uint4s)
+        const uint32_t q8 = qlo & ~7u, n16 = (qhi - q8 + 7) >> 3;
+        const uint4* srcv = reinterpret_cast<const uint4*>(mcode + q8);
+        uint4* dstv = reinterpret_cast<uint4*>(smc);
+        for (uint32_t v = tid; v < n16; v += blockDim.x) dstv[v] = __ldg(srcv + v);
+      }
       __syncthreads();
       for (uint64_t i = c0 + tid; i < c1; i += blockDim.x) {
         uint64_t key[8];
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(NT, MINB) codes_group_kernel(const uint64_t* _
           if (ci[u].x == 0) {
             code[u] = ci[u].y;  // (0, slot): whole cell inside one bucket
           } else {
-            const uint16_t mc = smc[(f[u] >> kGroupShift) - qlo];
+            const uint16_t mc = smc[(f[u] >> kGroupShift) - (qlo & ~7u)];
             code[u] = mc != kGroupNone ? (uint32_t)mc : __ldg(fcode + f[u]);
           }
         }
@@ -544,7 +549,7 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
     size_t b = 0;
     for (int jb0 = 0; jb0 < g.tb; jb0 += 8) {
       const uint64_t flo = tbf[jb0], fhi = jb0 + 8 < g.tb ? tbf[jb0 + 8] : nfb;
-      b = std::max<size_t>(b, (size_t)(((fhi + (1u << gs) - 1) >> gs) - (flo >> gs) + 1) * 2);
+      b = std::max<size_t>(b, (size_t)((((fhi + (1u << gs) - 1) >> gs) - ((flo >> gs) & ~7ull) + 15) & ~7ull) * 2);
     }
     return b;
   };
@@ -637,7 +642,7 @@ static int rank_split_batch(const uint64_t* keys, SplitGeom g, uint32_t* codes, 
   if (grouped) {  // group-level codes: the 8-table SMEM copy of the group codes (<= 104 KB: two blocks per SM)
     Scratch mcode;
     const uint64_t ncg = (nfb + (1u << gshift) - 1) >> gshift;
-    GEEK_TRY(mcode.alloc(ncg * 2 + 16, s));
+    GEEK_TRY(mcode.alloc((ncg + 16) * 2, s));  // + slack: the SMEM copies read whole uint4s
     group_code_kernel<<<grid_for(ncg, 256), 256, 0, s>>>(g, fcnt.as<uint32_t>(), fstart.as<uint32_t>(),
                                                           tbfirst.as<uint32_t>(), (uint32_t)nfb, mcode.as<uint16_t>(),
                                                           gshift);
