@@ -929,11 +929,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
     // ever inserted.  Any U is exact: a list that ends with an entry (value U,
     // center -1) inside the window reads as an overflow (full scan), and the
     // classifier never takes a -1 winner.
+    // |c'|max for the start bounds, read once (the prepare kernels wrote it before this launch)
+    const float cn_bound = bnd ? (float)__longlong_as_double((long long)__ldg(P.cmax)) : 0.f;
     auto start_bound = [&](uint32_t t) -> float {
       const int r = (warp & 3) * 32 + lane;
       const float2 h0 = Upart[((t & 1) * 128 + r) * 2], h1 = Upart[((t & 1) * 128 + r) * 2 + 1];
       const float xpp = h0.x + h1.x, xp = h0.y + h1.y;
-      const float cn = (float)__longlong_as_double((long long)P.cmax[0]);
+      const float cn = cn_bound;
       // twice the classifier's window (FP16: one product, error ~ |x''||c'| 2^-9;
       // FP16x3: ~ |x'||c'| (2^-19 + 6 d 2^-23)), plus the float32 error of xpp - xp
       const float win = Cfg::kLocal ? 2.2f * (1.953125e-3f * sqrtf(xpp) * cn + 1e-5f * cn * cn) + 1e-4f * xp
