@@ -95,7 +95,7 @@ struct TcCfg {
   // buffer), so the next tile's A lands while the MMAs still read this one's
   // (NPROD = 16 double-buffered measured 0.7-1.3 ms slower per 20M points:
   // the A writes then contend with the running MMAs)
-  static constexpr int kABuf = (NPROD == 1 || NPROD == 17) ? 2 : 1;
+  static constexpr int kABuf = (NPROD == 1 || NPROD == 17 || NPROD == 16) ? 2 : 1;
   static constexpr int kHalfStage = kSlices * kTcBSliceBytes;     // one part of a B stage
   static constexpr int kStageBytes = kParts * kHalfStage;
   static constexpr int kStages = 4;
@@ -103,6 +103,12 @@ struct TcCfg {
   static constexpr uint32_t kTmemA = 2 * kTcN;                   // TMEM A operand after the two accumulators
   static constexpr uint32_t kTmemAStride = kF16 ? 64 : 128;      // TMEM columns of one A buffer
   static constexpr size_t kSmemFixed = (size_t)kABuf * kABytes + (size_t)kStages * kStageBytes + 40 * 8;
+  // NPROD = 16: four dedicated loader warps (12-15, one per TMEM lane group)
+  // convert the point tiles, so the 8 epilogue warps only drain accumulators
+  // (warps 10-11 idle: the loaders form a whole warpgroup)
+  static constexpr bool kLoader = NPROD == 16;
+  static constexpr int kLoaderWarps = 8;  // two per TMEM lane group (row halves of 16 dims per chunk)
+  static constexpr int kThreads = kLoader ? (12 + kLoaderWarps) * 32 : 320;
 };
 
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
@@ -251,6 +257,15 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const float* v) {
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
       "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
       "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_st16u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 
@@ -404,7 +419,7 @@ constexpr int kTcEpiThreads = kTcEpiWarps * 32;
 constexpr int kTcThreads = kTcEpiThreads + 64;  // + MMA warp + TMA warp
 
 template <int NPROD>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams P) {
+__global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(const TcParams P) {
   using Cfg = TcCfg<NPROD>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* A = smem;                                           // kABuf x kABytes
@@ -420,6 +435,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
   uint64_t* aempty = bars + 28;             // [kABuf][4] point-tile chunk no longer read (MMA commit)
   uint64_t* c2full = bars + 36;             // resident |c'|^2 slices loaded (TMA tx)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 37);
+  uint64_t* upf = bars + 38;                // [2] (loader warps) a tile's |x''|^2, |x'|^2 are in Upart
   static_assert(Cfg::kStages <= 8 && Cfg::kABuf <= 2, "barrier map");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -437,9 +453,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       mbar_init(&acce[b], kTcEpiWarps);  // one arrival per epilogue warp
     }
     for (int b = 0; b < Cfg::kABuf * 4; ++b) {
-      mbar_init(&afull[b], kTcEpiWarps);
+      mbar_init(&afull[b], Cfg::kLoader ? Cfg::kLoaderWarps : kTcEpiWarps);  // one arrival per writing warp
       mbar_init(&aempty[b], 1);
     }
+    for (int b = 0; b < 2; ++b) mbar_init(&upf[b], Cfg::kLoaderWarps * 32);  // every loader thread
     mbar_init(c2full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -628,6 +645,151 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
         P.dbg[blockIdx.x * 8 + 4] = (unsigned long long)w_issue;
         P.dbg[blockIdx.x * 8 + 5] = (unsigned long long)w_c2;
         P.dbg[blockIdx.x * 8 + 6] = (unsigned long long)w_accf;
+      }
+    }
+  } else if (Cfg::kLoader && warp >= kTcEpiWarps + 2) {
+    // ---------------- warps 12-15: point-tile loaders (NPROD = 16) ----------------
+    // thread l of warp 12 + g owns row 32g + l (its TMEM lane) of every point
+    // tile: 32-dim chunks of the row are loaded one chunk ahead (the next
+    // tile's first chunk during this tile's last), converted to the scaled
+    // f16 hi (TMEM, one tcgen05.st of 16 columns) and lo (SMEM K-major) parts,
+    // with |x'|^2 per row half for the classifier and, with tile origins,
+    // |x - c'_j0|^2 for the epilogue's start bound (Upart, signalled on upf)
+    if constexpr (Cfg::kLoader) {
+      if (warp >= 12) {
+        const int lg = (warp - 12) & 3, hh = (warp - 12) >> 2, row = lg * 32 + lane;
+        const bool bnd16 = P.j0 != nullptr;
+        const bool getenv_sleep_l = P.sleepwait != 0;
+        auto tile_p0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM; };
+        // this thread's dims of chunk kc: kc*32 + 16 hh + 0..15
+        auto load_chunk = [&](uint32_t t, int kc, float4 (&dst)[4]) {
+          const uint64_t i = tile_p0(t) + row;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int e0 = kc * 32 + hh * 16 + 4 * v;
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < my_tiles && i < P.n && kc < nck) {
+              if (P.d == kTcKmax) {
+                x = __ldg(reinterpret_cast<const float4*>(P.X + i * kTcKmax + e0));
+              } else {
+                const float* xr = P.X + i * P.d;
+                if (e0 < P.d) x.x = xr[e0];
+                if (e0 + 1 < P.d) x.y = xr[e0 + 1];
+                if (e0 + 2 < P.d) x.z = xr[e0 + 2];
+                if (e0 + 3 < P.d) x.w = xr[e0 + 3];
+              }
+            }
+            dst[v] = x;
+          }
+        };
+        // origin coordinates 4 lane .. 4 lane + 3 of the current tile (og) and the
+        // next (ogn, loaded mid-tile from the index fetched at the tile's start)
+        float og[4] = {0.f, 0.f, 0.f, 0.f}, ogn[4] = {0.f, 0.f, 0.f, 0.f};
+        auto tile_j0 = [&](uint32_t t) -> int {
+          return (bnd16 && t < my_tiles) ? __ldg(P.j0 + blockIdx.x + (uint64_t)t * gridDim.x) : 0;
+        };
+        auto load_origin = [&](int j, float (&dst)[4]) {
+          const float* org = P.cf + (uint64_t)j * P.d;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) dst[r] = 4 * lane + r < P.d ? __ldg(org + 4 * lane + r) : 0.f;
+        };
+        float4 xa0[4], xa1[4];
+        load_chunk(0, 0, xa0);
+        if (bnd16 && my_tiles > 0) load_origin(tile_j0(0), og);
+        for (uint32_t t = 0; t < my_tiles; ++t) {
+          const uint64_t p0 = tile_p0(t);
+          const bool valid = p0 + row < P.n;
+          const int ab = (int)(t & 1);                 // A double buffer: tile t+1 is written while the MMAs read tile t
+          const uint32_t epar = ((t >> 1) & 1) ^ 1u;
+          float xs[4] = {0.f, 0.f, 0.f, 0.f};  // |x'|^2 chains over this row half
+          float xq[4] = {0.f, 0.f, 0.f, 0.f};  // |x''|^2 chains
+          bool big = false;
+          const int jn = tile_j0(t + 1);
+          if (hh == 0) {  // the next tile's rows towards L2 while this one converts
+            const uint64_t nrow = tile_p0(t + 1) + row;
+            if (t + 1 < my_tiles && nrow < P.n) {
+              const char* base = reinterpret_cast<const char*>(P.X + nrow * (uint64_t)P.d);
+              for (int b = 0; b < P.d * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
+            }
+          }
+#pragma unroll
+          for (int kc = 0; kc < 4; ++kc) {
+            float4 (&cur)[4] = (kc & 1) ? xa1 : xa0;
+            float4 (&nxt)[4] = (kc & 1) ? xa0 : xa1;
+            if (kc < 3) load_chunk(t, kc + 1, nxt);
+            else load_chunk(t + 1, 0, nxt);
+            if (kc == 1 && bnd16 && t + 1 < my_tiles) load_origin(jn, ogn);
+            if (kc >= nck) continue;
+            uint32_t hp[8];
+            uint2 lo[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int e0 = kc * 32 + hh * 16 + 4 * v;
+              float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (P.d == kTcKmax) {
+                m4 = __ldg(reinterpret_cast<const float4*>(P.mu + e0));
+              } else {
+                if (e0 < P.d) m4.x = __ldg(P.mu + e0);
+                if (e0 + 1 < P.d) m4.y = __ldg(P.mu + e0 + 1);
+                if (e0 + 2 < P.d) m4.z = __ldg(P.mu + e0 + 2);
+                if (e0 + 3 < P.d) m4.w = __ldg(P.mu + e0 + 3);
+              }
+              const float4 x = cur[v];
+              const float x0 = valid ? x.x - m4.x : 0.f, x1 = valid ? x.y - m4.y : 0.f;
+              const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
+              xs[v] = fmaf(x0, x0, xs[v]);
+              xs[v] = fmaf(x1, x1, xs[v]);
+              xs[v] = fmaf(x2, x2, xs[v]);
+              xs[v] = fmaf(x3, x3, xs[v]);
+              if (bnd16) {  // element e0 + j sits in lane e0 / 4 = 8 kc + 4 hh + v, slot j
+                const int sl = 8 * kc + 4 * hh + v;
+                const float z0 = x0 - __shfl_sync(0xffffffffu, og[0], sl);
+                const float z1 = x1 - __shfl_sync(0xffffffffu, og[1], sl);
+                const float z2 = x2 - __shfl_sync(0xffffffffu, og[2], sl);
+                const float z3 = x3 - __shfl_sync(0xffffffffu, og[3], sl);
+                xq[v] = fmaf(z0, z0, xq[v]);
+                xq[v] = fmaf(z1, z1, xq[v]);
+                xq[v] = fmaf(z2, z2, xq[v]);
+                xq[v] = fmaf(z3, z3, xq[v]);
+              }
+              const float y0 = x0 * xscale, y1 = x1 * xscale, y2 = x2 * xscale, y3 = x3 * xscale;
+              big |= fmaxf(fmaxf(fabsf(y0), fabsf(y1)), fmaxf(fabsf(y2), fabsf(y3))) > 32768.f;
+              const __half2 g01 = __floats2half2_rn(y0, y1), g23 = __floats2half2_rn(y2, y3);
+              const float2 b01 = __half22float2(g01), b23 = __half22float2(g23);
+              const __half2 l01 = __floats2half2_rn(y0 - b01.x, y1 - b01.y);
+              const __half2 l23 = __floats2half2_rn(y2 - b23.x, y3 - b23.y);
+              hp[2 * v] = *reinterpret_cast<const uint32_t*>(&g01);
+              hp[2 * v + 1] = *reinterpret_cast<const uint32_t*>(&g23);
+              lo[v] = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+            }
+            if (getenv_sleep_l) mbar_wait_sleep(&aempty[ab * 4 + kc], epar);  // tile t-2's MMAs on this chunk are done
+            else mbar_wait(&aempty[ab * 4 + kc], epar);
+            fence_after();
+            if (P.prof != 3 && (P.prof < 5 || P.prof > 7)) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const int e0 = kc * 32 + hh * 16 + 4 * v;
+                const uint32_t offh = (e0 >> 4) * kTcSliceBytes + core_off_b(row, (e0 & 15) * 2, P.lbo, P.sbo);
+                *reinterpret_cast<uint2*>(A + ab * Cfg::kABytes + offh) = lo[v];
+              }
+              tc_st8(tmem + ((uint32_t)(lg * 32) << 16) + Cfg::kTmemA + ab * Cfg::kTmemAStride + kc * 16 + hh * 8, hp);
+            }
+            tc_wait_st();
+            fence_before();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[ab * 4 + kc]);  // the warp's A writes are all done
+          }
+          if (big) atomicOr(P.ovf, 1u);
+          if (P.xpart && valid) P.xpart[(p0 + row) * 2 + hh] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
+          if (bnd16) {
+            Upart[((t & 1) * 128 + row) * 2 + hh] =
+                make_float2((xq[0] + xq[1]) + (xq[2] + xq[3]), (xs[0] + xs[1]) + (xs[2] + xs[3]));
+            mbar_arrive(&upf[t & 1]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) og[r] = ogn[r];
+          }
+        }
       }
     }
   } else {  // ---------------- warps 0-7: point tiles + epilogue ----------------
@@ -944,12 +1106,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       const float us = xpp - xp + 4.f * win + 1.f;  // s units
       return us / oscale;                            // accumulator units (v = s / oscale)
     };
-    if (my_tiles > 0) {
+    if (my_tiles > 0 && !Cfg::kLoader) {
       load_regs(0);
       store_chunks(0);
     }
     for (uint32_t t = 0; t < my_tiles; ++t) {
-      const bool more = t + 1 < my_tiles;
+      const bool more = t + 1 < my_tiles && !Cfg::kLoader;  // (the loader warps load the point tiles)
       if (more) load_regs(t + 1);  // in flight during the epilogues below
       if (Cfg::kLocal) {  // the tile's E row -> SMEM buffer t & 1 (read by every epilogue warp)
         const float4* src =
@@ -959,6 +1121,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(const TcParams
       }
       if (Cfg::kLocal) {  // both halves' |x''|^2, |x'|^2 and the E row are in SMEM
         asm volatile("bar.sync 1, %0;" ::"r"(kTcEpiThreads) : "memory");
+        cur.init(start_bound(t));
+      } else if (Cfg::kLoader && bnd && P.prof != 9) {  // the loader warps have left this tile's |x''|^2, |x'|^2
+        mbar_wait(&upf[t & 1], (t >> 1) & 1);
         cur.init(start_bound(t));
       } else if (bnd && P.prof != 9) {  // the other half of these rows (warp w ^ 4) has left its |x''|^2, |x'|^2
         asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
@@ -1207,7 +1372,7 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t ntiles = (P.n + kTcM - 1) / kTcM;
   const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
-  tc_screen_kernel<NPROD><<<grid, kTcThreads, smem, s>>>(P);
+  tc_screen_kernel<NPROD><<<grid, TcCfg<NPROD>::kThreads, smem, s>>>(P);
   GEEK_CHECK_LAUNCH();
   return GEEK_OK;
 }
