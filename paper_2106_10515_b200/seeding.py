@@ -456,6 +456,8 @@ def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=N
         form = _bins_per_table_singletons if _SINGLETON_BINS and params.min_group_size >= 2 else _bins_per_table
         bins, csr = form(buckets, scheme, params.num_hashes, params.num_tables, universe, owner,
                          params.min_group_size)
+        if info is not None:
+            info["silk_bins_path"] = form.__name__
     else:
         sig, nb, csr = silk_signatures(buckets, scheme, info)
         bins = find_bins(sig, params.num_hashes, params.num_tables, universe, owner)
@@ -464,6 +466,8 @@ def silk_votes(buckets, params: SeedingParams, universe: int, owner=None, info=N
             bins = _prune_bins(bins, buckets.bucket_sizes(), params.min_group_size)
     if isinstance(buckets, BucketTable):
         sizes = buckets.bucket_sizes()
+        if info is not None:
+            info["silk_buckets"] = len(buckets)
     else:
         sizes = _lib.to_dev(np.array([b.members.size for b in buckets], dtype=np.int64))
     if csr is None:

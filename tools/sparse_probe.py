@@ -10,8 +10,11 @@ labels / distances against numpy's Jaccard on the reduced sets.
     python tools/sparse_probe.py N [C]
 """
 import json
+import os
 import sys
 import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch
@@ -86,4 +89,5 @@ bad = int((a_ != lab).sum() + (dist[np.arange(idx.size), a_] != best).sum())
 print(json.dumps(dict(n=n, clusters=C, nnz=int(flat.numel()), gen_s=gen_s, ms=ms, wall_s=wall,
                       points_per_s=n / ms * 1e3, k_star=out.k_star, stages_s=out.timings,
                       calls_ms={k: round(v[0], 2) for k, v in tm.ms_by_name().items()},
-                      spot_check=dict(samples=int(idx.size), mismatches=bad)), indent=1))
+                      info={k: v for k, v in out.info.items() if isinstance(v, (int, float, str))},
+                      spot_check=dict(samples=int(idx.size), mismatches=bad)), indent=1, default=str))
