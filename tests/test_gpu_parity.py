@@ -64,6 +64,28 @@ def test_signatures_golden():
             assert np.array_equal(sch.signatures_for_sets(tb, sets), arr[f"{p}_{tb}"])
 
 
+@pytest.mark.parametrize("u,lo,hi", [(50_000, 20, 300), (5_000_000, 1, 90), (3000, 30, 200)])
+def test_set_minhash_large_sets_vs_oracle(u, lo, hi, monkeypatch):
+    """Set signatures of large sets (cycle-walking permutations over universes
+    above the rank-table limit, and rank tables below it) through the default
+    kernels and the per-element kernel (GEEK_MINHASH_GENERIC=1) equal the
+    oracle's min-pi over every function; ragged sizes incl. singletons,
+    duplicate ids."""
+    rng = np.random.default_rng(u + lo)
+    sets = [rng.integers(0, u, rng.integers(lo, hi)) for _ in range(700)]
+    sch = G.SignatureScheme(3, 20, u, seed=9)
+    funcs = sch.all_functions()
+    fseeds = [f.seed for f in funcs]
+    want = O.set_signatures(fseeds, u, sets)
+    from paper_2106_10515_b200.hashing import csr_from_sets, set_signatures_device
+    flat, off, _ = csr_from_sets(sets)
+    got = set_signatures_device(funcs, flat, off, len(sets)).cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(got, want)
+    monkeypatch.setenv("GEEK_MINHASH_GENERIC", "1")
+    got2 = set_signatures_device(funcs, flat, off, len(sets)).cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(got2, want)
+
+
 def test_minhash_known_answers():
     assert G.MinHashFunction.identity(10)({3, 5, 7}) == 3
     assert G.MinHashFunction(42, 100)(np.arange(100)) == 0
