@@ -337,9 +337,10 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
       const uint64_t tile = blockIdx.x + (q / nck) * gridDim.x;
       const int kc = (int)(q % nck);
       float* st = sX + (q % kPsStages) * kPsStageFloats;
+      // each warp stages only its own 32 rows: the warps never wait for each other
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int piece = tid + u * 128, r = piece >> 3, c4 = piece & 7;
+        const int r = warp * 32 + (lane >> 3) + 4 * u, c4 = lane & 7;
         const uint64_t row = tile * 128 + r;
         const int dim = kc * 32 + c4 * 4;
         const bool ok = row < n && dim < d;
@@ -365,9 +366,10 @@ __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __r
       const int t = j * 8 + kr * 2 + h;
       kdst[j][h] = t < m ? dst.tptr[t] : nullptr;
     }
+  __syncthreads();  // the directions are in SMEM
   for (uint64_t q = 0; q < total; ++q) {
     cp_async_wait<kPsStages - 2>();
-    __syncthreads();                // chunk q landed for all threads; stage (q-1) % S is free
+    __syncwarp();                   // chunk q of this warp's rows landed; its rows of stage (q-1) % S are free
     issue(q + kPsStages - 1);
     const int kc = (int)(q % nck);
     if (kc == 0) {
