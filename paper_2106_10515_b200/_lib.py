@@ -212,7 +212,10 @@ def to_dev(a, dtype=None) -> torch.Tensor:
     t = torch.from_numpy(arr)
     if dtype is not None:
         t = t.to(dtype)
-    return t.to(device(), non_blocking=False).contiguous()
+    # through a (cached) pinned staging copy: the upload is stream-ordered and
+    # the host does not wait for the queued kernels, as a pageable copy would
+    dev = device()  # (raises EngineError without a GPU before any pinned allocation)
+    return t.pin_memory().to(dev, non_blocking=True).contiguous()
 
 
 def dtype_code(t: torch.Tensor) -> int:

@@ -141,7 +141,7 @@ def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Ten
     cols = [tcol]
     if owner is not None:
         cols.append(owner.to(torch.int32).repeat(nt))
-    idx = torch.tensor([st * K for st in tables], dtype=torch.int64, device=dev)
+    idx = _lib.to_dev(np.array([st * K for st in tables], dtype=np.int64))
     for j in range(K):
         cols.append(sig.index_select(0, idx + j).reshape(-1).to(torch.int32))
     rows = torch.stack(cols, dim=1).contiguous()
@@ -161,7 +161,7 @@ def find_bins(sig: torch.Tensor, K: int, L: int, universe: int, owner: torch.Ten
     first = torch.ones_like(sel)
     first[1:] = g[1:] != g[:-1]
     heads = p64[sel & first]
-    bt = torch.tensor(tables, dtype=torch.int64, device=dev)[rows[heads, 0].to(torch.int64)]
+    bt = _lib.to_dev(np.asarray(tables, dtype=np.int64))[rows[heads, 0].to(torch.int64)]
     bins = Bins(psel % nb, newid[g][sel], counts[binned].to(torch.int32), bt, rows[heads][:, -K:])
     return _prune_bins(bins, *prune) if prune is not None else bins
 
