@@ -1590,7 +1590,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     const char* sel = getenv("GEEK_SCREEN");
     const bool local_ok = k <= 3840 && d % 8 == 0;  // 4 x 48 KB B stages + two origin-table rows in SMEM
     const int nprod = !sel ? 16 : atoi(sel) == 1 ? 1 : atoi(sel) == 3 ? 3 : (atoi(sel) == 17 && local_ok) ? 17 : 16;
-    Scratch img, c2s, mus, img3, c2s3, mus3, ts, ti, xn, amb, full, cnt, lcf, les, lj0, xp;
+    Scratch img, c2s, mus, img3, c2s3, mus3, ts, ti, xn, amb, full, cnt, lcf, les, lj0, xp, ldm;
     TcLocal loc{nullptr, nullptr, nullptr, nullptr};
     GEEK_TRY(cnt.alloc(48, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
@@ -1606,8 +1606,12 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     const char* bsel = getenv("GEEK_SCREEN_BOUND");
     const bool bound16 = nprod == 16 && !(bsel && atoi(bsel) == 0);
     if (nprod == 17 || bound16) {
+      // FP16x3: + the center-tile distance bounds that let a point tile skip
+      // center tiles no row can reach (GEEK_SCREEN_SKIP=0: every tile)
+      const char* ksel = getenv("GEEK_SCREEN_SKIP");
+      const bool skip = nprod == 16 && !(ksel && atoi(ksel) == 0);
       GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s,
-                                nprod == 17));
+                                nprod == 17, skip ? &ldm : nullptr));
       loc.cmax = cmax;
     }
     GEEK_TRY(ts.alloc(n * 32, s));

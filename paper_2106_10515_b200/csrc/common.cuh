@@ -240,6 +240,7 @@ struct TcLocal {
   const int* j0;    // [ntiles] origin center per 128-point tile
   const float* Es;  // [k][nct * 192] origin table
   const unsigned long long* cmax;  // [0] |c'|max bits (from tc_screen_prepare)
+  const float* dmin = nullptr;     // NPROD = 16: [k][nct] center-tile distance bounds (tile skipping)
 };
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,
@@ -247,7 +248,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
                      int xstride = 1, const unsigned* run_if = nullptr);
 int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
                      const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
-                     cudaStream_t s, bool with_E = true);
+                     cudaStream_t s, bool with_E = true, Scratch* dmin = nullptr);
 
 __global__ void iota_u32(uint32_t* p, uint64_t n);
 __global__ void fill_u32(uint32_t* p, uint32_t v, uint64_t n);

@@ -411,6 +411,11 @@ struct TcParams {
   int xstride;        // rows between consecutive screened points (1; kTcM for the tiles' first rows)
   const unsigned* run_if;  // may be null: the kernel does nothing unless *run_if != 0 (device-side fallback)
   const unsigned long long* cmax;  // NPROD = 17: [0] |c'|max bits, [3] 1/xscale bits (the lists' starting bound)
+  // NPROD = 16 with origins (may be null): dmin[j][ct] <= min over the centers c
+  // of center tile ct of |c' - c'_j| -- a point tile whose rows all satisfy
+  // r + sqrt(|x''|^2 + 5 win + 2 + 1e-5 |x'|^2) < dmin[j0][ct] (r = |x''|
+  // inflated) cannot insert any column of tile ct into its lists: the tile is skipped
+  const float* dmin;
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
@@ -443,6 +448,14 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
   const float xscale = __ldg(P.scal), oscale = __ldg(P.scal + 1);
   float* Ebuf = reinterpret_cast<float*>(bars + 40);  // NPROD = 17: E rows of the current / next point tile
   float2* Upart = reinterpret_cast<float2*>(Ebuf + 2 * P.kpadE);  // [2][128 rows][2 halves] (|x''|^2, |x'|^2)
+  uint64_t* mready = reinterpret_cast<uint64_t*>(Upart + 2 * 128 * 2);  // [2] (skipping) a tile's skip mask is set
+  uint32_t* skipmask = reinterpret_cast<uint32_t*>(mready + 2);           // [2] bit ct: center tile ct is skipped
+  float* thmax = reinterpret_cast<float*>(skipmask + 2);                   // [4] per loader warp: max row threshold
+  // [2] the epilogue warps have read a tile's Upart / skip mask (the loaders, up to
+  // two tiles ahead with the double-buffered A, wait before reusing the slot)
+  uint64_t* ucons = reinterpret_cast<uint64_t*>(thmax + 4);
+  // center-tile skipping (dedicated loaders + tile origins + the dmin table)
+  const bool skip_on = Cfg::kLoader && P.j0 != nullptr && P.dmin != nullptr && P.prof != 11;
   if (tid == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -457,6 +470,11 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
       mbar_init(&aempty[b], 1);
     }
     for (int b = 0; b < 2; ++b) mbar_init(&upf[b], Cfg::kLoaderWarps * 32);  // every loader thread
+    if (Cfg::kLoader)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&mready[b], 1);           // the loader thread that sets the mask
+        mbar_init(&ucons[b], kTcEpiWarps);  // one arrival per epilogue warp
+      }
     mbar_init(c2full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -498,25 +516,35 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         }
         __syncwarp();
       }
-      const uint64_t total_chunks = (uint64_t)my_tiles * total_q;
-      for (uint64_t q = 0; q < total_chunks; ++q) {
-        const uint32_t s = (uint32_t)(q % Cfg::kStages);
-        if (q >= (uint64_t)Cfg::kStages) {
-          if (P.sleepwait > 1) mbar_wait_sleep(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
-          else mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+      (void)total_q;
+      uint64_t q = 0;  // ring position: stages issued so far
+      for (uint32_t t = 0; t < my_tiles; ++t) {
+        uint32_t mask = 0;
+        if (skip_on) {  // the loaders decide which center tiles this point tile skips
+          mbar_wait(&mready[t & 1], (t >> 1) & 1);
+          mask = skipmask[t & 1];
         }
-        const uint32_t qq = (uint32_t)(q % total_q), cq = qq / qct, j = qq - cq * qct;
-        const uint32_t ct = (cq + rot) % (uint32_t)P.nct;  // CTAs start on different center tiles
-        const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
-        if (leader && P.prof == 6 && q >= (uint64_t)Cfg::kStages) {
-          mbar_arrive(&full[s]);  // profiling: keep the stale stage, no L2 traffic
-        } else if (leader) {
-          mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(B + s * Cfg::kStageBytes,
-                   reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes, bytes,
-                   &full[s]);
+        for (uint32_t cq = 0; cq < (uint32_t)P.nct; ++cq) {
+          const uint32_t ct = (cq + rot) % (uint32_t)P.nct;  // CTAs start on different center tiles
+          if ((mask >> ct) & 1u) continue;
+          for (uint32_t j = 0; j < qct; ++j, ++q) {
+            const uint32_t s = (uint32_t)(q % Cfg::kStages);
+            if (q >= (uint64_t)Cfg::kStages) {
+              if (P.sleepwait > 1) mbar_wait_sleep(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+              else mbar_wait(&empty[s], (uint32_t)((q / Cfg::kStages) - 1) & 1);
+            }
+            const uint32_t bytes = j < (uint32_t)nbk ? (uint32_t)Cfg::kStageBytes : (uint32_t)kTcC2Bytes;
+            if (leader && P.prof == 6 && q >= (uint64_t)Cfg::kStages) {
+              mbar_arrive(&full[s]);  // profiling: keep the stale stage, no L2 traffic
+            } else if (leader) {
+              mbar_expect_tx(&full[s], bytes);
+              bulk_g2s(B + s * Cfg::kStageBytes,
+                       reinterpret_cast<const uint8_t*>(P.Bimg) + ct * ct_bytes + (uint64_t)j * Cfg::kStageBytes,
+                       bytes, &full[s]);
+            }
+            __syncwarp();
+          }
         }
-        __syncwarp();
       }
     }
   } else if (warp == kTcEpiWarps) {
@@ -551,11 +579,27 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
       const uint64_t d0 = make_sdesc(smem_u32(B), P.lbo, P.sbo);
       const uint32_t b_lo32 = (uint32_t)d0, d_hi32 = (uint32_t)(d0 >> 32);
       const uint32_t a_lo32 = (uint32_t)make_sdesc(smem_u32(A), P.lbo, P.sbo);
+      uint64_t g = 0;          // center tiles processed (accumulator buffer g & 1)
+      bool c2_ready = false;
       for (uint32_t t = 0; t < my_tiles; ++t) {
         const int ab = t % Cfg::kABuf;
         const uint32_t apar = (t / Cfg::kABuf) & 1;
-        for (int ct = 0; ct < P.nct; ++ct) {
-          const uint64_t g = (uint64_t)t * P.nct + ct;
+        uint32_t mask = 0;
+        if (skip_on) {
+          mbar_wait(&mready[t & 1], (t >> 1) & 1);
+          mask = skipmask[t & 1];
+        }
+        int first_ct = -1, last_ct = -1;  // walk positions of the first / last processed center tile
+        for (int c = 0; c < P.nct; ++c)
+          if (!((mask >> ((c + rot) % P.nct)) & 1u)) {
+            if (first_ct < 0) first_ct = c;
+            last_ct = c;
+          }
+        for (int ct = 0; ct < P.nct; ++ct, ++g) {
+          if ((mask >> ((ct + rot) % P.nct)) & 1u) {
+            --g;
+            continue;
+          }
           const int buf = (int)(g & 1);
           timed_wait(&acce[buf], (uint32_t)((g >> 1) & 1) ^ 1u, w_acce);
           fence_after();
@@ -566,7 +610,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
             // point-tile chunks (32 dims) holding this B chunk's dims
             const int ac0 = kc * Cfg::kChunkDims / kTcAChunk;
             const int ac1 = min(nck - 1, ((kc + 1) * Cfg::kChunkDims - 1) / kTcAChunk);
-            if (ct == 0) {  // first use of a point-tile chunk: wait for its writers
+            if (ct == first_ct) {  // first use of a point-tile chunk: wait for its writers
               bool waited = false;
               for (int ac = ac0; ac <= ac1; ++ac)
                 if (ac * kTcAChunk >= kc * Cfg::kChunkDims) {
@@ -605,7 +649,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
               }
             }
             if (P.dbg) w_issue += clock64() - c_is;
-            if (ct == P.nct - 1 && leader)  // last read of these point-tile chunks
+            if (ct == last_ct && leader)  // last read of these point-tile chunks
               for (int ac = ac0; ac <= ac1; ++ac)
                 if ((ac + 1) * kTcAChunk <= (kc + 1) * Cfg::kChunkDims || kc == nbk - 1) tc_commit(&aempty[ab * 4 + ac]);
             stage_done(s);
@@ -614,9 +658,10 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           if (Cfg::kLocal) {
             // no |c'|^2 slice: the epilogue adds E[j0][j]
           } else if (P.c2res) {  // |c'|^2 / 2, added last, from the resident slices
-            if (t == 0 && ct == 0) {
+            if (!c2_ready) {
               mbar_wait(c2full, 0);
               fence_after();
+              c2_ready = true;
             }
             const uint32_t cta = (uint32_t)((ct + rot) % P.nct);
             const uint64_t a1 = make_sdesc(smem_u32(C2), P.lbo, P.sbo);
@@ -695,7 +740,9 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         };
         float4 xa0[4], xa1[4];
         load_chunk(0, 0, xa0);
-        if (bnd16 && my_tiles > 0) load_origin(tile_j0(0), og);
+        int jcur = tile_j0(0);  // the current tile's origin center
+        if (bnd16 && my_tiles > 0) load_origin(jcur, og);
+        const float cn_l = skip_on ? (float)__longlong_as_double((long long)__ldg(P.cmax)) : 0.f;
         for (uint32_t t = 0; t < my_tiles; ++t) {
           const uint64_t p0 = tile_p0(t);
           const bool valid = p0 + row < P.n;
@@ -783,12 +830,40 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           if (big) atomicOr(P.ovf, 1u);
           if (P.xpart && valid) P.xpart[(p0 + row) * 2 + hh] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
           if (bnd16) {
+            if (t >= 2) mbar_wait(&ucons[t & 1], ((t >> 1) - 1) & 1);  // tile t-2's Upart / mask were read
             Upart[((t & 1) * 128 + row) * 2 + hh] =
                 make_float2((xq[0] + xq[1]) + (xq[2] + xq[3]), (xs[0] + xs[1]) + (xs[2] + xs[3]));
             mbar_arrive(&upf[t & 1]);
 #pragma unroll
             for (int r = 0; r < 4; ++r) og[r] = ogn[r];
           }
+          if (skip_on) {  // which center tiles can no row of this tile reach below its start bound?
+            asm volatile("bar.sync 3, %0;" ::"r"(Cfg::kLoaderWarps * 32) : "memory");  // both row halves are in
+            if (hh == 0) {
+              const float2 h0 = Upart[((t & 1) * 128 + row) * 2], h1 = Upart[((t & 1) * 128 + row) * 2 + 1];
+              const float xpp = h0.x + h1.x, xp = h0.y + h1.y;
+              // the epilogue's window (start_bound); a column of center c is
+              // inserted only below U = xpp - xp + 4 win + 1 (s units), and
+              // s(x, c) >= (|c' - c'_j0| - |x''|)^2 - |x'|^2 with screen error <= win / 2
+              const float win = 2.2f * ((2e-6f + 7.2e-7f * P.d) * sqrtf(xp) * cn_l + 1e-5f * cn_l * cn_l) +
+                                1e-4f * (xp + xpp);
+              float th = sqrtf(xpp * 1.00001f) * 1.000001f + sqrtf(xpp * 1.00001f + 5.f * win + 2.f + 1e-5f * xp);
+              if (!valid) th = 0.f;
+              for (int o = 16; o; o >>= 1) th = fmaxf(th, __shfl_xor_sync(0xffffffffu, th, o));
+              if (lane == 0) thmax[lg] = th;
+            }
+            asm volatile("bar.sync 3, %0;" ::"r"(Cfg::kLoaderWarps * 32) : "memory");
+            if (warp == 12 && lane == 0) {
+              const float TH = fmaxf(fmaxf(thmax[0], thmax[1]), fmaxf(thmax[2], thmax[3]));
+              uint32_t m = 0;
+              const float* dr = P.dmin + (uint64_t)jcur * P.nct;
+              for (int c = 0; c < P.nct; ++c)
+                if (__ldg(dr + c) > TH) m |= 1u << c;
+              skipmask[t & 1] = m;
+              mbar_arrive(&mready[t & 1]);
+            }
+          }
+          jcur = jn;
         }
       }
     }
@@ -811,8 +886,9 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
     };
     Top4 cur;
     cur.init();
+    uint64_t eg = 0;  // center tiles drained so far (the MMA warp's accumulator order)
     auto epilogue = [&](uint32_t t, int ct, Top4& top) {
-      const uint64_t g = (uint64_t)t * P.nct + ct;
+      const uint64_t g = eg++;
       const int buf = (int)(g & 1);
       const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
       if (getenv_sleep) mbar_wait_sleep(&accf[buf], (uint32_t)((g >> 1) & 1));
@@ -875,8 +951,8 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[buf]);  // the warp's TMEM reads are all done
     };
-    auto finish = [&](uint32_t t, Top4& top) {
-      epilogue(t, P.nct - 1, top);
+    auto finish = [&](uint32_t t, int last_ct, Top4& top) {
+      epilogue(t, last_ct, top);
       const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + (warp & 3) * 32 + lane;
       if (i < P.n) {  // two column halves -> [n][8] of s = 2 * (s / 2) (exact); the classifier merges them
         const int h = (warp >> 2) * 4;
@@ -1129,9 +1205,22 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
         cur.init(start_bound(t));
       }
-      for (int ct = 0; ct + 1 < P.nct; ++ct) epilogue(t, ct, cur);
+      uint32_t mask = 0;
+      if (skip_on) {
+        mbar_wait(&mready[t & 1], (t >> 1) & 1);
+        mask = skipmask[t & 1];
+      }
+      if (Cfg::kLoader && bnd) {  // this tile's Upart and mask are read: the slot may be reused
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ucons[t & 1]);
+      }
+      int last_ct = -1;
+      for (int c = 0; c < P.nct; ++c)
+        if (!((mask >> ((c + rot) % P.nct)) & 1u)) last_ct = c;
+      for (int ct = 0; ct < last_ct; ++ct)
+        if (!((mask >> ((ct + rot) % P.nct)) & 1u)) epilogue(t, ct, cur);
       if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
-      finish(t, cur);
+      finish(t, last_ct, cur);
       if (!bnd || P.prof == 9) cur.init();
     }
   }
@@ -1272,6 +1361,29 @@ __global__ void origin_table_kernel(const float* cf, uint64_t k, int d, int kpad
   }
 }
 
+// dmin[j][ct] = a lower bound of min over the centers c of center tile ct of
+// |c'_c - c'_j| (float64 over the float32 c', rounded down, minus 1e-6 relative)
+__global__ void dmin_kernel(const float* cf, uint64_t k, int d, int nct, float* dmin) {
+  const uint64_t total = k * (uint64_t)nct;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = q / nct;
+    const int ct = (int)(q % nct);
+    const float* cj = cf + j * d;
+    double best = INFINITY;
+    const uint64_t c1 = min(k, (uint64_t)(ct + 1) * kTcN);
+    for (uint64_t c = (uint64_t)ct * kTcN; c < c1; ++c) {
+      const float* cc = cf + c * d;
+      double s = 0.0;
+      for (int e = 0; e < d; ++e) {
+        const double z = (double)cc[e] - (double)cj[e];
+        s = fma(z, z, s);
+      }
+      best = fmin(best, s);
+    }
+    dmin[q] = __double2float_rd(sqrt(best) * (1.0 - 1e-6));
+  }
+}
+
 // origin of every point tile: the screened nearest center of its first row
 __global__ void pick_origin_kernel(const float* top_s, const int* top_i, uint64_t ntiles, int* j0) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
@@ -1364,7 +1476,7 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
                     TcCfg<NPROD>::kTmemCols, "TMEM map");
   const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0) +
                       (TcCfg<NPROD>::kLocal ? (size_t)2 * P.kpadE * sizeof(float) : 0) +
-                      (TcCfg<NPROD>::kF16 ? (size_t)2 * 128 * 2 * sizeof(float2) : 0);
+                      (TcCfg<NPROD>::kF16 ? (size_t)2 * 128 * 2 * sizeof(float2) + 64 : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -1393,6 +1505,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.xstride = xstride;
   P.run_if = run_if;
   P.cmax = loc ? loc->cmax : nullptr;
+  P.dmin = (loc && nprod == 16) ? loc->dmin : nullptr;
   P.X = X;
   P.n = n;
   P.d = d;
@@ -1430,7 +1543,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   }
 #endif
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed + 2 * 128 * 2 * sizeof(float2)
+  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed + 2 * 128 * 2 * sizeof(float2) + 64
               : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
@@ -1466,7 +1579,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
 // |x''| and with it the recheck rate small).
 int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_t n, uint32_t lbo, uint32_t sbo,
                      const Scratch& mu17, float xscale, int nct17, Scratch& cf, Scratch& Es, Scratch& j0, TcLocal& loc,
-                     cudaStream_t s, bool with_E) {
+                     cudaStream_t s, bool with_E, Scratch* dmin) {
   const int kpadE = nct17 * kTcN;
   const uint64_t ntiles = (n + kTcM - 1) / kTcM;
   GEEK_TRY(cf.alloc(k * (uint64_t)d * 4, s));
@@ -1494,6 +1607,13 @@ int tc_local_prepare(const double* C, uint64_t k, int d, const float* X, uint64_
   loc.cf = cf.as<float>();
   loc.j0 = j0.as<int>();
   loc.Es = with_E ? Es.as<float>() : nullptr;
+  loc.dmin = nullptr;
+  if (dmin) {  // center-tile distance bounds from every origin (FP16x3 tile skipping)
+    GEEK_TRY(dmin->alloc(k * (uint64_t)nct17 * 4, s));
+    dmin_kernel<<<grid_for(k * (uint64_t)nct17, 128), 128, 0, s>>>(cf.as<float>(), k, d, nct17, dmin->as<float>());
+    GEEK_CHECK_LAUNCH();
+    loc.dmin = dmin->as<float>();
+  }
   return GEEK_OK;
 }
 
