@@ -258,7 +258,8 @@ typedef struct {
   unsigned long long full_scans;  /* of those, points whose candidate window overflowed: all centers */
   unsigned long long screen_mode; /* 16 FP16x3, 3 TF32x3 (also after an f16 overflow), 17 tile-local
                                      FP16, 1 TF32, 0 no tensor-core screen */
-  unsigned long long reserved;
+  unsigned long long screen_tiles; /* FP16x3 screen: (point tile, center tile) pairs multiplied --
+                                     the rest were skipped as out of reach (0 for other screens) */
 } geek_assign_stats_t;
 
 /* Nearest center by float64 direct-difference distance with numpy's pairwise

@@ -50,7 +50,7 @@ class AssignStats:
         self.ev1.synchronize()
         ms = self.ev0.elapsed_time(self.ev1)
         return dict(assign_rechecked=int(v[0]), assign_full_scans=int(v[1]), screen_mode=int(v[2]),
-                    screen_ms=float(ms) if v[2] else 0.0)
+                    screen_ms=float(ms) if v[2] else 0.0, screen_tiles=int(v[3]))
 
 
 _LAST = [None]

@@ -1408,7 +1408,8 @@ static int launch_top8(const T* G, uint64_t rows, uint64_t k, uint64_t ldg, cons
 }
 
 __global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
-                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st);
+                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st,
+                                    const unsigned long long* tiles = nullptr);
 
 // float64 GEMM screen for wide float32 rows: cuBLAS DGEMM in point chunks, the
 // top-8 per point, then the exact classification / recheck of the tensor-core path
@@ -1530,11 +1531,12 @@ static int assign_wide_screen(const void* X, int dtype, uint64_t n, int d, const
 }
 
 __global__ void assign_stats_kernel(const unsigned long long* namb, const unsigned long long* nfull,
-                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st) {
+                                    const unsigned* ovf, int nprod, geek_assign_stats_t* st,
+                                    const unsigned long long* tiles) {
   st->rechecked = (namb ? *namb : 0ull) + (nfull ? *nfull : 0ull);
   st->full_scans = nfull ? *nfull : 0ull;
   st->screen_mode = (unsigned long long)eff_mode(nprod, ovf);
-  st->reserved = 0;
+  st->screen_tiles = tiles ? *tiles : 0ull;
 }
 
 }  // namespace geek
@@ -1594,7 +1596,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
     TcLocal loc{nullptr, nullptr, nullptr, nullptr};
     GEEK_TRY(cnt.alloc(48, s));
     GEEK_CHECK_CUDA(cudaMemsetAsync(cnt.ptr, 0, 48, s));
-    unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16)
+    unsigned long long* cmax = cnt.as<unsigned long long>();  // [0] |c'|max, [3] 1/s (FP16), [5] screen tiles
     unsigned long long* namb = cmax + 1;
     unsigned long long* nfull = cmax + 2;
     unsigned* ovf = reinterpret_cast<unsigned*>(cmax + 4);
@@ -1613,6 +1615,7 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
       GEEK_TRY(tc_local_prepare(C, k, d, (const float*)X, n, kTcLBO, kTcSBO, mus, xscale, nct, lcf, les, lj0, loc, s,
                                 nprod == 17, skip ? &ldm : nullptr));
       loc.cmax = cmax;
+      loc.tiles_done = cmax + 5;
     }
     GEEK_TRY(ts.alloc(n * 32, s));
     GEEK_TRY(ti.alloc(n * 32, s));
@@ -1663,7 +1666,9 @@ int geek_assign_l2(const void* X, int dtype, uint64_t n, int d, const double* C,
                                                                      full.as<uint32_t>(), nfull, labels, best);
     GEEK_CHECK_LAUNCH();
     if (stats) {
-      assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, ovf, nprod, stats);
+      // (screen tiles: the FP16x3 screen's multiplied pairs; a TF32x3 redo after an
+      // f16 overflow does not count them)
+      assign_stats_kernel<<<1, 1, 0, s>>>(namb, nfull, ovf, nprod, stats, nprod == 16 ? cmax + 5 : nullptr);
       GEEK_CHECK_LAUNCH();
     }
     return GEEK_OK;

@@ -241,6 +241,7 @@ struct TcLocal {
   const float* Es;  // [k][nct * 192] origin table
   const unsigned long long* cmax;  // [0] |c'|max bits (from tc_screen_prepare)
   const float* dmin = nullptr;     // NPROD = 16: [k][nct] center-tile distance bounds (tile skipping)
+  unsigned long long* tiles_done = nullptr;  // (point tile, center tile) pairs multiplied (device counter)
 };
 int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch& img, const Scratch& c2,
                      const Scratch& mu, uint64_t k, int nct, uint32_t lbo, uint32_t sbo, float* top_s, int* top_i,

@@ -416,6 +416,7 @@ struct TcParams {
   // r + sqrt(|x''|^2 + 5 win + 2 + 1e-5 |x'|^2) < dmin[j0][ct] (r = |x''|
   // inflated) cannot insert any column of tile ct into its lists: the tile is skipped
   const float* dmin;
+  unsigned long long* tiles_done;  // may be null: += the (point tile, center tile) pairs this launch multiplied
 };
 
 // warps 0-7: A loader + epilogue, warp 8: TMA + MMA issuer
@@ -682,6 +683,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           if (P.dbg) w_accf += clock64() - c_af;
         }
       }
+      if (P.tiles_done && leader) atomicAdd(P.tiles_done, (unsigned long long)g);
       if (P.dbg && leader) {
         P.dbg[blockIdx.x * 8 + 0] = (unsigned long long)w_full;
         P.dbg[blockIdx.x * 8 + 1] = (unsigned long long)w_acce;
@@ -1506,6 +1508,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   P.run_if = run_if;
   P.cmax = loc ? loc->cmax : nullptr;
   P.dmin = (loc && nprod == 16) ? loc->dmin : nullptr;
+  P.tiles_done = loc ? loc->tiles_done : nullptr;
   P.X = X;
   P.n = n;
   P.d = d;

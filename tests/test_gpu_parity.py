@@ -410,14 +410,17 @@ def test_fp16_screen_range_fallback(mode, monkeypatch):
     assert got.objective == obj
 
 
-@pytest.mark.parametrize("bound", ["1", "0"])
+@pytest.mark.parametrize("bound", ["1", "0", "noskip"])
 @pytest.mark.parametrize("order", ["clustered", "shuffled", "far"])
 def test_fp16x3_start_bound_orders(order, bound, monkeypatch):
     """The default FP16x3 screen with its lists starting at a bound from each
-    point tile's origin center (and without, GEEK_SCREEN_BOUND=0): exact labels
+    point tile's origin center and the center tiles out of reach skipped (and
+    without skipping, and without bounds, GEEK_SCREEN_BOUND=0): exact labels
     for cluster-ordered ids, shuffled ids (poor origins: more insertions) and
     points far from every center (the bound sits far above the best)."""
-    monkeypatch.setenv("GEEK_SCREEN_BOUND", bound)
+    monkeypatch.setenv("GEEK_SCREEN_BOUND", "1" if bound == "noskip" else bound)
+    if bound == "noskip":  # origin bounds without center-tile skipping
+        monkeypatch.setenv("GEEK_SCREEN_SKIP", "0")
     rng = np.random.default_rng(23)
     k, d, n = 700, 96, 50_000
     C = np.cumsum(rng.standard_normal((k, d)) * 2.0, axis=0) + 100.0
@@ -490,6 +493,9 @@ def test_assign_abi_workspace_stats_events():
     assert np.array_equal(lab.cpu().numpy(), want_lab)
     assert np.array_equal(best.cpu().numpy(), want_best)
     assert info["screen_mode"] == 16 and info["screen_ms"] > 0 and info["assign_rechecked"] >= info["assign_full_scans"]
+    # center tiles out of every row's reach are skipped (cluster-ordered rows, 2 center tiles)
+    total = -(-n // 128) * -(-k // 192)
+    assert 0 < info["screen_tiles"] < total
     small = torch.empty(1 << 16, dtype=torch.uint8, device="cuda")
     with pytest.raises(G.EngineError, match="workspace"):
         _lib.call("geek_assign_l2", _lib.ptr(Xd), 0, n, d, _lib.ptr(Cd), k, _lib.ptr(lab), _lib.ptr(best), None, None,
