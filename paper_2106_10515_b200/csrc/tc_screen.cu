@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         const uint32_t apar = (t / Cfg::kABuf) & 1;
         uint32_t mask = 0;
         if (skip_on) {
-          mbar_wait(&mready[t & 1], (t >> 1) & 1);
+          timed_wait(&mready[t & 1], (t >> 1) & 1, w_done);  // (w_done: the wait for the tile's skip mask)
           mask = skipmask[t & 1];
         }
         int first_ct = -1, last_ct = -1;  // walk positions of the first / last processed center tile
@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         P.dbg[blockIdx.x * 8 + 4] = (unsigned long long)w_issue;
         P.dbg[blockIdx.x * 8 + 5] = (unsigned long long)w_c2;
         P.dbg[blockIdx.x * 8 + 6] = (unsigned long long)w_accf;
+        P.dbg[blockIdx.x * 8 + 7] = (unsigned long long)w_done;
       }
     }
   } else if (Cfg::kLoader && warp >= kTcEpiWarps + 2) {
@@ -745,7 +746,9 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         int jcur = tile_j0(0);  // the current tile's origin center
         if (bnd16 && my_tiles > 0) load_origin(jcur, og);
         const float cn_l = skip_on ? (float)__longlong_as_double((long long)__ldg(P.cmax)) : 0.f;
+        long long l_start = clock64(), l_conv = 0, l_ucons = 0, l_mask = 0;
         for (uint32_t t = 0; t < my_tiles; ++t) {
+          const long long l0 = P.dbg ? clock64() : 0;
           const uint64_t p0 = tile_p0(t);
           const bool valid = p0 + row < P.n;
           const int ab = (int)(t & 1);                 // A double buffer: tile t+1 is written while the MMAs read tile t
@@ -823,22 +826,37 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
               }
               tc_st8(tmem + ((uint32_t)(lg * 32) << 16) + Cfg::kTmemA + ab * Cfg::kTmemAStride + kc * 16 + hh * 8, hp);
             }
+            if (!skip_on) {  // chunk by chunk: the MMAs may start on chunk 0 while the rest converts
+              tc_wait_st();
+              fence_before();
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&afull[ab * 4 + kc]);  // the warp's A writes are all done
+            }
+          }
+          if (skip_on) {  // the MMAs wait for the tile's skip mask anyway: one store wait for all chunks
             tc_wait_st();
             fence_before();
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[ab * 4 + kc]);  // the warp's A writes are all done
+            if (lane == 0)
+              for (int kc = 0; kc < nck; ++kc) mbar_arrive(&afull[ab * 4 + kc]);
           }
           if (big) atomicOr(P.ovf, 1u);
           if (P.xpart && valid) P.xpart[(p0 + row) * 2 + hh] = ((double)xs[0] + xs[1]) + ((double)xs[2] + xs[3]);
+          const long long l1 = P.dbg ? clock64() : 0;
+          if (P.dbg) l_conv += l1 - l0;
           if (bnd16) {
             if (t >= 2) mbar_wait(&ucons[t & 1], ((t >> 1) - 1) & 1);  // tile t-2's Upart / mask were read
+            if (P.dbg) l_ucons += clock64() - l1;
             Upart[((t & 1) * 128 + row) * 2 + hh] =
                 make_float2((xq[0] + xq[1]) + (xq[2] + xq[3]), (xs[0] + xs[1]) + (xs[2] + xs[3]));
             mbar_arrive(&upf[t & 1]);
 #pragma unroll
             for (int r = 0; r < 4; ++r) og[r] = ogn[r];
           }
+          (void)0;
+          const long long l2 = P.dbg ? clock64() : 0;
           if (skip_on) {  // which center tiles can no row of this tile reach below its start bound?
             asm volatile("bar.sync 3, %0;" ::"r"(Cfg::kLoaderWarps * 32) : "memory");  // both row halves are in
             if (hh == 0) {
@@ -865,7 +883,15 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
               mbar_arrive(&mready[t & 1]);
             }
           }
+          if (P.dbg) l_mask += clock64() - l2;
           jcur = jn;
+        }
+        if (P.dbg && warp == 12 && lane == 0) {
+          unsigned long long* L = P.dbg + 148 * 8 + blockIdx.x * 8;
+          L[0] = (unsigned long long)(clock64() - l_start);
+          L[1] = (unsigned long long)l_conv;
+          L[2] = (unsigned long long)l_ucons;
+          L[3] = (unsigned long long)l_mask;
         }
       }
     }
@@ -1540,8 +1566,8 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   if (getenv("GEEK_SCREEN_PROF")) P.prof = atoi(getenv("GEEK_SCREEN_PROF"));
   if (getenv("GEEK_SCREEN_SLEEP")) P.sleepwait = atoi(getenv("GEEK_SCREEN_SLEEP"));
   if (getenv("GEEK_SCREEN_DBG")) {
-    GEEK_TRY(dbg.alloc(148 * 4 * 8 * 2, s));
-    GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 4 * 8 * 2, s));
+    GEEK_TRY(dbg.alloc(148 * 16 * 8, s));
+    GEEK_CHECK_CUDA(cudaMemsetAsync(dbg.ptr, 0, 148 * 16 * 8, s));
     P.dbg = dbg.as<unsigned long long>();
   }
 #endif
@@ -1555,11 +1581,16 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
                  : nprod == 3  ? launch_screen<3>(P, s)
                                : launch_screen<1>(P, s);
   if (st == GEEK_OK && P.dbg) {  // diagnostics (GEEK_DEBUG_KNOBS builds): where the MMA warp waits
-    unsigned long long h[148 * 8];
+    unsigned long long h[148 * 16];
     GEEK_CHECK_CUDA(cudaMemcpyAsync(h, P.dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
     GEEK_CHECK_CUDA(cudaStreamSynchronize(s));
-    double f = 0, a = 0, af = 0, tot = 0, is = 0, c2 = 0, cf = 0;
+    double f = 0, a = 0, af = 0, tot = 0, is = 0, c2 = 0, cf = 0, wm = 0, lt = 0, lc = 0, lu = 0, lm = 0;
     for (int b = 0; b < 148; ++b) {
+      wm += h[8 * b + 7];
+      lt += h[148 * 8 + 8 * b];
+      lc += h[148 * 8 + 8 * b + 1];
+      lu += h[148 * 8 + 8 * b + 2];
+      lm += h[148 * 8 + 8 * b + 3];
       f += h[8 * b];
       a += h[8 * b + 1];
       af += h[8 * b + 2];
@@ -1572,6 +1603,11 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
             "[screen dbg] MMA warp cycles: total %.3g, wait B %.1f%%, wait acc %.1f%%, wait A %.1f%%, issuing the "
             "12 MMAs of a chunk %.1f%%, |c'|^2 block %.1f%%, accumulator commit %.1f%%\n",
             tot / 148, 100 * f / tot, 100 * a / tot, 100 * af / tot, 100 * is / tot, 100 * c2 / tot, 100 * cf / tot);
+    if (lt > 0)
+      fprintf(stderr,
+              "[screen dbg] MMA warp waits for skip masks %.1f%%; loader warp 12 cycles: total %.3g, converting "
+              "%.1f%%, waiting for the epilogue (Upart slot) %.1f%%, skip mask %.1f%%\n",
+              100 * wm / tot, lt / 148, 100 * lc / lt, 100 * lu / lt, 100 * lm / lt);
   }
   return st;
 }
