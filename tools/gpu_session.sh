@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 1200 python tools/sparse_probe.py 20000000 > gpurun_out/sparse_now.json 2> gpurun_out/sparse_now.err
+timeout 1500 python -m pytest tests/ -q -x -m gpu > gpurun_out/t_all.log 2>&1
+echo "rc=$?" >> gpurun_out/t_all.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_skip.json 2> gpurun_out/bench_skip.err
