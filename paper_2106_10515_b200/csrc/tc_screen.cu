@@ -108,7 +108,12 @@ struct TcCfg {
   // (warps 10-11 idle: the loaders form a whole warpgroup)
   static constexpr bool kLoader = NPROD == 16;
   static constexpr int kLoaderWarps = 8;  // two per TMEM lane group (row halves of 16 dims per chunk)
-  static constexpr int kThreads = kLoader ? (12 + kLoaderWarps) * 32 : 320;
+  // with loaders: 4 epilogue warps (one per TMEM lane group, both column
+  // halves), MMA warp 4, TMA warp 5, 6-7 idle, loaders 8-15 (512 threads: 128
+  // registers, so the loaders keep two chunks of rows in flight)
+  static constexpr int kEpiWarps = kLoader ? 4 : 8;
+  static constexpr int kLoaderBase = 8;
+  static constexpr int kThreads = kLoader ? (kLoaderBase + kLoaderWarps) * 32 : 320;
 };
 
 // bytes of one center tile in the operand image: data chunks + the |c'|^2
@@ -455,6 +460,9 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
   // [2] the epilogue warps have read a tile's Upart / skip mask (the loaders, up to
   // two tiles ahead with the double-buffered A, wait before reusing the slot)
   uint64_t* ucons = reinterpret_cast<uint64_t*>(thmax + 4);
+  // (loaders) the 128 mean coordinates, 16-byte aligned 64 bytes past mready: SMEM broadcasts
+  float* smu = reinterpret_cast<float*>(reinterpret_cast<char*>(mready) + 64);
+  static_assert(2 * 8 + 2 * 4 + 4 * 4 + 2 * 8 <= 64, "mready / skipmask / thmax / ucons fit 64 bytes");
   // center-tile skipping (dedicated loaders + tile origins + the dmin table)
   const bool skip_on = Cfg::kLoader && P.j0 != nullptr && P.dmin != nullptr && P.prof != 11;
   if (tid == 0) {
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], kTcEpiWarps);  // one arrival per epilogue warp
+      mbar_init(&acce[b], Cfg::kEpiWarps);  // one arrival per epilogue warp
     }
     for (int b = 0; b < Cfg::kABuf * 4; ++b) {
       mbar_init(&afull[b], Cfg::kLoader ? Cfg::kLoaderWarps : kTcEpiWarps);  // one arrival per writing warp
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
     if (Cfg::kLoader)
       for (int b = 0; b < 2; ++b) {
         mbar_init(&mready[b], 1);           // the loader thread that sets the mask
-        mbar_init(&ucons[b], kTcEpiWarps);  // one arrival per epilogue warp
+        mbar_init(&ucons[b], Cfg::kEpiWarps);  // one arrival per epilogue warp
       }
     mbar_init(c2full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
 
   // The producer and MMA warps run their loops warp-wide (so addresses and
   // descriptors stay warp-uniform) and issue through one elected lane.
-  if (warp == kTcEpiWarps + 1) {
+  if (warp == Cfg::kEpiWarps + 1) {
     const bool leader = elect_one();
     {  // ---------------- TMA producer: the B ring ----------------
       if (P.c2res && my_tiles > 0) {  // the |c'|^2 slices, once
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         }
       }
     }
-  } else if (warp == kTcEpiWarps) {
+  } else if (warp == Cfg::kEpiWarps) {
     const bool leader = elect_one();
     {  // ---------------- MMA issuer ----------------
       const uint32_t idesc_full = make_idesc(kTcM, kTcN, Cfg::kF16), idesc_last = make_idesc(kTcM, P.nlast, Cfg::kF16);
@@ -695,7 +703,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         P.dbg[blockIdx.x * 8 + 7] = (unsigned long long)w_done;
       }
     }
-  } else if (Cfg::kLoader && warp >= kTcEpiWarps + 2) {
+  } else if (Cfg::kLoader && warp >= Cfg::kEpiWarps + 2) {
     // ---------------- warps 12-15: point-tile loaders (NPROD = 16) ----------------
     // thread l of warp 12 + g owns row 32g + l (its TMEM lane) of every point
     // tile: 32-dim chunks of the row are loaded one chunk ahead (the next
@@ -704,8 +712,8 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
     // with |x'|^2 per row half for the classifier and, with tile origins,
     // |x - c'_j0|^2 for the epilogue's start bound (Upart, signalled on upf)
     if constexpr (Cfg::kLoader) {
-      if (warp >= 12) {
-        const int lg = (warp - 12) & 3, hh = (warp - 12) >> 2, row = lg * 32 + lane;
+      if (warp >= Cfg::kLoaderBase) {
+        const int lg = (warp - Cfg::kLoaderBase) & 3, hh = (warp - Cfg::kLoaderBase) >> 2, row = lg * 32 + lane;
         const bool bnd16 = P.j0 != nullptr;
         const bool getenv_sleep_l = P.sleepwait != 0;
         auto tile_p0 = [&](uint32_t t) { return (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM; };
@@ -741,9 +749,16 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
 #pragma unroll
           for (int r = 0; r < 4; ++r) dst[r] = 4 * lane + r < P.d ? __ldg(org + 4 * lane + r) : 0.f;
         };
-        float4 xa0[4], xa1[4];
+        // mu in SMEM: the row stream evicts it from L1, and an L2 round trip per
+        // coordinate group was the loaders' largest stall
+        for (int e = (warp - Cfg::kLoaderBase) * 32 + lane; e < kTcKmax; e += Cfg::kLoaderWarps * 32)
+          smu[e] = e < P.d ? __ldg(P.mu + e) : 0.f;
+        asm volatile("bar.sync 3, %0;" ::"r"(Cfg::kLoaderWarps * 32) : "memory");
+        float4 xa0[4], xa1[4];  // the next two chunks of this thread's row (loads in flight)
         load_chunk(0, 0, xa0);
+        load_chunk(0, 1, xa1);
         int jcur = tile_j0(0);  // the current tile's origin center
+        int jnext = tile_j0(1);  // the next one's (origin indices are fetched a tile ahead of their use)
         if (bnd16 && my_tiles > 0) load_origin(jcur, og);
         const float cn_l = skip_on ? (float)__longlong_as_double((long long)__ldg(P.cmax)) : 0.f;
         long long l_start = clock64(), l_conv = 0, l_ucons = 0, l_mask = 0;
@@ -756,7 +771,8 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           float xs[4] = {0.f, 0.f, 0.f, 0.f};  // |x'|^2 chains over this row half
           float xq[4] = {0.f, 0.f, 0.f, 0.f};  // |x''|^2 chains
           bool big = false;
-          const int jn = tile_j0(t + 1);
+          const int jn = jnext;
+          jnext = tile_j0(t + 2);
           if (hh == 0) {  // the next tile's rows towards L2 while this one converts
             const uint64_t nrow = tile_p0(t + 1) + row;
             if (t + 1 < my_tiles && nrow < P.n) {
@@ -766,10 +782,14 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           }
 #pragma unroll
           for (int kc = 0; kc < 4; ++kc) {
-            float4 (&cur)[4] = (kc & 1) ? xa1 : xa0;
-            float4 (&nxt)[4] = (kc & 1) ? xa0 : xa1;
-            if (kc < 3) load_chunk(t, kc + 1, nxt);
-            else load_chunk(t + 1, 0, nxt);
+            float4 cur[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              cur[v] = xa0[v];
+              xa0[v] = xa1[v];
+            }
+            if (kc < 2) load_chunk(t, kc + 2, xa1);  // two chunks ahead
+            else load_chunk(t + 1, kc - 2, xa1);
             if (kc == 1 && bnd16 && t + 1 < my_tiles) load_origin(jn, ogn);
             if (kc >= nck) continue;
             uint32_t hp[8];
@@ -777,15 +797,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               const int e0 = kc * 32 + hh * 16 + 4 * v;
-              float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (P.d == kTcKmax) {
-                m4 = __ldg(reinterpret_cast<const float4*>(P.mu + e0));
-              } else {
-                if (e0 < P.d) m4.x = __ldg(P.mu + e0);
-                if (e0 + 1 < P.d) m4.y = __ldg(P.mu + e0 + 1);
-                if (e0 + 2 < P.d) m4.z = __ldg(P.mu + e0 + 2);
-                if (e0 + 3 < P.d) m4.w = __ldg(P.mu + e0 + 3);
-              }
+              const float4 m4 = reinterpret_cast<const float4*>(smu)[e0 >> 2];  // (zero past d)
               const float4 x = cur[v];
               const float x0 = valid ? x.x - m4.x : 0.f, x1 = valid ? x.y - m4.y : 0.f;
               const float x2 = valid ? x.z - m4.z : 0.f, x3 = valid ? x.w - m4.w : 0.f;
@@ -873,7 +885,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
               if (lane == 0) thmax[lg] = th;
             }
             asm volatile("bar.sync 3, %0;" ::"r"(Cfg::kLoaderWarps * 32) : "memory");
-            if (warp == 12 && lane == 0) {
+            if (warp == Cfg::kLoaderBase && lane == 0) {
               const float TH = fmaxf(fmaxf(thmax[0], thmax[1]), fmaxf(thmax[2], thmax[3]));
               uint32_t m = 0;
               const float* dr = P.dmin + (uint64_t)jcur * P.nct;
@@ -886,7 +898,7 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           if (P.dbg) l_mask += clock64() - l2;
           jcur = jn;
         }
-        if (P.dbg && warp == 12 && lane == 0) {
+        if (P.dbg && warp == Cfg::kLoaderBase && lane == 0) {
           unsigned long long* L = P.dbg + 148 * 8 + blockIdx.x * 8;
           L[0] = (unsigned long long)(clock64() - l_start);
           L[1] = (unsigned long long)l_conv;
@@ -912,16 +924,24 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
       }
       return o4;
     };
-    Top4 cur;
-    cur.init();
+    // 8 epilogue warps: warp w keeps the top-4 of column half w / 4; 4 warps
+    // (with loaders): each keeps both halves' lists
+    constexpr int kHalves = Cfg::kEpiWarps == 4 ? 2 : 1;
+    Top4 cur[kHalves];
+#pragma unroll
+    for (int hx = 0; hx < kHalves; ++hx) cur[hx].init();
     uint64_t eg = 0;  // center tiles drained so far (the MMA warp's accumulator order)
-    auto epilogue = [&](uint32_t t, int ct, Top4& top) {
+    auto epilogue = [&](uint32_t t, int ct, Top4* tops) {
       const uint64_t g = eg++;
       const int buf = (int)(g & 1);
-      const int lg = warp & 3, ch = warp >> 2;  // TMEM lane group, column half
+      const int lg = warp & 3;  // TMEM lane group
       if (getenv_sleep) mbar_wait_sleep(&accf[buf], (uint32_t)((g >> 1) & 1));
       else mbar_wait(&accf[buf], (uint32_t)((g >> 1) & 1));
       fence_after();
+#pragma unroll
+      for (int hx = 0; hx < kHalves; ++hx) {
+      const int ch = kHalves == 2 ? hx : (warp >> 2);  // column half
+      Top4& top = tops[hx];
       const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16) + buf * kTcN + ch * (kTcN / 2);
       if (P.prof == 0 || (P.prof >= 2 && P.prof <= 3) || P.prof >= 8) {
         const int cta = (int)((ct + rot) % P.nct);
@@ -975,18 +995,23 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
           }
         }
       }
+      }
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[buf]);  // the warp's TMEM reads are all done
     };
-    auto finish = [&](uint32_t t, int last_ct, Top4& top) {
-      epilogue(t, last_ct, top);
+    auto finish = [&](uint32_t t, int last_ct, Top4* tops) {
+      epilogue(t, last_ct, tops);
       const uint64_t i = (blockIdx.x + (uint64_t)t * gridDim.x) * kTcM + (warp & 3) * 32 + lane;
       if (i < P.n) {  // two column halves -> [n][8] of s = 2 * (s / 2) (exact); the classifier merges them
-        const int h = (warp >> 2) * 4;
-        *reinterpret_cast<float4*>(P.top_s + i * 8 + h) =
-            make_float4(oscale * top.s[0], oscale * top.s[1], oscale * top.s[2], oscale * top.s[3]);
-        *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
+#pragma unroll
+        for (int hx = 0; hx < kHalves; ++hx) {
+          const Top4& top = tops[hx];
+          const int h = (kHalves == 2 ? hx : (warp >> 2)) * 4;
+          *reinterpret_cast<float4*>(P.top_s + i * 8 + h) =
+              make_float4(oscale * top.s[0], oscale * top.s[1], oscale * top.s[2], oscale * top.s[3]);
+          *reinterpret_cast<int4*>(P.top_i + i * 8 + h) = make_int4(top.i[0], top.i[1], top.i[2], top.i[3]);
+        }
       }
     };
     // Point tiles travel global -> registers -> A.  The global loads of tile
@@ -1225,13 +1250,25 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
       }
       if (Cfg::kLocal) {  // both halves' |x''|^2, |x'|^2 and the E row are in SMEM
         asm volatile("bar.sync 1, %0;" ::"r"(kTcEpiThreads) : "memory");
-        cur.init(start_bound(t));
+        {
+          const float ub = start_bound(t);
+#pragma unroll
+          for (int hx = 0; hx < kHalves; ++hx) cur[hx].init(ub);
+        }
       } else if (Cfg::kLoader && bnd && P.prof != 9) {  // the loader warps have left this tile's |x''|^2, |x'|^2
         mbar_wait(&upf[t & 1], (t >> 1) & 1);
-        cur.init(start_bound(t));
+        {
+          const float ub = start_bound(t);
+#pragma unroll
+          for (int hx = 0; hx < kHalves; ++hx) cur[hx].init(ub);
+        }
       } else if (bnd && P.prof != 9) {  // the other half of these rows (warp w ^ 4) has left its |x''|^2, |x'|^2
         asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
-        cur.init(start_bound(t));
+        {
+          const float ub = start_bound(t);
+#pragma unroll
+          for (int hx = 0; hx < kHalves; ++hx) cur[hx].init(ub);
+        }
       }
       uint32_t mask = 0;
       if (skip_on) {
@@ -1249,7 +1286,9 @@ __global__ void __launch_bounds__(TcCfg<NPROD>::kThreads, 1) tc_screen_kernel(co
         if (!((mask >> ((ct + rot) % P.nct)) & 1u)) epilogue(t, ct, cur);
       if (more) store_chunks(t + 1);  // chunk kc as soon as tile t's last MMAs on it retire
       finish(t, last_ct, cur);
-      if (!bnd || P.prof == 9) cur.init();
+      if (!bnd || P.prof == 9)
+#pragma unroll
+        for (int hx = 0; hx < kHalves; ++hx) cur[hx].init();
     }
   }
   fence_before();
@@ -1504,7 +1543,7 @@ static int launch_screen(const TcParams& P, cudaStream_t s) {
                     TcCfg<NPROD>::kTmemCols, "TMEM map");
   const size_t smem = TcCfg<NPROD>::kSmemFixed + (P.c2res ? (size_t)kTcSliceBytes + (size_t)P.nct * kTcBSliceBytes : 0) +
                       (TcCfg<NPROD>::kLocal ? (size_t)2 * P.kpadE * sizeof(float) : 0) +
-                      (TcCfg<NPROD>::kF16 ? (size_t)2 * 128 * 2 * sizeof(float2) + 64 : 0);
+                      (TcCfg<NPROD>::kF16 ? (size_t)2 * 128 * 2 * sizeof(float2) + 64 + 512 : 0);
   GEEK_CHECK_CUDA(
       cudaFuncSetAttribute(tc_screen_kernel<NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 148, dev = 0;
@@ -1572,7 +1611,7 @@ int tc_screen_launch(const float* X, uint64_t n, int d, int nprod, const Scratch
   }
 #endif
   // resident |c'|^2 slices while they fit next to the operand buffers (227 KB)
-  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed + 2 * 128 * 2 * sizeof(float2) + 64
+  P.c2res = (nprod == 16 ? TcCfg<16>::kSmemFixed + 2 * 128 * 2 * sizeof(float2) + 64 + 512
               : nprod == 3 ? TcCfg<3>::kSmemFixed : TcCfg<1>::kSmemFixed) + (size_t)kTcSliceBytes + (size_t)nct * kTcBSliceBytes <= 227 * 1024
                 ? 1 : 0;
   if (nprod == 17) P.c2res = 0;  // E carries |c'|^2
