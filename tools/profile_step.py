@@ -11,6 +11,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2106_10515_b200 as G  # noqa: E402
+from paper_2106_10515_b200 import _lib  # noqa: E402
+
+if os.environ.get("PROBE_DEBUG"):  # the -DGEEK_DEBUG_KNOBS build (tools/build_debug.py)
+    _lib.load_library(os.path.join(os.path.dirname(_lib.LIB_PATH), "libgeek_dbg.so"))
 from paper_2106_10515_b200.synth import gaussian_mixture_device  # noqa: E402
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10_000_000
