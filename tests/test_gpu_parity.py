@@ -128,9 +128,18 @@ def test_rank_split_edge_cases():
         G.transform_homo(G.DenseData(np.zeros((3, 2))), G.HomoTransformParams(1, 4))
 
 
+@pytest.mark.parametrize("path", ["grouped", "per-bin", "coarse-groups"])
 @pytest.mark.parametrize("n,t,dup", [(20_000, 3, True), (50_000, 997, False), (30_000, 30_000, False),
                                      (123_457, 1000, False)])
-def test_rank_split_random_vs_oracle(n, t, dup):
+def test_rank_split_random_vs_oracle(n, t, dup, path, monkeypatch):
+    """(path: the grouped split -- SMEM group counts, fine counts only in
+    straddling groups, group codes -- the per-bin split of round 1, and coarse
+    2^7 code groups over 2^3 counting groups)"""
+    if path == "per-bin":
+        monkeypatch.setenv("GEEK_SPLIT_GROUPS", "0")
+    elif path == "coarse-groups":
+        monkeypatch.setenv("GEEK_SPLIT_GROUPS", "7")
+        monkeypatch.setenv("GEEK_SPLIT_CSHIFT", "3")
     rng = np.random.default_rng(n + t)
     X = rng.standard_normal((n, 5)).astype(np.float32)
     if dup:  # giant tie classes exercise the sorted fallback

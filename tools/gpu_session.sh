@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests/ -q -x -m gpu > gpurun_out/t_all.log 2>&1
-echo "rc=$?" >> gpurun_out/t_all.log
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_skip.json 2> gpurun_out/bench_skip.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "rank_split" > gpurun_out/t_rs.log 2>&1
+echo "rc=$?" >> gpurun_out/t_rs.log
