@@ -3,6 +3,7 @@
 // uint64 keys for the rank split.  HBM-streaming: X is read once per table
 // block through shared memory; directions stay resident in shared memory.
 #include "common.cuh"
+#include "project.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -292,27 +293,6 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Where table t's key of local point p goes: dst[t % G] + (t / G) * ntot +
-// row_lo + p.  G = 1 is the local [m][n] array; G > 1 stores every key
-// straight into its owner rank's buffer (peer memory over NVLink), which is
-// the bucket synchronisation of engine.py:199-238 without a separate
-// all-to-all.
-constexpr int kMaxKeyDst = 8;
-constexpr int kMaxKeyTables = 48;
-struct KeyDst {
-  uint64_t* ptr[kMaxKeyDst];
-  int G;
-  uint64_t ntot, row_lo;
-  uint64_t* tptr[kMaxKeyTables];  // table t's row-0 address for this shard (host-computed)
-  int vec16;                      // every tptr is 16-byte aligned: 16-byte stores
-  // optional fused fine-bin histogram of the rank split (fine_hist_kernel's
-  // count, done here while the key is in a register): cinfo [m][2^cb] of
-  // (fine bins, first global fine bin) per coarse cell, counters fcnt
-  const uint2* cinfo;
-  uint32_t* fcnt;
-  int cb;
-};
-
 template <int NT>
 __global__ void __launch_bounds__(128, 2) project_stream_kernel(const float* __restrict__ X, uint64_t n, int d,
                                                                 const double* __restrict__ A, int m,
@@ -499,7 +479,9 @@ static int launch_stream_any(const float* X, uint64_t n, int d, const double* A,
     GEEK_CHECK_CUDA(cudaMemsetAsync(flag.ptr, 0, 4, s));
     nf = flag.as<unsigned>();
   }
-  switch ((m + 7) / 8) {
+  bool tc = false;
+  GEEK_TRY(tc_project_launch(X, n, d, A, m, keys, er, nf, s, &tc));
+  if (!tc) switch ((m + 7) / 8) {
     case 1: GEEK_TRY(launch_stream<1>(X, n, d, A, m, keys, er, nf, s)); break;
     case 2: GEEK_TRY(launch_stream<2>(X, n, d, A, m, keys, er, nf, s)); break;
     case 3: GEEK_TRY(launch_stream<3>(X, n, d, A, m, keys, er, nf, s)); break;

@@ -34,6 +34,7 @@
 // SBO between M/N-adjacent core matrices (validated on the GPU by
 // geek_tc_selftest).
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 #include <cuda_fp16.h>
 
@@ -123,17 +124,10 @@ __host__ __device__ inline uint64_t tc_ct_bytes(int d, int parts, int chunk_dims
   return (uint64_t)((d + chunk_dims - 1) / chunk_dims) * parts * slices * kTcBSliceBytes + kTcC2Bytes;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 // byte offset of element (row r, k e) inside one K=8 slice of a 128-row operand
 __device__ __forceinline__ uint32_t core_off(int r, int e, uint32_t lbo, uint32_t sbo) {
   return (r >> 3) * sbo + (e >> 2) * lbo + (r & 7) * 16 + (e & 3) * 4;
-}
-// the same for byte kb (0..31) of row r's 32-byte slice row (any element size)
-__device__ __forceinline__ uint32_t core_off_b(int r, int kb, uint32_t lbo, uint32_t sbo) {
-  return (r >> 3) * sbo + (kb >> 4) * lbo + (r & 7) * 16 + (kb & 15);
 }
 
 __device__ __forceinline__ float tf32_round(float x) {
@@ -144,14 +138,6 @@ __device__ __forceinline__ float tf32_round(float x) {
 
 __device__ __forceinline__ uint64_t desc_of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); base offset 0, SWIZZLE_NONE
-  return d;
-}
 
 // kind::tf32 (A=B=tf32, format 2) or kind::f16 (A=B=f16, format 0); D=f32,
 // K-major both, N>>3 at [17,23), M>>4 at [24,29)
@@ -160,44 +146,14 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool f16 = false
          ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
-// the epilogue warps' waits: try_wait with a suspend-time hint, so a waiting
-// warp sleeps until the phase completes instead of re-polling the barrier
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITS_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITS_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x100000)
-      : "memory");
-}
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -276,10 +232,6 @@ __device__ __forceinline__ void tc_st16u(uint32_t taddr, const uint32_t* v) {
 
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
 
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -317,21 +269,7 @@ __device__ __forceinline__ void tc_regs_ready(float* v) {
   asm volatile("" : "+f"(v[0]),"+f"(v[1]),"+f"(v[2]),"+f"(v[3]),"+f"(v[4]),"+f"(v[5]),"+f"(v[6]),"+f"(v[7]),"+f"(v[8]),"+f"(v[9]),"+f"(v[10]),"+f"(v[11]),"+f"(v[12]),"+f"(v[13]),"+f"(v[14]),"+f"(v[15]),"+f"(v[16]),"+f"(v[17]),"+f"(v[18]),"+f"(v[19]),"+f"(v[20]),"+f"(v[21]),"+f"(v[22]),"+f"(v[23]),"+f"(v[24]),"+f"(v[25]),"+f"(v[26]),"+f"(v[27]),"+f"(v[28]),"+f"(v[29]),"+f"(v[30]),"+f"(v[31]) :: "memory");
 }
 
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n"
-      ".reg .pred P;\n"
-      "elect.sync _|P, 0xffffffff;\n"
-      "selp.b32 %0, 1, 0, P;\n"
-      "}\n"
-      : "=r"(pred));
-  return pred != 0;
-}
 
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 struct Top4 {
   float s[4];

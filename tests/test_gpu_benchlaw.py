@@ -52,8 +52,13 @@ def _sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def test_benchlaw_codes_and_boundary_counts(law):
+@pytest.mark.parametrize("proj", ["dmma", "tcgen05"])
+def test_benchlaw_codes_and_boundary_counts(law, proj, monkeypatch):
+    """(proj: K1 on DMMA, the default, or on kind::i8 tcgen05 digits, GEEK_TCPROJ=1)"""
     from paper_2106_10515_b200 import transform as T
+
+    if proj == "tcgen05":
+        monkeypatch.setenv("GEEK_TCPROJ", "1")
 
     m, arr, X = law
     n, t = m["n"], m["t"]

@@ -178,7 +178,11 @@ def test_codes_golden(name):
     assert np.array_equal(bt.codes_host(), arr[name + "_codes"])
 
 
-def test_cfg1_codes_golden_sha():
+@pytest.mark.parametrize("proj", ["dmma", "tcgen05"])
+def test_cfg1_codes_golden_sha(proj, monkeypatch):
+    """(proj: K1 on DMMA, the default, or on kind::i8 tcgen05 digits, GEEK_TCPROJ=1)"""
+    if proj == "tcgen05":
+        monkeypatch.setenv("GEEK_TCPROJ", "1")
     m = meta()["pipelines"]["cfg1"]
     _, n, d, C, sep, seed = m["spec"]
     X, _ = O.gaussian_mixture(n, d, C, sep, seed)
@@ -677,6 +681,78 @@ def test_singleton_bins_equal_group_by(K, G_, delta):
         assert torch.equal(getattr(a, f), getattr(b, f)), f
     # some kept bins do mix singletons with larger buckets
     assert bool((sizes[b.pair_bucket] == 1).any())
+
+
+def _key_values(k):
+    """float64 values of f64_key's order-preserving uint64 keys (common.cuh)."""
+    u = k.astype(np.uint64)
+    neg = (u & np.uint64(1 << 63)) == 0
+    b = np.where(neg, ~u, u & np.uint64((1 << 63) - 1))
+    return b.view(np.float64)
+
+
+def _exact_dot_err(X, A, V, rows):
+    """|V - exact X @ A.T| for the sampled rows, with exact rational sums."""
+    from fractions import Fraction
+    out = np.zeros((len(rows), A.shape[0]))
+    for r, i in enumerate(rows):
+        xs = [Fraction(float(v)) for v in X[i]]
+        for j in range(A.shape[0]):
+            ex = sum(x * Fraction(float(a)) for x, a in zip(xs, A[j]))
+            out[r, j] = abs(float(Fraction(float(V[j, i])) - ex)) if np.isfinite(V[j, i]) else 0.0
+    return out
+
+
+@pytest.mark.parametrize("n,d,m,case", [(1000, 128, 40, "gauss"), (777, 4, 3, "gauss"), (3001, 36, 20, "tiny"),
+                                        (2048, 100, 8, "wide"), (513, 64, 48, "gauss"), (300, 128, 1, "special"),
+                                        (5000, 128, 48, "gauss")])
+def test_tc_projection_keys(n, d, m, case, monkeypatch):
+    """K1 on kind::i8 tcgen05 MMAs (tc_project.cu, GEEK_TCPROJ=1): every key within the
+    float64 order bound (gamma_d 2^xmax |a|_1) of the exact dot product --
+    checked with rational arithmetic on sampled rows -- so within
+    projection_tolerance of numpy's BLAS keys and of the DMMA kernel's; the
+    exponent window equals the DMMA pass's.  Cases: Gaussian rows, rows with
+    elements 2^16..2^30 below their maximum (the remainder path), rows
+    spanning many binades, and special rows (zeros, subnormal, huge, inf)."""
+    from paper_2106_10515_b200 import transform as T
+    rng = np.random.default_rng(n * 7 + d)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    if case == "tiny":
+        mask = rng.random((n, d)) < 0.05
+        X[mask] *= np.float32(2.0) ** -rng.integers(16, 30, mask.sum()).astype(np.float32)
+    elif case == "wide":
+        X *= (np.float32(2.0) ** rng.integers(-20, 20, (n, 1))).astype(np.float32)
+        X[:, ::7] *= np.float32(1e-6)
+    elif case == "special":
+        X[0] = 0
+        X[1] = np.float32(1e-42)
+        X[2, 5] = np.float32(2.0 ** 60)
+        X[3, 7] = np.inf
+        X[4] *= np.float32(2.0 ** -100)
+    A = O.directions(5, m, d)
+    Xd = torch.from_numpy(X).cuda()
+
+    def run():
+        er = torch.tensor([2 ** 30, -2 ** 30], dtype=torch.int32, device="cuda")
+        k = T.project_keys(Xd, A, er).cpu().numpy()
+        return _key_values(k), er.cpu().numpy()
+
+    monkeypatch.setenv("GEEK_TCPROJ", "1")
+    V, er = run()
+    monkeypatch.delenv("GEEK_TCPROJ")
+    Vd, erd = run()
+    assert np.array_equal(er, erd)
+    fin = np.isfinite(X).all(1)
+    xmax = int(np.frexp(np.abs(X[fin]).max())[1])
+    tol = T.projection_tolerance(A, xmax)[:, None]
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = (X[fin].astype(np.float64) @ A.T).T
+    assert (np.abs(V[:, fin] - ref) <= tol).all()
+    assert (np.abs(V[:, fin] - Vd[:, fin]) <= tol).all()
+    assert np.array_equal(np.isnan(V[:, ~fin]), np.isnan(Vd[:, ~fin]))
+    rows = [i for i in np.linspace(0, n - 1, 12).astype(int) if fin[i]]
+    err = _exact_dot_err(X, A, V, rows)
+    assert (err <= tol.T / 2).all(), (err / (tol.T / 2)).max()
 
 
 @pytest.mark.parametrize("owners", [2, 3, 8])
