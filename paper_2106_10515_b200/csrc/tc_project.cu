@@ -281,8 +281,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
       // x = 2^(e_r-39) F + rho, F = trunc(x 2^(39-e_r)) (any integer's two's
       // complement bytes are its digits); rho != 0 only for |x| < 2^(e_r-16),
       // and rho (the tail of x's significand) is exact in float32
-      int nrl = 0;
-      uint2 re0 = make_uint2(0u, 0u), re1 = make_uint2(0u, 0u);
+      uint32_t rb = 0u;  // elements with a remainder (bit 4c + e), branch-free in the digit loop
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < nc) {
@@ -295,12 +294,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
             const long long F = __float2ll_rz(ty);
             lo[e] = (uint32_t)F;
             hi[e] = (uint32_t)((unsigned long long)F >> 32);
-            if ((__float_as_uint(f[e]) & 0x7FFFFFFFu) - 1u < rthr && ty != y) {
-              const uint2 en = make_uint2((uint32_t)(16 * c + 4 * q + e), __float_as_uint((y - ty) * rback));
-              if (nrl == 0) re0 = en;
-              else if (nrl == 1) re1 = en;
-              ++nrl;
-            }
+            rb |= ((__float_as_uint(f[e]) & 0x7FFFFFFFu) - 1u < rthr && ty != y ? 1u : 0u) << (c * 4 + e);
           }
           const uint32_t t0 = __byte_perm(lo[0], lo[1], 0x5140), t1 = __byte_perm(lo[0], lo[1], 0x7362);
           const uint32_t u0 = __byte_perm(lo[2], lo[3], 0x5140), u1 = __byte_perm(lo[2], lo[3], 0x7362);
@@ -315,7 +309,23 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
           for (int s = 0; s < kPjXd; ++s) *reinterpret_cast<uint32_t*>(Ab + (uint32_t)(s * nks) * kPjStep + off) = w[s];
         }
       }
-      if (special) nrl = 0;
+      // the rare remainder entries (x re-read from L2): at most 2 per lane kept
+      int nrl = 0;
+      uint2 re0 = make_uint2(0u, 0u), re1 = make_uint2(0u, 0u);
+      if (rb && !special) {
+        const uint64_t row = (blockIdx.x + ti * gridDim.x) * kPjM + rl;
+#pragma unroll 1
+        while (rb) {
+          const int bi = __ffs(rb) - 1;
+          rb &= rb - 1u;
+          const int k = 16 * (bi >> 2) + 4 * q + (bi & 3);
+          const float y = __ldg(P.X + row * P.d + k) * scale;
+          const uint2 en = make_uint2((uint32_t)k, __float_as_uint((y - truncf(y)) * rback));
+          if (nrl == 0) re0 = en;
+          else if (nrl == 1) re1 = en;
+          ++nrl;
+        }
+      }
       // the row's entries: exclusive scan over its 4 lanes, at most 2 kept
       const int qbase = lane & ~3;
       const int c1 = __shfl_sync(0xffffffffu, nrl, qbase), c2 = __shfl_sync(0xffffffffu, nrl, qbase + 1),
@@ -472,33 +482,43 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
               if (nr > 1) corr[qj] = fma(r1, __ldg(a + k1), corr[qj]);
             }
           }
+          // branch-free per table: the keys first, then predicated global stores
+          uint64_t kk[8];
+          if (!nr) {
 #pragma unroll
-          for (int qj = 0; qj < 8; ++qj) {  // no calls in here: the 8 tables' chains interleave
-            const int j = gq * 8 + qj;
-            if ((full || j < P.m) && !(fma_row && (frow || tsc[j] == 0.0))) {
-              uint64_t bv;
-              if (nr) {
-                const double key = w[qj] * (rs * tsc[j]) + corr[qj];
-                bv = key == 0.0 ? 0ull : static_cast<uint64_t>(__double_as_longlong(key));
-              } else {
-                // w is 0 or an integer-valued double >= 1 in magnitude: scaling by
-                // 2^(e_r + e_j - 69) is an add to its exponent field (the result stays normal)
-                const uint64_t wb = static_cast<uint64_t>(__double_as_longlong(w[qj]));
-                bv = wb ? wb + (static_cast<uint64_t>(static_cast<int64_t>(erb + tse[j])) << 52) : 0ull;
-              }
-              const uint64_t kk = bv ^ (static_cast<uint64_t>(static_cast<long long>(bv) >> 63) | 0x8000000000000000ull);
-              if (P.prof != 1 || kk == 7) tpp[j][row] = kk;
-              if (P.dst.fcnt) pj_count(P.dst, j, kk);
+            for (int qj = 0; qj < 8; ++qj) {
+              // w is 0 or an integer-valued double >= 1 in magnitude: scaling by
+              // 2^(e_r + e_j - 69) is an add to its exponent field (the result stays normal)
+              const uint64_t wb = static_cast<uint64_t>(__double_as_longlong(w[qj]));
+              const uint64_t bv = wb ? wb + (static_cast<uint64_t>(static_cast<int64_t>(erb + tse[gq * 8 + qj])) << 52) : 0ull;
+              kk[qj] = bv ^ (static_cast<uint64_t>(static_cast<long long>(bv) >> 63) | 0x8000000000000000ull);
+            }
+          } else {
+#pragma unroll
+            for (int qj = 0; qj < 8; ++qj) {
+              const double key = w[qj] * (rs * tsc[gq * 8 + qj]) + corr[qj];
+              const uint64_t bv = key == 0.0 ? 0ull : static_cast<uint64_t>(__double_as_longlong(key));
+              kk[qj] = bv ^ (static_cast<uint64_t>(static_cast<long long>(bv) >> 63) | 0x8000000000000000ull);
             }
           }
-          if (fma_row) {
-#pragma unroll 1
+#pragma unroll
+          for (int qj = 0; qj < 8; ++qj)
+            if (full || gq * 8 + qj < P.m)
+              asm volatile("st.global.u64 [%0], %1;" ::"l"(tpp[gq * 8 + qj] + row), "l"(kk[qj]) : "memory");
+          if (P.dst.fcnt && !fma_row) {
+#pragma unroll
+            for (int qj = 0; qj < 8; ++qj)
+              if (gq * 8 + qj < P.m) pj_count(P.dst, gq * 8 + qj, kk[qj]);
+          }
+          if (fma_row) {  // special rows / tables: float64 FMAs overwrite the keys
+#pragma unroll
             for (int qj = 0; qj < 8; ++qj) {
               const int j = gq * 8 + qj;
-              if (j < P.m && (frow || tsc[j] == 0.0)) {
-                const uint64_t kk = pj_fma_key(P.X, P.A, P.d, row, j);
-                P.dst.tptr[j][row] = kk;
-                if (P.dst.fcnt) pj_count(P.dst, j, kk);
+              if (j < P.m) {
+                const bool fm = frow || tsc[j] == 0.0;
+                const uint64_t k2 = fm ? pj_fma_key(P.X, P.A, P.d, row, j) : kk[qj];
+                if (fm) P.dst.tptr[j][row] = k2;
+                if (P.dst.fcnt) pj_count(P.dst, j, k2);
               }
             }
           }
