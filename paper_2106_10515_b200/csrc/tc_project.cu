@@ -289,12 +289,11 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float y = f[e] * scale;
-            const float ty = truncf(y);
-            const long long F = __float2ll_rz(ty);
+            const long long F = __float2ll_rz(f[e] * scale);
             lo[e] = (uint32_t)F;
             hi[e] = (uint32_t)((unsigned long long)F >> 32);
-            rb |= ((__float_as_uint(f[e]) & 0x7FFFFFFFu) - 1u < rthr && ty != y ? 1u : 0u) << (c * 4 + e);
+            // candidates only (|x| < 2^(e_r-16)); the rare pass below keeps those with rho != 0
+            rb |= ((__float_as_uint(f[e]) & 0x7FFFFFFFu) - 1u < rthr ? 1u : 0u) << (c * 4 + e);
           }
           const uint32_t t0 = __byte_perm(lo[0], lo[1], 0x5140), t1 = __byte_perm(lo[0], lo[1], 0x7362);
           const uint32_t u0 = __byte_perm(lo[2], lo[3], 0x5140), u1 = __byte_perm(lo[2], lo[3], 0x7362);
@@ -320,10 +319,13 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
           rb &= rb - 1u;
           const int k = 16 * (bi >> 2) + 4 * q + (bi & 3);
           const float y = __ldg(P.X + row * P.d + k) * scale;
-          const uint2 en = make_uint2((uint32_t)k, __float_as_uint((y - truncf(y)) * rback));
-          if (nrl == 0) re0 = en;
-          else if (nrl == 1) re1 = en;
-          ++nrl;
+          const float rho = (y - truncf(y)) * rback;  // exact: the tail of x's significand
+          if (rho != 0.f) {
+            const uint2 en = make_uint2((uint32_t)k, __float_as_uint(rho));
+            if (nrl == 0) re0 = en;
+            else if (nrl == 1) re1 = en;
+            ++nrl;
+          }
         }
       }
       // the row's entries: exclusive scan over its 4 lanes, at most 2 kept
@@ -502,9 +504,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
             }
           }
 #pragma unroll
-          for (int qj = 0; qj < 8; ++qj)
+          for (int qj = 0; qj < 8; ++qj)  // streaming global stores the compiler may schedule freely
             if (full || gq * 8 + qj < P.m)
-              asm volatile("st.global.u64 [%0], %1;" ::"l"(tpp[gq * 8 + qj] + row), "l"(kk[qj]) : "memory");
+              __stcs(reinterpret_cast<unsigned long long*>(tpp[gq * 8 + qj] + row), (unsigned long long)kk[qj]);
           if (P.dst.fcnt && !fma_row) {
 #pragma unroll
             for (int qj = 0; qj < 8; ++qj)
@@ -535,9 +537,9 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
 int tc_project_launch(const float* X, uint64_t n, int d, const double* A, int m, const KeyDst& dst, int* er,
                       unsigned* nf, cudaStream_t s, bool* used) {
   *used = false;
-  // opt-in (GEEK_TCPROJ=1): parity-green, but the DMMA stream kernel is faster on B200 (K1t)
+  // the default K1 where it fits; GEEK_TCPROJ=0 selects the DMMA stream kernel (K1t)
   const char* on = getenv("GEEK_TCPROJ");
-  if (!on || !atoi(on) || d < 4 || d > 128 || d % 4 || m < 1 || m > kMaxKeyTables) return GEEK_OK;
+  if ((on && !atoi(on)) || d < 4 || d > 128 || d % 4 || m < 1 || m > kMaxKeyTables) return GEEK_OK;
   const int mp = (m + 7) / 8 * 8, kp = (d + 31) / 32 * 32, nks = kp / 32;
   const size_t abytes = (size_t)kPjXd * nks * kPjStep, pk = (size_t)11 * mp * 32;
   const size_t smem = 2 * abytes + nks * pk + kMaxKeyTables * 20 + kPjSlots * kPjM * 2 + kPjSlots * kPjM * 16 + 8 * 8 + 16;

@@ -54,11 +54,11 @@ def _sha(a):
 
 @pytest.mark.parametrize("proj", ["dmma", "tcgen05"])
 def test_benchlaw_codes_and_boundary_counts(law, proj, monkeypatch):
-    """(proj: K1 on DMMA, the default, or on kind::i8 tcgen05 digits, GEEK_TCPROJ=1)"""
+    """(proj: K1 on kind::i8 tcgen05 digits, the default, or on DMMA, GEEK_TCPROJ=0)"""
     from paper_2106_10515_b200 import transform as T
 
-    if proj == "tcgen05":
-        monkeypatch.setenv("GEEK_TCPROJ", "1")
+    if proj == "dmma":
+        monkeypatch.setenv("GEEK_TCPROJ", "0")
 
     m, arr, X = law
     n, t = m["n"], m["t"]

@@ -180,9 +180,9 @@ def test_codes_golden(name):
 
 @pytest.mark.parametrize("proj", ["dmma", "tcgen05"])
 def test_cfg1_codes_golden_sha(proj, monkeypatch):
-    """(proj: K1 on DMMA, the default, or on kind::i8 tcgen05 digits, GEEK_TCPROJ=1)"""
-    if proj == "tcgen05":
-        monkeypatch.setenv("GEEK_TCPROJ", "1")
+    """(proj: K1 on kind::i8 tcgen05 digits, the default, or on DMMA, GEEK_TCPROJ=0)"""
+    if proj == "dmma":
+        monkeypatch.setenv("GEEK_TCPROJ", "0")
     m = meta()["pipelines"]["cfg1"]
     _, n, d, C, sep, seed = m["spec"]
     X, _ = O.gaussian_mixture(n, d, C, sep, seed)
@@ -707,7 +707,7 @@ def _exact_dot_err(X, A, V, rows):
                                         (2048, 100, 8, "wide"), (513, 64, 48, "gauss"), (300, 128, 1, "special"),
                                         (5000, 128, 48, "gauss")])
 def test_tc_projection_keys(n, d, m, case, monkeypatch):
-    """K1 on kind::i8 tcgen05 MMAs (tc_project.cu, GEEK_TCPROJ=1): every key within the
+    """K1 on kind::i8 tcgen05 MMAs (tc_project.cu, the default): every key within the
     float64 order bound (gamma_d 2^xmax |a|_1) of the exact dot product --
     checked with rational arithmetic on sampled rows -- so within
     projection_tolerance of numpy's BLAS keys and of the DMMA kernel's; the
@@ -737,10 +737,9 @@ def test_tc_projection_keys(n, d, m, case, monkeypatch):
         k = T.project_keys(Xd, A, er).cpu().numpy()
         return _key_values(k), er.cpu().numpy()
 
-    monkeypatch.setenv("GEEK_TCPROJ", "1")
-    V, er = run()
-    monkeypatch.delenv("GEEK_TCPROJ")
-    Vd, erd = run()
+    V, er = run()  # K1 on tcgen05 (the default)
+    monkeypatch.setenv("GEEK_TCPROJ", "0")
+    Vd, erd = run()  # K1 on DMMA
     assert np.array_equal(er, erd)
     fin = np.isfinite(X).all(1)
     xmax = int(np.frexp(np.abs(X[fin]).max())[1])
