@@ -145,7 +145,9 @@ def rank_split_codes(keys: torch.Tensor, t: int, stats=None) -> torch.Tensor:
 
 def projection_tolerance(A: np.ndarray, xmax_exp: int) -> np.ndarray:
     """Per-table bound on |K1 key - reference key| (transform.py:125 / engine.py:180
-    form X @ a with OpenBLAS dgemv; K1 with DMMA FMA chains).  Any float64
+    form X @ a with OpenBLAS dgemv; K1 with exact integer tensor-core products
+    rounded within 2^-6 of the same bound plus 2 ulps, tc_project.cu, or with
+    DMMA FMA chains under GEEK_TCPROJ=0).  Any float64
     summation order of d products is within gamma_d * sum_k |x_k a_k| of the
     exact dot product (gamma_d = d u / (1 - d u), u = 2^-53), and
     sum_k |x_k a_k| <= 2^xmax_exp * |a|_1 when every |x_k| < 2^xmax_exp, so
