@@ -173,9 +173,11 @@ __device__ __noinline__ uint64_t pj_fma_key(const float* X, const double* A, int
     if (P.tl && blockIdx.x == 0 && (ti) < 64) P.tl[(ti) * 8 + (k)] = clock64();           \
   } while (0)
 
+template <int NKS>  // 32-dim K steps (d <= 32 NKS): compile-time digit-tile offsets
 __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int nks = P.kp >> 5, mp = P.mp;
+  constexpr int nks = NKS;
+  const int mp = P.mp;
   const uint32_t abytes = (uint32_t)kPjXd * nks * kPjStep;
   const uint32_t pk = (uint32_t)11 * mp * 32;  // bytes of one K step of the B image
   const uint32_t nb = 4 * mp;                  // accumulator columns of one level block
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
     // loader warps); lane (row r8 = lane / 4, quarter q = lane % 4) holds
     // dims 16c + 4q .. +3 of its row; the next group's rows are in flight
     const int lw = warp - kPjLoadBase, r8 = lane >> 2, q = lane & 3;
-    const int nc = P.kp >> 4;  // 16-dim chunks
+    constexpr int nc = 2 * NKS;  // 16-dim chunks
     uint32_t amax = 0u, amin = 0xFFFFFFFFu;
     const uint64_t items = my_tiles * (kPjM / 8);
     float4 cur[8], nxt[8];
@@ -578,11 +580,20 @@ int tc_project_launch(const float* X, uint64_t n, int d, const double* A, int m,
     P.tl = tl_buf;
   }
 #endif
-  GEEK_CHECK_CUDA(cudaFuncSetAttribute(tc_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint64_t ntiles = (n + kPjM - 1) / kPjM;
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms);
-  tc_project_kernel<<<grid, kPjThreads, smem, s>>>(P);
-  GEEK_CHECK_LAUNCH();
+  auto go = [&](auto kern) -> int {
+    GEEK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, kPjThreads, smem, s>>>(P);
+    GEEK_CHECK_LAUNCH();
+    return GEEK_OK;
+  };
+  switch (nks) {
+    case 1: GEEK_TRY(go(tc_project_kernel<1>)); break;
+    case 2: GEEK_TRY(go(tc_project_kernel<2>)); break;
+    case 3: GEEK_TRY(go(tc_project_kernel<3>)); break;
+    default: GEEK_TRY(go(tc_project_kernel<4>)); break;
+  }
 #ifdef GEEK_DEBUG_KNOBS
   if (P.tl) {  // per-tile phase durations of CTA 0 (clock64 deltas, tiles 8..63)
     unsigned long long h[64 * 8];
