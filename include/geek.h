@@ -91,7 +91,11 @@ int geek_silk_invscan(const uint32_t* codes, uint64_t n, int m, uint64_t t,
  * onto the top key, matching np.lexsort.  dtype 0 = float32 X, 1 = float64.
  * `exprange` (device int[2], may be NULL; caller initialises {INT_MAX-ish,
  * INT_MIN-ish}) receives atomic min/max of the exact-sum exponent window of
- * X (as geek_exponent_range), fused into the same pass over X.              */
+ * X (as geek_exponent_range), fused into the same pass over X.  float32 rows
+ * with d % 4 == 0, d <= 128 (and the digit tiles within SMEM: m <= 40 at
+ * d = 128) run as exact integer-digit products on tcgen05 (kind::i8), keys
+ * within the float64 order bound of the exact dot product; other shapes and
+ * GEEK_TCPROJ=0 use float64 DMMA / FMA chains.                              */
 int geek_project_keys(const void* X, int dtype, uint64_t n, int d, const double* A, int m,
                       uint64_t* keys, int* exprange, void* stream);
 
