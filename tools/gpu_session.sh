@@ -1,5 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_benchlaw.py -q -k "tc_projection or cfg1_codes or benchlaw_codes or routed or counted or streamed" > gpurun_out/t_tcp.log 2>&1
-echo "rc=$?" >> gpurun_out/t_tcp.log
-PROBE_DEBUG=1 GEEK_PJ_TIMELINE=1 timeout 300 python tools/profile_step.py 2e7 > gpurun_out/tl0.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"project" --csv python tools/profile_step.py 2e7 > gpurun_out/tcp_launch.csv 2>&1
+timeout 2400 python -m pytest tests/ -q -m gpu > gpurun_out/final_gpu_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/final_gpu_tests.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1
+timeout 1200 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
+timeout 900 python bench.py --impl reference > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err
