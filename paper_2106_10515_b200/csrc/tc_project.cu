@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
   uint8_t* Abuf = smem;                        // [2][kPjXd][nks][4 KB]
   uint8_t* Pb = smem + 2 * abytes;             // [nks][11 mp rows]
   double* tsc = reinterpret_cast<double*>(Pb + nks * pk);           // [48]: 2^(e_j - 69), 0 = special table
-  int* tse = reinterpret_cast<int*>(tsc + kMaxKeyTables);            // [48]: e_j - 69 (exponent-field add)
+  int* tse = reinterpret_cast<int*>(tsc + kMaxKeyTables);            // [48]: (e_j - 69) 2^20 (exponent-field add)
   uint64_t** tpp = reinterpret_cast<uint64_t**>(tse + kMaxKeyTables);  // [48]: the key destinations
   uint16_t* meta = reinterpret_cast<uint16_t*>(tpp + kMaxKeyTables);  // [slots][128]: e_r + 128 | nrem << 8 | fma << 10
   uint2* rems = reinterpret_cast<uint2*>(meta + kPjSlots * kPjM);  // [slots][128][2]: (k, rho_k as f32)
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
     for (int j = threadIdx.x; j < kMaxKeyTables; j += blockDim.x) {
       const int e = j < P.m ? P.ej[j] : kPjSpecialE;
       tsc[j] = e == kPjSpecialE ? 0.0 : pj_pow2(e - 69);  // 2^(e_j - 13) 2^-56
-      tse[j] = e == kPjSpecialE ? 0 : e - 69;
+      tse[j] = e == kPjSpecialE ? 0 : (e - 69) * (1 << 20);  // the exponent-field add, high word
       tpp[j] = P.dst.tptr[j];
     }
   }
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
       const int er = (int)(mt & 0xFF) - 128;
       const bool frow = (mt >> 10) & 1u;  // special row or > 2 remainder elements
       const double rs = pj_pow2(er);
-      const int erb = er;  // + tse[j]: the exponent-field add of the fast keys
+      const uint32_t erb20 = (uint32_t)(er * (1 << 20));  // + tse[j]: the exponent-field add of the fast keys
       // drain: every group of 8 tables -> sum_l 2^(-8l) D_l as a float64 (one
       // rounding), then release both TMEM slots before the key stores
       constexpr int kMaxG = (kMaxKeyTables / 8 + 1) / 2;  // column groups per warp
@@ -493,9 +493,12 @@ __global__ void __launch_bounds__(kPjThreads, 1) tc_project_kernel(const PjParam
             for (int qj = 0; qj < 8; ++qj) {
               // w is 0 or an integer-valued double >= 1 in magnitude: scaling by
               // 2^(e_r + e_j - 69) is an add to its exponent field (the result stays normal)
-              const uint64_t wb = static_cast<uint64_t>(__double_as_longlong(w[qj]));
-              const uint64_t bv = wb ? wb + (static_cast<uint64_t>(static_cast<int64_t>(erb + tse[gq * 8 + qj])) << 52) : 0ull;
-              kk[qj] = bv ^ (static_cast<uint64_t>(static_cast<long long>(bv) >> 63) | 0x8000000000000000ull);
+              // on the 32-bit halves: the exponent add touches the high word only (w is 0,
+              // or >= 1 in magnitude so its high word is nonzero), then the order transform
+              const uint32_t wl = (uint32_t)__double2loint(w[qj]), wh = (uint32_t)__double2hiint(w[qj]);
+              const uint32_t h2 = wh ? wh + erb20 + (uint32_t)tse[gq * 8 + qj] : 0u;
+              const uint32_t sg = (uint32_t)((int32_t)h2 >> 31);
+              kk[qj] = ((uint64_t)(h2 ^ (sg | 0x80000000u)) << 32) | (uint64_t)(wl ^ sg);
             }
           } else {
 #pragma unroll
